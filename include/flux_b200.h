@@ -1,0 +1,197 @@
+/*
+ * flux_b200.h — C ABI of the B200-native fused tensor-parallel operators
+ * (AllGather-GEMM and GEMM-ReduceScatter, Flux arXiv 2406.06858).
+ *
+ * This is the drop-in boundary for the reference's hot path. Every entry point
+ * names the reference interface it replaces (paths relative to
+ * /root/reference/proj). Plain C types only: pointers, ints, sizes. All device
+ * work is asynchronous on the caller's streams; flux_sync() joins it and
+ * surfaces device-side failures (e.g. a signal wait that timed out) as
+ * FLUX_ERR_DEADLOCK, mirroring overlap::DeadlockError.
+ *
+ * Data model (reference workspace.hpp:12-19, problem.hpp:14-38):
+ *   AllGatherGemm     rank r: A shard [m/tp, k] bf16, B shard [n/tp, k] bf16
+ *                     (weight stored [out, in] = K-major, i.e. the transpose of
+ *                     the reference's b_shard [k, n/tp]), gathered A a_agg
+ *                     [m, k], output C [m, n/tp].
+ *   GemmReduceScatter rank r: A shard [m, k/tp], B shard [n, k/tp] (K-major),
+ *                     output C [m/tp, n] = rows owned by r of the rank-ordered
+ *                     sum of all partial products.
+ * The library owns these buffers inside a per-rank symmetric heap (the
+ * reference ShardedWorkspace + its peer directory, workspace.cpp:5-29,56-65);
+ * callers address them through flux_buffer().
+ */
+#ifndef FLUX_B200_H_
+#define FLUX_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FLUX_ABI_VERSION 1
+
+/* Return codes. The reference raises C++ exceptions (errors.hpp:9-31); each
+ * maps to one code. The C++ shim (include/flux/overlap.hpp) rethrows them. */
+typedef enum {
+    FLUX_OK = 0,
+    FLUX_ERR_CONFIG = 1,    /* overlap::ConfigError   */
+    FLUX_ERR_SHAPE = 2,     /* overlap::ShapeError    */
+    FLUX_ERR_DIRECTORY = 3, /* overlap::DirectoryError (peer mapping missing) */
+    FLUX_ERR_DEADLOCK = 4,  /* overlap::DeadlockError (device wait timed out) */
+    FLUX_ERR_BOUNDS = 5,    /* overlap::BoundsError   */
+    FLUX_ERR_CUDA = 6       /* CUDA runtime / driver failure */
+} flux_status;
+
+/* overlap::Pattern (problem.hpp:10) */
+typedef enum { FLUX_ALLGATHER_GEMM = 0, FLUX_GEMM_REDUCESCATTER = 1 } flux_pattern;
+/* overlap::TransferMode (engine.hpp:16) */
+typedef enum { FLUX_PULL = 0, FLUX_PUSH = 1 } flux_transfer_mode;
+/* overlap::WriteMode (engine.hpp:17) */
+typedef enum { FLUX_WRITE_ALLTOALL = 0, FLUX_FUSED_REDUCE = 1 } flux_write_mode;
+/* overlap::SwizzleKind (swizzle.hpp:10) */
+typedef enum { FLUX_SWIZZLE_NAIVE = 0, FLUX_SWIZZLE_RANK_SHIFTED = 1, FLUX_SWIZZLE_ARRIVAL_ALIGNED = 2 } flux_swizzle_kind;
+typedef enum { FLUX_BF16 = 0, FLUX_F32 = 1 } flux_dtype;
+
+/* Buffers of one rank (overlap::RankBuffers, workspace.hpp:12-19). */
+typedef enum {
+    FLUX_BUF_A_SHARD = 0,
+    FLUX_BUF_B_SHARD = 1,
+    FLUX_BUF_A_AGG = 2,
+    FLUX_BUF_C_OUT = 3,
+    FLUX_BUF_STAGING = 4
+} flux_buffer_kind;
+
+/* overlap::ProblemSpec (problem.hpp:22-38) */
+typedef struct {
+    int m, n, k, tp;
+    int pattern; /* flux_pattern */
+} flux_problem;
+
+/* overlap::TileShape (problem.hpp:40-43): ownership / comm granularity. The
+ * device MMA tile is fixed by the kernel (128x256); (tm, tn) keeps the
+ * reference's divisibility contract and error messages. */
+typedef struct {
+    int tm, tn;
+} flux_tile;
+
+/* overlap::EngineOptions (engine.hpp:65-72) plus the B200 knobs. */
+typedef struct {
+    int workers_per_rank;      /* accepted for API parity; the device uses every SM */
+    int deterministic_reduce;  /* 1: WriteAlltoAll-style source-ordered sum */
+    long long poll_budget;     /* accepted for API parity (device waits are time-bounded) */
+    double wall_budget_s;      /* device spin-wait timeout (default 10 s, engine.hpp:69) */
+    uint64_t interleave_seed;  /* nonzero: device jitter (nanosleep) before tiles, race testing */
+    int shift_offset;          /* RankShifted offset (swizzle.hpp:27), default 1 */
+    int out_dtype;             /* flux_dtype of C (default BF16) */
+    int emulated_order;        /* single-device multi-rank launch order: 0 step-major, 1 rank-major */
+} flux_opts;
+
+typedef struct {
+    size_t heap_bytes;         /* per-rank symmetric heap size (0 = 1 GiB) */
+} flux_comm_opts;
+
+typedef struct flux_comm flux_comm;
+
+/* Device view of one buffer: element (i, j) is at ptr + (i*ld + j)*elem_size. */
+typedef struct {
+    void* ptr;
+    int rows, cols, ld;
+    int dtype; /* flux_dtype */
+} flux_buffer_desc;
+
+/* ---- diagnostics ---------------------------------------------------------- */
+const char* flux_last_error(void);          /* thread-local message of the last failure */
+int flux_abi_version(void);
+int flux_device_sm_count(int device);       /* 0 without a GPU */
+void flux_default_opts(flux_opts* opts);    /* EngineOptions{} defaults */
+
+/* ---- problem / tiling (problem.cpp:15-47) ---------------------------------- */
+/* ProblemSpec::validate + validate_tiling; same rules and messages. */
+int flux_problem_validate(const flux_problem* problem, const flux_tile* tile);
+/* grid_for (problem.cpp:40-47) */
+int flux_grid_for(const flux_problem* problem, const flux_tile* tile, int* tile_rows,
+                  int* tile_cols, int* row_blocks);
+
+/* ---- schedules (swizzle.cpp:23-80, topology.cpp:46-178) -------------------- */
+/* tile_order(SwizzlePolicy{kind, rank, tp, shift_offset, arrival_blocks}, grid_for(problem, tile))
+ * writes grid.tiles() coordinates. n_arrival == 0 means the default ring order. */
+int flux_tile_order(const flux_problem* problem, const flux_tile* tile, int kind, int rank,
+                    int shift_offset, const int* arrival_blocks, int n_arrival, int* out_rows,
+                    int* out_cols);
+/* comm_order(Topology{NVLinkRing}, rank, tp, rows_per_rank, rpct): descriptors
+ * (peer, row_begin, rows). *count receives the number written (<= max). */
+int flux_comm_order(int rank, int tp, int rows_per_rank, int rows_per_comm_tile, int* out_peer,
+                    int* out_row_begin, int* out_rows, int max, int* count);
+/* make_comm_specs(problem, Topology{}, rpct, mode) (engine.cpp:77-99) for one
+ * rank, including CommTileSpec::validate (engine.cpp:40-75). */
+int flux_make_comm_spec(const flux_problem* problem, int rank, int rows_per_comm_tile,
+                        int transfer, int* out_peer, int* out_row_begin, int* out_rows, int max,
+                        int* count);
+
+/* ---- communicator = symmetric heap + peer directory (workspace.hpp:22-43) --- */
+size_t flux_required_heap_bytes(const flux_problem* problem);
+/* Single process: rank r lives on devices[r]. Devices may repeat (several ranks
+ * emulated on one GPU, the reference's threads-as-ranks model, engine.cpp:172-191);
+ * distinct devices get peer access over NVLink. */
+int flux_comm_create(int tp, const int* devices, const flux_comm_opts* opts, flux_comm** out);
+/* One process per GPU (torchrun): create, export a handle blob, all-gather the
+ * blobs out of band (torch.distributed), connect. */
+int flux_comm_create_ipc(int rank, int tp, int device, const flux_comm_opts* opts,
+                         flux_comm** out);
+size_t flux_comm_ipc_blob_bytes(void);
+int flux_comm_ipc_handle(flux_comm* comm, void* blob);
+int flux_comm_ipc_connect(flux_comm* comm, const void* blobs /* tp * blob_bytes, rank order */);
+/* Host-only validation of a gathered blob set (magic, ranks, tp, heap size). */
+int flux_ipc_blobs_check(const void* blobs, int tp, size_t heap_bytes);
+int flux_comm_destroy(flux_comm* comm);
+int flux_comm_tp(const flux_comm* comm);
+int flux_comm_rank(const flux_comm* comm); /* IPC: own rank; single process: -1 */
+/* Simulates an incomplete init-phase exchange (workspace.cpp:67-69, tests only). */
+int flux_comm_drop_peer(flux_comm* comm, int from_rank, int peer_rank);
+/* Buffer of `rank` for `problem` (any rank in single-process mode; own rank in IPC mode). */
+int flux_buffer(flux_comm* comm, int rank, int kind, const flux_problem* problem,
+                flux_buffer_desc* out);
+/* Copy a dense host matrix (rows x cols, row pitch host_ld elements, dtype of
+ * the buffer) into / out of a buffer, asynchronously on `stream` (NULL = the
+ * rank's default stream). Host memory should be pinned for async behaviour. */
+int flux_copy_in(flux_comm* comm, int rank, int kind, const flux_problem* problem,
+                 const void* host, int host_ld, void* stream);
+int flux_copy_out(flux_comm* comm, int rank, int kind, const flux_problem* problem, void* host,
+                  int host_ld, void* stream);
+
+/* ---- the fused operators -------------------------------------------------- */
+/* run_fused_allgather_gemm (engine.hpp:107-111, engine.cpp:443-556; paper Alg. 2+3).
+ * streams: one per rank in single-process mode (NULL = library streams), one in
+ * IPC mode. Comm tiles move on copy engines (Alg. 3) and raise per-comm-tile
+ * flags; the tcgen05 GEMM's TMA producer waits on them (Alg. 2). */
+int flux_ag_gemm(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
+                 int rows_per_comm_tile, int transfer, int swizzle_on, const flux_opts* opts,
+                 void* const* streams);
+/* run_fused_gemm_reducescatter (engine.hpp:101-103, engine.cpp:221-352; paper Alg. 1).
+ * The epilogue stores each partial tile into the owner's staging plane over
+ * NVLink and raises a per-(tile, source) flag; the owner reduces in source
+ * order 0..tp-1 inside its local-tile epilogue (deterministic). */
+int flux_gemm_rs(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
+                 int write_mode, int swizzle_on, const flux_opts* opts, void* const* streams);
+/* Local GEMM only (tp ranks each compute their own C = A_agg B^T / A B^T with no
+ * communication): T_gemm_nonsplit of Eq. 1 and the TP=1 path. */
+int flux_local_gemm(flux_comm* comm, const flux_problem* problem, const flux_opts* opts,
+                    void* const* streams);
+/* run_nonoverlap (engine.hpp:125-126, engine.cpp:558-605): serial copy-engine
+ * collective then the same GEMM kernel (or GEMM then serial reduce). */
+int flux_nonoverlap(flux_comm* comm, const flux_problem* problem, const flux_opts* opts,
+                    void* const* streams);
+/* Joins all work of the last operator; returns FLUX_ERR_DEADLOCK if a device
+ * wait timed out (message names the flag, as spin_wait does, engine.cpp:149-162). */
+int flux_sync(flux_comm* comm);
+/* Number of this library's kernels launched by the last operator call. */
+int flux_last_launch_count(const flux_comm* comm);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* FLUX_B200_H_ */

@@ -1,0 +1,15 @@
+"""B200-native fused AllGather-GEMM / GEMM-ReduceScatter (Flux, arXiv 2406.06858).
+
+The operators live in the native library libflux_b200.so (C ABI:
+include/flux_b200.h); this package is the Python host mirror of the
+reference's operator API over that ABI.
+"""
+from . import _native
+from ._native import (ALLGATHER_GEMM, GEMM_REDUCESCATTER, PULL, PUSH, WRITE_ALLTOALL, FUSED_REDUCE,
+                      SWIZZLE_NAIVE, SWIZZLE_RANK_SHIFTED, SWIZZLE_ARRIVAL_ALIGNED, BF16, F32,
+                      ConfigError, ShapeError, DirectoryError, DeadlockError, BoundsError, CudaError,
+                      FluxError, default_opts)
+from .comm import (Communicator, ProblemSpec, TileShape, comm_order, grid_for, make_comm_spec,
+                   required_heap_bytes, tile_order, validate_tiling)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,160 @@
+"""ctypes binding of the C ABI in include/flux_b200.h.
+
+This module is the only place Python touches the native library. It fails
+loudly when `libflux_b200.so` is missing: there is no Python or CPU fallback
+for the operators.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libflux_b200.so")
+
+# Return codes (flux_status) -> reference exception taxonomy (errors.hpp:9-31).
+OK, ERR_CONFIG, ERR_SHAPE, ERR_DIRECTORY, ERR_DEADLOCK, ERR_BOUNDS, ERR_CUDA = range(7)
+ALLGATHER_GEMM, GEMM_REDUCESCATTER = 0, 1
+PULL, PUSH = 0, 1
+WRITE_ALLTOALL, FUSED_REDUCE = 0, 1
+SWIZZLE_NAIVE, SWIZZLE_RANK_SHIFTED, SWIZZLE_ARRIVAL_ALIGNED = 0, 1, 2
+BF16, F32 = 0, 1
+BUF_A_SHARD, BUF_B_SHARD, BUF_A_AGG, BUF_C_OUT, BUF_STAGING, BUF_C_OUT_F32 = 0, 1, 2, 3, 4, 5
+
+
+class FluxError(RuntimeError):
+    code = -1
+
+
+class ConfigError(FluxError):
+    code = ERR_CONFIG
+
+
+class ShapeError(FluxError):
+    code = ERR_SHAPE
+
+
+class DirectoryError(FluxError):
+    code = ERR_DIRECTORY
+
+
+class DeadlockError(FluxError):
+    code = ERR_DEADLOCK
+
+
+class BoundsError(FluxError):
+    code = ERR_BOUNDS
+
+
+class CudaError(FluxError):
+    code = ERR_CUDA
+
+
+_EXC = {ERR_CONFIG: ConfigError, ERR_SHAPE: ShapeError, ERR_DIRECTORY: DirectoryError,
+        ERR_DEADLOCK: DeadlockError, ERR_BOUNDS: BoundsError, ERR_CUDA: CudaError}
+
+
+class Problem(C.Structure):
+    _fields_ = [("m", C.c_int), ("n", C.c_int), ("k", C.c_int), ("tp", C.c_int), ("pattern", C.c_int)]
+
+
+class Tile(C.Structure):
+    _fields_ = [("tm", C.c_int), ("tn", C.c_int)]
+
+
+class Opts(C.Structure):
+    _fields_ = [("workers_per_rank", C.c_int), ("deterministic_reduce", C.c_int),
+                ("poll_budget", C.c_longlong), ("wall_budget_s", C.c_double),
+                ("interleave_seed", C.c_uint64), ("shift_offset", C.c_int), ("out_dtype", C.c_int),
+                ("emulated_order", C.c_int)]
+
+
+class CommOpts(C.Structure):
+    _fields_ = [("heap_bytes", C.c_size_t)]
+
+
+class BufferDesc(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("rows", C.c_int), ("cols", C.c_int), ("ld", C.c_int),
+                ("dtype", C.c_int)]
+
+
+_P = C.POINTER
+_SIGS = {
+    "flux_last_error": (C.c_char_p, []),
+    "flux_abi_version": (C.c_int, []),
+    "flux_device_sm_count": (C.c_int, [C.c_int]),
+    "flux_default_opts": (None, [_P(Opts)]),
+    "flux_problem_validate": (C.c_int, [_P(Problem), _P(Tile)]),
+    "flux_grid_for": (C.c_int, [_P(Problem), _P(Tile), _P(C.c_int), _P(C.c_int), _P(C.c_int)]),
+    "flux_tile_order": (C.c_int, [_P(Problem), _P(Tile), C.c_int, C.c_int, C.c_int, _P(C.c_int), C.c_int,
+                                  _P(C.c_int), _P(C.c_int)]),
+    "flux_comm_order": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P(C.c_int), _P(C.c_int), _P(C.c_int),
+                                  C.c_int, _P(C.c_int)]),
+    "flux_make_comm_spec": (C.c_int, [_P(Problem), C.c_int, C.c_int, C.c_int, _P(C.c_int), _P(C.c_int),
+                                      _P(C.c_int), C.c_int, _P(C.c_int)]),
+    "flux_required_heap_bytes": (C.c_size_t, [_P(Problem)]),
+    "flux_comm_create": (C.c_int, [C.c_int, _P(C.c_int), _P(CommOpts), _P(C.c_void_p)]),
+    "flux_comm_create_ipc": (C.c_int, [C.c_int, C.c_int, C.c_int, _P(CommOpts), _P(C.c_void_p)]),
+    "flux_comm_ipc_blob_bytes": (C.c_size_t, []),
+    "flux_comm_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "flux_comm_ipc_connect": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "flux_ipc_blobs_check": (C.c_int, [C.c_void_p, C.c_int, C.c_size_t]),
+    "flux_comm_destroy": (C.c_int, [C.c_void_p]),
+    "flux_comm_tp": (C.c_int, [C.c_void_p]),
+    "flux_comm_rank": (C.c_int, [C.c_void_p]),
+    "flux_comm_drop_peer": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "flux_buffer": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _P(Problem), _P(BufferDesc)]),
+    "flux_copy_in": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _P(Problem), C.c_void_p, C.c_int, C.c_void_p]),
+    "flux_copy_out": (C.c_int, [C.c_void_p, C.c_int, C.c_int, _P(Problem), C.c_void_p, C.c_int, C.c_void_p]),
+    "flux_ag_gemm": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, C.c_int, C.c_int, _P(Opts),
+                               _P(C.c_void_p)]),
+    "flux_gemm_rs": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, C.c_int, _P(Opts), _P(C.c_void_p)]),
+    "flux_local_gemm": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
+    "flux_nonoverlap": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
+    "flux_sync": (C.c_int, [C.c_void_p]),
+    "flux_last_launch_count": (C.c_int, [C.c_void_p]),
+}
+
+# Symbols include/flux_b200.h declares (tests check the library exports all of them).
+EXPORTED = sorted(_SIGS)
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libflux_b200.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2406_06858_b200.build` "
+                "(the fused operators have no CPU fallback)")
+        l = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != OK:
+        msg = lib().flux_last_error().decode(errors="replace")
+        raise _EXC.get(rc, FluxError)(msg)
+
+
+def default_opts(**kw) -> Opts:
+    o = Opts()
+    lib().flux_default_opts(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def stream_array(streams):
+    """List of raw cudaStream_t ints (or None) -> void*[] (or NULL)."""
+    if streams is None:
+        return None
+    arr = (C.c_void_p * len(streams))(*[s if s else None for s in streams])
+    return arr

@@ -1,0 +1,58 @@
+"""Builds the native library `libflux_b200.so` in-tree for sm_100a.
+
+The library is the C ABI declared in include/flux_b200.h (host C++ + CUDA
+kernels). It is built with nvcc directly (no torch extension machinery): the
+product has no torch types at its boundary. `-cudart static` keeps it
+independent of whichever libcudart the host process already loaded.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libflux_b200.so")
+
+SOURCES = ["flux_kernels.cu", "flux_api.cpp"]
+HEADERS = ["flux_internal.hpp"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    cand = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
+    return cand if os.path.exists(cand) else "nvcc"
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
+    deps += [os.path.join(ROOT, "include", "flux_b200.h"), os.path.join(ROOT, "include", "flux", "overlap.hpp")]
+    deps.append(os.path.abspath(__file__))
+    if not force and not _stale(LIB, deps):
+        return LIB
+    cmd = [
+        nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+        "-Xcompiler", "-fvisibility=default", "-cudart", "static",
+        "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+        "-o", LIB + ".tmp",
+        *[os.path.join(CSRC, s) for s in SOURCES],
+        "-lrt", "-ldl", "-lpthread",
+    ]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,215 @@
+"""Python host mirror of the communicator and the fused operators.
+
+Thin object layer over the C ABI (include/flux_b200.h) with the reference's
+vocabulary: a communicator owns every rank's symmetric buffers (the reference
+ShardedWorkspace + peer directory, workspace.hpp:22-43) and runs
+`run_fused_allgather_gemm` / `run_fused_gemm_reducescatter`
+(engine.hpp:101-111) on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Callable, Optional, Sequence
+
+from . import _native as N
+
+
+@dataclass(frozen=True)
+class ProblemSpec:
+    """overlap::ProblemSpec (problem.hpp:22-38)."""
+
+    m: int
+    n: int
+    k: int
+    tp: int = 1
+    pattern: int = N.ALLGATHER_GEMM
+
+    def c(self) -> N.Problem:
+        return N.Problem(self.m, self.n, self.k, self.tp, self.pattern)
+
+    def validate(self) -> None:
+        N.check(N.lib().flux_problem_validate(C.byref(self.c()), None))
+
+    def rows_per_rank(self) -> int:
+        return self.m // self.tp
+
+    def local_cols(self) -> int:
+        return self.n // self.tp if self.pattern == N.ALLGATHER_GEMM else self.n
+
+    def local_k(self) -> int:
+        return self.k // self.tp if self.pattern == N.GEMM_REDUCESCATTER else self.k
+
+    def owner_of_row(self, row: int) -> int:
+        return row // self.rows_per_rank()
+
+    def flops(self) -> float:
+        """Whole-job algorithmic FLOPs (all ranks)."""
+        return 2.0 * self.m * self.n * self.k
+
+
+@dataclass(frozen=True)
+class TileShape:
+    """overlap::TileShape (problem.hpp:40-43)."""
+
+    tm: int
+    tn: int
+
+    def c(self) -> N.Tile:
+        return N.Tile(self.tm, self.tn)
+
+
+def validate_tiling(problem: ProblemSpec, tile: TileShape) -> None:
+    N.check(N.lib().flux_problem_validate(C.byref(problem.c()), C.byref(tile.c())))
+
+
+def grid_for(problem: ProblemSpec, tile: TileShape) -> tuple[int, int, int]:
+    a, b, r = C.c_int(), C.c_int(), C.c_int()
+    N.check(N.lib().flux_grid_for(C.byref(problem.c()), C.byref(tile.c()), C.byref(a), C.byref(b), C.byref(r)))
+    return a.value, b.value, r.value
+
+
+def tile_order(problem: ProblemSpec, tile: TileShape, kind: int, rank: int, shift_offset: int = 1,
+               arrival_blocks: Optional[Sequence[int]] = None) -> list[tuple[int, int]]:
+    """tile_order(SwizzlePolicy, grid) (swizzle.cpp:75-80) as (row, col) pairs."""
+    rows, cols, _ = grid_for(problem, tile)
+    n = rows * cols
+    out_r, out_c = (C.c_int * n)(), (C.c_int * n)()
+    arr = (C.c_int * len(arrival_blocks))(*arrival_blocks) if arrival_blocks else None
+    N.check(N.lib().flux_tile_order(C.byref(problem.c()), C.byref(tile.c()), kind, rank, shift_offset, arr,
+                                    len(arrival_blocks or []), out_r, out_c))
+    return list(zip(out_r, out_c))
+
+
+def comm_order(rank: int, tp: int, rows_per_rank: int, rows_per_comm_tile: int) -> list[tuple[int, int, int]]:
+    """comm_order(Topology{NVLinkRing}, ...) (topology.cpp:102-168): (peer, row_begin, rows)."""
+    cap = max(1, tp * max(1, rows_per_rank // max(1, rows_per_comm_tile)))
+    p, b, r, n = (C.c_int * cap)(), (C.c_int * cap)(), (C.c_int * cap)(), C.c_int()
+    N.check(N.lib().flux_comm_order(rank, tp, rows_per_rank, rows_per_comm_tile, p, b, r, cap, C.byref(n)))
+    return [(p[i], b[i], r[i]) for i in range(n.value)]
+
+
+def make_comm_spec(problem: ProblemSpec, rank: int, rows_per_comm_tile: int, transfer: int) -> list[tuple[int, int, int]]:
+    """make_comm_specs(...)[rank].order (engine.cpp:77-99), validated."""
+    cap = max(1, problem.m)
+    p, b, r, n = (C.c_int * cap)(), (C.c_int * cap)(), (C.c_int * cap)(), C.c_int()
+    N.check(N.lib().flux_make_comm_spec(C.byref(problem.c()), rank, rows_per_comm_tile, transfer, p, b, r, cap,
+                                        C.byref(n)))
+    return [(p[i], b[i], r[i]) for i in range(n.value)]
+
+
+class _CAI:
+    """__cuda_array_interface__ holder so torch can view a library buffer."""
+
+    def __init__(self, ptr: int, rows: int, cols: int, ld: int, typestr: str, esize: int):
+        self.__cuda_array_interface__ = {
+            "shape": (rows, cols), "strides": (ld * esize, esize), "typestr": typestr,
+            "data": (ptr, False), "version": 3,
+        }
+
+
+class Communicator:
+    """Symmetric-heap communicator over `tp` ranks.
+
+    Single-process mode: rank r lives on devices[r] (devices may repeat: ranks
+    emulated on one GPU). IPC mode: one process per GPU, see `Communicator.ipc`.
+    """
+
+    def __init__(self, tp: int, devices: Optional[Sequence[int]] = None, heap_bytes: int = 0, *, _handle=None):
+        self.tp = tp
+        self._h = C.c_void_p(_handle) if _handle is not None else C.c_void_p()
+        if _handle is None:
+            devs = (C.c_int * tp)(*(devices if devices is not None else [0] * tp))
+            N.check(N.lib().flux_comm_create(tp, devs, C.byref(N.CommOpts(heap_bytes)), C.byref(self._h)))
+        self.rank = N.lib().flux_comm_rank(self._h)
+
+    @classmethod
+    def ipc(cls, rank: int, tp: int, device: int, heap_bytes: int,
+            all_gather_bytes: Callable[[bytes], list[bytes]]) -> "Communicator":
+        """Multi-process constructor: `all_gather_bytes` exchanges handle blobs
+        (e.g. torch.distributed.all_gather_object), the paper's init-phase IPC
+        exchange."""
+        h = C.c_void_p()
+        N.check(N.lib().flux_comm_create_ipc(rank, tp, device, C.byref(N.CommOpts(heap_bytes)), C.byref(h)))
+        nb = N.lib().flux_comm_ipc_blob_bytes()
+        blob = C.create_string_buffer(nb)
+        N.check(N.lib().flux_comm_ipc_handle(h, blob))
+        blobs = all_gather_bytes(blob.raw)
+        joined = C.create_string_buffer(b"".join(blobs), nb * tp)
+        N.check(N.lib().flux_comm_ipc_connect(h, joined))
+        return cls(tp, _handle=h.value)
+
+    # ---- buffers -------------------------------------------------------------
+    def buffer(self, rank: int, kind: int, problem: ProblemSpec) -> N.BufferDesc:
+        d = N.BufferDesc()
+        N.check(N.lib().flux_buffer(self._h, rank, kind, C.byref(problem.c()), C.byref(d)))
+        return d
+
+    def tensor(self, rank: int, kind: int, problem: ProblemSpec):
+        """torch view (no copy) of a rank's buffer: bf16 or fp32, strided by the padded pitch."""
+        import torch
+
+        d = self.buffer(rank, kind, problem)
+        if d.dtype == N.F32:
+            return torch.as_tensor(_CAI(d.ptr, d.rows, d.cols, d.ld, "<f4", 4), device="cuda")
+        t = torch.as_tensor(_CAI(d.ptr, d.rows, d.cols, d.ld, "<i2", 2), device="cuda")
+        return t.view(torch.bfloat16)
+
+    def copy_in(self, rank: int, kind: int, problem: ProblemSpec, host_ptr: int, host_ld: int, stream=None):
+        N.check(N.lib().flux_copy_in(self._h, rank, kind, C.byref(problem.c()), C.c_void_p(host_ptr), host_ld,
+                                     C.c_void_p(stream) if stream else None))
+
+    def copy_out(self, rank: int, kind: int, problem: ProblemSpec, host_ptr: int, host_ld: int, stream=None):
+        N.check(N.lib().flux_copy_out(self._h, rank, kind, C.byref(problem.c()), C.c_void_p(host_ptr), host_ld,
+                                      C.c_void_p(stream) if stream else None))
+
+    # ---- operators -------------------------------------------------------------
+    def ag_gemm(self, problem: ProblemSpec, tile: TileShape, rows_per_comm_tile: int = 0, transfer: int = N.PULL,
+                swizzle: bool = True, opts: Optional[N.Opts] = None, streams=None) -> None:
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_ag_gemm(self._h, C.byref(problem.c()), C.byref(tile.c()), rows_per_comm_tile,
+                                     transfer, int(swizzle), C.byref(o), N.stream_array(streams)))
+
+    def gemm_rs(self, problem: ProblemSpec, tile: TileShape, write_mode: int = N.WRITE_ALLTOALL,
+                swizzle: bool = True, opts: Optional[N.Opts] = None, streams=None) -> None:
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_gemm_rs(self._h, C.byref(problem.c()), C.byref(tile.c()), write_mode, int(swizzle),
+                                     C.byref(o), N.stream_array(streams)))
+
+    def local_gemm(self, problem: ProblemSpec, opts: Optional[N.Opts] = None, streams=None) -> None:
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_local_gemm(self._h, C.byref(problem.c()), C.byref(o), N.stream_array(streams)))
+
+    def nonoverlap(self, problem: ProblemSpec, opts: Optional[N.Opts] = None, streams=None) -> None:
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_nonoverlap(self._h, C.byref(problem.c()), C.byref(o), N.stream_array(streams)))
+
+    def sync(self) -> None:
+        N.check(N.lib().flux_sync(self._h))
+
+    def last_launch_count(self) -> int:
+        return N.lib().flux_last_launch_count(self._h)
+
+    def drop_peer(self, from_rank: int, peer_rank: int) -> None:
+        N.check(N.lib().flux_comm_drop_peer(self._h, from_rank, peer_rank))
+
+    def close(self) -> None:
+        if self._h:
+            N.lib().flux_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def required_heap_bytes(problem: ProblemSpec) -> int:
+    return int(N.lib().flux_required_heap_bytes(C.byref(problem.c())))

@@ -1,0 +1,1175 @@
+// C ABI of the B200 fused operators: problem validation, schedules, the
+// symmetric-heap communicator, and the AllGather-GEMM / GEMM-ReduceScatter
+// drivers. See include/flux_b200.h for the contract and DESIGN.md for the
+// data layout.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "flux_b200.h"
+#include "flux_internal.hpp"
+
+using namespace fluxb200;
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// errors (reference errors.hpp:9-31 -> status codes)
+// ---------------------------------------------------------------------------
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define FLUX_CUDA(expr)                                                                    \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return fail(FLUX_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define FLUX_TRY(expr)          \
+    do {                        \
+        int _rc = (expr);       \
+        if (_rc != FLUX_OK) return _rc; \
+    } while (0)
+
+std::string S(long long v) { return std::to_string(v); }
+
+// ---------------------------------------------------------------------------
+// driver entry points (no link-time dependency on libcuda)
+// ---------------------------------------------------------------------------
+struct Driver {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    PFN_cuStreamWriteValue32_v11070 write32 = nullptr;
+    PFN_cuStreamWaitValue32_v11070 wait32 = nullptr;
+    bool ok = false;
+};
+
+Driver& driver() {
+    static Driver d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            d.encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            d.write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fn);
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            d.wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fn);
+        d.ok = d.encode && d.write32 && d.wait32;
+    });
+    return d;
+}
+
+int need_driver() {
+    if (!driver().ok) return fail(FLUX_ERR_CUDA, "CUDA driver entry points unavailable (no GPU driver?)");
+    return FLUX_OK;
+}
+
+int write_value(cudaStream_t s, void* addr, uint32_t v) {
+    CUresult r = driver().write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                                  CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "cuStreamWriteValue32 failed (" + S(r) + ")");
+    return FLUX_OK;
+}
+
+int wait_value_geq(cudaStream_t s, const void* addr, uint32_t v) {
+    if (v == 0) return FLUX_OK;  // epoch 0 is always satisfied
+    CUresult r = driver().wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                                 CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "cuStreamWaitValue32 failed (" + S(r) + ")");
+    return FLUX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// problem validation: ProblemSpec::validate / validate_tiling (problem.cpp:15-38)
+// ---------------------------------------------------------------------------
+int validate_problem(const flux_problem* p) {
+    if (!p) return fail(FLUX_ERR_CONFIG, "null problem");
+    if (p->m <= 0 || p->n <= 0 || p->k <= 0) return fail(FLUX_ERR_CONFIG, "problem dimensions must be positive");
+    if (p->tp <= 0) return fail(FLUX_ERR_CONFIG, "tp must be positive");
+    if (p->pattern != FLUX_ALLGATHER_GEMM && p->pattern != FLUX_GEMM_REDUCESCATTER)
+        return fail(FLUX_ERR_CONFIG, "unknown pattern");
+    if (p->m % p->tp != 0)
+        return fail(FLUX_ERR_CONFIG, "m=" + S(p->m) + " not divisible by tp=" + S(p->tp));
+    if (p->pattern == FLUX_ALLGATHER_GEMM && p->n % p->tp != 0)
+        return fail(FLUX_ERR_CONFIG,
+                    "AllGatherGemm requires n divisible by tp (weight is column-sharded); n=" + S(p->n) +
+                        " tp=" + S(p->tp));
+    if (p->pattern == FLUX_GEMM_REDUCESCATTER && p->k % p->tp != 0)
+        return fail(FLUX_ERR_CONFIG,
+                    "GemmReduceScatter requires k divisible by tp (weight is row-sharded); k=" + S(p->k) +
+                        " tp=" + S(p->tp));
+    return FLUX_OK;
+}
+
+int rows_per_rank(const flux_problem* p) { return p->m / p->tp; }
+int local_cols(const flux_problem* p) { return p->pattern == FLUX_ALLGATHER_GEMM ? p->n / p->tp : p->n; }
+int local_k(const flux_problem* p) { return p->pattern == FLUX_GEMM_REDUCESCATTER ? p->k / p->tp : p->k; }
+
+int validate_tiling(const flux_problem* p, const flux_tile* t) {
+    FLUX_TRY(validate_problem(p));
+    if (!t) return fail(FLUX_ERR_CONFIG, "null tile");
+    if (t->tm <= 0 || t->tn <= 0) return fail(FLUX_ERR_CONFIG, "tile extents must be positive");
+    const int rpr = rows_per_rank(p);
+    if (t->tm > rpr || rpr % t->tm != 0)
+        return fail(FLUX_ERR_CONFIG, "tm=" + S(t->tm) + " must divide m/tp=" + S(rpr));
+    const int lc = local_cols(p);
+    if (lc % t->tn != 0)
+        return fail(FLUX_ERR_CONFIG, "tn=" + S(t->tn) + " must divide the local output cols=" + S(lc));
+    return FLUX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// schedules: block order (swizzle.cpp:23-47), comm order (topology.cpp:46-55,102-178)
+// ---------------------------------------------------------------------------
+std::vector<int> block_order(int kind, int rank, int tp, int shift, const std::vector<int>& arrival) {
+    std::vector<int> b;
+    if (kind == FLUX_SWIZZLE_ARRIVAL_ALIGNED) {
+        if (!arrival.empty()) return arrival;
+        b.push_back(rank);
+        for (int d = 1; d < tp; ++d) b.push_back((rank + d) % tp);
+    } else {  // RankShifted: start after `shift`, local block last for shift = 1
+        for (int d = 0; d < tp; ++d) b.push_back(((rank + shift) % tp + d) % tp);
+    }
+    return b;
+}
+
+struct Desc {
+    int peer, row_begin, rows;
+};
+
+// NVLinkRing pull order: peers rank+1, rank+2, ..., each block cut into comm tiles.
+std::vector<Desc> ring_order(int rank, int tp, int rpr, int rpct) {
+    std::vector<Desc> out;
+    for (int d = 1; d < tp; ++d) {
+        const int peer = (rank + d) % tp;
+        for (int off = 0; off < rpr; off += rpct) out.push_back({peer, peer * rpr + off, rpct});
+    }
+    return out;
+}
+
+// Peers in order of first appearance (topology.cpp:170-178).
+std::vector<int> peer_order(const std::vector<Desc>& order, int rank, int rpr) {
+    std::vector<int> seq;
+    for (const Desc& d : order) {
+        const int block = d.row_begin / rpr;
+        if (block == rank) continue;
+        if (std::find(seq.begin(), seq.end(), block) == seq.end()) seq.push_back(block);
+    }
+    return seq;
+}
+
+// CommTileSpec::validate (engine.cpp:40-75).
+int validate_comm_spec(const flux_problem* p, int rank, int rpct, int transfer, const std::vector<Desc>& order) {
+    const int rpr = rows_per_rank(p);
+    if (rpct <= 0 || rpr % rpct != 0)
+        return fail(FLUX_ERR_CONFIG, "rows_per_comm_tile=" + S(rpct) + " must divide m/tp=" + S(rpr));
+    const int ct = rpr / rpct;
+    std::vector<int> seen(p->m / rpct, 0);
+    for (const Desc& d : order) {
+        if (d.rows != rpct || d.row_begin % rpct != 0 || d.row_begin < 0 || d.row_begin + d.rows > p->m)
+            return fail(FLUX_ERR_BOUNDS, "transfer descriptor rows [" + S(d.row_begin) + ",+" + S(d.rows) + ") invalid");
+        ++seen[d.row_begin / rpct];
+    }
+    for (int t = 0; t < static_cast<int>(seen.size()); ++t) {
+        const bool local = t / ct == rank;
+        if (transfer == FLUX_PULL) {
+            if (!local && seen[t] != 1)
+                return fail(FLUX_ERR_CONFIG, "comm order must cover non-local comm tile " + S(t) +
+                                                 " exactly once (saw " + S(seen[t]) + ")");
+            if (local && seen[t] != 0) return fail(FLUX_ERR_CONFIG, "comm order must not include local comm tiles");
+        } else {
+            if (local && seen[t] != p->tp - 1)
+                return fail(FLUX_ERR_CONFIG, "push order must carry local comm tile " + S(t) + " to every peer");
+            if (!local && seen[t] != 0) return fail(FLUX_ERR_CONFIG, "push order may only move local comm tiles");
+        }
+    }
+    return FLUX_OK;
+}
+
+// make_comm_specs for one rank (engine.cpp:77-99).
+int make_spec(const flux_problem* p, int rank, int rpct, int transfer, std::vector<Desc>& out) {
+    FLUX_TRY(validate_problem(p));
+    const int rpr = rows_per_rank(p);
+    if (rpct <= 0 || rpr % rpct != 0)
+        return fail(FLUX_ERR_CONFIG, "rows_per_comm_tile=" + S(rpct) + " must divide rows_per_rank=" + S(rpr));
+    if (rank < 0 || rank >= p->tp) return fail(FLUX_ERR_CONFIG, "rank " + S(rank) + " >= tp");
+    std::vector<Desc> pull = ring_order(rank, p->tp, rpr, rpct);
+    if (transfer == FLUX_PULL) {
+        out = pull;
+    } else if (transfer == FLUX_PUSH) {
+        out.clear();
+        for (int peer : peer_order(pull, rank, rpr))
+            for (int off = 0; off < rpr; off += rpct) out.push_back({peer, rank * rpr + off, rpct});
+    } else {
+        return fail(FLUX_ERR_CONFIG, "unknown transfer mode");
+    }
+    return validate_comm_spec(p, rank, rpct, transfer, out);
+}
+
+// Row-block visit order used by the AG kernel (engine.cpp:475-505).
+std::vector<int> ag_block_order(const flux_problem* p, int rank, int transfer, bool swizzle, int rpct) {
+    const int tp = p->tp, rpr = rows_per_rank(p);
+    if (!swizzle) {
+        std::vector<int> b;
+        for (int i = 0; i < tp; ++i) b.push_back(i);
+        return b;
+    }
+    if (transfer == FLUX_PULL) {  // arrival_aligned_policy: local first, then peer_order(comm)
+        std::vector<int> b{rank};
+        for (int q : peer_order(ring_order(rank, tp, rpr, rpct), rank, rpr)) b.push_back(q);
+        return b;
+    }
+    // Push: sources sorted by how early their list targets this rank.
+    std::vector<std::pair<int, int>> arrivals;
+    for (int s = 0; s < tp; ++s) {
+        if (s == rank) continue;
+        std::vector<Desc> spec;
+        flux_problem q = *p;
+        make_spec(&q, s, rpct, FLUX_PUSH, spec);
+        for (size_t i = 0; i < spec.size(); ++i)
+            if (spec[i].peer == rank) {
+                arrivals.emplace_back(static_cast<int>(i), s);
+                break;
+            }
+    }
+    std::sort(arrivals.begin(), arrivals.end());
+    std::vector<int> b{rank};
+    for (auto& a : arrivals) b.push_back(a.second);
+    for (int s = 0; s < tp; ++s)
+        if (std::find(b.begin(), b.end(), s) == b.end()) b.push_back(s);
+    return b;
+}
+
+// Device tile sequence of one rank over the kBM x kBN grid. When ownership
+// blocks align with device tile rows the reference's block-then-column-major
+// order is reproduced (swizzle.cpp:51-73); otherwise tiles straddle blocks and
+// the order is row-major (every rank walks the same sequence).
+std::vector<uint32_t> device_sequence(int m, int ncols, int rpr, const std::vector<int>& blocks, int slot) {
+    const int tiles_m = (m + kBM - 1) / kBM, tiles_n = (ncols + kBN - 1) / kBN;
+    std::vector<uint32_t> seq;
+    seq.reserve(static_cast<size_t>(tiles_m) * tiles_n);
+    if (!blocks.empty() && rpr % kBM == 0) {
+        const int rpb = rpr / kBM;
+        for (int b : blocks)
+            for (int c = 0; c < tiles_n; ++c)
+                for (int r = 0; r < rpb; ++r) seq.push_back(pack_tile(slot, b * rpb + r, c));
+    } else {
+        for (int r = 0; r < tiles_m; ++r)
+            for (int c = 0; c < tiles_n; ++c) seq.push_back(pack_tile(slot, r, c));
+    }
+    return seq;
+}
+
+// ---------------------------------------------------------------------------
+// symmetric heap layout (identical on every rank)
+// ---------------------------------------------------------------------------
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+int pad_to(int v, int a) { return (v + a - 1) / a * a; }
+
+struct Region {
+    size_t off = 0;
+    int rows = 0, cols = 0, ld = 0, dtype = FLUX_BF16;
+    size_t bytes() const { return static_cast<size_t>(rows) * ld * (dtype == FLUX_F32 ? 4 : 2); }
+};
+
+struct Layout {
+    Region a_shard, b, a_agg, c, c32, staging;
+    long long stage_plane = 0, stage_parity = 0;
+    int ld_stage = 0;
+    size_t total = 0;
+};
+
+Layout layout_for(const flux_problem* p) {
+    Layout L;
+    const int rpr = rows_per_rank(p), lc = local_cols(p), lk = local_k(p);
+    size_t off = kDataOffset;
+    auto place = [&](Region& r, int rows, int cols, int dtype, int pad) {
+        r.off = off;
+        r.rows = rows;
+        r.cols = cols;
+        r.ld = pad_to(cols, pad);
+        r.dtype = dtype;
+        off = align_up(off + std::max<size_t>(r.bytes(), 1), 4096);
+    };
+    if (p->pattern == FLUX_ALLGATHER_GEMM) {
+        place(L.a_shard, rpr, lk, FLUX_BF16, 64);
+        place(L.a_agg, p->m, lk, FLUX_BF16, 64);
+        place(L.b, lc, lk, FLUX_BF16, 64);
+        place(L.c32, p->m, lc, FLUX_F32, 32);  // C region sized for fp32; bf16 view shares it
+    } else {
+        place(L.a_shard, p->m, lk, FLUX_BF16, 64);
+        place(L.b, lc, lk, FLUX_BF16, 64);
+        place(L.c32, rpr, lc, FLUX_F32, 32);
+        L.ld_stage = pad_to(lc, 32);
+        L.stage_plane = static_cast<long long>(rpr) * L.ld_stage;
+        L.stage_parity = L.stage_plane * p->tp;
+        L.staging.off = off;
+        L.staging.rows = 2 * p->m;  // 2 parities x tp planes x rpr rows
+        L.staging.cols = lc;
+        L.staging.ld = L.ld_stage;
+        L.staging.dtype = FLUX_F32;
+        off = align_up(off + static_cast<size_t>(2) * L.stage_parity * 4, 4096);
+    }
+    L.c = L.c32;
+    L.c.dtype = FLUX_BF16;
+    L.total = off;
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+// communicator
+// ---------------------------------------------------------------------------
+struct RankState {
+    int device = 0;
+    char* heap = nullptr;     // address of this rank's heap in our VA (own or peer-mapped)
+    bool owned = false;       // allocated by us (free on destroy) vs IPC-opened
+    bool local = false;       // we drive this rank (launch work for it)
+    cudaStream_t stream = nullptr;       // default compute stream
+    cudaStream_t copy_stream = nullptr;  // copy-engine transfer loop
+    cudaEvent_t start_evt = nullptr, kernel_evt = nullptr, copy_evt = nullptr;
+    bool kernel_evt_valid = false;
+};
+
+constexpr uint32_t kIpcMagic = 0xF1u << 24 | 0xB200u;
+
+struct IpcBlob {
+    uint32_t magic;
+    int32_t rank, tp, device;
+    uint64_t heap_bytes;
+    int32_t pid;
+    int32_t pad;
+    cudaIpcMemHandle_t handle;
+};
+
+}  // namespace
+
+struct flux_comm {
+    int tp = 0;
+    int my_rank = -1;  // IPC mode
+    bool ipc = false;
+    bool connected = false;
+    size_t heap_bytes = 0;
+    uint32_t epoch = 0;
+    std::vector<RankState> ranks;
+    std::vector<std::vector<bool>> directory;  // [from][peer] usable
+    int last_launches = 0;
+    std::vector<uint32_t*> order_dev;  // per device group scratch for tile orders
+    std::vector<size_t> order_cap;
+};
+
+namespace {
+
+int check_comm(flux_comm* c) {
+    if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
+    if (c->ipc && !c->connected) return fail(FLUX_ERR_DIRECTORY, "IPC communicator not connected");
+    return FLUX_OK;
+}
+
+int check_directory(flux_comm* c, int from, int peer) {
+    if (from < 0 || from >= c->tp || peer < 0 || peer >= c->tp)
+        return fail(FLUX_ERR_DIRECTORY, "directory lookup out of range: rank " + S(from) + " -> peer " + S(peer));
+    if (!c->directory[from][peer] || c->ranks[peer].heap == nullptr)
+        return fail(FLUX_ERR_DIRECTORY,
+                    "missing peer buffer: rank " + S(from) + " has no directory entry for peer " + S(peer));
+    return FLUX_OK;
+}
+
+int init_rank_streams(RankState& r) {
+    FLUX_CUDA(cudaSetDevice(r.device));
+    FLUX_CUDA(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
+    FLUX_CUDA(cudaStreamCreateWithFlags(&r.copy_stream, cudaStreamNonBlocking));
+    FLUX_CUDA(cudaEventCreateWithFlags(&r.start_evt, cudaEventDisableTiming));
+    FLUX_CUDA(cudaEventCreateWithFlags(&r.kernel_evt, cudaEventDisableTiming));
+    FLUX_CUDA(cudaEventCreateWithFlags(&r.copy_evt, cudaEventDisableTiming));
+    return FLUX_OK;
+}
+
+int alloc_heap(RankState& r, size_t bytes) {
+    FLUX_CUDA(cudaSetDevice(r.device));
+    void* p = nullptr;
+    FLUX_CUDA(cudaMalloc(&p, bytes));
+    FLUX_CUDA(cudaMemset(p, 0, bytes));
+    FLUX_CUDA(cudaDeviceSynchronize());
+    r.heap = static_cast<char*>(p);
+    r.owned = true;
+    return FLUX_OK;
+}
+
+template <class T>
+T* at(const RankState& r, size_t off) {
+    return reinterpret_cast<T*>(r.heap + off);
+}
+
+int make_tmap(CUtensorMap* m, const void* base, int rows, int cols, int ld, int box_rows) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = driver().encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + S(r) + ")");
+    return FLUX_OK;
+}
+
+int sm_count(int device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+    return v;
+}
+
+// Ranks this process drives, grouped by device (one fused launch per device).
+std::vector<std::vector<int>> device_groups(flux_comm* c) {
+    std::vector<std::vector<int>> groups;
+    std::vector<int> devs;
+    for (int r = 0; r < c->tp; ++r) {
+        if (!c->ranks[r].local) continue;
+        auto it = std::find(devs.begin(), devs.end(), c->ranks[r].device);
+        if (it == devs.end()) {
+            devs.push_back(c->ranks[r].device);
+            groups.push_back({r});
+        } else {
+            groups[it - devs.begin()].push_back(r);
+        }
+    }
+    return groups;
+}
+
+cudaStream_t stream_for(flux_comm* c, int rank, void* const* streams) {
+    if (streams) {
+        const int idx = c->ipc ? 0 : rank;
+        if (streams[idx]) return static_cast<cudaStream_t>(streams[idx]);
+    }
+    return c->ranks[rank].stream;
+}
+
+int upload_order(flux_comm* c, int gi, int device, const std::vector<uint32_t>& order, cudaStream_t s,
+                 uint32_t** out) {
+    if (static_cast<int>(c->order_dev.size()) <= gi) {
+        c->order_dev.resize(gi + 1, nullptr);
+        c->order_cap.resize(gi + 1, 0);
+    }
+    FLUX_CUDA(cudaSetDevice(device));
+    const size_t bytes = order.size() * sizeof(uint32_t);
+    if (c->order_cap[gi] < bytes) {
+        if (c->order_dev[gi]) {
+            FLUX_CUDA(cudaStreamSynchronize(s));
+            FLUX_CUDA(cudaFree(c->order_dev[gi]));
+        }
+        FLUX_CUDA(cudaMalloc(&c->order_dev[gi], bytes * 2));
+        c->order_cap[gi] = bytes * 2;
+    }
+    // Ordered on the launching stream; host data is copied before the call returns.
+    FLUX_CUDA(cudaMemcpyAsync(c->order_dev[gi], order.data(), bytes, cudaMemcpyHostToDevice, s));
+    FLUX_CUDA(cudaStreamSynchronize(s));
+    *out = c->order_dev[gi];
+    return FLUX_OK;
+}
+
+struct OpCommon {
+    flux_opts o;
+    uint64_t timeout_ns;
+};
+
+OpCommon common_opts(const flux_opts* opts) {
+    OpCommon oc;
+    if (opts) oc.o = *opts;
+    else flux_default_opts(&oc.o);
+    double s = oc.o.wall_budget_s > 0 ? oc.o.wall_budget_s : 10.0;
+    oc.timeout_ns = static_cast<uint64_t>(s * 1e9);
+    return oc;
+}
+
+// Launch one fused kernel per device group. `mode` selects the role.
+int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon& oc, void* const* streams,
+                  const std::vector<std::vector<uint32_t>>& seq_of_rank, int rpct, bool step_major,
+                  bool plain_on_agg = false, long long partial_off = -1) {
+    const bool plain_f32_to_staging = partial_off >= 0;
+    const Layout L = layout_for(p);
+    const int lk = local_k(p), lc = local_cols(p);
+    const int m_rows = p->m;  // per-rank GEMM rows (AG: gathered m; RS: full m)
+    auto groups = device_groups(c);
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const auto& g = groups[gi];
+        if (g.size() > static_cast<size_t>(kMaxRanks)) return fail(FLUX_ERR_CONFIG, "too many ranks on one device");
+        const int dev = c->ranks[g[0]].device;
+        FLUX_CUDA(cudaSetDevice(dev));
+        cudaStream_t lead = stream_for(c, g[0], streams);
+        GemmParams prm;
+        std::memset(&prm, 0, sizeof(prm));
+        for (size_t li = 0; li < g.size(); ++li) {
+            const RankState& rs = c->ranks[g[li]];
+            const Region& A = (mode == kModeAG || plain_on_agg) ? L.a_agg : L.a_shard;
+            FLUX_TRY(make_tmap(&prm.tma_a[li], rs.heap + A.off, A.rows, lk, A.ld, kBM));
+            FLUX_TRY(make_tmap(&prm.tma_b[li], rs.heap + L.b.off, lc, lk, L.b.ld, kBN));
+            if (plain_f32_to_staging) prm.c[li] = rs.heap + partial_off;  // full [m, n] fp32 partial
+            else prm.c[li] = rs.heap + L.c32.off;
+            prm.global_rank[li] = g[li];
+            prm.ag_flags[li] = at<uint32_t>(rs, kAgFlagOffset);
+            prm.ctrl[li] = at<uint32_t>(rs, kCtrlErr);
+        }
+        if (mode == kModeRS) {
+            for (int r = 0; r < c->tp; ++r) {
+                prm.staging[r] = reinterpret_cast<float*>(c->ranks[r].heap + L.staging.off);
+                prm.rs_flags[r] = at<uint32_t>(c->ranks[r], kRsFlagOffset);
+            }
+        }
+        // Interleave the per-rank sequences into one device schedule.
+        std::vector<uint32_t> order;
+        const size_t T = seq_of_rank[g[0]].size();
+        order.reserve(T * g.size());
+        if (step_major || g.size() == 1) {
+            for (size_t i = 0; i < T; ++i)
+                for (size_t li = 0; li < g.size(); ++li) {
+                    uint32_t e = seq_of_rank[g[li]][i];
+                    order.push_back((e & 0x0FFFFFFFu) | (uint32_t(li) << 28));
+                }
+        } else {
+            for (size_t li = 0; li < g.size(); ++li)
+                for (size_t i = 0; i < T; ++i) {
+                    uint32_t e = seq_of_rank[g[li]][i];
+                    order.push_back((e & 0x0FFFFFFFu) | (uint32_t(li) << 28));
+                }
+        }
+        uint32_t* order_dev = nullptr;
+        FLUX_TRY(upload_order(c, static_cast<int>(gi), dev, order, lead, &order_dev));
+        prm.order = order_dev;
+        prm.num_tiles = static_cast<int>(order.size());
+        prm.m = m_rows;
+        prm.n = lc;
+        prm.k = lk;
+        if (plain_f32_to_staging) {
+            prm.ldc = L.ld_stage;
+            prm.out_f32 = 1;
+        } else {
+            prm.ldc = L.c32.ld;
+            prm.out_f32 = oc.o.out_dtype == FLUX_F32 ? 1 : 0;
+        }
+        prm.tiles_n = (lc + kBN - 1) / kBN;
+        prm.tp = p->tp;
+        prm.rpr = rows_per_rank(p);
+        prm.rpct = rpct > 0 ? rpct : prm.rpr;
+        prm.ld_stage = L.ld_stage;
+        prm.stage_plane = L.stage_plane;
+        prm.stage_parity = L.stage_parity;
+        prm.epoch = c->epoch;
+        prm.timeout_ns = oc.timeout_ns;
+        prm.jitter_seed = oc.o.interleave_seed;
+        // Join the other local ranks' streams into the launch stream.
+        for (size_t li = 0; li < g.size(); ++li) {
+            cudaStream_t s = stream_for(c, g[li], streams);
+            if (s != lead) {
+                FLUX_CUDA(cudaEventRecord(c->ranks[g[li]].start_evt, s));
+                FLUX_CUDA(cudaStreamWaitEvent(lead, c->ranks[g[li]].start_evt, 0));
+            }
+        }
+        const int grid = std::max(1, std::min(prm.num_tiles, sm_count(dev)));
+        FLUX_CUDA(launch_gemm(mode, prm, grid, lead));
+        ++c->last_launches;
+        FLUX_CUDA(cudaEventRecord(c->ranks[g[0]].kernel_evt, lead));
+        for (size_t li = 0; li < g.size(); ++li) {
+            RankState& rs = c->ranks[g[li]];
+            rs.kernel_evt_valid = true;
+            cudaStream_t s = stream_for(c, g[li], streams);
+            if (li > 0) FLUX_CUDA(cudaEventRecord(rs.kernel_evt, lead));
+            if (s != lead) FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[g[0]].kernel_evt, 0));
+        }
+    }
+    return FLUX_OK;
+}
+
+int local_ranks_only(flux_comm* c, std::vector<int>& out) {
+    out.clear();
+    for (int r = 0; r < c->tp; ++r)
+        if (c->ranks[r].local) out.push_back(r);
+    return FLUX_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+extern "C" {
+
+const char* flux_last_error(void) { return g_last_error.c_str(); }
+int flux_abi_version(void) { return FLUX_ABI_VERSION; }
+
+int flux_device_sm_count(int device) { return sm_count(device); }
+
+void flux_default_opts(flux_opts* o) {
+    if (!o) return;
+    o->workers_per_rank = 0;
+    o->deterministic_reduce = 1;
+    o->poll_budget = 10000000LL;
+    o->wall_budget_s = 10.0;
+    o->interleave_seed = 0;
+    o->shift_offset = 1;
+    o->out_dtype = FLUX_BF16;
+    o->emulated_order = 0;
+}
+
+int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
+    if (!tile) return validate_problem(problem);
+    return validate_tiling(problem, tile);
+}
+
+int flux_grid_for(const flux_problem* p, const flux_tile* t, int* tile_rows, int* tile_cols, int* row_blocks) {
+    FLUX_TRY(validate_tiling(p, t));
+    if (tile_rows) *tile_rows = p->m / t->tm;
+    if (tile_cols) *tile_cols = local_cols(p) / t->tn;
+    if (row_blocks) *row_blocks = p->tp;
+    return FLUX_OK;
+}
+
+int flux_tile_order(const flux_problem* p, const flux_tile* t, int kind, int rank, int shift_offset,
+                    const int* arrival_blocks, int n_arrival, int* out_rows, int* out_cols) {
+    FLUX_TRY(validate_tiling(p, t));
+    const int tile_rows = p->m / t->tm, tile_cols = local_cols(p) / t->tn, tiles = tile_rows * tile_cols;
+    if (kind == FLUX_SWIZZLE_NAIVE) {  // map_tile Naive: row-major (swizzle.cpp:54-56)
+        for (int i = 0; i < tiles; ++i) {
+            out_rows[i] = i / tile_cols;
+            out_cols[i] = i % tile_cols;
+        }
+        return FLUX_OK;
+    }
+    if (kind != FLUX_SWIZZLE_RANK_SHIFTED && kind != FLUX_SWIZZLE_ARRIVAL_ALIGNED)
+        return fail(FLUX_ERR_CONFIG, "unknown swizzle kind");
+    std::vector<int> arrival(arrival_blocks ? arrival_blocks : nullptr,
+                             arrival_blocks ? arrival_blocks + n_arrival : nullptr);
+    std::vector<int> blocks = block_order(kind, rank, p->tp, shift_offset, arrival);
+    if (static_cast<int>(blocks.size()) != p->tp)
+        return fail(FLUX_ERR_CONFIG, "arrival block list does not cover the grid (" + S(blocks.size()) +
+                                         " blocks for " + S(p->tp) + ")");
+    const int rpb = tile_rows / p->tp, per_block = rpb * tile_cols;
+    for (int i = 0; i < tiles; ++i) {
+        const int block = blocks[i / per_block];
+        const int within = i % per_block;
+        out_rows[i] = block * rpb + within % rpb;  // column-major within the block
+        out_cols[i] = within / rpb;
+    }
+    return FLUX_OK;
+}
+
+int flux_comm_order(int rank, int tp, int rpr, int rpct, int* out_peer, int* out_row_begin, int* out_rows, int max,
+                    int* count) {
+    if (rank < 0 || rank >= tp) return fail(FLUX_ERR_CONFIG, "rank " + S(rank) + " >= tp");
+    if (rpct <= 0 || rpr % rpct != 0)
+        return fail(FLUX_ERR_CONFIG, "rows_per_comm_tile=" + S(rpct) + " must divide rows_per_rank=" + S(rpr));
+    std::vector<Desc> o = ring_order(rank, tp, rpr, rpct);
+    const int n = std::min<int>(max, static_cast<int>(o.size()));
+    for (int i = 0; i < n; ++i) {
+        out_peer[i] = o[i].peer;
+        out_row_begin[i] = o[i].row_begin;
+        out_rows[i] = o[i].rows;
+    }
+    if (count) *count = static_cast<int>(o.size());
+    return FLUX_OK;
+}
+
+int flux_make_comm_spec(const flux_problem* p, int rank, int rpct, int transfer, int* out_peer, int* out_row_begin,
+                        int* out_rows, int max, int* count) {
+    std::vector<Desc> o;
+    FLUX_TRY(make_spec(p, rank, rpct, transfer, o));
+    const int n = std::min<int>(max, static_cast<int>(o.size()));
+    for (int i = 0; i < n; ++i) {
+        out_peer[i] = o[i].peer;
+        out_row_begin[i] = o[i].row_begin;
+        out_rows[i] = o[i].rows;
+    }
+    if (count) *count = static_cast<int>(o.size());
+    return FLUX_OK;
+}
+
+size_t flux_required_heap_bytes(const flux_problem* p) {
+    if (validate_problem(p) != FLUX_OK) return 0;
+    return layout_for(p).total;
+}
+
+int flux_comm_create(int tp, const int* devices, const flux_comm_opts* opts, flux_comm** out) {
+    if (!out) return fail(FLUX_ERR_CONFIG, "null output");
+    *out = nullptr;
+    if (tp <= 0 || tp > kMaxRanks) return fail(FLUX_ERR_CONFIG, "tp must be in [1, " + S(kMaxRanks) + "]");
+    FLUX_TRY(need_driver());
+    auto* c = new flux_comm();
+    c->tp = tp;
+    c->heap_bytes = (opts && opts->heap_bytes) ? opts->heap_bytes : (size_t(1) << 30);
+    c->ranks.resize(tp);
+    c->directory.assign(tp, std::vector<bool>(tp, true));
+    for (int r = 0; r < tp; ++r) {
+        RankState& rs = c->ranks[r];
+        rs.device = devices ? devices[r] : 0;
+        rs.local = true;
+        int rc = alloc_heap(rs, c->heap_bytes);
+        if (rc == FLUX_OK) rc = init_rank_streams(rs);
+        if (rc != FLUX_OK) {
+            std::string msg = g_last_error;
+            flux_comm_destroy(c);
+            return fail(rc, msg);
+        }
+    }
+    // Peer access between distinct devices (NVLink P2P).
+    for (int a = 0; a < tp; ++a)
+        for (int b = 0; b < tp; ++b) {
+            const int da = c->ranks[a].device, db = c->ranks[b].device;
+            if (da == db) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, da, db);
+            if (!can) {
+                c->directory[a][b] = false;
+                continue;
+            }
+            cudaSetDevice(da);
+            cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) c->directory[a][b] = false;
+            cudaGetLastError();
+        }
+    c->connected = true;
+    *out = c;
+    return FLUX_OK;
+}
+
+int flux_comm_create_ipc(int rank, int tp, int device, const flux_comm_opts* opts, flux_comm** out) {
+    if (!out) return fail(FLUX_ERR_CONFIG, "null output");
+    *out = nullptr;
+    if (tp <= 0 || tp > kMaxRanks) return fail(FLUX_ERR_CONFIG, "tp must be in [1, " + S(kMaxRanks) + "]");
+    if (rank < 0 || rank >= tp) return fail(FLUX_ERR_CONFIG, "rank " + S(rank) + " >= tp");
+    FLUX_TRY(need_driver());
+    auto* c = new flux_comm();
+    c->tp = tp;
+    c->ipc = true;
+    c->my_rank = rank;
+    c->heap_bytes = (opts && opts->heap_bytes) ? opts->heap_bytes : (size_t(1) << 30);
+    c->ranks.resize(tp);
+    c->directory.assign(tp, std::vector<bool>(tp, false));
+    RankState& me = c->ranks[rank];
+    me.device = device;
+    me.local = true;
+    int rc = alloc_heap(me, c->heap_bytes);
+    if (rc == FLUX_OK) rc = init_rank_streams(me);
+    if (rc != FLUX_OK) {
+        std::string msg = g_last_error;
+        flux_comm_destroy(c);
+        return fail(rc, msg);
+    }
+    c->directory[rank][rank] = true;
+    *out = c;
+    return FLUX_OK;
+}
+
+size_t flux_comm_ipc_blob_bytes(void) { return sizeof(IpcBlob); }
+
+int flux_comm_ipc_handle(flux_comm* c, void* blob) {
+    if (!c || !c->ipc) return fail(FLUX_ERR_CONFIG, "not an IPC communicator");
+    IpcBlob b;
+    std::memset(&b, 0, sizeof(b));
+    b.magic = kIpcMagic;
+    b.rank = c->my_rank;
+    b.tp = c->tp;
+    b.device = c->ranks[c->my_rank].device;
+    b.heap_bytes = c->heap_bytes;
+    b.pid = static_cast<int32_t>(getpid());
+    FLUX_CUDA(cudaSetDevice(b.device));
+    FLUX_CUDA(cudaIpcGetMemHandle(&b.handle, c->ranks[c->my_rank].heap));
+    std::memcpy(blob, &b, sizeof(b));
+    return FLUX_OK;
+}
+
+int flux_ipc_blobs_check(const void* blobs, int tp, size_t heap_bytes) {
+    if (!blobs || tp <= 0) return fail(FLUX_ERR_CONFIG, "bad blob set");
+    for (int r = 0; r < tp; ++r) {
+        IpcBlob b;
+        std::memcpy(&b, static_cast<const char*>(blobs) + r * sizeof(IpcBlob), sizeof(b));
+        if (b.magic != kIpcMagic) return fail(FLUX_ERR_DIRECTORY, "peer " + S(r) + " blob has a bad magic");
+        if (b.rank != r) return fail(FLUX_ERR_DIRECTORY, "blob " + S(r) + " carries rank " + S(b.rank));
+        if (b.tp != tp) return fail(FLUX_ERR_CONFIG, "peer " + S(r) + " has tp=" + S(b.tp) + ", expected " + S(tp));
+        if (b.heap_bytes != heap_bytes)
+            return fail(FLUX_ERR_CONFIG, "peer " + S(r) + " heap is " + S(b.heap_bytes) + " bytes, expected " +
+                                             S(heap_bytes) + " (heaps must be symmetric)");
+    }
+    return FLUX_OK;
+}
+
+int flux_comm_ipc_connect(flux_comm* c, const void* blobs) {
+    if (!c || !c->ipc) return fail(FLUX_ERR_CONFIG, "not an IPC communicator");
+    FLUX_TRY(flux_ipc_blobs_check(blobs, c->tp, c->heap_bytes));
+    FLUX_CUDA(cudaSetDevice(c->ranks[c->my_rank].device));
+    for (int r = 0; r < c->tp; ++r) {
+        if (r == c->my_rank) continue;
+        IpcBlob b;
+        std::memcpy(&b, static_cast<const char*>(blobs) + r * sizeof(IpcBlob), sizeof(b));
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(FLUX_ERR_DIRECTORY, "rank " + S(c->my_rank) + " cannot map peer " + S(r) + " heap: " +
+                                                cudaGetErrorString(e));
+        }
+        c->ranks[r].heap = static_cast<char*>(p);
+        c->ranks[r].device = b.device;
+        c->ranks[r].owned = false;
+        c->directory[c->my_rank][r] = true;
+    }
+    c->connected = true;
+    return FLUX_OK;
+}
+
+int flux_comm_destroy(flux_comm* c) {
+    if (!c) return FLUX_OK;
+    for (int r = 0; r < c->tp; ++r) {
+        RankState& rs = c->ranks[r];
+        if (!rs.heap && !rs.stream) continue;
+        cudaSetDevice(rs.local ? rs.device : c->ranks[c->my_rank >= 0 ? c->my_rank : r].device);
+        if (rs.stream) cudaStreamSynchronize(rs.stream);
+        if (rs.copy_stream) cudaStreamSynchronize(rs.copy_stream);
+        if (rs.heap) {
+            if (rs.owned) cudaFree(rs.heap);
+            else cudaIpcCloseMemHandle(rs.heap);
+        }
+        if (rs.stream) cudaStreamDestroy(rs.stream);
+        if (rs.copy_stream) cudaStreamDestroy(rs.copy_stream);
+        if (rs.start_evt) cudaEventDestroy(rs.start_evt);
+        if (rs.kernel_evt) cudaEventDestroy(rs.kernel_evt);
+        if (rs.copy_evt) cudaEventDestroy(rs.copy_evt);
+    }
+    for (size_t i = 0; i < c->order_dev.size(); ++i)
+        if (c->order_dev[i]) cudaFree(c->order_dev[i]);
+    delete c;
+    return FLUX_OK;
+}
+
+int flux_comm_tp(const flux_comm* c) { return c ? c->tp : 0; }
+int flux_comm_rank(const flux_comm* c) { return c ? c->my_rank : -1; }
+
+int flux_comm_drop_peer(flux_comm* c, int from_rank, int peer_rank) {
+    if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
+    if (from_rank < 0 || from_rank >= c->tp || peer_rank < 0 || peer_rank >= c->tp)
+        return fail(FLUX_ERR_DIRECTORY, "directory lookup out of range");
+    c->directory[from_rank][peer_rank] = false;
+    return FLUX_OK;
+}
+
+int flux_buffer(flux_comm* c, int rank, int kind, const flux_problem* p, flux_buffer_desc* out) {
+    FLUX_TRY(check_comm(c));
+    FLUX_TRY(validate_problem(p));
+    if (p->tp != c->tp) return fail(FLUX_ERR_SHAPE, "problem tp=" + S(p->tp) + " but communicator tp=" + S(c->tp));
+    if (rank < 0 || rank >= c->tp || !c->ranks[rank].local)
+        return fail(FLUX_ERR_DIRECTORY, "rank " + S(rank) + " is not driven by this process");
+    const Layout L = layout_for(p);
+    if (L.total > c->heap_bytes)
+        return fail(FLUX_ERR_SHAPE, "problem needs " + S(L.total) + " heap bytes, communicator has " + S(c->heap_bytes));
+    const Region* r = nullptr;
+    switch (kind) {
+        case FLUX_BUF_A_SHARD: r = &L.a_shard; break;
+        case FLUX_BUF_B_SHARD: r = &L.b; break;
+        case FLUX_BUF_A_AGG: r = p->pattern == FLUX_ALLGATHER_GEMM ? &L.a_agg : nullptr; break;
+        case FLUX_BUF_C_OUT: r = &L.c; break;
+        case FLUX_BUF_STAGING: r = p->pattern == FLUX_GEMM_REDUCESCATTER ? &L.staging : nullptr; break;
+        case 5: r = &L.c32; break;  // fp32 view of C
+        default: return fail(FLUX_ERR_CONFIG, "unknown buffer kind " + S(kind));
+    }
+    if (!r) return fail(FLUX_ERR_CONFIG, "buffer kind " + S(kind) + " does not exist for this pattern");
+    out->ptr = c->ranks[rank].heap + r->off;
+    out->rows = r->rows;
+    out->cols = r->cols;
+    out->ld = r->ld;
+    out->dtype = r->dtype;
+    return FLUX_OK;
+}
+
+static int copy_2d(flux_comm* c, int rank, int kind, const flux_problem* p, void* host, int host_ld, void* stream,
+                   bool in) {
+    flux_buffer_desc d;
+    FLUX_TRY(flux_buffer(c, rank, kind, p, &d));
+    const size_t es = d.dtype == FLUX_F32 ? 4 : 2;
+    if (host_ld < d.cols) return fail(FLUX_ERR_SHAPE, "host_ld smaller than the buffer width");
+    FLUX_CUDA(cudaSetDevice(c->ranks[rank].device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->ranks[rank].stream;
+    if (in)
+        FLUX_CUDA(cudaMemcpy2DAsync(d.ptr, d.ld * es, host, host_ld * es, d.cols * es, d.rows, cudaMemcpyHostToDevice, s));
+    else
+        FLUX_CUDA(cudaMemcpy2DAsync(host, host_ld * es, d.ptr, d.ld * es, d.cols * es, d.rows, cudaMemcpyDeviceToHost, s));
+    return FLUX_OK;
+}
+
+int flux_copy_in(flux_comm* c, int rank, int kind, const flux_problem* p, const void* host, int host_ld, void* stream) {
+    return copy_2d(c, rank, kind, p, const_cast<void*>(host), host_ld, stream, true);
+}
+int flux_copy_out(flux_comm* c, int rank, int kind, const flux_problem* p, void* host, int host_ld, void* stream) {
+    return copy_2d(c, rank, kind, p, host, host_ld, stream, false);
+}
+
+static int check_heap(flux_comm* c, const flux_problem* p) {
+    if (p->tp != c->tp) return fail(FLUX_ERR_SHAPE, "workspace has " + S(c->tp) + " ranks, problem tp=" + S(p->tp));
+    const size_t need = layout_for(p).total;
+    if (need > c->heap_bytes)
+        return fail(FLUX_ERR_SHAPE, "problem needs " + S(need) + " heap bytes per rank, communicator has " + S(c->heap_bytes));
+    const int lc = local_cols(p), lk = local_k(p);
+    if (p->m / kBM >= (1 << 14) || lc / kBN >= (1 << 14)) return fail(FLUX_ERR_CONFIG, "problem too large for the tile schedule");
+    if (lk > (1 << 28)) return fail(FLUX_ERR_CONFIG, "k too large");
+    return FLUX_OK;
+}
+
+int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer, int swizzle_on,
+                 const flux_opts* opts, void* const* streams) {
+    FLUX_TRY(check_comm(c));
+    if (p && p->pattern != FLUX_ALLGATHER_GEMM)
+        return fail(FLUX_ERR_CONFIG, "run_fused_allgather_gemm requires AllGatherGemm pattern");
+    FLUX_TRY(validate_tiling(p, tile));
+    FLUX_TRY(check_heap(c, p));
+    const int tp = p->tp, rpr = rows_per_rank(p);
+    if (rpct <= 0) rpct = rpr;
+    if (p->m / rpct > static_cast<int>(kAgFlagCap)) return fail(FLUX_ERR_CONFIG, "too many comm tiles");
+    std::vector<std::vector<Desc>> specs(tp);
+    for (int r = 0; r < tp; ++r) FLUX_TRY(make_spec(p, r, rpct, transfer, specs[r]));
+    std::vector<int> mine;
+    local_ranks_only(c, mine);
+    // Directory check: every peer this rank touches must be mapped (workspace.cpp:56-65).
+    for (int r : mine)
+        for (int q = 0; q < tp; ++q) FLUX_TRY(check_directory(c, r, q));
+    const OpCommon oc = common_opts(opts);
+    const Layout L = layout_for(p);
+    c->last_launches = 0;
+    const uint32_t e = ++c->epoch;
+    const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
+    const int lk = local_k(p);
+
+    // ---- Alg. 3: host transfer loop on each rank's copy-engine stream ----
+    for (int r : mine) {
+        RankState& rs = c->ranks[r];
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        cudaStream_t s = stream_for(c, r, streams);
+        cudaStream_t cs = rs.copy_stream;
+        FLUX_CUDA(cudaEventRecord(rs.start_evt, s));
+        FLUX_CUDA(cudaStreamWaitEvent(cs, rs.start_evt, 0));
+        if (rs.kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(cs, rs.kernel_evt, 0));
+        // Peers finished pulling my previous shard before I overwrite it.
+        if (transfer == FLUX_PULL)
+            for (int q = 0; q < tp; ++q)
+                if (q != r) FLUX_TRY(wait_value_geq(cs, c->ranks[q].heap + kCtrlDone, e - 1));
+        // Local shard -> own a_agg slot, local flags preset (engine.cpp:469-472).
+        FLUX_CUDA(cudaMemcpy2DAsync(rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes,
+                                    rs.heap + L.a_shard.off, static_cast<size_t>(L.a_shard.ld) * 2, lk * 2, rpr,
+                                    cudaMemcpyDeviceToDevice, cs));
+        FLUX_TRY(write_value(cs, rs.heap + kCtrlReady, e));
+        for (int f = r * rpr / rpct; f < (r + 1) * rpr / rpct; ++f)
+            FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + f, e));
+        int last_peer = -1;
+        for (const Desc& d : specs[r]) {
+            const int q = d.peer;
+            const RankState& qs = c->ranks[q];
+            if (transfer == FLUX_PULL) {
+                if (q != last_peer) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlReady, e));
+                FLUX_CUDA(cudaMemcpy2DAsync(rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
+                                            qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
+                                            lk * 2, d.rows, cudaMemcpyDeviceToDevice, cs));
+                FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
+            } else {
+                if (q != last_peer) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlKdone, e - 1));
+                FLUX_CUDA(cudaMemcpy2DAsync(
+                    qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
+                    rs.heap + L.a_shard.off + static_cast<size_t>(d.row_begin - r * rpr) * L.a_shard.ld * 2,
+                    static_cast<size_t>(L.a_shard.ld) * 2, lk * 2, d.rows, cudaMemcpyDeviceToDevice, cs));
+                FLUX_TRY(write_value(cs, at<uint32_t>(qs, kAgFlagOffset) + d.row_begin / rpct, e));
+            }
+            last_peer = q;
+        }
+        FLUX_TRY(write_value(cs, rs.heap + kCtrlDone, e));
+        FLUX_CUDA(cudaEventRecord(rs.copy_evt, cs));
+    }
+
+    // ---- Alg. 2: the fused GEMM, tiles ordered by expected arrival ----
+    std::vector<std::vector<uint32_t>> seq(tp);
+    for (int r : mine)
+        seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct), 0);
+    FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, oc.o.emulated_order == 0));
+    for (int r : mine) {
+        RankState& rs = c->ranks[r];
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        cudaStream_t s = stream_for(c, r, streams);
+        FLUX_TRY(write_value(s, rs.heap + kCtrlKdone, e));
+        // Later work on the caller's stream is ordered after our transfers.
+        FLUX_CUDA(cudaStreamWaitEvent(s, rs.copy_evt, 0));
+    }
+    return FLUX_OK;
+}
+
+int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
+                 const flux_opts* opts, void* const* streams) {
+    FLUX_TRY(check_comm(c));
+    if (p && p->pattern != FLUX_GEMM_REDUCESCATTER)
+        return fail(FLUX_ERR_CONFIG, "run_fused_gemm_reducescatter requires GemmReduceScatter pattern");
+    FLUX_TRY(validate_tiling(p, tile));
+    FLUX_TRY(check_heap(c, p));
+    if (write_mode != FLUX_WRITE_ALLTOALL && write_mode != FLUX_FUSED_REDUCE)
+        return fail(FLUX_ERR_CONFIG, "unknown write mode");
+    const int tp = p->tp, rpr = rows_per_rank(p);
+    const int tiles = ((p->m + kBM - 1) / kBM) * ((p->n + kBN - 1) / kBN);
+    if (static_cast<size_t>(tiles) * tp > kRsFlagCap) return fail(FLUX_ERR_CONFIG, "too many output tiles for the flag table");
+    std::vector<int> mine;
+    local_ranks_only(c, mine);
+    for (int r : mine)
+        for (int q = 0; q < tp; ++q) FLUX_TRY(check_directory(c, r, q));
+    OpCommon oc = common_opts(opts);
+    c->last_launches = 0;
+    ++c->epoch;
+    // Tile order: RankShifted (local block last) or Naive (engine.cpp:210-217,256-261).
+    std::vector<std::vector<uint32_t>> seq(tp);
+    for (int r : mine) {
+        std::vector<int> blocks;
+        if (swizzle_on) blocks = block_order(FLUX_SWIZZLE_RANK_SHIFTED, r, tp, oc.o.shift_offset, {});
+        else for (int i = 0; i < tp; ++i) blocks.push_back(i);
+        seq[r] = device_sequence(p->m, p->n, rpr, blocks, 0);
+    }
+    // Deadlock freedom of the single-device multi-rank launch needs step-major
+    // interleaving (a tile only waits on partials scheduled before it).
+    return launch_groups(c, p, kModeRS, oc, streams, seq, 0, true);
+}
+
+int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
+    FLUX_TRY(check_comm(c));
+    FLUX_TRY(validate_problem(p));
+    FLUX_TRY(check_heap(c, p));
+    OpCommon oc = common_opts(opts);
+    c->last_launches = 0;
+    std::vector<int> mine;
+    local_ranks_only(c, mine);
+    std::vector<std::vector<uint32_t>> seq(p->tp);
+    for (int r : mine) seq[r] = device_sequence(p->m, local_cols(p), rows_per_rank(p), {}, 0);
+    return launch_groups(c, p, kModePlain, oc, streams, seq, 0, oc.o.emulated_order == 0,
+                         p->pattern == FLUX_ALLGATHER_GEMM);
+}
+
+int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
+    FLUX_TRY(check_comm(c));
+    FLUX_TRY(validate_problem(p));
+    FLUX_TRY(check_heap(c, p));
+    const int tp = p->tp, rpr = rows_per_rank(p), lk = local_k(p);
+    std::vector<int> mine;
+    local_ranks_only(c, mine);
+    for (int r : mine)
+        for (int q = 0; q < tp; ++q) FLUX_TRY(check_directory(c, r, q));
+    OpCommon oc = common_opts(opts);
+    const Layout L = layout_for(p);
+    c->last_launches = 0;
+    const uint32_t e = ++c->epoch;
+    std::vector<std::vector<uint32_t>> seq(tp);
+    for (int r : mine) seq[r] = device_sequence(p->m, local_cols(p), rpr, {}, 0);
+    if (p->pattern == FLUX_ALLGATHER_GEMM) {
+        // Serial AllGather in rank order (engine.cpp:568-571), then the GEMM.
+        const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
+        for (int r : mine) {
+            RankState& rs = c->ranks[r];
+            FLUX_CUDA(cudaSetDevice(rs.device));
+            cudaStream_t s = stream_for(c, r, streams);
+            if (rs.kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(s, rs.kernel_evt, 0));
+            for (int q = 0; q < tp; ++q)
+                if (q != r) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
+            FLUX_CUDA(cudaMemcpy2DAsync(rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes,
+                                        rs.heap + L.a_shard.off, static_cast<size_t>(L.a_shard.ld) * 2, lk * 2, rpr,
+                                        cudaMemcpyDeviceToDevice, s));
+            FLUX_TRY(write_value(s, rs.heap + kCtrlReady, e));
+        }
+        for (int r : mine) {
+            RankState& rs = c->ranks[r];
+            FLUX_CUDA(cudaSetDevice(rs.device));
+            cudaStream_t s = stream_for(c, r, streams);
+            for (int q = 0; q < tp; ++q) {
+                if (q == r) continue;
+                FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlReady, e));
+                FLUX_CUDA(cudaMemcpy2DAsync(rs.heap + L.a_agg.off + static_cast<size_t>(q) * rpr * rowbytes, rowbytes,
+                                            c->ranks[q].heap + L.a_agg.off + static_cast<size_t>(q) * rpr * rowbytes,
+                                            rowbytes, lk * 2, rpr, cudaMemcpyDeviceToDevice, s));
+            }
+            FLUX_TRY(write_value(s, rs.heap + kCtrlDone, e));
+        }
+        FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0, oc.o.emulated_order == 0, true));
+        return FLUX_OK;
+    }
+    // GEMM-RS: full fp32 partial into this epoch's staging parity, then the
+    // serial source-ordered reduce once every rank's GEMM finished.
+    const size_t parity_off = L.staging.off + static_cast<size_t>(e & 1u) * L.stage_parity * 4;
+    FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0, true, false, static_cast<long long>(parity_off)));
+    for (int r : mine) {
+        RankState& rs = c->ranks[r];
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        cudaStream_t s = stream_for(c, r, streams);
+        FLUX_TRY(write_value(s, rs.heap + kCtrlKdone, e));
+    }
+    for (int r : mine) {
+        RankState& rs = c->ranks[r];
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        cudaStream_t s = stream_for(c, r, streams);
+        for (int q = 0; q < tp; ++q) {
+            if (q == r) continue;
+            if (c->ranks[q].local) FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[q].kernel_evt, 0));
+            else FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlKdone, e));
+        }
+        RsReduceParams rp;
+        std::memset(&rp, 0, sizeof(rp));
+        for (int q = 0; q < tp; ++q)
+            rp.partials[q] = reinterpret_cast<const float*>(c->ranks[q].heap + parity_off);
+        rp.c = rs.heap + L.c32.off;
+        rp.ldc = L.c32.ld;
+        rp.out_f32 = oc.o.out_dtype == FLUX_F32;
+        rp.rpr = rpr;
+        rp.n = p->n;
+        rp.ld_src = L.ld_stage;
+        rp.owner = r;
+        rp.tp = tp;
+        FLUX_CUDA(launch_rs_reduce(rp, std::max(1, sm_count(rs.device)) * 4, s));
+        ++c->last_launches;
+        FLUX_CUDA(cudaEventRecord(rs.kernel_evt, s));
+    }
+    return FLUX_OK;
+}
+
+int flux_sync(flux_comm* c) {
+    if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
+    std::string deadlock;
+    for (int r = 0; r < c->tp; ++r) {
+        RankState& rs = c->ranks[r];
+        if (!rs.local) continue;
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        FLUX_CUDA(cudaStreamSynchronize(rs.copy_stream));
+        FLUX_CUDA(cudaDeviceSynchronize());
+        uint32_t err[4] = {0, 0, 0, 0};
+        FLUX_CUDA(cudaMemcpy(err, rs.heap + kCtrlErr, sizeof(err), cudaMemcpyDeviceToHost));
+        if (err[0] != 0) {
+            if (deadlock.empty()) {
+                if (err[0] == kErrAgFlagTimeout)
+                    deadlock = "deadlock budget exhausted waiting for signal " + S(err[1]) + " for tile (" +
+                               S(err[2] >> 16) + "," + S(err[2] & 0xFFFF) + ") on rank " + S(r);
+                else
+                    deadlock = "deadlock budget exhausted waiting for partial of tile " + S(err[1]) + " from source " +
+                               S(err[2]) + " on rank " + S(r);
+            }
+            const uint32_t zero[4] = {0, 0, 0, 0};
+            FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlErr, zero, sizeof(zero), cudaMemcpyHostToDevice));
+        }
+    }
+    if (!deadlock.empty()) return fail(FLUX_ERR_DEADLOCK, deadlock);
+    return FLUX_OK;
+}
+
+int flux_last_launch_count(const flux_comm* c) { return c ? c->last_launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// Shared host/device definitions of the B200 fused-operator kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fluxb200 {
+
+// Device GEMM tile (one CTA, cta_group::1): D[128 x 256] fp32 in TMEM,
+// A/B staged by TMA in 128B-swizzled K-major shared memory, BK = 64 bf16.
+constexpr int kBM = 128;
+constexpr int kBN = 256;
+constexpr int kBK = 64;
+constexpr int kStages = 4;
+constexpr int kUmmaK = 16;
+constexpr int kThreads = 256;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 spare, w4-7 epilogue
+constexpr int kAStageBytes = kBM * kBK * 2;
+constexpr int kBStageBytes = kBN * kBK * 2;
+constexpr int kTmemCols = 512;  // two 256-column accumulators (epilogue/MMA overlap)
+constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*align*/ + 256 /*barriers*/;
+
+constexpr int kMaxRanks = 8;   // TP degree supported by one communicator (one NVSwitch node)
+
+enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2 };
+
+// Control block at the start of every rank's symmetric heap. All words are
+// epoch-stamped (monotonic), so nothing needs resetting between operators.
+constexpr size_t kCtrlErr = 0;          // u32[4]: code, info0, info1, info2
+constexpr size_t kCtrlReady = 64;       // u32: epoch at which this rank's A shard is staged (AG pull source ready)
+constexpr size_t kCtrlDone = 68;        // u32: epoch whose peer pulls this rank has finished
+constexpr size_t kCtrlKdone = 72;       // u32: epoch whose kernel finished on this rank (push targets)
+constexpr size_t kAgFlagOffset = 4096;  // u32[kAgFlagCap]: one flag per comm tile (SignalBoard)
+constexpr size_t kAgFlagCap = 32768;
+constexpr size_t kRsFlagOffset = 256 * 1024;  // u32[tile][src]: partial of tile from src landed
+constexpr size_t kRsFlagCap = (768 * 1024) / 4;
+constexpr size_t kDataOffset = 1 << 20;
+
+// Error codes written by device waits into the control block.
+constexpr uint32_t kErrAgFlagTimeout = 1;
+constexpr uint32_t kErrRsFlagTimeout = 2;
+
+// Tile order entry: local rank (4 bits) | tile row (14 bits) | tile col (14 bits).
+__host__ __device__ inline uint32_t pack_tile(int l, int tm, int tn) {
+    return (uint32_t(l) << 28) | (uint32_t(tm) << 14) | uint32_t(tn);
+}
+
+struct GemmParams {
+    CUtensorMap tma_a[kMaxRanks];  // per local rank: A operand [m, k] (AG: a_agg, RS: A shard)
+    CUtensorMap tma_b[kMaxRanks];  // per local rank: B operand [n, k] K-major
+    void* c[kMaxRanks];            // per local rank: output
+    int global_rank[kMaxRanks];    // local slot -> global rank id
+    const uint32_t* ag_flags[kMaxRanks];   // per local rank: comm-tile flags
+    uint32_t* ctrl[kMaxRanks];             // per local rank: control block (error word)
+    float* staging[kMaxRanks];             // per GLOBAL rank: staging planes base (peer pointers)
+    uint32_t* rs_flags[kMaxRanks];         // per GLOBAL rank: (tile, src) flags (peer pointers)
+    const uint32_t* order;                 // tile schedule (pack_tile entries)
+    int num_tiles;
+    int m, n, k;                   // per-rank GEMM: A [m, k], B [n, k], C [m, n]
+    int ldc;                       // C row pitch (elements)
+    int out_f32;                   // C element type
+    int tiles_n;                   // ceil(n / kBN)
+    int tp, rpr;                   // TP degree, rows per rank
+    int rpct;                      // AG rows per comm tile
+    int ld_stage;                  // staging row pitch (elements) = n padded
+    long long stage_plane;         // elements per (src) plane = rpr * ld_stage
+    long long stage_parity;        // elements per parity set = tp * stage_plane
+    uint32_t epoch;
+    unsigned long long timeout_ns;
+    unsigned long long jitter_seed;
+};
+
+struct RsReduceParams {
+    const float* partials[kMaxRanks];  // per source rank: full [m, n] fp32 partial (peer pointers)
+    void* c;
+    int ldc, out_f32, rpr, n, ld_src, owner, tp;
+};
+
+// Host launchers (flux_kernels.cu).
+cudaError_t launch_gemm(int mode, const GemmParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t stream);
+
+}  // namespace fluxb200

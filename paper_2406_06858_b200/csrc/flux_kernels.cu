@@ -1,0 +1,515 @@
+// Fused tensor-parallel GEMM kernels for sm_100a (B200).
+//
+// One persistent, warp-specialised tcgen05 GEMM serves three roles
+// (KernelMode):
+//   Plain — C = A B^T, no communication (TP=1 and the Eq. 1 "non-split GEMM").
+//   AG    — paper Alg. 2 (reference engine.cpp:516-547): before the TMA
+//           producer loads the A rows of a tile it spins on the per-comm-tile
+//           flags covering those rows (reference spin_wait on SignalBoard,
+//           engine.cpp:529-539); flags are raised by the copy-engine transfer
+//           loop (Alg. 3, engine.cpp:367-423) running on a side stream.
+//   RS    — paper Alg. 1 (reference engine.cpp:265-341): the epilogue routes
+//           every accumulator row to its owner (owner_of_row, problem.hpp:37),
+//           storing fp32 partials into the owner's staging plane for this
+//           source over NVLink (WriteAlltoAll, engine.cpp:285-292) and raising
+//           a per-(tile, source) flag; the owner reduces its own rows in source
+//           order 0..tp-1 inside its local-tile epilogue, replacing the
+//           reference's discrete reduce agent (engine.cpp:324-341).
+//
+// Roles: warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one lane),
+// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM lane quadrants 0..3).
+// Pipelines: kStages smem ring (TMA -> MMA), two TMEM accumulators
+// (MMA -> epilogue). The tile schedule is a host-built table (reference
+// tile_order, swizzle.cpp:75-80) walked with a static stride of gridDim.x.
+#include <cuda_bf16.h>
+
+#include "flux_internal.hpp"
+
+namespace fluxb200 {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier -----------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// ---- TMA ------------------------------------------------------------------------
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+// ---- tcgen05 ----------------------------------------------------------------------
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(slot)),
+                 "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+                 : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, bf16 in, fp32 accumulate.
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns: thread i receives row (lane base + i).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row core groups
+// 1024 B apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+    const uint64_t addr = smem_u32(p);
+    return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+// Instruction descriptor: D f32, A/B bf16, both K-major, M = 128, N = 256.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kBN >> 3) << 17) |
+                            (uint32_t(kBM >> 4) << 24);
+
+// ---- cross-rank signalling (system scope: peers are other GPUs) -------------------
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ float4 ld_cg_f4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Bounded spin (reference spin_wait, engine.cpp:149-162): epoch-stamped flag
+// reaches `target`, or the timeout records an error naming the flag.
+__device__ bool wait_flag(const uint32_t* flag, uint32_t target, const GemmParams& p,
+                          uint32_t* ctrl, uint32_t code, uint32_t info0, uint32_t info1) {
+    if (static_cast<int32_t>(ld_acquire_sys(flag) - target) >= 0) return true;
+    const uint64_t t0 = globaltimer();
+    uint32_t ns = 32;
+    for (;;) {
+        __nanosleep(ns);
+        if (ns < 2048) ns <<= 1;
+        if (static_cast<int32_t>(ld_acquire_sys(flag) - target) >= 0) return true;
+        if (globaltimer() - t0 > p.timeout_ns) {
+            if (atomicCAS(ctrl + 0, 0u, code) == 0u) {
+                ctrl[1] = info0;
+                ctrl[2] = info1;
+                ctrl[3] = target;
+                __threadfence_system();
+            }
+            return false;
+        }
+        if (*reinterpret_cast<volatile uint32_t*>(ctrl) != 0u) return false;  // sibling failed
+    }
+}
+
+__device__ __forceinline__ void decode(uint32_t e, int& l, int& tm, int& tn) {
+    l = static_cast<int>(e >> 28);
+    tm = static_cast<int>((e >> 14) & 0x3FFFu);
+    tn = static_cast<int>(e & 0x3FFFu);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo, uint32_t hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Store 32 fp32 accumulators of one row (cols [col, col+32)) to C.
+__device__ __forceinline__ void store_row32(void* c, long long off, int col, int n, int out_f32,
+                                            const float (&v)[32]) {
+    if (out_f32) {
+        float* dst = static_cast<float*>(c) + off;
+        if (col + 32 <= n) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+            for (int j = 0; j < 32 && col + j < n; ++j) dst[j] = v[j];
+        }
+    } else {
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(c) + off;
+        if (col + 32 <= n) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+                uint4 w;
+                w.x = pack_bf16x2(__float_as_uint(v[j + 0]), __float_as_uint(v[j + 1]));
+                w.y = pack_bf16x2(__float_as_uint(v[j + 2]), __float_as_uint(v[j + 3]));
+                w.z = pack_bf16x2(__float_as_uint(v[j + 4]), __float_as_uint(v[j + 5]));
+                w.w = pack_bf16x2(__float_as_uint(v[j + 6]), __float_as_uint(v[j + 7]));
+                *reinterpret_cast<uint4*>(dst + j) = w;
+            }
+        } else {
+            for (int j = 0; j < 32 && col + j < n; ++j) dst[j] = __float2bfloat16_rn(v[j]);
+        }
+    }
+}
+
+}  // namespace
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_constant__ GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kAStageBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStageBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        for (int l = 0; l < kMaxRanks; ++l) {
+            if (p.c[l] == nullptr) break;
+            tma_prefetch(&p.tma_a[l]);
+            tma_prefetch(&p.tma_b[l]);
+        }
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int k_blocks = (p.k + kBK - 1) / kBK;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            uint64_t jit = p.jitter_seed ? p.jitter_seed * 0x9e3779b97f4a7c15ull + blockIdx.x : 0;
+            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                int l, tm, tn;
+                decode(p.order[t], l, tm, tn);
+                const int row0 = tm * kBM;
+                const int col0 = tn * kBN;
+                if (jit) {  // reference Jitter (engine.cpp:116-128): perturb interleavings
+                    jit ^= jit >> 12; jit ^= jit << 25; jit ^= jit >> 27;
+                    const uint32_t r = static_cast<uint32_t>((jit * 0x2545F4914F6CDD1Dull) >> 40);
+                    if ((r & 15u) == 0u) __nanosleep(r & 0xFFFFu);
+                }
+                if (MODE == kModeAG) {
+                    // Alg. 2: wait for every comm tile covering rows [row0, row0+BM).
+                    const int rlast = min(row0 + kBM, p.m) - 1;
+                    const int f0 = row0 / p.rpct, f1 = rlast / p.rpct;
+                    for (int f = f0; f <= f1; ++f)
+                        wait_flag(p.ag_flags[l] + f, p.epoch, p, p.ctrl[l], kErrAgFlagTimeout,
+                                  static_cast<uint32_t>(f), static_cast<uint32_t>(tm * 65536 + tn));
+                    // Flag acquire (generic proxy) before TMA reads (async proxy).
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                for (int kb = 0; kb < k_blocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    mbar_expect_tx(&full[stage], kAStageBytes + kBStageBytes);
+                    tma_load_2d(sA + stage * kAStageBytes, &p.tma_a[l], &full[stage], kb * kBK, row0);
+                    tma_load_2d(sB + stage * kBStageBytes, &p.tma_b[l], &full[stage], kb * kBK, col0);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int as = 0;
+            uint32_t aphase = 0;
+            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                mbar_wait(&tempty[as], aphase ^ 1u);
+                tc_fence_after();
+                const uint32_t d = tmem_base + static_cast<uint32_t>(as * kBN);
+                for (int kb = 0; kb < k_blocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t adesc = smem_desc_sw128(sA + stage * kAStageBytes);
+                    const uint64_t bdesc = smem_desc_sw128(sB + stage * kBStageBytes);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
+                        // +32 B along K inside the 128B swizzle atom = +2 in the >>4 address field.
+                        umma_bf16(d, adesc + 2ull * kk, bdesc + 2ull * kk, kIdesc,
+                                  (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                umma_commit(&tfull[as]);  // accumulator ready for the epilogue
+                if (++as == 2) {
+                    as = 0;
+                    aphase ^= 1u;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue =====
+        const int q = warp - 4;          // TMEM lane quadrant (warp % 4)
+        const int et = threadIdx.x - 128;  // epilogue thread 0..127
+        int as = 0;
+        uint32_t aphase = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            int l, tm, tn;
+            decode(p.order[t], l, tm, tn);
+            const int row0 = tm * kBM;
+            const int col0 = tn * kBN;
+            const int row = row0 + q * 32 + lane;
+            const bool valid = row < p.m;
+            mbar_wait(&tfull[as], aphase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                   static_cast<uint32_t>(as * kBN);
+            if (MODE != kModeRS) {
+                for (int c = 0; c < kBN / 32; ++c) {
+                    const int col = col0 + c * 32;
+                    if (col >= p.n) break;  // warp-uniform
+                    uint32_t r[32];
+                    tmem_ld32(tbase + c * 32, r);
+                    tmem_ld_wait();
+                    if (valid) {
+                        float v[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                        store_row32(p.c[l], static_cast<long long>(row) * p.ldc + col, col, p.n,
+                                    p.out_f32, v);
+                    }
+                }
+            } else {
+                const int me = p.global_rank[l];
+                const uint32_t parity = p.epoch & 1u;
+                const int owner = valid ? row / p.rpr : -1;
+                const bool remote = valid && owner != me;
+                const int tile_id = tm * p.tiles_n + tn;
+                // Phase 1: ship remote rows to their owners' staging planes (Alg. 1 line 5).
+                if (__any_sync(0xffffffffu, remote)) {
+                    float* dst = nullptr;
+                    if (remote)
+                        dst = p.staging[owner] + parity * p.stage_parity + me * p.stage_plane +
+                              static_cast<long long>(row - owner * p.rpr) * p.ld_stage;
+                    for (int c = 0; c < kBN / 32; ++c) {
+                        const int col = col0 + c * 32;
+                        if (col >= p.n) break;
+                        uint32_t r[32];
+                        tmem_ld32(tbase + c * 32, r);
+                        tmem_ld_wait();
+                        if (remote) {
+                            float4* d4 = reinterpret_cast<float4*>(dst + col);
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                        __uint_as_float(r[j + 2]),
+                                                        __uint_as_float(r[j + 3]));
+                        }
+                    }
+                    if (remote) __threadfence_system();
+                }
+                named_bar_sync(1, 128);
+                // Signal each owner in this tile that our partial landed.
+                const int rlast = min(row0 + kBM, p.m) - 1;
+                const int o0 = row0 / p.rpr, o1 = rlast / p.rpr;
+                if (et <= o1 - o0) {
+                    const int o = o0 + et;
+                    if (o != me) st_release_sys(p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
+                }
+                // Phase 2: owned rows = source-ordered sum of all partials.
+                const bool mine_in_tile = (me >= o0 && me <= o1);
+                if (mine_in_tile) {
+                    if (et == 0) {
+                        for (int s = 0; s < p.tp; ++s)
+                            if (s != me)
+                                wait_flag(p.rs_flags[me] + tile_id * p.tp + s, p.epoch, p, p.ctrl[l],
+                                          kErrRsFlagTimeout, static_cast<uint32_t>(tile_id),
+                                          static_cast<uint32_t>(s));
+                    }
+                    named_bar_sync(1, 128);
+                    const bool owned = valid && owner == me;
+                    if (__any_sync(0xffffffffu, owned)) {
+                        const long long lrow = row - me * p.rpr;
+                        const float* src0 = p.staging[me] + parity * p.stage_parity + lrow * p.ld_stage;
+                        for (int c = 0; c < kBN / 32; ++c) {
+                            const int col = col0 + c * 32;
+                            if (col >= p.n) break;
+                            uint32_t r[32];
+                            tmem_ld32(tbase + c * 32, r);
+                            tmem_ld_wait();
+                            if (owned) {
+                                float acc[32];
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+                                for (int s = 0; s < p.tp; ++s) {
+                                    if (s == me) {
+#pragma unroll
+                                        for (int j = 0; j < 32; ++j) acc[j] += __uint_as_float(r[j]);
+                                    } else {
+                                        const float* src = src0 + s * p.stage_plane + col;
+#pragma unroll
+                                        for (int j = 0; j < 32; j += 4) {
+                                            const float4 v = ld_cg_f4(src + j);
+                                            acc[j] += v.x;
+                                            acc[j + 1] += v.y;
+                                            acc[j + 2] += v.z;
+                                            acc[j + 3] += v.w;
+                                        }
+                                    }
+                                }
+                                store_row32(p.c[l], lrow * p.ldc + col, col, p.n, p.out_f32, acc);
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[as]);
+            if (++as == 2) {
+                as = 0;
+                aphase ^= 1u;
+            }
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// Serial reduction of the rank partial planes in source order (reference
+// run_nonoverlap RS branch, engine.cpp:595-602, and the WriteAlltoAll reduce
+// agent, engine.cpp:335-339): C[i, j] = sum_{s=0..tp-1} P_s[owner*rpr + i, j].
+__global__ void rs_reduce_kernel(RsReduceParams p) {
+    const long long total = static_cast<long long>(p.rpr) * p.n;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx / p.n), j = static_cast<int>(idx % p.n);
+        const long long src = (static_cast<long long>(p.owner) * p.rpr + i) * p.ld_src + j;
+        float acc = 0.0f;
+        for (int s = 0; s < p.tp; ++s) acc += __ldcg(p.partials[s] + src);
+        if (p.out_f32) static_cast<float*>(p.c)[static_cast<long long>(i) * p.ldc + j] = acc;
+        else static_cast<__nv_bfloat16*>(p.c)[static_cast<long long>(i) * p.ldc + j] = __float2bfloat16_rn(acc);
+    }
+}
+
+cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t stream) {
+    rs_reduce_kernel<<<grid, 256, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(int mode, const GemmParams& p, int grid, cudaStream_t stream) {
+    static bool configured[3] = {false, false, false};
+    void (*fn)(GemmParams) = nullptr;
+    switch (mode) {
+        case kModePlain: fn = flux_gemm_kernel<kModePlain>; break;
+        case kModeAG: fn = flux_gemm_kernel<kModeAG>; break;
+        case kModeRS: fn = flux_gemm_kernel<kModeRS>; break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (!configured[mode]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        configured[mode] = true;
+    }
+    fn<<<grid, kThreads, kSmemBytes, stream>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace fluxb200
