@@ -1,0 +1,413 @@
+"""Benchmark of the fused tensor-parallel operators (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload llama70b-up-ag|llama70b-down-rs|gpt3-ag|gpt3-rs]
+
+A step is one fused operator over the whole workload. N=1: all TP ranks of
+the workload are emulated on cuda:0 (one fused launch covering every rank,
+copy-engine transfers between the ranks' symmetric heaps). N>1 (torchrun): one
+process per GPU, TP = N over cudaIpc-mapped heaps (NVLink), the same global
+GEMM (strong scaling). Prints ONE JSON line on rank 0.
+
+`--impl reference` times the reference's own CPU engine (oracle/_ref, compiled
+from /root/reference; oracle port if absent) on a bounded sample of the same
+workload, on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused AG-GEMM/GEMM-RS TFLOPS + comm-overlap % at TP=2/4/8 vs cuBLAS+NCCL"
+
+WORKLOADS = {
+    # name: (pattern, m, n, k, tp, description)  — BASELINE.json configs[1..3]
+    "llama70b-up-ag": (0, 4096, 28672, 8192, 8, "AllGather-GEMM Llama-2-70B MLP up-proj (M=4096, K=8192, N=28672) bf16"),
+    "llama70b-down-rs": (1, 4096, 8192, 28672, 8, "GEMM-ReduceScatter Llama-2-70B MLP down-proj (M=4096, K=28672, N=8192) bf16"),
+    "gpt3-ag": (0, 8192, 49152, 12288, 8, "AllGather-GEMM GPT-3 175B MLP (M=8192, K=12288, N=49152) bf16"),
+    "gpt3-rs": (1, 8192, 12288, 49152, 8, "GEMM-ReduceScatter GPT-3 175B MLP (M=8192, K=49152, N=12288) bf16"),
+}
+FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference engine (or the oracle port) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_sample_shape(pattern, m, n, k, tp):
+    """Bounded sample of the workload: the same K/N (and TP), M cut to 8 rows per rank."""
+    ms = 8 * tp
+    return ms, n, k
+
+
+def run_cpu_reference(pattern, m, n, k, tp, reps=1):
+    """Times the reference's fused engine on the host cores; returns the
+    cpu_baseline object (TFLOPS over the sample)."""
+    from oracle import oracle as O
+
+    ms, ns, ks = cpu_sample_shape(pattern, m, n, k, tp)
+    cores = os.cpu_count() or 1
+    flops = 2.0 * ms * ns * ks
+    times = []
+    if O.ref_available():
+        workers = max(1, cores // tp)
+        tn = 256 if (ns // tp if pattern == 0 else ns) % 256 == 0 else 1
+        which = O.FUSED_AG if pattern == 0 else O.FUSED_RS
+        for _ in range(reps):
+            secs, _ = O.ref_run(which, pattern, ms, ns, ks, tp, 42, True, tm=8, tn=tn, rpct=8, transfer=0,
+                                write_mode=0, swizzle=True, workers=workers, want_outputs=False)
+            times.append(secs)
+        kind, used = "reference", tp * workers + (tp if pattern == 0 else tp)
+        what = (f"reference {'run_fused_allgather_gemm (Pull, swizzle)' if pattern == 0 else 'run_fused_gemm_reducescatter (WriteAlltoAll, swizzle)'}"
+                f" fp64, oracle/_ref built from /root/reference, {workers} workers/rank")
+    else:
+        import numpy as np
+
+        for _ in range(reps):
+            a, b = zip(*[O.rank_inputs(pattern, ms, ns, ks, tp, 42, r, True) for r in range(tp)])
+            t0 = time.perf_counter()
+            O.dense_oracle(pattern, ms, ns, ks, tp, a, b)
+            times.append(time.perf_counter() - t0)
+            del np
+        kind, used = "port", 1
+        what = "oracle port (oracle/flux_oracle.c dense fp64 restatement, 1 thread)"
+    t = statistics.median(times)
+    return {"value": flops / t / 1e12, "unit": "TFLOPS", "cores": used, "kind": kind,
+            "sample": f"{what}; M={ms} (8 rows/rank), N={ns}, K={ks}, TP={tp}; {flops / 1e9:.1f} GFLOP per run; "
+                      f"median of {len(times)} run(s) = {t:.2f} s; host has {cores} cores"}
+
+
+def reference_arm(args, wl):
+    pattern, m, n, k, tp, desc = WORKLOADS[wl]
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    base = None
+    for _ in range(args.warmup):
+        run_cpu_reference(pattern, m, n, k, tp, reps=1)
+    vals = []
+    for _ in range(args.steps):
+        base = run_cpu_reference(pattern, m, n, k, tp, reps=1)
+        vals.append(base["value"])
+    v = statistics.median(vals)
+    base["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng stream)",
+            "config": {"workload": wl, "description": desc, "m": m, "n": n, "k": k, "tp": tp,
+                       "sample_m": cpu_sample_shape(pattern, m, n, k, tp)[0]},
+            "cpu_baseline": base,
+            "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def our_arm(args, wl):
+    import torch
+
+    import paper_2406_06858_b200 as fx
+    from paper_2406_06858_b200 import _native as N
+    from paper_2406_06858_b200 import baselines as BL
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+
+    pattern, m, n, k, tp_wl, desc = WORKLOADS[wl]
+    emulated = world == 1
+    tp = tp_wl if emulated else world
+    prob = fx.ProblemSpec(m, n, k, tp, pattern)
+    heap = fx.required_heap_bytes(prob) + (64 << 20)
+    if emulated:
+        comm = fx.Communicator(tp, [local_rank] * tp, heap_bytes=heap)
+        my_ranks = list(range(tp))
+    else:
+        def gather(blob):
+            out = [None] * world
+            dist.all_gather_object(out, blob)
+            return out
+        comm = fx.Communicator.ipc(rank, tp, local_rank, heap, gather)
+        my_ranks = [rank]
+
+    # synthetic inputs (uniform [-1, 1), bf16) straight into the symmetric heaps
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    for r in my_ranks:
+        for kind in (N.BUF_A_SHARD, N.BUF_B_SHARD):
+            t = comm.tensor(r, kind, prob)
+            t.copy_(torch.rand(t.shape, generator=g, device=dev).mul_(2).sub_(1))
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream().cuda_stream
+    streams = [stream] * (tp if emulated else 1)
+    tile = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
+    opts = fx.default_opts()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def op():
+        if pattern == 0:
+            comm.ag_gemm(prob, tile, prob.rows_per_rank(), fx.PULL, True, opts, streams)
+        else:
+            comm.gemm_rs(prob, tile, fx.WRITE_ALLTOALL, True, opts, streams)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps, warmup, kernel_times=None):
+        """Sum of per-step device times (CUDA events on the launch stream), L2
+        flushed between steps outside the timed events; max over ranks."""
+        for _ in range(warmup):
+            fn()
+        barrier()
+        total = 0.0
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(steps):
+            flush.zero_()
+            ev0.record()
+            fn()
+            ev1.record()
+            ev1.synchronize()
+            total += ev0.elapsed_time(ev1)
+            if kernel_times is not None:
+                kernel_times.append(comm.last_kernel_ms())
+        barrier()
+        t = torch.tensor([total], device=dev)
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item() / steps
+
+    # ---- headline: the fused operator ----
+    comm.set_timing(True)
+    kernel_ms = []
+    with ClockSampler(local_rank) as clk:
+        ms_fused = timed(op, args.steps, max(3, args.warmup), kernel_ms)
+    comm.sync()
+    launches_per_step = comm.last_launch_count()
+    comm.set_timing(False)
+    flops = prob.flops()
+    value = flops / (ms_fused * 1e-3) / 1e12
+
+    # ---- Eq. 1 / Eq. 2 ingredients ----
+    extra = {}
+    if not args.quick:
+        ms_local = timed(lambda: comm.local_gemm(prob, opts, streams), max(3, args.steps // 2), 2)
+        ms_nonov = timed(lambda: comm.nonoverlap(prob, opts, streams), max(3, args.steps // 2), 2)
+        # cuBLAS + NCCL (or device copies when emulated): B1, and cuBLAS non-split GEMM
+        if emulated:
+            if pattern == 0:
+                shards = [comm.tensor(r, N.BUF_A_SHARD, prob).contiguous() for r in range(tp)]
+                weights = [comm.tensor(r, N.BUF_B_SHARD, prob).contiguous() for r in range(tp)]
+                b = BL.EmulatedAG(shards, weights)
+            else:
+                a_s = [comm.tensor(r, N.BUF_A_SHARD, prob).contiguous() for r in range(tp)]
+                w_s = [comm.tensor(r, N.BUF_B_SHARD, prob).contiguous() for r in range(tp)]
+                b = BL.EmulatedRS(a_s, w_s)
+        else:
+            if pattern == 0:
+                b = BL.DistAG(comm.tensor(rank, N.BUF_A_SHARD, prob).contiguous(),
+                              comm.tensor(rank, N.BUF_B_SHARD, prob).contiguous())
+            else:
+                b = BL.DistRS(comm.tensor(rank, N.BUF_A_SHARD, prob).contiguous(),
+                              comm.tensor(rank, N.BUF_B_SHARD, prob).contiguous())
+        if pattern == 0:
+            b.unfused()  # fills the gathered buffers for gemm_only
+        ms_cublas_gemm = timed(b.gemm_only, max(3, args.steps // 2), 2)
+        ms_b1 = timed(b.unfused, max(3, args.steps // 2), 2)
+        ms_b2 = None
+        if emulated and pattern == 0:
+            ms_b2 = timed(b.decomposed, max(3, args.steps // 2), 2)
+        del b
+        t_gemm = min(ms_local, ms_cublas_gemm)
+        ect_fused = ms_fused - t_gemm
+        ect_b1 = ms_b1 - t_gemm
+        extra = {
+            "t_gemm_nonsplit_ms": t_gemm, "t_gemm_ours_ms": ms_local, "t_gemm_cublas_ms": ms_cublas_gemm,
+            "t_unfused_cublas_ms": ms_b1, "t_decomposed_ms": ms_b2, "t_nonoverlap_ours_ms": ms_nonov,
+            "ect_fused_ms": ect_fused, "ect_unfused_ms": ect_b1,
+            "overlap_efficiency": (1.0 - ect_fused / ect_b1) if ect_b1 > 0 else None,
+            "speedup_vs_unfused": ms_b1 / ms_fused,
+            "unfused_baseline": ("device copies + cuBLAS (ranks emulated on one GPU)" if emulated
+                                 else "NCCL + cuBLAS"),
+        }
+
+    # ---- e2e through the C ABI with host buffers ----
+    e2e = None
+    if not args.quick:
+        a_host = {r: torch.empty(prob.rows_per_rank() if pattern == 0 else m, prob.local_k(), dtype=torch.bfloat16,
+                                 pin_memory=True) for r in my_ranks}
+        c_rows = m if pattern == 0 else prob.rows_per_rank()
+        c_host = {r: torch.empty(c_rows, prob.local_cols(), dtype=torch.bfloat16, pin_memory=True) for r in my_ranks}
+        for r in my_ranks:
+            a_host[r].copy_(comm.tensor(r, N.BUF_A_SHARD, prob).cpu())
+
+        def e2e_step():
+            for r in my_ranks:
+                comm.copy_in(r, N.BUF_A_SHARD, prob, a_host[r].data_ptr(), a_host[r].shape[1], stream)
+            op()
+            for r in my_ranks:
+                comm.copy_out(r, N.BUF_C_OUT, prob, c_host[r].data_ptr(), c_host[r].shape[1], stream)
+
+        ms_e2e = timed(e2e_step, max(3, args.steps // 2), 2)
+        h2d = sum(t.numel() * 2 for t in a_host.values())
+        d2h = sum(t.numel() * 2 for t in c_host.values())
+        if dist is not None:
+            tt = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt)
+            h2d, d2h = int(tt[0].item()), int(tt[1].item())
+        e2e = {"value": flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOPS", "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "flux_copy_in(A shards from pinned host) -> flux_ag_gemm/flux_gemm_rs -> flux_copy_out(C)"}
+
+    # ---- roofline of the dominant kernel (the fused GEMM) ----
+    pk, src = peaks()
+    kms = statistics.mean(kernel_ms) if kernel_ms else ms_fused
+    flops_per_launch = flops / (world if not emulated else 1)
+    achieved = flops_per_launch / (kms * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(wl)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "peak_source": src + " burst bf16",
+                "kernel": "flux_gemm_kernel<AG>" if pattern == 0 else "flux_gemm_kernel<RS>",
+                "kernel_ms": kms, "flops_per_launch": flops_per_launch}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = run_cpu_reference(pattern, m, n, k, tp)
+        except Exception as e:  # reported, never fatal for the GPU number
+            cpu = {"value": None, "unit": "TFLOPS", "cores": 0, "kind": "unavailable", "sample": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_fused, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform[-1,1) bf16)",
+            "config": {"workload": wl, "description": desc, "m": m, "n": n, "k": k, "tp": tp,
+                       "ranks": "emulated on one GPU" if emulated else "one process per GPU (cudaIpc heaps)",
+                       "parallelism": f"tp{tp}", "transfer": "copy-engine pull" if pattern == 0 else "epilogue P2P",
+                       "l2": "flushed between timed steps (256 MiB write outside the events)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "overlap": extra,
+        }
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama70b-up-ag")
+    ap.add_argument("--quick", action="store_true", help="headline number only")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args, args.workload)
+    else:
+        our_arm(args, args.workload)
+
+
+if __name__ == "__main__":
+    main()

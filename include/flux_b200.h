@@ -189,6 +189,11 @@ int flux_nonoverlap(flux_comm* comm, const flux_problem* problem, const flux_opt
 int flux_sync(flux_comm* comm);
 /* Number of this library's kernels launched by the last operator call. */
 int flux_last_launch_count(const flux_comm* comm);
+/* Measurement hooks: when enabled, every fused launch is bracketed by CUDA
+ * events on its launching stream; flux_last_kernel_ms returns the longest
+ * launch of the last operator (waits for it). */
+int flux_comm_set_timing(flux_comm* comm, int enable);
+int flux_last_kernel_ms(flux_comm* comm, float* ms);
 
 #ifdef __cplusplus
 } /* extern "C" */

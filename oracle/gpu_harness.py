@@ -1,0 +1,48 @@
+"""TEST INFRASTRUCTURE — GPU test harness: oracle inputs -> communicator buffers -> operator -> float64.
+
+Inputs are the reference Rng stream (workspace.cpp:5-29) rounded to bf16 by the
+CPU oracle, uploaded bit-exactly; expected values come from the oracle
+restatement (oracle/flux_oracle.c), which tests/test_oracle.py pins against
+the reference's golden vectors.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import paper_2406_06858_b200 as fx
+from paper_2406_06858_b200 import _native as N
+from oracle import oracle as O
+
+
+def make_comm(problem: fx.ProblemSpec, devices=None) -> fx.Communicator:
+    return fx.Communicator(problem.tp, devices or [0] * problem.tp,
+                           heap_bytes=max(fx.required_heap_bytes(problem), 8 << 20))
+
+
+def upload(comm: fx.Communicator, problem: fx.ProblemSpec, seed: int):
+    """Fills every rank's A/B shard; returns the float64 inputs in reference layout."""
+    pat = problem.pattern
+    a_list, b_list = [], []
+    for r in range(problem.tp):
+        a_bits, bt_bits = O.rank_inputs_bits(pat, problem.m, problem.n, problem.k, problem.tp, seed, r)
+        ta = torch.from_numpy(a_bits.view(np.int16)).cuda().view(torch.bfloat16)
+        tb = torch.from_numpy(bt_bits.view(np.int16)).cuda().view(torch.bfloat16)
+        comm.tensor(r, N.BUF_A_SHARD, problem).copy_(ta)
+        comm.tensor(r, N.BUF_B_SHARD, problem).copy_(tb)
+        a_list.append(O.bits_to_f64(a_bits))
+        b_list.append(np.ascontiguousarray(O.bits_to_f64(bt_bits).T))
+    torch.cuda.synchronize()
+    return a_list, b_list
+
+
+def outputs(comm: fx.Communicator, problem: fx.ProblemSpec, f32: bool):
+    kind = N.BUF_C_OUT_F32 if f32 else N.BUF_C_OUT
+    return [comm.tensor(r, kind, problem).double().cpu().numpy() for r in range(problem.tp)]
+
+
+def tol(f32: bool) -> float:
+    """Parity tolerance (BASELINE.md parity contract): bf16
+    inputs, fp32 accumulation and fp32 cross-rank partials; max_rel_error
+    (matrix.cpp:11-25) against the fp64 oracle."""
+    return 1e-4 if f32 else 8e-3

@@ -113,6 +113,8 @@ _SIGS = {
     "flux_nonoverlap": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
     "flux_sync": (C.c_int, [C.c_void_p]),
     "flux_last_launch_count": (C.c_int, [C.c_void_p]),
+    "flux_comm_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "flux_last_kernel_ms": (C.c_int, [C.c_void_p, _P(C.c_float)]),
 }
 
 # Symbols include/flux_b200.h declares (tests check the library exports all of them).

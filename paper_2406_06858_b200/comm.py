@@ -190,6 +190,14 @@ class Communicator:
     def last_launch_count(self) -> int:
         return N.lib().flux_last_launch_count(self._h)
 
+    def set_timing(self, enable: bool = True) -> None:
+        N.check(N.lib().flux_comm_set_timing(self._h, int(enable)))
+
+    def last_kernel_ms(self) -> float:
+        v = C.c_float()
+        N.check(N.lib().flux_last_kernel_ms(self._h, C.byref(v)))
+        return float(v.value)
+
     def drop_peer(self, from_rank: int, peer_rank: int) -> None:
         N.check(N.lib().flux_comm_drop_peer(self._h, from_rank, peer_rank))
 

@@ -371,6 +371,9 @@ struct flux_comm {
     std::vector<RankState> ranks;
     std::vector<std::vector<bool>> directory;  // [from][peer] usable
     int last_launches = 0;
+    bool timing = false;                          // bracket fused launches with events
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel_events;  // per device group
+    int kernel_events_used = 0;
     std::vector<uint32_t*> order_dev;  // per device group scratch for tile orders
     std::vector<size_t> order_cap;
 };
@@ -582,7 +585,19 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             }
         }
         const int grid = std::max(1, std::min(prm.num_tiles, sm_count(dev)));
+        std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+        if (c->timing) {
+            if (static_cast<int>(c->kernel_events.size()) <= c->kernel_events_used) {
+                std::pair<cudaEvent_t, cudaEvent_t> pr;
+                FLUX_CUDA(cudaEventCreate(&pr.first));
+                FLUX_CUDA(cudaEventCreate(&pr.second));
+                c->kernel_events.push_back(pr);
+            }
+            ev = &c->kernel_events[c->kernel_events_used++];
+            FLUX_CUDA(cudaEventRecord(ev->first, lead));
+        }
         FLUX_CUDA(launch_gemm(mode, prm, grid, lead));
+        if (ev) FLUX_CUDA(cudaEventRecord(ev->second, lead));
         ++c->last_launches;
         FLUX_CUDA(cudaEventRecord(c->ranks[g[0]].kernel_evt, lead));
         for (size_t li = 0; li < g.size(); ++li) {
@@ -852,6 +867,10 @@ int flux_comm_destroy(flux_comm* c) {
     }
     for (size_t i = 0; i < c->order_dev.size(); ++i)
         if (c->order_dev[i]) cudaFree(c->order_dev[i]);
+    for (auto& pr : c->kernel_events) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
     delete c;
     return FLUX_OK;
 }
@@ -948,6 +967,7 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     const OpCommon oc = common_opts(opts);
     const Layout L = layout_for(p);
     c->last_launches = 0;
+    c->kernel_events_used = 0;
     const uint32_t e = ++c->epoch;
     const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
     const int lk = local_k(p);
@@ -1030,6 +1050,7 @@ int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         for (int q = 0; q < tp; ++q) FLUX_TRY(check_directory(c, r, q));
     OpCommon oc = common_opts(opts);
     c->last_launches = 0;
+    c->kernel_events_used = 0;
     ++c->epoch;
     // Tile order: RankShifted (local block last) or Naive (engine.cpp:210-217,256-261).
     std::vector<std::vector<uint32_t>> seq(tp);
@@ -1050,6 +1071,7 @@ int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
     FLUX_TRY(check_heap(c, p));
     OpCommon oc = common_opts(opts);
     c->last_launches = 0;
+    c->kernel_events_used = 0;
     std::vector<int> mine;
     local_ranks_only(c, mine);
     std::vector<std::vector<uint32_t>> seq(p->tp);
@@ -1070,6 +1092,7 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
     OpCommon oc = common_opts(opts);
     const Layout L = layout_for(p);
     c->last_launches = 0;
+    c->kernel_events_used = 0;
     const uint32_t e = ++c->epoch;
     std::vector<std::vector<uint32_t>> seq(tp);
     for (int r : mine) seq[r] = device_sequence(p->m, local_cols(p), rpr, {}, 0);
@@ -1171,5 +1194,24 @@ int flux_sync(flux_comm* c) {
 }
 
 int flux_last_launch_count(const flux_comm* c) { return c ? c->last_launches : 0; }
+
+int flux_comm_set_timing(flux_comm* c, int enable) {
+    if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
+    c->timing = enable != 0;
+    return FLUX_OK;
+}
+
+int flux_last_kernel_ms(flux_comm* c, float* ms) {
+    if (!c || !ms) return fail(FLUX_ERR_CONFIG, "null argument");
+    float worst = 0.0f;
+    for (int i = 0; i < c->kernel_events_used; ++i) {
+        FLUX_CUDA(cudaEventSynchronize(c->kernel_events[i].second));
+        float t = 0.0f;
+        FLUX_CUDA(cudaEventElapsedTime(&t, c->kernel_events[i].first, c->kernel_events[i].second));
+        worst = std::max(worst, t);
+    }
+    *ms = worst;
+    return FLUX_OK;
+}
 
 }  // extern "C"

@@ -1,0 +1,53 @@
+"""The C-ABI library loads and exports every symbol include/flux_b200.h declares
+(no compute calls: this runs without a GPU)."""
+import os
+import re
+import subprocess
+
+from paper_2406_06858_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "flux_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(flux_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_abi():
+    syms = declared_symbols()
+    assert "flux_ag_gemm" in syms and "flux_gemm_rs" in syms and "flux_comm_create_ipc" in syms
+    assert len(syms) >= 25
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    out = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(flux_[a-z0-9_]+)$", out, flags=re.M))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    for s in declared_symbols():
+        getattr(lib, s)
+
+
+def test_python_binding_covers_the_header():
+    assert sorted(N.EXPORTED) == declared_symbols()
+
+
+def test_library_is_sm100a_and_uses_tcgen05():
+    out = subprocess.run(["cuobjdump", "-sass", N.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    assert "UTCHMMA" in out  # tcgen05.mma
+    assert "UTMALDG" in out  # TMA loads
+    assert "LDTM" in out     # tcgen05.ld (TMEM -> registers)
+    elf = subprocess.run(["cuobjdump", "-lelf", N.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in elf
+
+
+def test_abi_version_and_defaults():
+    lib = N.lib()
+    assert lib.flux_abi_version() == 1
+    o = N.default_opts()
+    assert o.deterministic_reduce == 1 and o.shift_offset == 1 and o.wall_budget_s == 10.0
+    assert o.poll_budget == 10_000_000  # EngineOptions defaults (engine.hpp:65-72)
