@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -374,8 +375,7 @@ struct flux_comm {
     bool timing = false;                          // bracket fused launches with events
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel_events;  // per device group
     int kernel_events_used = 0;
-    std::vector<uint32_t*> order_dev;  // per device group scratch for tile orders
-    std::vector<size_t> order_cap;
+    std::map<std::pair<int, std::vector<uint32_t>>, uint32_t*> order_cache;  // (device, schedule) -> table
 };
 
 namespace {
@@ -464,26 +464,22 @@ cudaStream_t stream_for(flux_comm* c, int rank, void* const* streams) {
     return c->ranks[rank].stream;
 }
 
-int upload_order(flux_comm* c, int gi, int device, const std::vector<uint32_t>& order, cudaStream_t s,
-                 uint32_t** out) {
-    if (static_cast<int>(c->order_dev.size()) <= gi) {
-        c->order_dev.resize(gi + 1, nullptr);
-        c->order_cap.resize(gi + 1, 0);
+// Tile schedules are immutable: upload each distinct table once per device and
+// reuse it (no host sync on the launch path).
+int upload_order(flux_comm* c, int device, const std::vector<uint32_t>& order, uint32_t** out) {
+    auto key = std::make_pair(device, order);
+    auto it = c->order_cache.find(key);
+    if (it != c->order_cache.end()) {
+        *out = it->second;
+        return FLUX_OK;
     }
     FLUX_CUDA(cudaSetDevice(device));
+    uint32_t* d = nullptr;
     const size_t bytes = order.size() * sizeof(uint32_t);
-    if (c->order_cap[gi] < bytes) {
-        if (c->order_dev[gi]) {
-            FLUX_CUDA(cudaStreamSynchronize(s));
-            FLUX_CUDA(cudaFree(c->order_dev[gi]));
-        }
-        FLUX_CUDA(cudaMalloc(&c->order_dev[gi], bytes * 2));
-        c->order_cap[gi] = bytes * 2;
-    }
-    // Ordered on the launching stream; host data is copied before the call returns.
-    FLUX_CUDA(cudaMemcpyAsync(c->order_dev[gi], order.data(), bytes, cudaMemcpyHostToDevice, s));
-    FLUX_CUDA(cudaStreamSynchronize(s));
-    *out = c->order_dev[gi];
+    FLUX_CUDA(cudaMalloc(&d, bytes));
+    FLUX_CUDA(cudaMemcpy(d, order.data(), bytes, cudaMemcpyHostToDevice));
+    c->order_cache.emplace(std::move(key), d);
+    *out = d;
     return FLUX_OK;
 }
 
@@ -553,7 +549,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 }
         }
         uint32_t* order_dev = nullptr;
-        FLUX_TRY(upload_order(c, static_cast<int>(gi), dev, order, lead, &order_dev));
+        FLUX_TRY(upload_order(c, dev, order, &order_dev));
         prm.order = order_dev;
         prm.num_tiles = static_cast<int>(order.size());
         prm.m = m_rows;
@@ -865,8 +861,10 @@ int flux_comm_destroy(flux_comm* c) {
         if (rs.kernel_evt) cudaEventDestroy(rs.kernel_evt);
         if (rs.copy_evt) cudaEventDestroy(rs.copy_evt);
     }
-    for (size_t i = 0; i < c->order_dev.size(); ++i)
-        if (c->order_dev[i]) cudaFree(c->order_dev[i]);
+    for (auto& kv : c->order_cache) {
+        cudaSetDevice(kv.first.first);
+        cudaFree(kv.second);
+    }
     for (auto& pr : c->kernel_events) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);
@@ -972,15 +970,29 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
     const int lk = local_k(p);
 
-    // ---- Alg. 3: host transfer loop on each rank's copy-engine stream ----
+    // The copy streams start after the caller's prior work (the A shards) and
+    // after this rank's previous kernel (WAR on a_agg).
     for (int r : mine) {
         RankState& rs = c->ranks[r];
         FLUX_CUDA(cudaSetDevice(rs.device));
         cudaStream_t s = stream_for(c, r, streams);
-        cudaStream_t cs = rs.copy_stream;
         FLUX_CUDA(cudaEventRecord(rs.start_evt, s));
-        FLUX_CUDA(cudaStreamWaitEvent(cs, rs.start_evt, 0));
-        if (rs.kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(cs, rs.kernel_evt, 0));
+        FLUX_CUDA(cudaStreamWaitEvent(rs.copy_stream, rs.start_evt, 0));
+        if (rs.kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(rs.copy_stream, rs.kernel_evt, 0));
+    }
+
+    // ---- Alg. 2: the fused GEMM, tiles ordered by expected arrival. Launched
+    // first so it computes ready (local) tiles while the host enqueues Alg. 3.
+    std::vector<std::vector<uint32_t>> seq(tp);
+    for (int r : mine)
+        seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct), 0);
+    FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, oc.o.emulated_order == 0));
+
+    // ---- Alg. 3: host transfer loop on each rank's copy-engine stream ----
+    for (int r : mine) {
+        RankState& rs = c->ranks[r];
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        cudaStream_t cs = rs.copy_stream;
         // Peers finished pulling my previous shard before I overwrite it.
         if (transfer == FLUX_PULL)
             for (int q = 0; q < tp; ++q)
@@ -1016,11 +1028,6 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         FLUX_CUDA(cudaEventRecord(rs.copy_evt, cs));
     }
 
-    // ---- Alg. 2: the fused GEMM, tiles ordered by expected arrival ----
-    std::vector<std::vector<uint32_t>> seq(tp);
-    for (int r : mine)
-        seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct), 0);
-    FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, oc.o.emulated_order == 0));
     for (int r : mine) {
         RankState& rs = c->ranks[r];
         FLUX_CUDA(cudaSetDevice(rs.device));

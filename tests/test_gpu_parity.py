@@ -86,7 +86,7 @@ def test_fused_matches_oracle(case):
 @pytest.mark.parametrize("tp,rpct", [(4, 64), (4, 32), (2, 512), (8, 16)])
 def test_allgather_comm_tile_sizes_and_transfer_modes(tp, rpct):
     """Comm tiles decoupled from GEMM tiles (SPEC §4.3), pull and push."""
-    m = 256 * tp if rpct >= 64 else 64 * tp
+    m = tp * max(256, rpct) if rpct >= 64 else 64 * tp
     p = fx.ProblemSpec(m, 256 * tp, 192, tp, AG)
     with H.make_comm(p) as comm:
         a, b = H.upload(comm, p, seed=7)
