@@ -200,6 +200,9 @@ def our_arm(args, wl):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    # A real (non-legacy) stream: the library runs on it and the CUDA events
+    # below are recorded on it.
+    torch.cuda.set_stream(torch.cuda.Stream(device=dev))
 
     pattern, m, n, k, tp_wl, desc = WORKLOADS[wl]
     emulated = world == 1

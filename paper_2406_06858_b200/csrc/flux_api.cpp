@@ -970,15 +970,20 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
     const int lk = local_k(p);
 
-    // The copy streams start after the caller's prior work (the A shards) and
-    // after this rank's previous kernel (WAR on a_agg).
-    for (int r : mine) {
-        RankState& rs = c->ranks[r];
-        FLUX_CUDA(cudaSetDevice(rs.device));
-        cudaStream_t s = stream_for(c, r, streams);
-        FLUX_CUDA(cudaEventRecord(rs.start_evt, s));
-        FLUX_CUDA(cudaStreamWaitEvent(rs.copy_stream, rs.start_evt, 0));
-        if (rs.kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(rs.copy_stream, rs.kernel_evt, 0));
+    // One copy-engine stream per device (several blocked stream-wait memops on
+    // many streams can starve each other on shared hardware queues). It starts
+    // after the caller's prior work (the A shards) and after the previous kernel
+    // of every rank it serves (WAR on a_agg).
+    auto groups = device_groups(c);
+    for (const auto& g : groups) {
+        RankState& lead = c->ranks[g[0]];
+        FLUX_CUDA(cudaSetDevice(lead.device));
+        for (int r : g) {
+            RankState& rs = c->ranks[r];
+            FLUX_CUDA(cudaEventRecord(rs.start_evt, stream_for(c, r, streams)));
+            FLUX_CUDA(cudaStreamWaitEvent(lead.copy_stream, rs.start_evt, 0));
+            if (rs.kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(lead.copy_stream, rs.kernel_evt, 0));
+        }
     }
 
     // ---- Alg. 2: the fused GEMM, tiles ordered by expected arrival. Launched
@@ -988,53 +993,71 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct), 0);
     FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, oc.o.emulated_order == 0));
 
-    // ---- Alg. 3: host transfer loop on each rank's copy-engine stream ----
-    for (int r : mine) {
-        RankState& rs = c->ranks[r];
-        FLUX_CUDA(cudaSetDevice(rs.device));
-        cudaStream_t cs = rs.copy_stream;
-        // Peers finished pulling my previous shard before I overwrite it.
+    // ---- Alg. 3: the transfer loop (engine.cpp:367-423) on the copy engines ----
+    const size_t shard_pitch = static_cast<size_t>(L.a_shard.ld) * 2;
+    auto copy_rows = [&](cudaStream_t cs, char* dst, size_t dpitch, const char* src, size_t spitch, int rows) -> int {
+        const size_t width = static_cast<size_t>(lk) * 2;
+        if (dpitch == width && spitch == width)
+            FLUX_CUDA(cudaMemcpyAsync(dst, src, width * rows, cudaMemcpyDeviceToDevice, cs));
+        else
+            FLUX_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToDevice, cs));
+        return FLUX_OK;
+    };
+    const int per_peer = rpr / rpct;
+    for (const auto& g : groups) {
+        RankState& lead = c->ranks[g[0]];
+        FLUX_CUDA(cudaSetDevice(lead.device));
+        cudaStream_t cs = lead.copy_stream;
+        auto in_group = [&](int q) { return std::find(g.begin(), g.end(), q) != g.end(); };
+        // Remote peers finished pulling my previous shard before I overwrite it
+        // (ranks sharing this stream are ordered by the stream itself).
         if (transfer == FLUX_PULL)
-            for (int q = 0; q < tp; ++q)
-                if (q != r) FLUX_TRY(wait_value_geq(cs, c->ranks[q].heap + kCtrlDone, e - 1));
+            for (int r : g)
+                for (int q = 0; q < tp; ++q)
+                    if (q != r && !in_group(q)) FLUX_TRY(wait_value_geq(cs, c->ranks[q].heap + kCtrlDone, e - 1));
         // Local shard -> own a_agg slot, local flags preset (engine.cpp:469-472).
-        FLUX_CUDA(cudaMemcpy2DAsync(rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes,
-                                    rs.heap + L.a_shard.off, static_cast<size_t>(L.a_shard.ld) * 2, lk * 2, rpr,
-                                    cudaMemcpyDeviceToDevice, cs));
-        FLUX_TRY(write_value(cs, rs.heap + kCtrlReady, e));
-        for (int f = r * rpr / rpct; f < (r + 1) * rpr / rpct; ++f)
-            FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + f, e));
-        int last_peer = -1;
-        for (const Desc& d : specs[r]) {
-            const int q = d.peer;
-            const RankState& qs = c->ranks[q];
-            if (transfer == FLUX_PULL) {
-                if (q != last_peer) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlReady, e));
-                FLUX_CUDA(cudaMemcpy2DAsync(rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
-                                            qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
-                                            lk * 2, d.rows, cudaMemcpyDeviceToDevice, cs));
-                FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
-            } else {
-                if (q != last_peer) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlKdone, e - 1));
-                FLUX_CUDA(cudaMemcpy2DAsync(
-                    qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
-                    rs.heap + L.a_shard.off + static_cast<size_t>(d.row_begin - r * rpr) * L.a_shard.ld * 2,
-                    static_cast<size_t>(L.a_shard.ld) * 2, lk * 2, d.rows, cudaMemcpyDeviceToDevice, cs));
-                FLUX_TRY(write_value(cs, at<uint32_t>(qs, kAgFlagOffset) + d.row_begin / rpct, e));
-            }
-            last_peer = q;
+        for (int r : g) {
+            RankState& rs = c->ranks[r];
+            FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes,
+                               rs.heap + L.a_shard.off, shard_pitch, rpr));
+            FLUX_TRY(write_value(cs, rs.heap + kCtrlReady, e));
+            for (int f = r * rpr / rpct; f < (r + 1) * rpr / rpct; ++f)
+                FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + f, e));
         }
-        FLUX_TRY(write_value(cs, rs.heap + kCtrlDone, e));
-        FLUX_CUDA(cudaEventRecord(rs.copy_evt, cs));
-    }
-
-    for (int r : mine) {
-        RankState& rs = c->ranks[r];
-        FLUX_CUDA(cudaSetDevice(rs.device));
-        cudaStream_t s = stream_for(c, r, streams);
-        FLUX_TRY(write_value(s, rs.heap + kCtrlKdone, e));
-        // Later work on the caller's stream is ordered after our transfers.
-        FLUX_CUDA(cudaStreamWaitEvent(s, rs.copy_evt, 0));
+        // Ring steps, every rank of the device interleaved per step.
+        for (int step = 0; step < tp - 1; ++step) {
+            for (int r : g) {
+                RankState& rs = c->ranks[r];
+                for (int i = step * per_peer; i < (step + 1) * per_peer; ++i) {
+                    const Desc& d = specs[r][i];
+                    const int q = d.peer;
+                    const RankState& qs = c->ranks[q];
+                    const bool first = i == step * per_peer;
+                    if (transfer == FLUX_PULL) {
+                        if (first && !in_group(q)) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlReady, e));
+                        FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
+                                           rowbytes, qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
+                                           rowbytes, d.rows));
+                        FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
+                    } else {
+                        if (first && !in_group(q)) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlKdone, e - 1));
+                        FLUX_TRY(copy_rows(cs, qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
+                                           rowbytes,
+                                           rs.heap + L.a_shard.off + static_cast<size_t>(d.row_begin - r * rpr) * shard_pitch,
+                                           shard_pitch, d.rows));
+                        FLUX_TRY(write_value(cs, at<uint32_t>(qs, kAgFlagOffset) + d.row_begin / rpct, e));
+                    }
+                }
+            }
+        }
+        for (int r : g) FLUX_TRY(write_value(cs, c->ranks[r].heap + kCtrlDone, e));
+        FLUX_CUDA(cudaEventRecord(lead.copy_evt, cs));
+        for (int r : g) {
+            cudaStream_t s = stream_for(c, r, streams);
+            FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlKdone, e));
+            // Later work on the caller's stream is ordered after our transfers.
+            FLUX_CUDA(cudaStreamWaitEvent(s, lead.copy_evt, 0));
+        }
     }
     return FLUX_OK;
 }
@@ -1110,13 +1133,20 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
             RankState& rs = c->ranks[r];
             FLUX_CUDA(cudaSetDevice(rs.device));
             cudaStream_t s = stream_for(c, r, streams);
-            if (rs.kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(s, rs.kernel_evt, 0));
-            for (int q = 0; q < tp; ++q)
-                if (q != r) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
+            // WAR on my slot: in-process peers are ordered by their previous kernel
+            // event, other processes by their epoch-stamped `done` word.
+            for (int q = 0; q < tp; ++q) {
+                if (c->ranks[q].local) {
+                    if (c->ranks[q].kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[q].kernel_evt, 0));
+                } else if (q != r) {
+                    FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
+                }
+            }
             FLUX_CUDA(cudaMemcpy2DAsync(rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes,
                                         rs.heap + L.a_shard.off, static_cast<size_t>(L.a_shard.ld) * 2, lk * 2, rpr,
                                         cudaMemcpyDeviceToDevice, s));
             FLUX_TRY(write_value(s, rs.heap + kCtrlReady, e));
+            FLUX_CUDA(cudaEventRecord(rs.copy_evt, s));
         }
         for (int r : mine) {
             RankState& rs = c->ranks[r];
@@ -1124,7 +1154,8 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
             cudaStream_t s = stream_for(c, r, streams);
             for (int q = 0; q < tp; ++q) {
                 if (q == r) continue;
-                FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlReady, e));
+                if (c->ranks[q].local) FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[q].copy_evt, 0));
+                else FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlReady, e));
                 FLUX_CUDA(cudaMemcpy2DAsync(rs.heap + L.a_agg.off + static_cast<size_t>(q) * rpr * rowbytes, rowbytes,
                                             c->ranks[q].heap + L.a_agg.off + static_cast<size_t>(q) * rpr * rowbytes,
                                             rowbytes, lk * 2, rpr, cudaMemcpyDeviceToDevice, s));

@@ -16,6 +16,7 @@ ap.add_argument("--op", default="fused", choices=["fused", "local", "nonoverlap"
 args = ap.parse_args()
 pattern, m, n, k, tp, _ = WORKLOADS[args.workload]
 prob = fx.ProblemSpec(m, n, k, tp, pattern)
+torch.cuda.set_stream(torch.cuda.Stream())
 comm = fx.Communicator(tp, [0] * tp, heap_bytes=fx.required_heap_bytes(prob) + (64 << 20))
 for r in range(tp):
     for kind in (N.BUF_A_SHARD, N.BUF_B_SHARD):
