@@ -86,7 +86,8 @@ typedef struct {
     uint64_t interleave_seed;  /* nonzero: device jitter (nanosleep) before tiles, race testing */
     int shift_offset;          /* RankShifted offset (swizzle.hpp:27), default 1 */
     int out_dtype;             /* flux_dtype of C (default BF16) */
-    int emulated_order;        /* single-device multi-rank launch order: 0 step-major, 1 rank-major */
+    int emulated_order;        /* several ranks on one device: 0 locality-first (rank-major,
+                                  RS own blocks last), 1 position-major across ranks */
 } flux_opts;
 
 typedef struct {

@@ -483,6 +483,8 @@ int upload_order(flux_comm* c, int device, const std::vector<uint32_t>& order, u
     return FLUX_OK;
 }
 
+enum { kInterleaveStep = 0, kInterleaveRank = 1, kInterleaveRankTail = 2 };
+
 struct OpCommon {
     flux_opts o;
     uint64_t timeout_ns;
@@ -499,8 +501,8 @@ OpCommon common_opts(const flux_opts* opts) {
 
 // Launch one fused kernel per device group. `mode` selects the role.
 int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon& oc, void* const* streams,
-                  const std::vector<std::vector<uint32_t>>& seq_of_rank, int rpct, bool step_major,
-                  bool plain_on_agg = false, long long partial_off = -1) {
+                  const std::vector<std::vector<uint32_t>>& seq_of_rank, int rpct, int interleave,
+                  bool plain_on_agg = false, long long partial_off = -1, int rs_tail = 0) {
     const bool plain_f32_to_staging = partial_off >= 0;
     const Layout L = layout_for(p);
     const int lk = local_k(p), lc = local_cols(p);
@@ -535,18 +537,24 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         std::vector<uint32_t> order;
         const size_t T = seq_of_rank[g[0]].size();
         order.reserve(T * g.size());
-        if (step_major || g.size() == 1) {
+        // kInterleaveStep: position-major across ranks (every tile waits only on
+        //   tiles at lower positions). kInterleaveRank: each rank's GEMM in turn
+        //   (its operands stay L2-resident). kInterleaveRankTail: rank-major, but
+        //   every rank's last `tail` tiles (its own RS block, which waits on the
+        //   other ranks' partials) are moved behind all other tiles.
+        auto push = [&](size_t li, size_t i) {
+            const uint32_t e = seq_of_rank[g[li]][i];
+            order.push_back((e & 0x0FFFFFFFu) | (uint32_t(li) << 28));
+        };
+        if (interleave == kInterleaveStep || g.size() == 1) {
             for (size_t i = 0; i < T; ++i)
-                for (size_t li = 0; li < g.size(); ++li) {
-                    uint32_t e = seq_of_rank[g[li]][i];
-                    order.push_back((e & 0x0FFFFFFFu) | (uint32_t(li) << 28));
-                }
+                for (size_t li = 0; li < g.size(); ++li) push(li, i);
         } else {
+            const size_t tail = interleave == kInterleaveRankTail ? std::min<size_t>(T, static_cast<size_t>(rs_tail)) : 0;
             for (size_t li = 0; li < g.size(); ++li)
-                for (size_t i = 0; i < T; ++i) {
-                    uint32_t e = seq_of_rank[g[li]][i];
-                    order.push_back((e & 0x0FFFFFFFu) | (uint32_t(li) << 28));
-                }
+                for (size_t i = 0; i < T - tail; ++i) push(li, i);
+            for (size_t li = 0; li < g.size(); ++li)
+                for (size_t i = T - tail; i < T; ++i) push(li, i);
         }
         uint32_t* order_dev = nullptr;
         FLUX_TRY(upload_order(c, dev, order, &order_dev));
@@ -991,7 +999,8 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     std::vector<std::vector<uint32_t>> seq(tp);
     for (int r : mine)
         seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct), 0);
-    FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, oc.o.emulated_order == 0));
+    FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct,
+                           oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank));
 
     // ---- Alg. 3: the transfer loop (engine.cpp:367-423) on the copy engines ----
     const size_t shard_pitch = static_cast<size_t>(L.a_shard.ld) * 2;
@@ -1024,9 +1033,16 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
             for (int f = r * rpr / rpct; f < (r + 1) * rpr / rpct; ++f)
                 FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + f, e));
         }
-        // Ring steps, every rank of the device interleaved per step.
-        for (int step = 0; step < tp - 1; ++step) {
-            for (int r : g) {
+        // Transfers in the order the kernel consumes them: rank-major when the
+        // ranks sharing this device run rank by rank, else ring step by step.
+        std::vector<std::pair<int, int>> jobs;  // (rank, step)
+        const bool rank_major = transfer == FLUX_PULL && oc.o.emulated_order != 1 && g.size() > 1;
+        for (int a = 0; a < (rank_major ? static_cast<int>(g.size()) : tp - 1); ++a)
+            for (int b = 0; b < (rank_major ? tp - 1 : static_cast<int>(g.size())); ++b)
+                jobs.emplace_back(rank_major ? g[a] : g[b], rank_major ? b : a);
+        for (const auto& job : jobs) {
+            {
+                const int r = job.first, step = job.second;
                 RankState& rs = c->ranks[r];
                 for (int i = step * per_peer; i < (step + 1) * per_peer; ++i) {
                     const Desc& d = specs[r][i];
@@ -1090,9 +1106,15 @@ int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         else for (int i = 0; i < tp; ++i) blocks.push_back(i);
         seq[r] = device_sequence(p->m, p->n, rpr, blocks, 0);
     }
-    // Deadlock freedom of the single-device multi-rank launch needs step-major
-    // interleaving (a tile only waits on partials scheduled before it).
-    return launch_groups(c, p, kModeRS, oc, streams, seq, 0, true);
+    // Deadlock freedom of the single-device multi-rank launch: a tile may only
+    // wait on partials scheduled before it. With ownership blocks aligned to
+    // device tiles, RankShifted puts each rank's own block last, so rank-major
+    // order with those blocks moved to the end qualifies (and keeps each rank's
+    // operands L2-resident); otherwise fall back to position-major.
+    const bool aligned = swizzle_on && rpr % kBM == 0 && oc.o.emulated_order != 1;
+    const int tail = aligned ? (rpr / kBM) * ((p->n + kBN - 1) / kBN) : 0;
+    return launch_groups(c, p, kModeRS, oc, streams, seq, 0, aligned ? kInterleaveRankTail : kInterleaveStep, false,
+                         -1, tail);
 }
 
 int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
@@ -1106,7 +1128,7 @@ int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
     local_ranks_only(c, mine);
     std::vector<std::vector<uint32_t>> seq(p->tp);
     for (int r : mine) seq[r] = device_sequence(p->m, local_cols(p), rows_per_rank(p), {}, 0);
-    return launch_groups(c, p, kModePlain, oc, streams, seq, 0, oc.o.emulated_order == 0,
+    return launch_groups(c, p, kModePlain, oc, streams, seq, 0, oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank,
                          p->pattern == FLUX_ALLGATHER_GEMM);
 }
 
@@ -1162,13 +1184,16 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
             }
             FLUX_TRY(write_value(s, rs.heap + kCtrlDone, e));
         }
-        FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0, oc.o.emulated_order == 0, true));
+        FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0,
+                               oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, true));
         return FLUX_OK;
     }
     // GEMM-RS: full fp32 partial into this epoch's staging parity, then the
     // serial source-ordered reduce once every rank's GEMM finished.
     const size_t parity_off = L.staging.off + static_cast<size_t>(e & 1u) * L.stage_parity * 4;
-    FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0, true, false, static_cast<long long>(parity_off)));
+    FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0,
+                           oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, false,
+                           static_cast<long long>(parity_off)));
     for (int r : mine) {
         RankState& rs = c->ranks[r];
         FLUX_CUDA(cudaSetDevice(rs.device));
