@@ -88,6 +88,7 @@ typedef struct {
     int out_dtype;             /* flux_dtype of C (default BF16) */
     int emulated_order;        /* several ranks on one device: 0 locality-first (rank-major,
                                   RS own blocks last), 1 position-major across ranks */
+    int cta_group;             /* 0 auto, 1 = 128x256 tiles per CTA, 2 = CTA pairs (256x256, cta_group::2) */
 } flux_opts;
 
 typedef struct {

@@ -263,12 +263,13 @@ std::vector<int> ag_block_order(const flux_problem* p, int rank, int transfer, b
 // blocks align with device tile rows the reference's block-then-column-major
 // order is reproduced (swizzle.cpp:51-73); otherwise tiles straddle blocks and
 // the order is row-major (every rank walks the same sequence).
-std::vector<uint32_t> device_sequence(int m, int ncols, int rpr, const std::vector<int>& blocks, int slot) {
-    const int tiles_m = (m + kBM - 1) / kBM, tiles_n = (ncols + kBN - 1) / kBN;
+std::vector<uint32_t> device_sequence(int m, int ncols, int rpr, const std::vector<int>& blocks, int tile_m) {
+    const int slot = 0;
+    const int tiles_m = (m + tile_m - 1) / tile_m, tiles_n = (ncols + kBN - 1) / kBN;
     std::vector<uint32_t> seq;
     seq.reserve(static_cast<size_t>(tiles_m) * tiles_n);
-    if (!blocks.empty() && rpr % kBM == 0) {
-        const int rpb = rpr / kBM;
+    if (!blocks.empty() && rpr % tile_m == 0) {
+        const int rpb = rpr / tile_m;
         for (int b : blocks)
             for (int c = 0; c < tiles_n; ++c)
                 for (int r = 0; r < rpb; ++r) seq.push_back(pack_tile(slot, b * rpb + r, c));
@@ -485,6 +486,16 @@ int upload_order(flux_comm* c, int device, const std::vector<uint32_t>& order, u
 
 enum { kInterleaveStep = 0, kInterleaveRank = 1, kInterleaveRankTail = 2 };
 
+// CTAs per MMA tile: CTA pairs (256-row tiles, cta_group::2) unless ownership
+// blocks only align with 128-row tiles; opts.cta_group forces 1 or 2.
+int choose_cg(const flux_problem* p, const flux_opts& o) {
+    if (o.cta_group == 1 || o.cta_group == 2) return o.cta_group;
+    const int rpr = rows_per_rank(p);
+    if (rpr % (2 * kBM) == 0) return 2;
+    if (rpr % kBM == 0) return 1;
+    return p->m >= 2 * kBM ? 2 : 1;
+}
+
 struct OpCommon {
     flux_opts o;
     uint64_t timeout_ns;
@@ -502,7 +513,7 @@ OpCommon common_opts(const flux_opts* opts) {
 // Launch one fused kernel per device group. `mode` selects the role.
 int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon& oc, void* const* streams,
                   const std::vector<std::vector<uint32_t>>& seq_of_rank, int rpct, int interleave,
-                  bool plain_on_agg = false, long long partial_off = -1, int rs_tail = 0) {
+                  int cg, bool plain_on_agg = false, long long partial_off = -1, int rs_tail = 0) {
     const bool plain_f32_to_staging = partial_off >= 0;
     const Layout L = layout_for(p);
     const int lk = local_k(p), lc = local_cols(p);
@@ -520,7 +531,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             const RankState& rs = c->ranks[g[li]];
             const Region& A = (mode == kModeAG || plain_on_agg) ? L.a_agg : L.a_shard;
             FLUX_TRY(make_tmap(&prm.tma_a[li], rs.heap + A.off, A.rows, lk, A.ld, kBM));
-            FLUX_TRY(make_tmap(&prm.tma_b[li], rs.heap + L.b.off, lc, lk, L.b.ld, kBN));
+            FLUX_TRY(make_tmap(&prm.tma_b[li], rs.heap + L.b.off, lc, lk, L.b.ld, kBN / cg));
             if (plain_f32_to_staging) prm.c[li] = rs.heap + partial_off;  // full [m, n] fp32 partial
             else prm.c[li] = rs.heap + L.c32.off;
             prm.global_rank[li] = g[li];
@@ -565,7 +576,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.k = lk;
         if (plain_f32_to_staging) {
             prm.ldc = L.ld_stage;
-            prm.out_f32 = 1;
+            prm.out_f32 = oc.o.out_dtype == FLUX_F32 ? 1 : 0;
         } else {
             prm.ldc = L.c32.ld;
             prm.out_f32 = oc.o.out_dtype == FLUX_F32 ? 1 : 0;
@@ -588,7 +599,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 FLUX_CUDA(cudaStreamWaitEvent(lead, c->ranks[g[li]].start_evt, 0));
             }
         }
-        const int grid = std::max(1, std::min(prm.num_tiles, sm_count(dev)));
+        const int grid = cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
         std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
         if (c->timing) {
             if (static_cast<int>(c->kernel_events.size()) <= c->kernel_events_used) {
@@ -600,7 +611,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             ev = &c->kernel_events[c->kernel_events_used++];
             FLUX_CUDA(cudaEventRecord(ev->first, lead));
         }
-        FLUX_CUDA(launch_gemm(mode, prm, grid, lead));
+        FLUX_CUDA(launch_gemm(mode, cg, prm, grid, lead));
         if (ev) FLUX_CUDA(cudaEventRecord(ev->second, lead));
         ++c->last_launches;
         FLUX_CUDA(cudaEventRecord(c->ranks[g[0]].kernel_evt, lead));
@@ -644,6 +655,7 @@ void flux_default_opts(flux_opts* o) {
     o->shift_offset = 1;
     o->out_dtype = FLUX_BF16;
     o->emulated_order = 0;
+    o->cta_group = 0;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -994,13 +1006,15 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         }
     }
 
+    const int cg = choose_cg(p, oc.o);
     // ---- Alg. 2: the fused GEMM, tiles ordered by expected arrival. Launched
     // first so it computes ready (local) tiles while the host enqueues Alg. 3.
     std::vector<std::vector<uint32_t>> seq(tp);
     for (int r : mine)
-        seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct), 0);
+        seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct),
+                                 kBM * cg);
     FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct,
-                           oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank));
+                           oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, cg));
 
     // ---- Alg. 3: the transfer loop (engine.cpp:367-423) on the copy engines ----
     const size_t shard_pitch = static_cast<size_t>(L.a_shard.ld) * 2;
@@ -1098,23 +1112,24 @@ int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     c->last_launches = 0;
     c->kernel_events_used = 0;
     ++c->epoch;
+    const int cg = choose_cg(p, oc.o);
     // Tile order: RankShifted (local block last) or Naive (engine.cpp:210-217,256-261).
     std::vector<std::vector<uint32_t>> seq(tp);
     for (int r : mine) {
         std::vector<int> blocks;
         if (swizzle_on) blocks = block_order(FLUX_SWIZZLE_RANK_SHIFTED, r, tp, oc.o.shift_offset, {});
         else for (int i = 0; i < tp; ++i) blocks.push_back(i);
-        seq[r] = device_sequence(p->m, p->n, rpr, blocks, 0);
+        seq[r] = device_sequence(p->m, p->n, rpr, blocks, kBM * cg);
     }
     // Deadlock freedom of the single-device multi-rank launch: a tile may only
     // wait on partials scheduled before it. With ownership blocks aligned to
     // device tiles, RankShifted puts each rank's own block last, so rank-major
     // order with those blocks moved to the end qualifies (and keeps each rank's
     // operands L2-resident); otherwise fall back to position-major.
-    const bool aligned = swizzle_on && rpr % kBM == 0 && oc.o.emulated_order != 1;
-    const int tail = aligned ? (rpr / kBM) * ((p->n + kBN - 1) / kBN) : 0;
-    return launch_groups(c, p, kModeRS, oc, streams, seq, 0, aligned ? kInterleaveRankTail : kInterleaveStep, false,
-                         -1, tail);
+    const bool aligned = swizzle_on && rpr % (kBM * cg) == 0 && oc.o.emulated_order != 1;
+    const int tail = aligned ? (rpr / (kBM * cg)) * ((p->n + kBN - 1) / kBN) : 0;
+    return launch_groups(c, p, kModeRS, oc, streams, seq, 0, aligned ? kInterleaveRankTail : kInterleaveStep, cg,
+                         false, -1, tail);
 }
 
 int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
@@ -1126,10 +1141,14 @@ int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
     c->kernel_events_used = 0;
     std::vector<int> mine;
     local_ranks_only(c, mine);
+    const int cg = choose_cg(p, oc.o);
     std::vector<std::vector<uint32_t>> seq(p->tp);
-    for (int r : mine) seq[r] = device_sequence(p->m, local_cols(p), rows_per_rank(p), {}, 0);
-    return launch_groups(c, p, kModePlain, oc, streams, seq, 0, oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank,
-                         p->pattern == FLUX_ALLGATHER_GEMM);
+    for (int r : mine) seq[r] = device_sequence(p->m, local_cols(p), rows_per_rank(p), {}, kBM * cg);
+    const int il = oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank;
+    if (p->pattern == FLUX_ALLGATHER_GEMM) return launch_groups(c, p, kModePlain, oc, streams, seq, 0, il, cg, true);
+    // GEMM-RS: the full [m, n] partial goes to the staging region (parity 0).
+    return launch_groups(c, p, kModePlain, oc, streams, seq, 0, il, cg, false,
+                         static_cast<long long>(layout_for(p).staging.off));
 }
 
 int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
@@ -1146,8 +1165,9 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
     c->last_launches = 0;
     c->kernel_events_used = 0;
     const uint32_t e = ++c->epoch;
+    const int cg = choose_cg(p, oc.o);
     std::vector<std::vector<uint32_t>> seq(tp);
-    for (int r : mine) seq[r] = device_sequence(p->m, local_cols(p), rpr, {}, 0);
+    for (int r : mine) seq[r] = device_sequence(p->m, local_cols(p), rpr, {}, kBM * cg);
     if (p->pattern == FLUX_ALLGATHER_GEMM) {
         // Serial AllGather in rank order (engine.cpp:568-571), then the GEMM.
         const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
@@ -1185,14 +1205,16 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
             FLUX_TRY(write_value(s, rs.heap + kCtrlDone, e));
         }
         FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0,
-                               oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, true));
+                               oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, cg, true));
         return FLUX_OK;
     }
     // GEMM-RS: full fp32 partial into this epoch's staging parity, then the
     // serial source-ordered reduce once every rank's GEMM finished.
     const size_t parity_off = L.staging.off + static_cast<size_t>(e & 1u) * L.stage_parity * 4;
-    FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0,
-                           oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, false,
+    OpCommon oc32 = oc;
+    oc32.o.out_dtype = FLUX_F32;  // fp32 partials, reduced in source order below
+    FLUX_TRY(launch_groups(c, p, kModePlain, oc32, streams, seq, 0,
+                           oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, cg, false,
                            static_cast<long long>(parity_off)));
     for (int r : mine) {
         RankState& rs = c->ranks[r];

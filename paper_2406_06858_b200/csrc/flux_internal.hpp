@@ -77,7 +77,9 @@ struct RsReduceParams {
 };
 
 // Host launchers (flux_kernels.cu).
-cudaError_t launch_gemm(int mode, const GemmParams& p, int grid, cudaStream_t stream);
+// cg: CTAs per MMA tile (1 = 128x256 tiles, 2 = CTA pairs with 256x256 tiles).
+cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStream_t stream);
+int gemm_tile_rows(int cg);
 cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t stream);
 
 }  // namespace fluxb200

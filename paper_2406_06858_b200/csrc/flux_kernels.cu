@@ -122,6 +122,61 @@ __device__ __forceinline__ void tmem_ld_wait() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ---- clusters / CTA pairs (cta_group::2) --------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same shared variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load whose completion is signalled to the pair leader's mbarrier.
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t cols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols) : "memory");
+}
+// D[256 x N] across the pair: A rows 0-127 / 128-255 and B rows (N) halves
+// come from each CTA's shared memory at the same offsets.
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Arrive on the same barrier in both CTAs of the pair once the MMAs retire.
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
 // Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row core groups
 // 1024 B apart (SBO), version 1 (sm_100).
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
@@ -129,9 +184,10 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
     return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
            (2ull << 61);
 }
-// Instruction descriptor: D f32, A/B bf16, both K-major, M = 128, N = 256.
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(kBN >> 3) << 17) |
-                            (uint32_t(kBM >> 4) << 24);
+// Instruction descriptor: D f32, A/B bf16, both K-major, M x N.
+__host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
 
 // ---- cross-rank signalling (system scope: peers are other GPUs) -------------------
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -225,21 +281,41 @@ __device__ __forceinline__ void store_row32(void* c, long long off, int col, int
 
 }  // namespace
 
-template <int MODE>
+// Per-variant geometry. CG = CTAs cooperating on one MMA tile: 1 (cta_group::1,
+// 128 x 256 tile per CTA) or 2 (cta_group::2 CTA pair, 256 x 256 tile; each CTA
+// stages half of A (128 rows) and half of B (128 of the 256 N rows)).
+template <int CG>
+struct Geo {
+    static constexpr int kTileM = kBM * CG;                 // rows of one scheduled tile
+    static constexpr int kBRows = kBN / CG;                 // B rows (N) staged per CTA
+    static constexpr int kABytes = kBM * kBK * 2;
+    static constexpr int kBBytes = kBRows * kBK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStagesN = CG == 2 ? 6 : 4;
+    static constexpr int kSmem = kStagesN * kStageBytes + 1024 + 256;
+    static constexpr uint32_t kIdescV = make_idesc(kTileM, kBN);
+};
+
+template <int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_constant__ GemmParams p) {
+    using G = Geo<CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + kStages * kAStageBytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStageBytes);
-    uint64_t* empty = full + kStages;
-    uint64_t* tfull = empty + kStages;
+    uint8_t* sB = smem + G::kStagesN * G::kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + G::kStagesN * G::kBBytes);
+    uint64_t* empty = full + G::kStagesN;
+    uint64_t* tfull = empty + G::kStagesN;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t cta_rank = CG == 2 ? cluster_ctarank() : 0u;
+    const bool leader = cta_rank == 0;
+    const int cluster_id = blockIdx.x / CG;
+    const int num_clusters = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
         for (int l = 0; l < kMaxRanks; ++l) {
@@ -249,42 +325,46 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         }
     }
     if (warp == 1 && lane == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < G::kStagesN; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], 4 * CG);  // every epilogue warp of the pair drains it
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 2) {
+        if (CG == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
+        else tmem_alloc(tmem_slot, kTmemCols);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     const int k_blocks = (p.k + kBK - 1) / kBK;
 
     if (warp == 0) {
-        // ===== TMA producer =====
+        // ===== TMA producer (both CTAs of a pair load their halves) =====
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
             uint64_t jit = p.jitter_seed ? p.jitter_seed * 0x9e3779b97f4a7c15ull + blockIdx.x : 0;
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 int l, tm, tn;
                 decode(p.order[t], l, tm, tn);
-                const int row0 = tm * kBM;
-                const int col0 = tn * kBN;
+                const int row0 = tm * G::kTileM + static_cast<int>(cta_rank) * kBM;
+                const int bcol0 = tn * kBN + static_cast<int>(cta_rank) * G::kBRows;
                 if (jit) {  // reference Jitter (engine.cpp:116-128): perturb interleavings
                     jit ^= jit >> 12; jit ^= jit << 25; jit ^= jit >> 27;
                     const uint32_t r = static_cast<uint32_t>((jit * 0x2545F4914F6CDD1Dull) >> 40);
                     if ((r & 15u) == 0u) __nanosleep(r & 0xFFFFu);
                 }
-                if (MODE == kModeAG) {
-                    // Alg. 2: wait for every comm tile covering rows [row0, row0+BM).
+                if (MODE == kModeAG && row0 < p.m) {
+                    // Alg. 2: wait for every comm tile covering this CTA's A rows.
                     const int rlast = min(row0 + kBM, p.m) - 1;
                     const int f0 = row0 / p.rpct, f1 = rlast / p.rpct;
                     for (int f = f0; f <= f1; ++f)
@@ -295,10 +375,16 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 }
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
-                    mbar_expect_tx(&full[stage], kAStageBytes + kBStageBytes);
-                    tma_load_2d(sA + stage * kAStageBytes, &p.tma_a[l], &full[stage], kb * kBK, row0);
-                    tma_load_2d(sB + stage * kBStageBytes, &p.tma_b[l], &full[stage], kb * kBK, col0);
-                    if (++stage == kStages) {
+                    if (CG == 2) {
+                        if (leader) mbar_expect_tx(&full[stage], 2 * G::kStageBytes);
+                        tma_load_2d_pair(sA + stage * G::kABytes, &p.tma_a[l], &full[stage], kb * kBK, row0);
+                        tma_load_2d_pair(sB + stage * G::kBBytes, &p.tma_b[l], &full[stage], kb * kBK, bcol0);
+                    } else {
+                        mbar_expect_tx(&full[stage], G::kStageBytes);
+                        tma_load_2d(sA + stage * G::kABytes, &p.tma_a[l], &full[stage], kb * kBK, row0);
+                        tma_load_2d(sB + stage * G::kBBytes, &p.tma_b[l], &full[stage], kb * kBK, bcol0);
+                    }
+                    if (++stage == G::kStagesN) {
                         stage = 0;
                         phase ^= 1u;
                     }
@@ -306,34 +392,39 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer =====
-        if (lane == 0) {
+        // ===== MMA issuer (the pair leader issues for both CTAs) =====
+        if (lane == 0 && leader) {
             int stage = 0;
             uint32_t phase = 0;
             int as = 0;
             uint32_t aphase = 0;
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+            for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
                 mbar_wait(&tempty[as], aphase ^ 1u);
                 tc_fence_after();
                 const uint32_t d = tmem_base + static_cast<uint32_t>(as * kBN);
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint64_t adesc = smem_desc_sw128(sA + stage * kAStageBytes);
-                    const uint64_t bdesc = smem_desc_sw128(sB + stage * kBStageBytes);
+                    const uint64_t adesc = smem_desc_sw128(sA + stage * G::kABytes);
+                    const uint64_t bdesc = smem_desc_sw128(sB + stage * G::kBBytes);
 #pragma unroll
                     for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
                         // +32 B along K inside the 128B swizzle atom = +2 in the >>4 address field.
-                        umma_bf16(d, adesc + 2ull * kk, bdesc + 2ull * kk, kIdesc,
-                                  (kb | kk) != 0 ? 1u : 0u);
+                        if (CG == 2)
+                            umma_bf16_pair(d, adesc + 2ull * kk, bdesc + 2ull * kk, G::kIdescV, (kb | kk) != 0 ? 1u : 0u);
+                        else
+                            umma_bf16(d, adesc + 2ull * kk, bdesc + 2ull * kk, G::kIdescV, (kb | kk) != 0 ? 1u : 0u);
                     }
-                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
-                    if (++stage == kStages) {
+                    // Frees the smem slot (in both CTAs) when these MMAs retire.
+                    if (CG == 2) umma_commit_pair(&empty[stage]);
+                    else umma_commit(&empty[stage]);
+                    if (++stage == G::kStagesN) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
-                umma_commit(&tfull[as]);  // accumulator ready for the epilogue
+                if (CG == 2) umma_commit_pair(&tfull[as]);  // accumulator ready for both epilogues
+                else umma_commit(&tfull[as]);
                 if (++as == 2) {
                     as = 0;
                     aphase ^= 1u;
@@ -341,14 +432,16 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             }
         }
     } else if (warp >= 4) {
-        // ===== epilogue =====
-        const int q = warp - 4;          // TMEM lane quadrant (warp % 4)
+        // ===== epilogue: each CTA drains its own 128 TMEM lanes (rows) =====
+        const int q = warp - 4;            // TMEM lane quadrant (warp % 4)
         const int et = threadIdx.x - 128;  // epilogue thread 0..127
+        const uint32_t tempty_leader = CG == 2 ? mapa(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
         int as = 0;
         uint32_t aphase = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-            int l, tm, tn;
-            decode(p.order[t], l, tm, tn);
+        for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            int l, tmp, tn;
+            decode(p.order[t], l, tmp, tn);
+            const int tm = tmp * CG + static_cast<int>(cta_rank);  // 128-row tile index
             const int row0 = tm * kBM;
             const int col0 = tn * kBN;
             const int row = row0 + q * 32 + lane;
@@ -357,7 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(as * kBN);
-            if (MODE != kModeRS) {
+            if (row0 >= p.m) {
+                // Fully out-of-range half of a pair tile: nothing to store or signal.
+            } else if (MODE != kModeRS) {
                 for (int c = 0; c < kBN / 32; ++c) {
                     const int col = col0 + c * 32;
                     if (col >= p.n) break;  // warp-uniform
@@ -395,8 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
 #pragma unroll
                             for (int j = 0; j < 32; j += 4)
                                 d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                        __uint_as_float(r[j + 2]),
-                                                        __uint_as_float(r[j + 3]));
+                                                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
                         }
                     }
                     if (remote) __threadfence_system();
@@ -415,9 +509,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     if (et == 0) {
                         for (int s = 0; s < p.tp; ++s)
                             if (s != me)
-                                wait_flag(p.rs_flags[me] + tile_id * p.tp + s, p.epoch, p, p.ctrl[l],
-                                          kErrRsFlagTimeout, static_cast<uint32_t>(tile_id),
-                                          static_cast<uint32_t>(s));
+                                wait_flag(p.rs_flags[me] + tile_id * p.tp + s, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+                                          static_cast<uint32_t>(tile_id), static_cast<uint32_t>(s));
                     }
                     named_bar_sync(1, 128);
                     const bool owned = valid && owner == me;
@@ -458,7 +551,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[as]);
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(as * 8));
+                else mbar_arrive(&tempty[as]);
+            }
             if (++as == 2) {
                 as = 0;
                 aphase ^= 1u;
@@ -466,10 +562,12 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         }
     }
 
-    __syncthreads();
+    if (CG == 2) cluster_sync();
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, kTmemCols);
+        if (CG == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
+        else tmem_dealloc(tmem_base, kTmemCols);
     }
 }
 
@@ -494,22 +592,49 @@ cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t str
     return cudaGetLastError();
 }
 
-cudaError_t launch_gemm(int mode, const GemmParams& p, int grid, cudaStream_t stream) {
-    static bool configured[3] = {false, false, false};
-    void (*fn)(GemmParams) = nullptr;
-    switch (mode) {
-        case kModePlain: fn = flux_gemm_kernel<kModePlain>; break;
-        case kModeAG: fn = flux_gemm_kernel<kModeAG>; break;
-        case kModeRS: fn = flux_gemm_kernel<kModeRS>; break;
-        default: return cudaErrorInvalidValue;
-    }
-    if (!configured[mode]) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+int gemm_tile_rows(int cg) { return kBM * cg; }
+
+template <int MODE, int CG>
+static cudaError_t launch_one(const GemmParams& p, int grid, cudaStream_t stream) {
+    static bool configured = false;
+    auto fn = flux_gemm_kernel<MODE, CG>;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<CG>::kSmem);
         if (e != cudaSuccess) return e;
-        configured[mode] = true;
+        configured = true;
     }
-    fn<<<grid, kThreads, kSmemBytes, stream>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Geo<CG>::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, p);
+}
+
+cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStream_t stream) {
+    if (cg == 2) {
+        grid &= ~1;
+        if (grid < 2) grid = 2;
+        switch (mode) {
+            case kModePlain: return launch_one<kModePlain, 2>(p, grid, stream);
+            case kModeAG: return launch_one<kModeAG, 2>(p, grid, stream);
+            case kModeRS: return launch_one<kModeRS, 2>(p, grid, stream);
+        }
+    } else {
+        switch (mode) {
+            case kModePlain: return launch_one<kModePlain, 1>(p, grid, stream);
+            case kModeAG: return launch_one<kModeAG, 1>(p, grid, stream);
+            case kModeRS: return launch_one<kModeRS, 1>(p, grid, stream);
+        }
+    }
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace fluxb200

@@ -83,6 +83,25 @@ def test_fused_matches_oracle(case):
         assert comm.last_launch_count() >= 1
 
 
+@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("case", [(AG, 1024, 1024, 512, 4), (AG, 600, 520, 136, 2), (RS, 2048, 768, 512, 4),
+                                  (RS, 1280, 640, 200, 2), (RS, 512, 512, 256, 8)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_single_cta_and_cta_pair_tiles(case, cta_group):
+    """Both MMA variants: one CTA per 128x256 tile (cta_group::1) and CTA pairs
+    sharing 256x256 tiles (cta_group::2), incl. tiles straddling rank blocks."""
+    pat, m, n, k, tp = case
+    p = fx.ProblemSpec(m, n, k, tp, pat)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=77 + m)
+        want = _oracle(p, a, b)
+        got = _run(comm, p, True, cta_group=cta_group)
+        for r in range(tp):
+            assert O.max_rel_error(got[r], want[r]) <= 1e-4, r
+        comm.local_gemm(p, fx.default_opts(out_dtype=fx.F32, cta_group=cta_group))
+        comm.sync()
+
+
 @pytest.mark.parametrize("tp,rpct", [(4, 64), (4, 32), (2, 512), (8, 16)])
 def test_allgather_comm_tile_sizes_and_transfer_modes(tp, rpct):
     """Comm tiles decoupled from GEMM tiles (SPEC §4.3), pull and push."""
