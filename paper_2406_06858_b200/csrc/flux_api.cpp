@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -1013,8 +1014,16 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     for (int r : mine)
         seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct),
                                  kBM * cg);
-    FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct,
-                           oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, cg));
+    auto launch_kernel = [&]() {
+        return launch_groups(c, p, kModeAG, oc, streams, seq, rpct,
+                             oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, cg);
+    };
+    // FLUX_SERIALIZE_TRANSFERS=1 (profiling / diagnosis only): all transfers
+    // complete before the kernel starts, so its flag waits never block (a
+    // profiler replaying the kernel alone cannot re-run the copy engines).
+    const char* ser_env = std::getenv("FLUX_SERIALIZE_TRANSFERS");
+    const bool serialize = ser_env && std::atoi(ser_env) != 0;
+    if (!serialize) FLUX_TRY(launch_kernel());
 
     // ---- Alg. 3: the transfer loop (engine.cpp:367-423) on the copy engines ----
     const size_t shard_pitch = static_cast<size_t>(L.a_shard.ld) * 2;
@@ -1082,13 +1091,23 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         }
         for (int r : g) FLUX_TRY(write_value(cs, c->ranks[r].heap + kCtrlDone, e));
         FLUX_CUDA(cudaEventRecord(lead.copy_evt, cs));
+    }
+    if (serialize) {
+        for (const auto& g : groups)
+            for (int r : g) {
+                FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
+                FLUX_CUDA(cudaStreamWaitEvent(stream_for(c, r, streams), c->ranks[g[0]].copy_evt, 0));
+            }
+        FLUX_TRY(launch_kernel());
+    }
+    for (const auto& g : groups)
         for (int r : g) {
+            FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
             cudaStream_t s = stream_for(c, r, streams);
             FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlKdone, e));
             // Later work on the caller's stream is ordered after our transfers.
-            FLUX_CUDA(cudaStreamWaitEvent(s, lead.copy_evt, 0));
+            FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[g[0]].copy_evt, 0));
         }
-    }
     return FLUX_OK;
 }
 

@@ -250,22 +250,25 @@ __device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo, uint32_t hi) {
 }
 
 // Store 32 fp32 accumulators of one row (cols [col, col+32)) to C.
-__device__ __forceinline__ void store_row32(void* c, long long off, int col, int n, int out_f32,
-                                            const float (&v)[32]) {
+// Store W fp32 accumulators of one row (cols [col, col+W)) to C as bf16 or fp32.
+template <int W>
+__device__ __forceinline__ void store_row(void* c, long long off, int col, int n, int out_f32, const float (&v)[W]) {
     if (out_f32) {
         float* dst = static_cast<float*>(c) + off;
-        if (col + 32 <= n) {
+        if (col + W <= n) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
+            for (int j = 0; j < W; j += 4)
                 *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         } else {
-            for (int j = 0; j < 32 && col + j < n; ++j) dst[j] = v[j];
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                if (col + j < n) dst[j] = v[j];
         }
     } else {
         __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(c) + off;
-        if (col + 32 <= n) {
+        if (col + W <= n) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
+            for (int j = 0; j < W; j += 8) {
                 uint4 w;
                 w.x = pack_bf16x2(__float_as_uint(v[j + 0]), __float_as_uint(v[j + 1]));
                 w.y = pack_bf16x2(__float_as_uint(v[j + 2]), __float_as_uint(v[j + 3]));
@@ -274,7 +277,9 @@ __device__ __forceinline__ void store_row32(void* c, long long off, int col, int
                 *reinterpret_cast<uint4*>(dst + j) = w;
             }
         } else {
-            for (int j = 0; j < 32 && col + j < n; ++j) dst[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                if (col + j < n) dst[j] = __float2bfloat16_rn(v[j]);
         }
     }
 }
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         float v[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                        store_row32(p.c[l], static_cast<long long>(row) * p.ldc + col, col, p.n,
+                        store_row<32>(p.c[l], static_cast<long long>(row) * p.ldc + col, col, p.n,
                                     p.out_f32, v);
                     }
                 }
@@ -524,26 +529,43 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                             tmem_ld32(tbase + c * 32, r);
                             tmem_ld_wait();
                             if (owned) {
-                                float acc[32];
+                                // Two 16-column halves; each issues every source's
+                                // loads before summing (memory-level parallelism),
+                                // then adds in source order 0..tp-1 (deterministic).
 #pragma unroll
-                                for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-                                for (int s = 0; s < p.tp; ++s) {
-                                    if (s == me) {
+                                for (int h = 0; h < 2; ++h) {
+                                    float4 v[kMaxRanks][4];
 #pragma unroll
-                                        for (int j = 0; j < 32; ++j) acc[j] += __uint_as_float(r[j]);
-                                    } else {
-                                        const float* src = src0 + s * p.stage_plane + col;
+                                    for (int s = 0; s < kMaxRanks; ++s) {
+                                        if (s < p.tp && s != me) {
+                                            const float* src = src0 + s * p.stage_plane + col + h * 16;
 #pragma unroll
-                                        for (int j = 0; j < 32; j += 4) {
-                                            const float4 v = ld_cg_f4(src + j);
-                                            acc[j] += v.x;
-                                            acc[j + 1] += v.y;
-                                            acc[j + 2] += v.z;
-                                            acc[j + 3] += v.w;
+                                            for (int j = 0; j < 4; ++j) v[s][j] = ld_cg_f4(src + 4 * j);
                                         }
                                     }
+                                    float acc[16];
+#pragma unroll
+                                    for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
+#pragma unroll
+                                    for (int s = 0; s < kMaxRanks; ++s) {
+                                        if (s < p.tp) {
+                                            if (s == me) {
+#pragma unroll
+                                                for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(r[h * 16 + j]);
+                                            } else {
+#pragma unroll
+                                                for (int j = 0; j < 4; ++j) {
+                                                    acc[4 * j] += v[s][j].x;
+                                                    acc[4 * j + 1] += v[s][j].y;
+                                                    acc[4 * j + 2] += v[s][j].z;
+                                                    acc[4 * j + 3] += v[s][j].w;
+                                                }
+                                            }
+                                        }
+                                    }
+                                    store_row<16>(p.c[l], lrow * p.ldc + col + h * 16, col + h * 16, p.n,
+                                                  p.out_f32, acc);
                                 }
-                                store_row32(p.c[l], lrow * p.ldc + col, col, p.n, p.out_f32, acc);
                             }
                         }
                     }
