@@ -1,0 +1,211 @@
+// flux/overlap.hpp — C++ drop-in for the reference operator API
+// (namespace overlap, /root/reference/proj/core/include/overlap/*.hpp),
+// executed by the B200 kernels behind the C ABI in flux_b200.h.
+//
+// A caller of the reference keeps its code: build a ProblemSpec and a
+// ShardedWorkspace, call run_fused_allgather_gemm / run_fused_gemm_reducescatter
+// / run_nonoverlap, compare with max_rel_error. What changes:
+//   * compute is bf16 x bf16 -> fp32 on tensor cores: inputs are rounded to
+//     bf16 on upload, outputs come back as fp32 (reported as double). Verify
+//     with the B200 tolerance (8e-3 bf16 / 1e-4 fp32 accumulate),
+//     not the reference's fp64 1e-8;
+//   * ranks run on GPUs: FLUX_DEVICES="0,1,..." picks them, otherwise ranks
+//     0..tp-1 map to devices 0..tp-1 when that many exist, else every rank is
+//     emulated on device 0 (the reference's threads-as-ranks model);
+//   * EngineOptions::workers_per_rank / poll_budget are accepted and ignored
+//     (the device uses every SM; waits are bounded by wall_budget_s).
+// Errors surface as the same exception types (reference errors.hpp).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace overlap {
+
+// ---- errors (reference errors.hpp) -------------------------------------------
+#define FLUX_OVERLAP_ERROR(Name)                                              \
+    struct Name : std::runtime_error {                                        \
+        explicit Name(const std::string& what) : std::runtime_error(what) {}  \
+    };
+FLUX_OVERLAP_ERROR(ConfigError)
+FLUX_OVERLAP_ERROR(ShapeError)
+FLUX_OVERLAP_ERROR(DirectoryError)
+FLUX_OVERLAP_ERROR(DeadlockError)
+FLUX_OVERLAP_ERROR(BoundsError)
+#undef FLUX_OVERLAP_ERROR
+
+// ---- host matrices and the reference input stream (reference matrix.hpp) -------
+class Matrix {
+public:
+    Matrix() = default;
+    Matrix(int rows, int cols, double init = 0.0) : r_(rows), c_(cols), v_(size_t(rows) * cols, init) {}
+    int rows() const { return r_; }
+    int cols() const { return c_; }
+    bool empty() const { return v_.empty(); }
+    double& operator()(int i, int j) { return v_[size_t(i) * c_ + j]; }
+    double operator()(int i, int j) const { return v_[size_t(i) * c_ + j]; }
+    double* row_ptr(int i) { return v_.data() + size_t(i) * c_; }
+    const double* row_ptr(int i) const { return v_.data() + size_t(i) * c_; }
+    std::vector<double>& data() { return v_; }
+    const std::vector<double>& data() const { return v_; }
+    void fill(double x) { v_.assign(v_.size(), x); }
+    bool same_shape(const Matrix& o) const { return r_ == o.r_ && c_ == o.c_; }
+
+private:
+    int r_ = 0, c_ = 0;
+    std::vector<double> v_;
+};
+
+double max_rel_error(const Matrix& a, const Matrix& b);
+bool approx_equal(const Matrix& a, const Matrix& b, double rel_tol);
+bool bitwise_equal(const Matrix& a, const Matrix& b);
+
+// splitmix64, uniform in [-1, 1): the stream the reference fills workspaces with.
+class Rng {
+public:
+    explicit Rng(uint64_t seed) : s_(seed ? seed : 0x9e3779b97f4a7c15ull) {}
+    uint64_t next_u64();
+    double next_uniform();
+    uint64_t next_below(uint64_t n) { return next_u64() % n; }
+
+private:
+    uint64_t s_;
+};
+void fill_uniform(Matrix& m, Rng& rng);
+
+// ---- problem and tiling (reference problem.hpp) --------------------------------
+enum class Pattern { AllGatherGemm, GemmReduceScatter };
+std::string to_string(Pattern p);
+Pattern pattern_from_string(const std::string& s);
+
+struct ProblemSpec {
+    int m = 0, n = 0, k = 0, tp = 1;
+    Pattern pattern = Pattern::AllGatherGemm;
+    void validate() const;
+    int rows_per_rank() const { return m / tp; }
+    int local_cols() const { return pattern == Pattern::AllGatherGemm ? n / tp : n; }
+    int local_k() const { return pattern == Pattern::GemmReduceScatter ? k / tp : k; }
+    int owner_of_row(int row) const { return row / rows_per_rank(); }
+};
+
+struct TileShape {
+    int tm = 0, tn = 0;
+};
+struct TileCoord {
+    int row = 0, col = 0;
+    bool operator==(const TileCoord& o) const { return row == o.row && col == o.col; }
+};
+struct GridDims {
+    int tile_rows = 0, tile_cols = 0, row_blocks = 0;
+    int tiles() const { return tile_rows * tile_cols; }
+    int tile_rows_per_block() const { return tile_rows / row_blocks; }
+};
+void validate_tiling(const ProblemSpec& problem, const TileShape& tile);
+GridDims grid_for(const ProblemSpec& problem, const TileShape& tile);
+std::vector<TileCoord> tile_grid(const ProblemSpec& problem, const TileShape& tile);
+
+// ---- communication order (reference topology.hpp; one NVSwitch node) -----------
+enum class TopologyKind { NVLinkRing };
+struct Topology {
+    TopologyKind kind = TopologyKind::NVLinkRing;
+    void validate(int /*tp*/) const {}
+};
+enum class LinkClass { IntraNuma, InterNuma, InterNode, Forward };
+struct TransferDesc {
+    int peer = -1, row_begin = 0, rows = 0;
+    LinkClass link = LinkClass::IntraNuma;
+    int dep_rank = -1, dep_index = -1;
+};
+std::vector<TransferDesc> comm_order(const Topology& topology, int rank, int tp, int rows_per_rank,
+                                     int rows_per_comm_tile, bool ring_forwarding = false);
+std::vector<int> peer_order(const std::vector<TransferDesc>& order, int rank, int rows_per_rank);
+
+// ---- tile swizzle (reference swizzle.hpp) --------------------------------------
+enum class SwizzleKind { Naive, RankShifted, ArrivalAligned };
+struct SwizzlePolicy {
+    SwizzleKind kind = SwizzleKind::Naive;
+    int rank = 0, tp = 1, shift_offset = 1;
+    std::vector<int> arrival_blocks;
+};
+SwizzlePolicy arrival_aligned_policy(int rank, int tp, const std::vector<TransferDesc>& order, int rows_per_rank);
+TileCoord map_tile(const SwizzlePolicy& policy, int flat_index, const GridDims& grid);
+std::vector<TileCoord> tile_order(const SwizzlePolicy& policy, const GridDims& grid);
+
+// ---- workspace (reference workspace.hpp): host mirror of the symmetric heaps ----
+struct RankBuffers {
+    Matrix a_shard, b_shard, a_agg, c_out;
+    std::vector<Matrix> staging;
+};
+
+class ShardedWorkspace {
+public:
+    static ShardedWorkspace make_random(const ProblemSpec& problem, uint64_t seed);
+    void validate(const ProblemSpec& problem) const;
+    RankBuffers& rank(int r) { return ranks_[r]; }
+    const RankBuffers& rank(int r) const { return ranks_[r]; }
+    int num_ranks() const { return static_cast<int>(ranks_.size()); }
+    RankBuffers& peer(int from_rank, int peer_rank);
+    void drop_directory_entry(int from_rank, int peer_rank);  // tests: incomplete init-phase exchange
+    void clear_outputs();
+    const std::vector<std::pair<int, int>>& dropped() const { return dropped_; }
+
+private:
+    std::vector<RankBuffers> ranks_;
+    std::vector<std::pair<int, int>> dropped_;
+};
+
+// ---- engine (reference engine.hpp) ----------------------------------------------
+enum class TransferMode { Pull, Push };
+enum class WriteMode { WriteAlltoAll, FusedReduce };
+std::string to_string(TransferMode m);
+TransferMode transfer_mode_from_string(const std::string& s);
+std::string to_string(WriteMode m);
+WriteMode write_mode_from_string(const std::string& s);
+
+struct CommTileSpec {
+    int rows_per_comm_tile = 0;
+    std::vector<TransferDesc> order;
+    void validate(const ProblemSpec& problem, int rank, TransferMode mode) const;
+};
+std::vector<CommTileSpec> make_comm_specs(const ProblemSpec& problem, const Topology& topology,
+                                          int rows_per_comm_tile, TransferMode mode);
+
+struct CausalityEvent {
+    std::string kind;
+    int rank = -1, tile_row = -1, tile_col = -1, target = -1;
+    uint64_t logical_ts = 0;
+    int64_t wall_ns = 0;
+};
+
+struct EngineOptions {
+    int workers_per_rank = 0;
+    bool deterministic_reduce = true;
+    long long poll_budget = 10'000'000;
+    double wall_budget_s = 10.0;
+    uint64_t interleave_seed = 0;
+    int shift_offset = 1;
+};
+
+struct EngineResult {
+    std::vector<Matrix> outputs;
+    std::vector<CausalityEvent> log;
+};
+
+struct TransferRecord {
+    TransferDesc desc;
+    int64_t copy_done_ns = 0, flag_set_ns = 0;
+    uint64_t copy_logical_ts = 0, flag_logical_ts = 0;
+};
+
+EngineResult run_fused_gemm_reducescatter(const ProblemSpec& problem, ShardedWorkspace& workspace,
+                                          const TileShape& tile, WriteMode write_mode, bool swizzle_on,
+                                          const EngineOptions& opts = {});
+EngineResult run_fused_allgather_gemm(const ProblemSpec& problem, ShardedWorkspace& workspace, const TileShape& tile,
+                                      const std::vector<CommTileSpec>& comm, TransferMode transfer, bool swizzle_on,
+                                      const EngineOptions& opts = {},
+                                      std::vector<std::vector<TransferRecord>>* traces = nullptr);
+std::vector<Matrix> run_nonoverlap(const ProblemSpec& problem, ShardedWorkspace& workspace, const TileShape& tile);
+
+}  // namespace overlap

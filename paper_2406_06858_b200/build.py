@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libflux_b200.so")
 
-SOURCES = ["flux_kernels.cu", "flux_api.cpp"]
+SOURCES = ["flux_kernels.cu", "flux_api.cpp", "flux_shim.cpp"]
 HEADERS = ["flux_internal.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
