@@ -500,6 +500,7 @@ int choose_cg(const flux_problem* p, const flux_opts& o) {
 struct OpCommon {
     flux_opts o;
     uint64_t timeout_ns;
+    int fused_reduce = 0;  // RS FusedReduce in arrival order (red.add into the owner accumulator)
 };
 
 OpCommon common_opts(const flux_opts* opts) {
@@ -543,6 +544,9 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             for (int r = 0; r < c->tp; ++r) {
                 prm.staging[r] = reinterpret_cast<float*>(c->ranks[r].heap + L.staging.off);
                 prm.rs_flags[r] = at<uint32_t>(c->ranks[r], kRsFlagOffset);
+                prm.fr_acc[r] = reinterpret_cast<float*>(c->ranks[r].heap + L.staging.off +
+                                                         static_cast<size_t>(c->epoch & 1u) * L.stage_parity * 4);
+                prm.fr_ready[r] = at<uint32_t>(c->ranks[r], kCtrlFrReady);
             }
         }
         // Interleave the per-rank sequences into one device schedule.
@@ -592,6 +596,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.epoch = c->epoch;
         prm.timeout_ns = oc.timeout_ns;
         prm.jitter_seed = oc.o.interleave_seed;
+        prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
         // Join the other local ranks' streams into the launch stream.
         for (size_t li = 0; li < g.size(); ++li) {
             cudaStream_t s = stream_for(c, g[li], streams);
@@ -1132,6 +1137,23 @@ int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     c->kernel_events_used = 0;
     ++c->epoch;
     const int cg = choose_cg(p, oc.o);
+    // FusedReduce (engine.cpp:304-319, arrival-order accumulation): sources red.add
+    // into the owner's fp32 accumulator. Deterministic FusedReduce (rank-ordered
+    // gate, :293-303) is served by the source-ordered owner sum, which gives the
+    // same result order without serialising the ranks.
+    if (write_mode == FLUX_FUSED_REDUCE && !oc.o.deterministic_reduce) {
+        oc.fused_reduce = 1;
+        const Layout L = layout_for(p);
+        const uint32_t e = c->epoch;
+        for (int r : mine) {
+            RankState& rs = c->ranks[r];
+            FLUX_CUDA(cudaSetDevice(rs.device));
+            cudaStream_t s = stream_for(c, r, streams);
+            FLUX_CUDA(cudaMemsetAsync(rs.heap + L.staging.off + static_cast<size_t>(e & 1u) * L.stage_parity * 4, 0,
+                                      static_cast<size_t>(L.stage_plane) * 4, s));
+            FLUX_TRY(write_value(s, rs.heap + kCtrlFrReady, e));
+        }
+    }
     // Tile order: RankShifted (local block last) or Naive (engine.cpp:210-217,256-261).
     std::vector<std::vector<uint32_t>> seq(tp);
     for (int r : mine) {

@@ -30,6 +30,7 @@ constexpr size_t kCtrlErr = 0;          // u32[4]: code, info0, info1, info2
 constexpr size_t kCtrlReady = 64;       // u32: epoch at which this rank's A shard is staged (AG pull source ready)
 constexpr size_t kCtrlDone = 68;        // u32: epoch whose peer pulls this rank has finished
 constexpr size_t kCtrlKdone = 72;       // u32: epoch whose kernel finished on this rank (push targets)
+constexpr size_t kCtrlFrReady = 76;     // u32: epoch whose FusedReduce accumulator is zeroed (RS FusedReduce)
 constexpr size_t kAgFlagOffset = 4096;  // u32[kAgFlagCap]: one flag per comm tile (SignalBoard)
 constexpr size_t kAgFlagCap = 32768;
 constexpr size_t kRsFlagOffset = 256 * 1024;  // u32[tile][src]: partial of tile from src landed
@@ -68,6 +69,9 @@ struct GemmParams {
     uint32_t epoch;
     unsigned long long timeout_ns;
     unsigned long long jitter_seed;
+    int fused_reduce;              // RS: 1 = red.add into the owner accumulator (arrival order)
+    float* fr_acc[kMaxRanks];      // per GLOBAL rank: FusedReduce fp32 accumulator [rpr, ld_stage] (this parity)
+    const uint32_t* fr_ready[kMaxRanks];  // per GLOBAL rank: control word, accumulator zeroed at epoch
 };
 
 struct RsReduceParams {

@@ -210,6 +210,10 @@ __device__ __forceinline__ float4 ld_cg_f4(const float* p) {
                  : "l"(p));
     return v;
 }
+__device__ __forceinline__ void red_add_f4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -478,12 +482,26 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 const int owner = valid ? row / p.rpr : -1;
                 const bool remote = valid && owner != me;
                 const int tile_id = tm * p.tiles_n + tn;
-                // Phase 1: ship remote rows to their owners' staging planes (Alg. 1 line 5).
+                const int rlast = min(row0 + kBM, p.m) - 1;
+                const int o0 = row0 / p.rpr, o1 = rlast / p.rpr;
+                if (p.fused_reduce) {
+                    // FusedReduce: each owner zeroes this parity's accumulator on its
+                    // stream before the launch and stamps fr_ready; wait for that once.
+                    if (et <= o1 - o0 && o0 + et != me)
+                        wait_flag(p.fr_ready[o0 + et], p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+                                  static_cast<uint32_t>(tile_id), static_cast<uint32_t>(o0 + et));
+                    named_bar_sync(1, 128);
+                }
+                // Phase 1: ship remote rows to their owners (Alg. 1 line 5): plain stores
+                // into the owner's staging plane for this source (WriteAlltoAll), or
+                // vector red.add into the owner's fp32 accumulator (FusedReduce).
                 if (__any_sync(0xffffffffu, remote)) {
                     float* dst = nullptr;
                     if (remote)
-                        dst = p.staging[owner] + parity * p.stage_parity + me * p.stage_plane +
-                              static_cast<long long>(row - owner * p.rpr) * p.ld_stage;
+                        dst = p.fused_reduce
+                                  ? p.fr_acc[owner] + static_cast<long long>(row - owner * p.rpr) * p.ld_stage
+                                  : p.staging[owner] + parity * p.stage_parity + me * p.stage_plane +
+                                        static_cast<long long>(row - owner * p.rpr) * p.ld_stage;
                     for (int c = 0; c < kBN / 32; ++c) {
                         const int col = col0 + c * 32;
                         if (col >= p.n) break;
@@ -491,19 +509,24 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         tmem_ld32(tbase + c * 32, r);
                         tmem_ld_wait();
                         if (remote) {
-                            float4* d4 = reinterpret_cast<float4*>(dst + col);
+                            if (p.fused_reduce) {
 #pragma unroll
-                            for (int j = 0; j < 32; j += 4)
-                                d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                                for (int j = 0; j < 32; j += 4)
+                                    red_add_f4(dst + col + j, __uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                               __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                            } else {
+                                float4* d4 = reinterpret_cast<float4*>(dst + col);
+#pragma unroll
+                                for (int j = 0; j < 32; j += 4)
+                                    d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                            }
                         }
                     }
                     if (remote) __threadfence_system();
                 }
                 named_bar_sync(1, 128);
                 // Signal each owner in this tile that our partial landed.
-                const int rlast = min(row0 + kBM, p.m) - 1;
-                const int o0 = row0 / p.rpr, o1 = rlast / p.rpr;
                 if (et <= o1 - o0) {
                     const int o = o0 + et;
                     if (o != me) st_release_sys(p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
@@ -519,7 +542,30 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     }
                     named_bar_sync(1, 128);
                     const bool owned = valid && owner == me;
-                    if (__any_sync(0xffffffffu, owned)) {
+                    if (p.fused_reduce && __any_sync(0xffffffffu, owned)) {
+                        // Remote contributions already summed (arrival order) in the accumulator.
+                        const float* acc_row = p.fr_acc[me] + static_cast<long long>(row - me * p.rpr) * p.ld_stage;
+                        for (int c = 0; c < kBN / 32; ++c) {
+                            const int col = col0 + c * 32;
+                            if (col >= p.n) break;
+                            uint32_t r[32];
+                            tmem_ld32(tbase + c * 32, r);
+                            tmem_ld_wait();
+                            if (owned) {
+                                float acc[32];
+#pragma unroll
+                                for (int j = 0; j < 32; j += 4) {
+                                    const float4 v = ld_cg_f4(acc_row + col + j);
+                                    acc[j] = v.x + __uint_as_float(r[j]);
+                                    acc[j + 1] = v.y + __uint_as_float(r[j + 1]);
+                                    acc[j + 2] = v.z + __uint_as_float(r[j + 2]);
+                                    acc[j + 3] = v.w + __uint_as_float(r[j + 3]);
+                                }
+                                store_row<32>(p.c[l], static_cast<long long>(row - me * p.rpr) * p.ldc + col, col,
+                                              p.n, p.out_f32, acc);
+                            }
+                        }
+                    } else if (__any_sync(0xffffffffu, owned)) {
                         const long long lrow = row - me * p.rpr;
                         const float* src0 = p.staging[me] + parity * p.stage_parity + lrow * p.ld_stage;
                         for (int c = 0; c < kBN / 32; ++c) {

@@ -19,14 +19,17 @@ static void check(bool ok, const std::string& what) {
 }
 
 // fp64 oracle on bf16-rounded inputs (what the tensor cores consume).
+// Round-to-nearest-even of the double itself (exact rational comparison via
+// frexp; no double rounding through float).
 static double bf16(double x) {
-    float f = static_cast<float>(x);
-    uint32_t u;
-    std::memcpy(&u, &f, 4);
-    uint32_t lsb = (u >> 16) & 1u;
-    u = (u + 0x7FFFu + lsb) & 0xFFFF0000u;
-    std::memcpy(&f, &u, 4);
-    return f;
+    if (x == 0.0) return x;
+    int e;
+    const double mant = std::frexp(std::fabs(x), &e);  // [0.5, 1)
+    const double scaled = mant * 256.0;                // 8 significant bits
+    double lo = std::floor(scaled);
+    const double frac = scaled - lo;
+    if (frac > 0.5 || (frac == 0.5 && std::fmod(lo, 2.0) == 1.0)) lo += 1.0;
+    return std::copysign(std::ldexp(lo / 256.0, e), x);
 }
 static std::vector<Matrix> oracle(const ProblemSpec& p, const ShardedWorkspace& ws) {
     std::vector<Matrix> out;

@@ -142,6 +142,24 @@ def test_reduce_scatter_is_deterministic_across_runs_and_orders():
             assert O.max_rel_error(nonov[r], want[r]) <= 1e-4
 
 
+@pytest.mark.parametrize("case", [(2048, 1024, 1024, 8), (1024, 512, 768, 4), (40, 24, 72, 4), (384, 256, 128, 2)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_fused_reduce_arrival_order(case):
+    """FusedReduce with deterministic_reduce=False (engine.cpp:304-319): vector
+    red.add into the owner's fp32 accumulator; mixed back to back with
+    WriteAlltoAll on the same communicator (epoch parity reuse)."""
+    m, n, k, tp = case
+    p = fx.ProblemSpec(m, n, k, tp, RS)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=5 + m)
+        want = _oracle(p, a, b)
+        for mode in (fx.FUSED_REDUCE, fx.WRITE_ALLTOALL, fx.FUSED_REDUCE, fx.FUSED_REDUCE):
+            for f32 in (True, False):
+                got = _run(comm, p, f32, write_mode=mode, deterministic_reduce=0)
+                for r in range(tp):
+                    assert O.max_rel_error(got[r], want[r]) <= H.tol(f32), (mode, f32, r)
+
+
 def test_nonoverlap_baseline_allgather():
     p = fx.ProblemSpec(512, 1024, 256, 4, AG)
     with H.make_comm(p) as comm:
