@@ -131,7 +131,7 @@ def lib() -> C.CDLL:
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python -m paper_2406_06858_b200.build` "
                 "(the fused operators have no CPU fallback)")
-        l = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        l = C.CDLL(LIB_PATH, mode=C.RTLD_LOCAL)
         for name, (res, args) in _SIGS.items():
             fn = getattr(l, name)
             fn.restype = res
