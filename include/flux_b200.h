@@ -89,6 +89,8 @@ typedef struct {
     int emulated_order;        /* several ranks on one device: 0 locality-first (rank-major,
                                   RS own blocks last), 1 position-major across ranks */
     int cta_group;             /* 0 auto, 1 = 128x256 tiles per CTA, 2 = CTA pairs (256x256, cta_group::2) */
+    int ag_engine;             /* AllGather transfers: 0 auto, 1 copy engines (stream memcpy + flag
+                                  writes), 2 in-kernel (TMA bulk copies by the GEMM's SMs, Pull) */
 } flux_opts;
 
 typedef struct {

@@ -66,7 +66,7 @@ class Opts(C.Structure):
     _fields_ = [("workers_per_rank", C.c_int), ("deterministic_reduce", C.c_int),
                 ("poll_budget", C.c_longlong), ("wall_budget_s", C.c_double),
                 ("interleave_seed", C.c_uint64), ("shift_offset", C.c_int), ("out_dtype", C.c_int),
-                ("emulated_order", C.c_int), ("cta_group", C.c_int)]
+                ("emulated_order", C.c_int), ("cta_group", C.c_int), ("ag_engine", C.c_int)]
 
 
 class CommOpts(C.Structure):

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -56,6 +57,7 @@ struct Driver {
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     PFN_cuStreamWriteValue32_v11070 write32 = nullptr;
     PFN_cuStreamWaitValue32_v11070 wait32 = nullptr;
+    PFN_cuMemsetD32Async_v3020 memset32 = nullptr;
     bool ok = false;
 };
 
@@ -74,7 +76,10 @@ Driver& driver() {
         if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
             d.wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fn);
-        d.ok = d.encode && d.write32 && d.wait32;
+        if (cudaGetDriverEntryPoint("cuMemsetD32Async", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            d.memset32 = reinterpret_cast<PFN_cuMemsetD32Async_v3020>(fn);
+        d.ok = d.encode && d.write32 && d.wait32 && d.memset32;
     });
     return d;
 }
@@ -515,7 +520,8 @@ OpCommon common_opts(const flux_opts* opts) {
 // Launch one fused kernel per device group. `mode` selects the role.
 int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon& oc, void* const* streams,
                   const std::vector<std::vector<uint32_t>>& seq_of_rank, int rpct, int interleave,
-                  int cg, bool plain_on_agg = false, long long partial_off = -1, int rs_tail = 0) {
+                  int cg, bool plain_on_agg = false, long long partial_off = -1, int rs_tail = 0,
+                  const std::function<int(const std::vector<int>&, GemmParams&)>& extra = nullptr) {
     const bool plain_f32_to_staging = partial_off >= 0;
     const Layout L = layout_for(p);
     const int lk = local_k(p), lc = local_cols(p);
@@ -605,6 +611,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 FLUX_CUDA(cudaStreamWaitEvent(lead, c->ranks[g[li]].start_evt, 0));
             }
         }
+        if (extra) FLUX_TRY(extra(g, prm));
         const int grid = cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
         std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
         if (c->timing) {
@@ -662,6 +669,7 @@ void flux_default_opts(flux_opts* o) {
     o->out_dtype = FLUX_BF16;
     o->emulated_order = 0;
     o->cta_group = 0;
+    o->ag_engine = 0;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -995,6 +1003,91 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     const uint32_t e = ++c->epoch;
     const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
     const int lk = local_k(p);
+
+    // ---- transfer engine: copy engines (Alg. 3 on a stream) or the GEMM's own
+    // SMs (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies) ----
+    const bool sm_ok = transfer == FLUX_PULL && lk % 8 == 0 && (p->m + kBM - 1) / kBM <= static_cast<int>(kAgGroupCap);
+    if (oc.o.ag_engine == 2 && !sm_ok)
+        return fail(FLUX_ERR_CONFIG, "in-kernel AllGather transfer needs Pull and k % 8 == 0");
+    const bool use_sm = oc.o.ag_engine == 2 ||
+                        (oc.o.ag_engine == 0 && sm_ok && static_cast<size_t>(p->m) * lk * 2 <= (size_t(32) << 20));
+    if (use_sm) {
+        const int cg = choose_cg(p, oc.o);
+        const int groups = (p->m + kBM - 1) / kBM;
+        const size_t ctr_off = kAgCtrOffset + static_cast<size_t>(e & 1u) * kAgGroupCap * 4;
+        // Piece geometry: whole contiguous rows up to kPieceBytes, or column splits of long rows.
+        const int row_bytes = lk * 2;
+        int piece_rows = 1, pieces_per_row = (row_bytes + kPieceBytes - 1) / kPieceBytes;
+        if (row_bytes <= kPieceBytes && L.a_shard.ld == lk && L.a_agg.ld == lk) {
+            pieces_per_row = 1;
+            while (piece_rows * 2 <= kBM && piece_rows * 2 * row_bytes <= kPieceBytes && rpr % (piece_rows * 2) == 0)
+                piece_rows *= 2;
+        }
+        for (int r : mine) {
+            RankState& rs = c->ranks[r];
+            FLUX_CUDA(cudaSetDevice(rs.device));
+            cudaStream_t s = stream_for(c, r, streams);
+            // WAR: remote peers finished pulling my a_agg slot of the previous operator.
+            for (int q = 0; q < tp; ++q)
+                if (q != r && !c->ranks[q].local) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
+            // Stamp this parity's piece counters with the epoch.
+            CUresult cr = driver().memset32(reinterpret_cast<CUdeviceptr>(rs.heap + ctr_off), e << 16,
+                                            static_cast<size_t>(groups), reinterpret_cast<CUstream>(s));
+            if (cr != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "cuMemsetD32Async failed (" + S(cr) + ")");
+        }
+        std::vector<std::vector<uint32_t>> seq(tp);
+        std::vector<std::vector<int>> blocks(tp);
+        for (int r : mine) {
+            blocks[r] = ag_block_order(p, r, FLUX_PULL, swizzle_on != 0, rpct);
+            seq[r] = device_sequence(p->m, local_cols(p), rpr, swizzle_on ? blocks[r] : std::vector<int>{}, kBM * cg);
+        }
+        const bool step_major = oc.o.emulated_order == 1;
+        auto extra = [&](const std::vector<int>& g, GemmParams& prm) -> int {
+            // Piece table in consumption order: every slot's own block first (peers
+            // copy from it), then the others in the order the tiles need them.
+            std::vector<uint32_t> jobs;
+            auto add_block = [&](int li, int b) {
+                for (int row = b * rpr; row < (b + 1) * rpr; row += piece_rows)
+                    jobs.push_back((uint32_t(li) << 28) | (uint32_t(b) << 24) | uint32_t(row));
+            };
+            for (size_t li = 0; li < g.size(); ++li) add_block(static_cast<int>(li), g[li]);
+            if (step_major) {
+                for (int step = 1; step < tp; ++step)
+                    for (size_t li = 0; li < g.size(); ++li) add_block(static_cast<int>(li), blocks[g[li]][step]);
+            } else {
+                for (size_t li = 0; li < g.size(); ++li)
+                    for (int step = 1; step < tp; ++step) add_block(static_cast<int>(li), blocks[g[li]][step]);
+            }
+            uint32_t* jobs_dev = nullptr;
+            FLUX_TRY(upload_order(c, c->ranks[g[0]].device, jobs, &jobs_dev));
+            prm.sm_transfer = 1;
+            prm.jobs = jobs_dev;
+            prm.num_jobs = static_cast<int>(jobs.size());
+            prm.piece_rows = piece_rows;
+            prm.pieces_per_row = pieces_per_row;
+            prm.row_bytes = row_bytes;
+            prm.src_ld_bytes = static_cast<long long>(L.a_shard.ld) * 2;
+            prm.dst_ld_bytes = static_cast<long long>(L.a_agg.ld) * 2;
+            for (int q = 0; q < tp; ++q) {
+                prm.agg_src[q] = c->ranks[q].heap + L.a_agg.off;
+                prm.ag_ctr[q] = at<uint32_t>(c->ranks[q], ctr_off);
+            }
+            for (size_t li = 0; li < g.size(); ++li) {
+                prm.shard_src[li] = c->ranks[g[li]].heap + L.a_shard.off;
+                prm.a_dst[li] = c->ranks[g[li]].heap + L.a_agg.off;
+            }
+            return FLUX_OK;
+        };
+        FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, step_major ? kInterleaveStep : kInterleaveRank,
+                               cg, false, -1, 0, extra));
+        for (int r : mine) {
+            FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
+            cudaStream_t s = stream_for(c, r, streams);
+            FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlDone, e));  // my pulls of this epoch are done
+            FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlKdone, e));
+        }
+        return FLUX_OK;
+    }
 
     // One copy-engine stream per device (several blocked stream-wait memops on
     // many streams can starve each other on shared hardware queues). It starts

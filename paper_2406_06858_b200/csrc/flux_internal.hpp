@@ -32,7 +32,12 @@ constexpr size_t kCtrlDone = 68;        // u32: epoch whose peer pulls this rank
 constexpr size_t kCtrlKdone = 72;       // u32: epoch whose kernel finished on this rank (push targets)
 constexpr size_t kCtrlFrReady = 76;     // u32: epoch whose FusedReduce accumulator is zeroed (RS FusedReduce)
 constexpr size_t kAgFlagOffset = 4096;  // u32[kAgFlagCap]: one flag per comm tile (SignalBoard)
-constexpr size_t kAgFlagCap = 32768;
+constexpr size_t kAgFlagCap = 16384;
+// In-kernel AllGather: u32[2 parities][kAgGroupCap] piece counters per 128-row
+// group of a_agg, stamped (epoch << 16) at operator start, +1 per landed piece.
+constexpr size_t kAgCtrOffset = 128 * 1024;
+constexpr size_t kAgGroupCap = 16384;
+constexpr int kPieceBytes = 16384;      // one TMA bulk copy (global -> smem -> global)
 constexpr size_t kRsFlagOffset = 256 * 1024;  // u32[tile][src]: partial of tile from src landed
 constexpr size_t kRsFlagCap = (768 * 1024) / 4;
 constexpr size_t kDataOffset = 1 << 20;
@@ -70,6 +75,18 @@ struct GemmParams {
     unsigned long long timeout_ns;
     unsigned long long jitter_seed;
     int fused_reduce;              // RS: 1 = red.add into the owner accumulator (arrival order)
+    // AG in-kernel transfer (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies)
+    int sm_transfer;
+    const uint32_t* jobs;          // (slot << 28) | (src rank << 24) | first row of the piece chunk
+    int num_jobs;
+    int piece_rows;                // rows per piece chunk (contiguous rows), >= 1
+    int pieces_per_row;            // column splits of one row (row bytes > kPieceBytes)
+    int row_bytes;                 // k * 2
+    long long src_ld_bytes, dst_ld_bytes;  // A shard / a_agg row pitch in bytes
+    const char* agg_src[kMaxRanks];    // per GLOBAL rank: its a_agg (peer pointers; pull source)
+    const char* shard_src[kMaxRanks];  // per local slot: its own A shard (local piece source)
+    char* a_dst[kMaxRanks];            // per local slot: its a_agg
+    uint32_t* ag_ctr[kMaxRanks];   // per GLOBAL rank: piece counters of this parity (peer pointers)
     float* fr_acc[kMaxRanks];      // per GLOBAL rank: FusedReduce fp32 accumulator [rpr, ld_stage] (this parity)
     const uint32_t* fr_ready[kMaxRanks];  // per GLOBAL rank: control word, accumulator zeroed at epoch
 };

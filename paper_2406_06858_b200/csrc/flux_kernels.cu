@@ -210,6 +210,26 @@ __device__ __forceinline__ float4 ld_cg_f4(const float* p) {
                  : "l"(p));
     return v;
 }
+// ---- bulk copies (in-kernel AllGather transfer) -----------------------------------
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_group() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_add_f4(float* p, float a, float b, float c, float d) {
     asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
@@ -240,6 +260,13 @@ __device__ bool wait_flag(const uint32_t* flag, uint32_t target, const GemmParam
         }
         if (*reinterpret_cast<volatile uint32_t*>(ctrl) != 0u) return false;  // sibling failed
     }
+}
+
+// Pieces that fill 128-row group g of a_agg (in-kernel AllGather transfer).
+__device__ __forceinline__ uint32_t ag_group_target(const GemmParams& p, int g) {
+    const int rows = min(kBM, p.m - g * kBM);
+    return p.piece_rows > 1 ? static_cast<uint32_t>(rows / p.piece_rows)
+                            : static_cast<uint32_t>(rows * p.pieces_per_row);
 }
 
 __device__ __forceinline__ void decode(uint32_t e, int& l, int& tm, int& tn) {
@@ -293,7 +320,7 @@ __device__ __forceinline__ void store_row(void* c, long long off, int col, int n
 // Per-variant geometry. CG = CTAs cooperating on one MMA tile: 1 (cta_group::1,
 // 128 x 256 tile per CTA) or 2 (cta_group::2 CTA pair, 256 x 256 tile; each CTA
 // stages half of A (128 rows) and half of B (128 of the 256 N rows)).
-template <int CG>
+template <int CG, int MODE = kModePlain>
 struct Geo {
     static constexpr int kTileM = kBM * CG;                 // rows of one scheduled tile
     static constexpr int kBRows = kBN / CG;                 // B rows (N) staged per CTA
@@ -301,23 +328,26 @@ struct Geo {
     static constexpr int kBBytes = kBRows * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagesN = CG == 2 ? 6 : 4;
-    static constexpr int kSmem = kStagesN * kStageBytes + 1024 + 256;
+    static constexpr int kCommBytes = MODE == kModeAG ? 2 * kPieceBytes : 0;  // in-kernel AG staging
+    static constexpr int kSmem = kStagesN * kStageBytes + kCommBytes + 1024 + 256;
     static constexpr uint32_t kIdescV = make_idesc(kTileM, kBN);
 };
 
 template <int MODE, int CG>
 __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_constant__ GemmParams p) {
-    using G = Geo<CG>;
+    using G = Geo<CG, MODE>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + G::kStagesN * G::kABytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + G::kStagesN * G::kBBytes);
+    uint8_t* sComm = sB + G::kStagesN * G::kBBytes;  // 2 x kPieceBytes (AG only)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sComm + G::kCommBytes);
     uint64_t* empty = full + G::kStagesN;
     uint64_t* tfull = empty + G::kStagesN;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* cbar = tempty + 2;  // 2 comm-piece barriers (AG)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -341,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4 * CG);  // every epilogue warp of the pair drains it
+            mbar_init(&cbar[a], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -373,12 +404,20 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     if ((r & 15u) == 0u) __nanosleep(r & 0xFFFFu);
                 }
                 if (MODE == kModeAG && row0 < p.m) {
-                    // Alg. 2: wait for every comm tile covering this CTA's A rows.
-                    const int rlast = min(row0 + kBM, p.m) - 1;
-                    const int f0 = row0 / p.rpct, f1 = rlast / p.rpct;
-                    for (int f = f0; f <= f1; ++f)
-                        wait_flag(p.ag_flags[l] + f, p.epoch, p, p.ctrl[l], kErrAgFlagTimeout,
-                                  static_cast<uint32_t>(f), static_cast<uint32_t>(tm * 65536 + tn));
+                    if (p.sm_transfer) {
+                        // In-kernel transfer: every piece of this 128-row group landed.
+                        const int g = row0 / kBM;
+                        wait_flag(p.ag_ctr[p.global_rank[l]] + g, (p.epoch << 16) + ag_group_target(p, g), p,
+                                  p.ctrl[l], kErrAgFlagTimeout, static_cast<uint32_t>(g),
+                                  static_cast<uint32_t>(tm * 65536 + tn));
+                    } else {
+                        // Alg. 2: wait for every comm tile covering this CTA's A rows.
+                        const int rlast = min(row0 + kBM, p.m) - 1;
+                        const int f0 = row0 / p.rpct, f1 = rlast / p.rpct;
+                        for (int f = f0; f <= f1; ++f)
+                            wait_flag(p.ag_flags[l] + f, p.epoch, p, p.ctrl[l], kErrAgFlagTimeout,
+                                      static_cast<uint32_t>(f), static_cast<uint32_t>(tm * 65536 + tn));
+                    }
                     // Flag acquire (generic proxy) before TMA reads (async proxy).
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
@@ -439,6 +478,65 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     aphase ^= 1u;
                 }
             }
+        }
+    } else if (warp == 3) {
+        // ===== in-kernel AllGather transfer (Alg. 3 on the SMs) =====
+        // Lane 0 walks this CTA's share of the piece table: TMA bulk copy
+        // global -> smem -> global (two buffers in flight), then a release
+        // increment of the destination group's counter. Remote pieces first
+        // wait until the source rank's own slot of a_agg is complete.
+        if (MODE == kModeAG && p.sm_transfer && lane == 0) {
+            uint32_t phase[2] = {0u, 0u};
+            uint32_t* pend[2] = {nullptr, nullptr};
+            int it = 0;
+            int checked_src = -1, checked_g = -1;
+            for (int j = blockIdx.x; j < p.num_jobs; j += gridDim.x) {
+                const uint32_t e = p.jobs[j];
+                const int l = static_cast<int>(e >> 28), q = static_cast<int>((e >> 24) & 0xFu);
+                const int row0 = static_cast<int>(e & 0xFFFFFFu);
+                const int me = p.global_rank[l];
+                const int g = row0 / kBM;
+                const char* src;
+                if (q == me) {
+                    src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_bytes;
+                } else {
+                    if (q != checked_src || g != checked_g) {
+                        wait_flag(p.ag_ctr[q] + g, (p.epoch << 16) + ag_group_target(p, g), p, p.ctrl[l],
+                                  kErrAgFlagTimeout, static_cast<uint32_t>(g), 0xFFFF0000u | static_cast<uint32_t>(q));
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        checked_src = q;
+                        checked_g = g;
+                    }
+                    src = p.agg_src[q] + static_cast<long long>(row0) * p.dst_ld_bytes;
+                }
+                char* dst = p.a_dst[l] + static_cast<long long>(row0) * p.dst_ld_bytes;
+                uint32_t* ctr = p.ag_ctr[me] + g;
+                const int npieces = p.piece_rows > 1 ? 1 : p.pieces_per_row;
+                for (int c = 0; c < npieces; ++c) {
+                    const int off = c * kPieceBytes;
+                    const uint32_t bytes = p.piece_rows > 1
+                                               ? static_cast<uint32_t>(p.piece_rows * p.row_bytes)
+                                               : static_cast<uint32_t>(min(kPieceBytes, p.row_bytes - off));
+                    const int b = it & 1;
+                    if (it >= 2) {
+                        // The store that last used buffer b is complete: publish its piece.
+                        bulk_wait_group<1>();
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        red_release_gpu_add(pend[b], 1u);
+                    }
+                    uint8_t* buf = sComm + b * kPieceBytes;
+                    mbar_expect_tx(&cbar[b], bytes);
+                    bulk_load(buf, src + off, bytes, &cbar[b]);
+                    mbar_wait(&cbar[b], phase[b]);
+                    phase[b] ^= 1u;
+                    bulk_store(dst + off, buf, bytes);
+                    pend[b] = ctr;
+                    ++it;
+                }
+            }
+            bulk_wait_group<0>();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) red_release_gpu_add(pend[k2 & 1], 1u);
         }
     } else if (warp >= 4) {
         // ===== epilogue: each CTA drains its own 128 TMEM lanes (rows) =====
@@ -667,14 +765,14 @@ static cudaError_t launch_one(const GemmParams& p, int grid, cudaStream_t stream
     static bool configured = false;
     auto fn = flux_gemm_kernel<MODE, CG>;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<CG>::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<CG, MODE>::kSmem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Geo<CG>::kSmem;
+    cfg.dynamicSmemBytes = Geo<CG, MODE>::kSmem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

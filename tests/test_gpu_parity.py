@@ -102,6 +102,25 @@ def test_single_cta_and_cta_pair_tiles(case, cta_group):
         comm.sync()
 
 
+@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("case", [(AG, 1024, 2048, 512, 8), (AG, 16, 1024, 8192, 8), (AG, 40, 24, 72, 4),
+                                  (AG, 256, 512, 20000, 2), (AG, 64, 256, 136, 1), (AG, 4096, 1024, 256, 4)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_allgather_transfer_engines(case, engine):
+    """Copy-engine transfer loop (ag_engine=1) and the in-kernel transfer by the
+    GEMM's own SMs (ag_engine=2): whole-row pieces, per-row pieces (padded
+    pitch) and column-split pieces (rows > 16 KiB)."""
+    pat, m, n, k, tp = case
+    p = fx.ProblemSpec(m, n, k, tp, pat)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=31 + k)
+        want = _oracle(p, a, b)
+        for _ in range(3):  # back to back: epoch-stamped counters, no resets
+            got = _run(comm, p, True, ag_engine=engine)
+            for r in range(tp):
+                assert O.max_rel_error(got[r], want[r]) <= 1e-4, r
+
+
 @pytest.mark.parametrize("tp,rpct", [(4, 64), (4, 32), (2, 512), (8, 16)])
 def test_allgather_comm_tile_sizes_and_transfer_modes(tp, rpct):
     """Comm tiles decoupled from GEMM tiles (SPEC §4.3), pull and push."""
