@@ -1006,7 +1006,7 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
 
     // ---- transfer engine: copy engines (Alg. 3 on a stream) or the GEMM's own
     // SMs (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies) ----
-    const bool sm_ok = transfer == FLUX_PULL && lk % 8 == 0 && (p->m + kBM - 1) / kBM <= static_cast<int>(kAgGroupCap);
+    const bool sm_ok = transfer == FLUX_PULL && lk % 8 == 0 && (p->m + kBM - 1) / kBM < static_cast<int>(kAgGroupCap);
     if (oc.o.ag_engine == 2 && !sm_ok)
         return fail(FLUX_ERR_CONFIG, "in-kernel AllGather transfer needs Pull and k % 8 == 0");
     const bool use_sm = oc.o.ag_engine == 2 ||
@@ -1032,7 +1032,7 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
                 if (q != r && !c->ranks[q].local) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
             // Stamp this parity's piece counters with the epoch.
             CUresult cr = driver().memset32(reinterpret_cast<CUdeviceptr>(rs.heap + ctr_off), e << 16,
-                                            static_cast<size_t>(groups), reinterpret_cast<CUstream>(s));
+                                            static_cast<size_t>(groups) + 1, reinterpret_cast<CUstream>(s));
             if (cr != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "cuMemsetD32Async failed (" + S(cr) + ")");
         }
         std::vector<std::vector<uint32_t>> seq(tp);
@@ -1066,6 +1066,8 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
             prm.piece_rows = piece_rows;
             prm.pieces_per_row = pieces_per_row;
             prm.row_bytes = row_bytes;
+            prm.ag_slot_index = groups;
+            prm.slot_pieces = static_cast<uint32_t>((rpr / piece_rows) * (piece_rows > 1 ? 1 : pieces_per_row));
             prm.src_ld_bytes = static_cast<long long>(L.a_shard.ld) * 2;
             prm.dst_ld_bytes = static_cast<long long>(L.a_agg.ld) * 2;
             for (int q = 0; q < tp; ++q) {

@@ -87,6 +87,8 @@ struct GemmParams {
     const char* shard_src[kMaxRanks];  // per local slot: its own A shard (local piece source)
     char* a_dst[kMaxRanks];            // per local slot: its a_agg
     uint32_t* ag_ctr[kMaxRanks];   // per GLOBAL rank: piece counters of this parity (peer pointers)
+    int ag_slot_index;             // counter index of "own block copied" (after the group counters)
+    uint32_t slot_pieces;          // pieces of one rank's own block
     float* fr_acc[kMaxRanks];      // per GLOBAL rank: FusedReduce fp32 accumulator [rpr, ld_stage] (this parity)
     const uint32_t* fr_ready[kMaxRanks];  // per GLOBAL rank: control word, accumulator zeroed at epoch
 };

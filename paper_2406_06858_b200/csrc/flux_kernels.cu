@@ -488,8 +488,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         if (MODE == kModeAG && p.sm_transfer && lane == 0) {
             uint32_t phase[2] = {0u, 0u};
             uint32_t* pend[2] = {nullptr, nullptr};
+            uint32_t* pend_slot[2] = {nullptr, nullptr};
             int it = 0;
-            int checked_src = -1, checked_g = -1;
+            int checked_src = -1;
             for (int j = blockIdx.x; j < p.num_jobs; j += gridDim.x) {
                 const uint32_t e = p.jobs[j];
                 const int l = static_cast<int>(e >> 28), q = static_cast<int>((e >> 24) & 0xFu);
@@ -500,17 +501,19 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 if (q == me) {
                     src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_bytes;
                 } else {
-                    if (q != checked_src || g != checked_g) {
-                        wait_flag(p.ag_ctr[q] + g, (p.epoch << 16) + ag_group_target(p, g), p, p.ctrl[l],
-                                  kErrAgFlagTimeout, static_cast<uint32_t>(g), 0xFFFF0000u | static_cast<uint32_t>(q));
+                    if (q != checked_src) {
+                        // The source's own slot (its shard copied into its a_agg) is complete.
+                        wait_flag(p.ag_ctr[q] + p.ag_slot_index, (p.epoch << 16) + p.slot_pieces, p, p.ctrl[l],
+                                  kErrAgFlagTimeout, static_cast<uint32_t>(p.ag_slot_index),
+                                  0xFFFF0000u | static_cast<uint32_t>(q));
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                         checked_src = q;
-                        checked_g = g;
                     }
                     src = p.agg_src[q] + static_cast<long long>(row0) * p.dst_ld_bytes;
                 }
                 char* dst = p.a_dst[l] + static_cast<long long>(row0) * p.dst_ld_bytes;
                 uint32_t* ctr = p.ag_ctr[me] + g;
+                uint32_t* slot_ctr = q == me ? p.ag_ctr[me] + p.ag_slot_index : nullptr;
                 const int npieces = p.piece_rows > 1 ? 1 : p.pieces_per_row;
                 for (int c = 0; c < npieces; ++c) {
                     const int off = c * kPieceBytes;
@@ -523,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         bulk_wait_group<1>();
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                         red_release_gpu_add(pend[b], 1u);
+                        if (pend_slot[b]) red_release_gpu_add(pend_slot[b], 1u);
                     }
                     uint8_t* buf = sComm + b * kPieceBytes;
                     mbar_expect_tx(&cbar[b], bytes);
@@ -531,12 +535,16 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     phase[b] ^= 1u;
                     bulk_store(dst + off, buf, bytes);
                     pend[b] = ctr;
+                    pend_slot[b] = slot_ctr;
                     ++it;
                 }
             }
             bulk_wait_group<0>();
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) red_release_gpu_add(pend[k2 & 1], 1u);
+            for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) {
+                red_release_gpu_add(pend[k2 & 1], 1u);
+                if (pend_slot[k2 & 1]) red_release_gpu_add(pend_slot[k2 & 1], 1u);
+            }
         }
     } else if (warp >= 4) {
         // ===== epilogue: each CTA drains its own 128 TMEM lanes (rows) =====
