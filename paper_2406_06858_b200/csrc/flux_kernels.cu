@@ -502,6 +502,16 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_bytes;
                 } else {
                     if (q != checked_src) {
+                        // Publish everything in flight before blocking: another CTA may be
+                        // waiting for our own-block pieces (no wait may hold a signal).
+                        bulk_wait_group<0>();
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) {
+                            if (pend[k2 & 1]) red_release_gpu_add(pend[k2 & 1], 1u);
+                            if (pend_slot[k2 & 1]) red_release_gpu_add(pend_slot[k2 & 1], 1u);
+                            pend[k2 & 1] = nullptr;
+                            pend_slot[k2 & 1] = nullptr;
+                        }
                         // The source's own slot (its shard copied into its a_agg) is complete.
                         wait_flag(p.ag_ctr[q] + p.ag_slot_index, (p.epoch << 16) + p.slot_pieces, p, p.ctrl[l],
                                   kErrAgFlagTimeout, static_cast<uint32_t>(p.ag_slot_index),
@@ -525,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         // The store that last used buffer b is complete: publish its piece.
                         bulk_wait_group<1>();
                         asm volatile("fence.proxy.async.global;" ::: "memory");
-                        red_release_gpu_add(pend[b], 1u);
+                        if (pend[b]) red_release_gpu_add(pend[b], 1u);
                         if (pend_slot[b]) red_release_gpu_add(pend_slot[b], 1u);
                     }
                     uint8_t* buf = sComm + b * kPieceBytes;
@@ -542,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             bulk_wait_group<0>();
             asm volatile("fence.proxy.async.global;" ::: "memory");
             for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) {
-                red_release_gpu_add(pend[k2 & 1], 1u);
+                if (pend[k2 & 1]) red_release_gpu_add(pend[k2 & 1], 1u);
                 if (pend_slot[k2 & 1]) red_release_gpu_add(pend_slot[k2 & 1], 1u);
             }
         }
