@@ -1038,7 +1038,9 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         std::vector<std::vector<uint32_t>> seq(tp);
         std::vector<std::vector<int>> blocks(tp);
         for (int r : mine) {
-            blocks[r] = ag_block_order(p, r, FLUX_PULL, swizzle_on != 0, rpct);
+            // Pieces always move in arrival order (own block first, then the ring);
+            // the swizzle only decides the order the tiles consume them.
+            blocks[r] = ag_block_order(p, r, FLUX_PULL, true, rpct);
             seq[r] = device_sequence(p->m, local_cols(p), rpr, swizzle_on ? blocks[r] : std::vector<int>{}, kBM * cg);
         }
         const bool step_major = oc.o.emulated_order == 1;
