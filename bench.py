@@ -232,7 +232,7 @@ def our_arm(args, wl):
     stream = torch.cuda.current_stream().cuda_stream
     streams = [stream] * (tp if emulated else 1)
     tile = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
-    opts = fx.default_opts()
+    opts = fx.default_opts(ag_engine=args.ag_engine, cta_group=args.cta_group)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def op():
@@ -405,6 +405,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama70b-up-ag")
     ap.add_argument("--quick", action="store_true", help="headline number only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ag-engine", type=int, default=0, help="0 auto, 1 copy engines, 2 in-kernel (SM) transfers")
+    ap.add_argument("--cta-group", type=int, default=0, help="0 auto, 1 single-CTA tiles, 2 CTA pairs")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args, args.workload)

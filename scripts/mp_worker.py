@@ -1,0 +1,58 @@
+"""One rank of a multi-process (one process per rank) run of the fused
+operators through the IPC communicator. Launched by tests/test_multiprocess_gpu.py
+with torchrun; every rank may share one physical GPU (handles are exchanged
+over gloo, so no NCCL is needed)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import paper_2406_06858_b200 as fx
+from paper_2406_06858_b200 import _native as N
+from oracle import oracle as O
+from oracle import gpu_harness as H
+
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+ndev = torch.cuda.device_count()
+dev = rank % ndev
+torch.cuda.set_device(dev)
+dist.init_process_group("gloo")
+
+
+def gather(blob):
+    out = [None] * world
+    dist.all_gather_object(out, blob)
+    return out
+
+
+results = {}
+cases = [(fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 1), (fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 2),
+         (fx.ALLGATHER_GEMM, 16 * world, 256 * world, 1024, 0), (fx.GEMM_REDUCESCATTER, 512 * world, 768, 256 * world, 0)]
+heap = max(fx.required_heap_bytes(fx.ProblemSpec(m, n, k, world, pat)) for pat, m, n, k, _ in cases) + (8 << 20)
+comm = fx.Communicator.ipc(rank, world, dev, heap, gather)
+for pat, m, n, k, engine in cases:
+    p = fx.ProblemSpec(m, n, k, world, pat)
+    a_bits, bt_bits = O.rank_inputs_bits(pat, m, n, k, world, 7, rank)
+    comm.tensor(rank, N.BUF_A_SHARD, p).copy_(torch.from_numpy(a_bits.view(np.int16)).cuda().view(torch.bfloat16))
+    comm.tensor(rank, N.BUF_B_SHARD, p).copy_(torch.from_numpy(bt_bits.view(np.int16)).cuda().view(torch.bfloat16))
+    torch.cuda.synchronize()
+    dist.barrier()
+    opts = fx.default_opts(out_dtype=fx.F32, wall_budget_s=20.0, ag_engine=engine)
+    for it in range(3):
+        if pat == fx.ALLGATHER_GEMM:
+            comm.ag_gemm(p, fx.TileShape(p.rows_per_rank(), p.local_cols()), 0, fx.PULL, True, opts)
+        else:
+            comm.gemm_rs(p, fx.TileShape(p.rows_per_rank(), p.local_cols()), fx.WRITE_ALLTOALL, True, opts)
+    comm.sync()
+    got = comm.tensor(rank, N.BUF_C_OUT_F32, p).double().cpu().numpy()
+    a_all, b_all = zip(*[O.rank_inputs(pat, m, n, k, world, 7, r, True) for r in range(world)])
+    want = O.dense_oracle(pat, m, n, k, world, a_all, b_all)[rank]
+    results[f"{pat}-{m}-{n}-{k}-e{engine}"] = (O.max_rel_error(got, want), H.tol(True, k))
+    dist.barrier()
+comm.close()
+print("RESULT", rank, json.dumps(results), flush=True)
+dist.destroy_process_group()
