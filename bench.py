@@ -232,14 +232,15 @@ def our_arm(args, wl):
     stream = torch.cuda.current_stream().cuda_stream
     streams = [stream] * (tp if emulated else 1)
     tile = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
-    opts = fx.default_opts(ag_engine=args.ag_engine, cta_group=args.cta_group)
+    opts = fx.default_opts(ag_engine=args.ag_engine, cta_group=args.cta_group,
+                           deterministic_reduce=0 if args.nondeterministic else 1)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def op():
         if pattern == 0:
             comm.ag_gemm(prob, tile, prob.rows_per_rank(), fx.PULL, True, opts, streams)
         else:
-            comm.gemm_rs(prob, tile, fx.WRITE_ALLTOALL, True, opts, streams)
+            comm.gemm_rs(prob, tile, args.write_mode, True, opts, streams)
 
     def barrier():
         torch.cuda.synchronize()
@@ -407,6 +408,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ag-engine", type=int, default=0, help="0 auto, 1 copy engines, 2 in-kernel (SM) transfers")
     ap.add_argument("--cta-group", type=int, default=0, help="0 auto, 1 single-CTA tiles, 2 CTA pairs")
+    ap.add_argument("--write-mode", type=int, default=0, help="RS: 0 WriteAlltoAll, 1 FusedReduce")
+    ap.add_argument("--nondeterministic", action="store_true", help="RS FusedReduce in arrival order (red.add)")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args, args.workload)

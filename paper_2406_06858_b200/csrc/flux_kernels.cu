@@ -639,7 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                             }
                         }
                     }
-                    if (remote) __threadfence_system();
+                    // No per-thread system fence: the named barrier below orders these stores
+                    // before the signalling thread's st.release.sys (release is cumulative).
                 }
                 named_bar_sync(1, 128);
                 // Signal each owner in this tile that our partial landed.
