@@ -380,6 +380,8 @@ struct flux_comm {
     std::vector<std::vector<bool>> directory;  // [from][peer] usable
     int last_launches = 0;
     bool timing = false;                          // bracket fused launches with events
+    uint64_t ag_sig = 0;                          // in-kernel AG: piece layout of the counters
+    uint32_t ag_mult = 0;                         // in-kernel AG: operators since the counter reset
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel_events;  // per device group
     int kernel_events_used = 0;
     std::map<std::pair<int, std::vector<uint32_t>>, uint32_t*> order_cache;  // (device, schedule) -> table
@@ -1014,7 +1016,7 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     if (use_sm) {
         const int cg = choose_cg(p, oc.o);
         const int groups = (p->m + kBM - 1) / kBM;
-        const size_t ctr_off = kAgCtrOffset + static_cast<size_t>(e & 1u) * kAgGroupCap * 4;
+        const size_t ctr_off = kAgCtrOffset;
         // Piece geometry: whole contiguous rows up to kPieceBytes, or column splits of long rows.
         const int row_bytes = lk * 2;
         int piece_rows = 1, pieces_per_row = (row_bytes + kPieceBytes - 1) / kPieceBytes;
@@ -1023,18 +1025,42 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
             while (piece_rows * 2 <= kBM && piece_rows * 2 * row_bytes <= kPieceBytes && rpr % (piece_rows * 2) == 0)
                 piece_rows *= 2;
         }
+        // Counters only grow: every operator adds the same pieces per group, so
+        // operator number `mult` since the last reset waits for mult x target.
+        // They are zeroed only when the piece layout changes (no per-op reset).
+        const uint64_t sig = (static_cast<uint64_t>(p->m) << 40) ^ (static_cast<uint64_t>(lk) << 16) ^
+                             (static_cast<uint64_t>(piece_rows) << 8) ^ static_cast<uint64_t>(pieces_per_row) ^
+                             (static_cast<uint64_t>(tp) << 60);
+        const bool reset = c->ag_sig != sig || c->ag_mult > (1u << 30) / std::max(1, kBM * pieces_per_row);
         for (int r : mine) {
             RankState& rs = c->ranks[r];
             FLUX_CUDA(cudaSetDevice(rs.device));
             cudaStream_t s = stream_for(c, r, streams);
-            // WAR: remote peers finished pulling my a_agg slot of the previous operator.
-            for (int q = 0; q < tp; ++q)
-                if (q != r && !c->ranks[q].local) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
-            // Stamp this parity's piece counters with the epoch.
-            CUresult cr = driver().memset32(reinterpret_cast<CUdeviceptr>(rs.heap + ctr_off), e << 16,
-                                            static_cast<size_t>(groups) + 1, reinterpret_cast<CUstream>(s));
-            if (cr != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "cuMemsetD32Async failed (" + S(cr) + ")");
+            // WAR on my a_agg slot and counters: peers of the previous operator are done
+            // (in-process peers on other devices by event, other processes by `done`).
+            for (int q = 0; q < tp; ++q) {
+                if (q == r) continue;
+                if (!c->ranks[q].local) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
+                else if (c->ranks[q].device != rs.device && c->ranks[q].kernel_evt_valid)
+                    FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[q].kernel_evt, 0));
+            }
+            if (reset) FLUX_CUDA(cudaMemsetAsync(rs.heap + ctr_off, 0, (static_cast<size_t>(groups) + 1) * 4, s));
         }
+        if (reset && c->ipc) {
+            // Layout change across processes: nobody may read a peer's counters
+            // before that peer has zeroed them (stream-level barrier, rare).
+            for (int r : mine) {
+                cudaStream_t s = stream_for(c, r, streams);
+                FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlReady, e));
+                for (int q = 0; q < tp; ++q)
+                    if (!c->ranks[q].local) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlReady, e));
+            }
+        }
+        if (reset) {
+            c->ag_sig = sig;
+            c->ag_mult = 0;
+        }
+        const uint32_t mult = ++c->ag_mult;
         std::vector<std::vector<uint32_t>> seq(tp);
         std::vector<std::vector<int>> blocks(tp);
         for (int r : mine) {
@@ -1069,6 +1095,7 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
             prm.pieces_per_row = pieces_per_row;
             prm.row_bytes = row_bytes;
             prm.ag_slot_index = groups;
+            prm.ag_mult = mult;
             prm.slot_pieces = static_cast<uint32_t>((rpr / piece_rows) * (piece_rows > 1 ? 1 : pieces_per_row));
             prm.src_ld_bytes = static_cast<long long>(L.a_shard.ld) * 2;
             prm.dst_ld_bytes = static_cast<long long>(L.a_agg.ld) * 2;
@@ -1084,11 +1111,13 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         };
         FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, step_major ? kInterleaveStep : kInterleaveRank,
                                cg, false, -1, 0, extra));
-        for (int r : mine) {
-            FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
-            cudaStream_t s = stream_for(c, r, streams);
-            FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlDone, e));  // my pulls of this epoch are done
-            FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlKdone, e));
+        if (c->ipc) {
+            for (int r : mine) {
+                FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
+                cudaStream_t s = stream_for(c, r, streams);
+                FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlDone, e));  // my pulls of this epoch are done
+                FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlKdone, e));
+            }
         }
         return FLUX_OK;
     }

@@ -33,10 +33,10 @@ constexpr size_t kCtrlKdone = 72;       // u32: epoch whose kernel finished on t
 constexpr size_t kCtrlFrReady = 76;     // u32: epoch whose FusedReduce accumulator is zeroed (RS FusedReduce)
 constexpr size_t kAgFlagOffset = 4096;  // u32[kAgFlagCap]: one flag per comm tile (SignalBoard)
 constexpr size_t kAgFlagCap = 16384;
-// In-kernel AllGather: u32[2 parities][kAgGroupCap] piece counters per 128-row
-// group of a_agg, stamped (epoch << 16) at operator start, +1 per landed piece.
+// In-kernel AllGather: u32[kAgGroupCap] monotonic piece counters per 128-row
+// group of a_agg (+ one own-block counter), +1 per landed piece, zeroed on layout change.
 constexpr size_t kAgCtrOffset = 128 * 1024;
-constexpr size_t kAgGroupCap = 16384;
+constexpr size_t kAgGroupCap = 32768;
 constexpr int kPieceBytes = 16384;      // one TMA bulk copy (global -> smem -> global)
 constexpr size_t kRsFlagOffset = 256 * 1024;  // u32[tile][src]: partial of tile from src landed
 constexpr size_t kRsFlagCap = (768 * 1024) / 4;
@@ -89,6 +89,7 @@ struct GemmParams {
     uint32_t* ag_ctr[kMaxRanks];   // per GLOBAL rank: piece counters of this parity (peer pointers)
     int ag_slot_index;             // counter index of "own block copied" (after the group counters)
     uint32_t slot_pieces;          // pieces of one rank's own block
+    uint32_t ag_mult;              // operators run on these counters since their last reset (targets scale by it)
     float* fr_acc[kMaxRanks];      // per GLOBAL rank: FusedReduce fp32 accumulator [rpr, ld_stage] (this parity)
     const uint32_t* fr_ready[kMaxRanks];  // per GLOBAL rank: control word, accumulator zeroed at epoch
 };

@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     if (p.sm_transfer) {
                         // In-kernel transfer: every piece of this 128-row group landed.
                         const int g = row0 / kBM;
-                        wait_flag(p.ag_ctr[p.global_rank[l]] + g, (p.epoch << 16) + ag_group_target(p, g), p,
+                        wait_flag(p.ag_ctr[p.global_rank[l]] + g, p.ag_mult * ag_group_target(p, g), p,
                                   p.ctrl[l], kErrAgFlagTimeout, static_cast<uint32_t>(g),
                                   static_cast<uint32_t>(tm * 65536 + tn));
                     } else {
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                             pend_slot[k2 & 1] = nullptr;
                         }
                         // The source's own slot (its shard copied into its a_agg) is complete.
-                        wait_flag(p.ag_ctr[q] + p.ag_slot_index, (p.epoch << 16) + p.slot_pieces, p, p.ctrl[l],
+                        wait_flag(p.ag_ctr[q] + p.ag_slot_index, p.ag_mult * p.slot_pieces, p, p.ctrl[l],
                                   kErrAgFlagTimeout, static_cast<uint32_t>(p.ag_slot_index),
                                   0xFFFF0000u | static_cast<uint32_t>(q));
                         asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -62,9 +62,17 @@ for name, (pat, n, k) in shapes.items():
                               [comm.tensor(r, N.BUF_B_SHARD, p).contiguous() for r in range(tp)])
         t_fused = timed(fused)
         comm.sync()
+        comm.set_timing(True)
+        kms = []
+        for _ in range(5):
+            fused()
+            kms.append(comm.last_kernel_ms())
+        comm.set_timing(False)
+        comm.sync()
         t_b1 = timed(b.unfused)
         wbytes = 2.0 * n * k  # all ranks' weight shards, streamed once
-        row = {"shape": name, "m": m, "tp": tp, "fused_ms": t_fused, "unfused_ms": t_b1,
+        row = {"shape": name, "m": m, "tp": tp, "fused_ms": t_fused, "kernel_ms": sorted(kms)[len(kms) // 2],
+               "unfused_ms": t_b1,
                "speedup": t_b1 / t_fused, "hbm_roofline_ms": wbytes / (HBM * 1e9) * 1e3,
                "roofline_frac": (wbytes / (HBM * 1e9) * 1e3) / t_fused}
         rows.append(row)
