@@ -354,6 +354,7 @@ struct RankState {
     cudaStream_t copy_stream = nullptr;  // copy-engine transfer loop
     cudaEvent_t start_evt = nullptr, kernel_evt = nullptr, copy_evt = nullptr;
     bool kernel_evt_valid = false;
+    uint32_t rs_done_cum = 0;  // tiles of mine finalised by last arrivers, cumulative (RS)
 };
 
 constexpr uint32_t kIpcMagic = 0xF1u << 24 | 0xB200u;
@@ -508,6 +509,7 @@ struct OpCommon {
     flux_opts o;
     uint64_t timeout_ns;
     int fused_reduce = 0;  // RS FusedReduce in arrival order (red.add into the owner accumulator)
+    int rs_last_arriver = 0;  // RS with ownership blocks narrower than a tile
 };
 
 OpCommon common_opts(const flux_opts* opts) {
@@ -555,6 +557,9 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 prm.fr_acc[r] = reinterpret_cast<float*>(c->ranks[r].heap + L.staging.off +
                                                          static_cast<size_t>(c->epoch & 1u) * L.stage_parity * 4);
                 prm.fr_ready[r] = at<uint32_t>(c->ranks[r], kCtrlFrReady);
+                prm.rs_ctr[r] = at<uint32_t>(c->ranks[r], kRsCtrOffset);
+                prm.rs_done[r] = at<uint32_t>(c->ranks[r], kRsDoneOffset);
+                prm.c_rank[r] = c->ranks[r].heap + L.c32.off;
             }
         }
         // Interleave the per-rank sequences into one device schedule.
@@ -605,6 +610,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.timeout_ns = oc.timeout_ns;
         prm.jitter_seed = oc.o.interleave_seed;
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
+        prm.rs_last_arriver = mode == kModeRS ? oc.rs_last_arriver : 0;
         // Join the other local ranks' streams into the launch stream.
         for (size_t li = 0; li < g.size(); ++li) {
             cudaStream_t s = stream_for(c, g[li], streams);
@@ -1295,8 +1301,34 @@ int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     // operands L2-resident); otherwise fall back to position-major.
     const bool aligned = swizzle_on && rpr % (kBM * cg) == 0 && oc.o.emulated_order != 1;
     const int tail = aligned ? (rpr / (kBM * cg)) * ((p->n + kBN - 1) / kBN) : 0;
-    return launch_groups(c, p, kModeRS, oc, streams, seq, 0, aligned ? kInterleaveRankTail : kInterleaveStep, cg,
-                         false, -1, tail);
+    // Ownership blocks narrower than a device tile (decode-sized M): no owner
+    // waits; the last of the tp arrivals of each tile reduces it (deterministic).
+    const int tiles_n = (p->n + kBN - 1) / kBN;
+    oc.rs_last_arriver = (rpr % kBM != 0 && !oc.fused_reduce) ? 1 : 0;
+    if (oc.rs_last_arriver && static_cast<size_t>(tiles) > kRsCtrCap)
+        return fail(FLUX_ERR_CONFIG, "too many output tiles for the arrival counters");
+    const int interleave = aligned ? kInterleaveRankTail : (oc.rs_last_arriver ? kInterleaveRank : kInterleaveStep);
+    FLUX_TRY(launch_groups(c, p, kModeRS, oc, streams, seq, 0, interleave, cg, false, -1, tail));
+    if (oc.rs_last_arriver) {
+        // Other ranks finalise my rows: I am done once every tile holding my rows is.
+        for (int r : mine) {
+            const int t0 = (r * rpr) / kBM, t1 = ((r + 1) * rpr - 1) / kBM;
+            c->ranks[r].rs_done_cum += static_cast<uint32_t>((t1 - t0 + 1) * tiles_n);
+            FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
+            cudaStream_t s = stream_for(c, r, streams);
+            bool remote_peer = false, other_device = false;
+            for (int q = 0; q < tp; ++q) {
+                if (!c->ranks[q].local) remote_peer = true;
+                else if (c->ranks[q].device != c->ranks[r].device) {
+                    other_device = true;
+                    FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[q].kernel_evt, 0));
+                }
+            }
+            if (remote_peer) FLUX_TRY(wait_value_geq(s, c->ranks[r].heap + kRsDoneOffset, c->ranks[r].rs_done_cum));
+            (void)other_device;
+        }
+    }
+    return FLUX_OK;
 }
 
 int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {

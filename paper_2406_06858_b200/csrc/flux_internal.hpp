@@ -39,7 +39,10 @@ constexpr size_t kAgCtrOffset = 128 * 1024;
 constexpr size_t kAgGroupCap = 32768;
 constexpr int kPieceBytes = 16384;      // one TMA bulk copy (global -> smem -> global)
 constexpr size_t kRsFlagOffset = 256 * 1024;  // u32[tile][src]: partial of tile from src landed
-constexpr size_t kRsFlagCap = (768 * 1024) / 4;
+constexpr size_t kRsFlagCap = (512 * 1024) / 4;
+constexpr size_t kRsCtrOffset = 768 * 1024;   // u32[tile]: monotonic arrival count (RS last arriver)
+constexpr size_t kRsCtrCap = 60 * 1024;
+constexpr size_t kRsDoneOffset = kRsCtrOffset + kRsCtrCap * 4;  // u32: tiles of mine finalised (monotonic)
 constexpr size_t kDataOffset = 1 << 20;
 
 // Error codes written by device waits into the control block.
@@ -89,7 +92,12 @@ struct GemmParams {
     uint32_t* ag_ctr[kMaxRanks];   // per GLOBAL rank: piece counters of this parity (peer pointers)
     int ag_slot_index;             // counter index of "own block copied" (after the group counters)
     uint32_t slot_pieces;          // pieces of one rank's own block
-    uint32_t ag_mult;              // operators run on these counters since their last reset (targets scale by it)
+    uint32_t ag_mult;
+    // RS with ownership blocks narrower than a tile: last-arriver reduction
+    int rs_last_arriver;
+    uint32_t* rs_ctr[kMaxRanks];   // per GLOBAL rank: tile arrival counters (peer pointers)
+    uint32_t* rs_done[kMaxRanks];  // per GLOBAL rank: finalised-tile counter (peer pointers)
+    void* c_rank[kMaxRanks];       // per GLOBAL rank: its C (peer pointers)              // operators run on these counters since their last reset (targets scale by it)
     float* fr_acc[kMaxRanks];      // per GLOBAL rank: FusedReduce fp32 accumulator [rpr, ld_stage] (this parity)
     const uint32_t* fr_ready[kMaxRanks];  // per GLOBAL rank: control word, accumulator zeroed at epoch
 };

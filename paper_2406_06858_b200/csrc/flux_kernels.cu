@@ -227,6 +227,14 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_group() {
     asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ uint32_t atom_add_acq_rel_sys(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -348,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     uint64_t* tempty = tfull + 2;
     uint64_t* cbar = tempty + 2;  // 2 comm-piece barriers (AG)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 2);
+    uint32_t* s_flag = tmem_slot + 1;  // epilogue broadcast (RS last arriver)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -571,6 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             const int col0 = tn * kBN;
             const int row = row0 + q * 32 + lane;
             const bool valid = row < p.m;
+            bool released = false;
             mbar_wait(&tfull[as], aphase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
@@ -591,6 +601,81 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         store_row<32>(p.c[l], static_cast<long long>(row) * p.ldc + col, col, p.n,
                                     p.out_f32, v);
                     }
+                }
+            } else if (p.rs_last_arriver) {
+                // Ownership blocks narrower than a tile (decode-sized M): every source
+                // stores its whole partial tile into the owners' staging planes and
+                // bumps the tile's arrival counter; the last of the tp arrivals sums
+                // the tile in source order 0..tp-1 and writes every owner's rows.
+                // Nobody waits, the result stays deterministic.
+                const int me = p.global_rank[l];
+                const uint32_t parity = p.epoch & 1u;
+                const int owner = valid ? row / p.rpr : 0;
+                const long long lrow = row - owner * p.rpr;
+                const int tile_id = tm * p.tiles_n + tn;
+                float* dst = p.staging[owner] + parity * p.stage_parity + me * p.stage_plane + lrow * p.ld_stage;
+                for (int c = 0; c < kBN / 32; ++c) {
+                    const int col = col0 + c * 32;
+                    if (col >= p.n) break;
+                    uint32_t r[32];
+                    tmem_ld32(tbase + c * 32, r);
+                    tmem_ld_wait();
+                    if (valid) {
+                        float4* d4 = reinterpret_cast<float4*>(dst + col);
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                    __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                    }
+                }
+                // The accumulator is in staging now: hand TMEM back to the MMA warp.
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(as * 8));
+                    else mbar_arrive(&tempty[as]);
+                }
+                released = true;
+                named_bar_sync(1, 128);
+                if (et == 0) {
+                    const uint32_t old = atom_add_acq_rel_sys(p.rs_ctr[row0 / p.rpr] + tile_id, 1u);
+                    *s_flag = ((old + 1u) % static_cast<uint32_t>(p.tp)) == 0u ? 1u : 0u;
+                }
+                named_bar_sync(1, 128);
+                if (*s_flag && valid) {
+                    const float* src0 = p.staging[owner] + parity * p.stage_parity + lrow * p.ld_stage;
+                    for (int c = 0; c < kBN / 8; ++c) {
+                        const int col = col0 + c * 8;
+                        if (col >= p.n) break;
+                        float4 v[kMaxRanks][2];
+#pragma unroll
+                        for (int s = 0; s < kMaxRanks; ++s)
+                            if (s < p.tp) {
+#pragma unroll
+                                for (int j = 0; j < 2; ++j) v[s][j] = ld_cg_f4(src0 + s * p.stage_plane + col + 4 * j);
+                            }
+                        float acc[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+#pragma unroll
+                        for (int s = 0; s < kMaxRanks; ++s)
+                            if (s < p.tp) {
+#pragma unroll
+                                for (int j = 0; j < 2; ++j) {
+                                    acc[4 * j] += v[s][j].x;
+                                    acc[4 * j + 1] += v[s][j].y;
+                                    acc[4 * j + 2] += v[s][j].z;
+                                    acc[4 * j + 3] += v[s][j].w;
+                                }
+                            }
+                        store_row<8>(p.c_rank[owner], lrow * p.ldc + col, col, p.n, p.out_f32, acc);
+                    }
+                }
+                // Tell each owner in the tile one more of its tiles is final.
+                if (*s_flag) {
+                    named_bar_sync(1, 128);
+                    const int o0 = row0 / p.rpr, o1 = (min(row0 + kBM, p.m) - 1) / p.rpr;
+                    if (et <= o1 - o0) red_release_sys_add(p.rs_done[o0 + et], 1u);
                 }
             } else {
                 const int me = p.global_rank[l];
@@ -734,11 +819,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (CG == 2) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(as * 8));
-                else mbar_arrive(&tempty[as]);
+            if (!released) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(as * 8));
+                    else mbar_arrive(&tempty[as]);
+                }
             }
             if (++as == 2) {
                 as = 0;
