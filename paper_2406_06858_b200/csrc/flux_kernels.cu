@@ -332,31 +332,47 @@ __device__ __forceinline__ void store_row(void* c, long long off, int col, int n
 // owners' C. Consecutive threads take consecutive 4-column groups of a row
 // (coalesced), and every source's float4 is loaded before the sum.
 __device__ __noinline__ void reduce_tile_coalesced(const GemmParams& p, int row0, int col0, uint32_t parity,
-                                                      int et) {
+                                                   int et) {
+    constexpr int kU = 4;  // positions per thread per iteration: kU x tp loads in flight
     const int rows_valid = min(kBM, p.m - row0);
     const int npos = rows_valid * (kBN / 4);
-    for (int pos = et; pos < npos; pos += 128) {
-        const int rr = pos / (kBN / 4);
-        const int col = col0 + (pos % (kBN / 4)) * 4;
-        if (col >= p.n) continue;
-        const int grow = row0 + rr;
-        const int o = grow / p.rpr;
-        const long long lr = grow - o * p.rpr;
-        const float* src = p.staging[o] + parity * p.stage_parity + lr * p.ld_stage + col;
-        float4 v[kMaxRanks];
+    for (int base = et; base < npos; base += 128 * kU) {
+        float4 v[kU][kMaxRanks];
 #pragma unroll
-        for (int s = 0; s < kMaxRanks; ++s)
-            if (s < p.tp) v[s] = ld_cg_f4(src + s * p.stage_plane);
-        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int u = 0; u < kU; ++u) {
+            const int pos = base + u * 128;
+            const int rr = pos / (kBN / 4);
+            const int col = col0 + (pos % (kBN / 4)) * 4;
+            if (pos < npos && col < p.n) {
+                const int grow = row0 + rr;
+                const int o = grow / p.rpr;
+                const float* src = p.staging[o] + parity * p.stage_parity + (grow - o * p.rpr) * p.ld_stage + col;
 #pragma unroll
-        for (int s = 0; s < kMaxRanks; ++s)
-            if (s < p.tp) {
-                acc[0] += v[s].x;
-                acc[1] += v[s].y;
-                acc[2] += v[s].z;
-                acc[3] += v[s].w;
+                for (int s = 0; s < kMaxRanks; ++s)
+                    if (s < p.tp) v[u][s] = ld_cg_f4(src + s * p.stage_plane);
             }
-        store_row<4>(p.c_rank[o], lr * p.ldc + col, col, p.n, p.out_f32, acc);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int pos = base + u * 128;
+            const int rr = pos / (kBN / 4);
+            const int col = col0 + (pos % (kBN / 4)) * 4;
+            if (pos < npos && col < p.n) {
+                const int grow = row0 + rr;
+                const int o = grow / p.rpr;
+                float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int s = 0; s < kMaxRanks; ++s)
+                    if (s < p.tp) {
+                        acc[0] += v[u][s].x;
+                        acc[1] += v[u][s].y;
+                        acc[2] += v[u][s].z;
+                        acc[3] += v[u][s].w;
+                    }
+                store_row<4>(p.c_rank[o], static_cast<long long>(grow - o * p.rpr) * p.ldc + col, col, p.n, p.out_f32,
+                             acc);
+            }
+        }
     }
 }
 
@@ -776,34 +792,6 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                               p.n, p.out_f32, acc);
                             }
                         }
-                    } else if (o0 == o1) {
-                        // Whole tile is mine: stage my own partial next to the others,
-                        // release TMEM, then reduce the tile with coalesced loads.
-                        float* dst = p.staging[me] + parity * p.stage_parity + me * p.stage_plane +
-                                     static_cast<long long>(row - me * p.rpr) * p.ld_stage;
-                        for (int c = 0; c < kBN / 32; ++c) {
-                            const int col = col0 + c * 32;
-                            if (col >= p.n) break;
-                            uint32_t r[32];
-                            tmem_ld32(tbase + c * 32, r);
-                            tmem_ld_wait();
-                            if (valid) {
-                                float4* d4 = reinterpret_cast<float4*>(dst + col);
-#pragma unroll
-                                for (int j = 0; j < 32; j += 4)
-                                    d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-                            }
-                        }
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (CG == 2) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(as * 8));
-                            else mbar_arrive(&tempty[as]);
-                        }
-                        released = true;
-                        named_bar_sync(1, 128);
-                        reduce_tile_coalesced(p, row0, col0, parity, et);
                     } else if (__any_sync(0xffffffffu, owned)) {
                         const long long lrow = row - me * p.rpr;
                         const float* src0 = p.staging[me] + parity * p.stage_parity + lrow * p.ld_stage;
