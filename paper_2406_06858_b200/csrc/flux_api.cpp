@@ -550,7 +550,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             prm.ag_flags[li] = at<uint32_t>(rs, kAgFlagOffset);
             prm.ctrl[li] = at<uint32_t>(rs, kCtrlErr);
         }
-        if (mode == kModeRS) {
+        if (mode == kModeRS || mode == kModeRSLast) {
             for (int r = 0; r < c->tp; ++r) {
                 prm.staging[r] = reinterpret_cast<float*>(c->ranks[r].heap + L.staging.off);
                 prm.rs_flags[r] = at<uint32_t>(c->ranks[r], kRsFlagOffset);
@@ -610,7 +610,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.timeout_ns = oc.timeout_ns;
         prm.jitter_seed = oc.o.interleave_seed;
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
-        prm.rs_last_arriver = mode == kModeRS ? oc.rs_last_arriver : 0;
+        prm.rs_last_arriver = mode == kModeRSLast ? 1 : 0;
         // Join the other local ranks' streams into the launch stream.
         for (size_t li = 0; li < g.size(); ++li) {
             cudaStream_t s = stream_for(c, g[li], streams);
@@ -1308,7 +1308,8 @@ int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     if (oc.rs_last_arriver && static_cast<size_t>(tiles) > kRsCtrCap)
         return fail(FLUX_ERR_CONFIG, "too many output tiles for the arrival counters");
     const int interleave = aligned ? kInterleaveRankTail : (oc.rs_last_arriver ? kInterleaveRank : kInterleaveStep);
-    FLUX_TRY(launch_groups(c, p, kModeRS, oc, streams, seq, 0, interleave, cg, false, -1, tail));
+    FLUX_TRY(launch_groups(c, p, oc.rs_last_arriver ? kModeRSLast : kModeRS, oc, streams, seq, 0, interleave, cg,
+                           false, -1, tail));
     if (oc.rs_last_arriver) {
         // Other ranks finalise my rows: I am done once every tile holding my rows is.
         for (int r : mine) {

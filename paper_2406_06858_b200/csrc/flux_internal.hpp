@@ -22,7 +22,8 @@ constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*alig
 
 constexpr int kMaxRanks = 8;   // TP degree supported by one communicator (one NVSwitch node)
 
-enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2 };
+// kModeRSLast: GEMM-RS whose ownership blocks are narrower than a tile (last-arriver reduction).
+enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2, kModeRSLast = 3 };
 
 // Control block at the start of every rank's symmetric heap. All words are
 // epoch-stamped (monotonic), so nothing needs resetting between operators.

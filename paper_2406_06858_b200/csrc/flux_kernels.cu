@@ -331,7 +331,7 @@ __device__ __forceinline__ void store_row(void* c, long long off, int col, int n
 // Source-ordered sum of the tp staged partials of one 128 x 256 tile into the
 // owners' C. Consecutive threads take consecutive 4-column groups of a row
 // (coalesced), and every source's float4 is loaded before the sum.
-__device__ __noinline__ void reduce_tile_coalesced(const GemmParams& p, int row0, int col0, uint32_t parity,
+__device__ __forceinline__ void reduce_tile_coalesced(const GemmParams& p, int row0, int col0, uint32_t parity,
                                                    int et) {
     constexpr int kU = 4;  // positions per thread per iteration: kU x tp loads in flight
     const int rows_valid = min(kBM, p.m - row0);
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                    static_cast<uint32_t>(as * kBN);
             if (row0 >= p.m) {
                 // Fully out-of-range half of a pair tile: nothing to store or signal.
-            } else if (MODE != kModeRS) {
+            } else if (MODE != kModeRS && MODE != kModeRSLast) {
                 for (int c = 0; c < kBN / 32; ++c) {
                     const int col = col0 + c * 32;
                     if (col >= p.n) break;  // warp-uniform
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                     p.out_f32, v);
                     }
                 }
-            } else if (p.rs_last_arriver) {
+            } else if (MODE == kModeRSLast) {
                 // Ownership blocks narrower than a tile (decode-sized M): every source
                 // stores its whole partial tile into the owners' staging planes and
                 // bumps the tile's arrival counter; the last of the tp arrivals sums
@@ -923,12 +923,14 @@ cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStr
             case kModePlain: return launch_one<kModePlain, 2>(p, grid, stream);
             case kModeAG: return launch_one<kModeAG, 2>(p, grid, stream);
             case kModeRS: return launch_one<kModeRS, 2>(p, grid, stream);
+            case kModeRSLast: return launch_one<kModeRSLast, 2>(p, grid, stream);
         }
     } else {
         switch (mode) {
             case kModePlain: return launch_one<kModePlain, 1>(p, grid, stream);
             case kModeAG: return launch_one<kModeAG, 1>(p, grid, stream);
             case kModeRS: return launch_one<kModeRS, 1>(p, grid, stream);
+            case kModeRSLast: return launch_one<kModeRSLast, 1>(p, grid, stream);
         }
     }
     return cudaErrorInvalidValue;
