@@ -35,6 +35,9 @@ WORKLOADS = {
     "llama70b-down-rs": (1, 4096, 8192, 28672, 8, "GEMM-ReduceScatter Llama-2-70B MLP down-proj (M=4096, K=28672, N=8192) bf16"),
     "gpt3-ag": (0, 8192, 49152, 12288, 8, "AllGather-GEMM GPT-3 175B MLP (M=8192, K=12288, N=49152) bf16"),
     "gpt3-rs": (1, 8192, 12288, 49152, 8, "GEMM-ReduceScatter GPT-3 175B MLP (M=8192, K=49152, N=12288) bf16"),
+    "llama70b-down-rs-tp4": (1, 4096, 8192, 28672, 4, "GEMM-ReduceScatter Llama-2-70B MLP down-proj at TP=4 (M=4096, K=28672, N=8192) bf16"),
+    "llama70b-down-rs-tp2": (1, 4096, 8192, 28672, 2, "GEMM-ReduceScatter Llama-2-70B MLP down-proj at TP=2 (M=4096, K=28672, N=8192) bf16"),
+    "rs-1024-tp2": (1, 1024, 1024, 1024, 2, "GEMM-ReduceScatter M=N=K=1024 at TP=2 (oracle plumbing config)"),
 }
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
 
