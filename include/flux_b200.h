@@ -91,6 +91,7 @@ typedef struct {
     int cta_group;             /* 0 auto, 1 = 128x256 tiles per CTA, 2 = CTA pairs (256x256, cta_group::2) */
     int ag_engine;             /* AllGather transfers: 0 auto, 1 copy engines (stream memcpy + flag
                                   writes), 2 in-kernel (TMA bulk copies by the GEMM's SMs, Pull) */
+    int trace;                 /* 1: record the device event trace of the next operators (flux_trace_read) */
 } flux_opts;
 
 typedef struct {
@@ -197,6 +198,12 @@ int flux_last_launch_count(const flux_comm* comm);
  * events on its launching stream; flux_last_kernel_ms returns the longest
  * launch of the last operator (waits for it). */
 int flux_comm_set_timing(flux_comm* comm, int enable);
+/* Device event trace of the last traced operator on `rank` (reference
+ * CausalityLog, engine.hpp:37-63): 16-byte records {u64 %globaltimer ns;
+ * u64 kind<<60 | rank<<56 | target<<32 | tile_row<<16 | tile_col}, kinds
+ * 1 compute_start, 2 signal_set, 3 tile_write, 4 reduce. Waits for the device. */
+int flux_trace_read(flux_comm* comm, int rank, const flux_problem* problem, void* out,
+                    size_t max_records, size_t* count);
 int flux_last_kernel_ms(flux_comm* comm, float* ms);
 
 #ifdef __cplusplus

@@ -66,7 +66,7 @@ class Opts(C.Structure):
     _fields_ = [("workers_per_rank", C.c_int), ("deterministic_reduce", C.c_int),
                 ("poll_budget", C.c_longlong), ("wall_budget_s", C.c_double),
                 ("interleave_seed", C.c_uint64), ("shift_offset", C.c_int), ("out_dtype", C.c_int),
-                ("emulated_order", C.c_int), ("cta_group", C.c_int), ("ag_engine", C.c_int)]
+                ("emulated_order", C.c_int), ("cta_group", C.c_int), ("ag_engine", C.c_int), ("trace", C.c_int)]
 
 
 class CommOpts(C.Structure):
@@ -115,6 +115,7 @@ _SIGS = {
     "flux_last_launch_count": (C.c_int, [C.c_void_p]),
     "flux_comm_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "flux_last_kernel_ms": (C.c_int, [C.c_void_p, _P(C.c_float)]),
+    "flux_trace_read": (C.c_int, [C.c_void_p, C.c_int, _P(Problem), C.c_void_p, C.c_size_t, _P(C.c_size_t)]),
 }
 
 # Symbols include/flux_b200.h declares (tests check the library exports all of them).

@@ -221,3 +221,38 @@ class Communicator:
 
 def required_heap_bytes(problem: ProblemSpec) -> int:
     return int(N.lib().flux_required_heap_bytes(C.byref(problem.c())))
+
+
+TRACE_KINDS = {1: "compute_start", 2: "signal_set", 3: "tile_write", 4: "reduce", 5: "wait"}
+
+
+def read_trace(comm: Communicator, rank: int, problem: ProblemSpec, max_records: int = 1 << 18) -> list[dict]:
+    """Device event trace of the last operator run with opts.trace=1, as the
+    reference's CausalityEvent records (engine.hpp:37-63): kind, rank,
+    tile_row, tile_col, target, logical_ts (order of the device timestamps),
+    wall_ns (%globaltimer relative to the first event)."""
+    buf = (C.c_uint64 * (2 * max_records))()
+    n = C.c_size_t()
+    N.check(N.lib().flux_trace_read(comm._h, rank, C.byref(problem.c()), buf, max_records, C.byref(n)))
+    recs = []
+    for i in range(n.value):
+        ts, w = buf[2 * i], buf[2 * i + 1]
+        recs.append({"event": TRACE_KINDS.get(w >> 60, "unknown"), "rank": (w >> 56) & 0xF,
+                     "tile_row": (w >> 16) & 0xFFFF, "tile_col": w & 0xFFFF, "target": (w >> 32) & 0xFFFFFF,
+                     "ts": ts})
+    recs.sort(key=lambda r: r["ts"])
+    t0 = recs[0]["ts"] if recs else 0
+    for i, r in enumerate(recs):
+        r["logical_ts"] = i + 1
+        r["wall_ns"] = r["ts"] - t0  # "ts": absolute %globaltimer (comparable across ranks of one GPU)
+    return recs
+
+
+def write_jsonl(path: str, events: list[dict]) -> None:
+    """The reference's JSONL schema (engine.cpp:101-109)."""
+    import json
+
+    with open(path, "w") as f:
+        for e in events:
+            f.write(json.dumps({k: e[k] for k in ("event", "rank", "tile_row", "tile_col", "target", "logical_ts",
+                                                  "wall_ns")}) + "\n")

@@ -300,6 +300,7 @@ struct Region {
 
 struct Layout {
     Region a_shard, b, a_agg, c, c32, staging;
+    size_t trace_off = 0;
     long long stage_plane = 0, stage_parity = 0;
     int ld_stage = 0;
     size_t total = 0;
@@ -338,6 +339,8 @@ Layout layout_for(const flux_problem* p) {
     }
     L.c = L.c32;
     L.c.dtype = FLUX_BF16;
+    L.trace_off = off;  // device event trace ring (flux_opts.trace)
+    off += kTraceBytes;
     L.total = off;
     return L;
 }
@@ -619,6 +622,15 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 FLUX_CUDA(cudaStreamWaitEvent(lead, c->ranks[g[li]].start_evt, 0));
             }
         }
+        if (oc.o.trace) {
+            prm.trace_cap = static_cast<uint32_t>(kTraceBytes / 16);
+            for (size_t li = 0; li < g.size(); ++li) {
+                RankState& rs = c->ranks[g[li]];
+                prm.trace[li] = reinterpret_cast<unsigned long long*>(rs.heap + L.trace_off);
+                prm.trace_cursor[li] = at<uint32_t>(rs, kCtrlTraceCursor);
+                FLUX_CUDA(cudaMemsetAsync(prm.trace_cursor[li], 0, 4, lead));
+            }
+        }
         if (extra) FLUX_TRY(extra(g, prm));
         const int grid = cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
         std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
@@ -678,6 +690,7 @@ void flux_default_opts(flux_opts* o) {
     o->emulated_order = 0;
     o->cta_group = 0;
     o->ag_engine = 0;
+    o->trace = 0;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -1479,6 +1492,22 @@ int flux_sync(flux_comm* c) {
 }
 
 int flux_last_launch_count(const flux_comm* c) { return c ? c->last_launches : 0; }
+
+int flux_trace_read(flux_comm* c, int rank, const flux_problem* p, void* out, size_t max_records, size_t* count) {
+    FLUX_TRY(check_comm(c));
+    FLUX_TRY(validate_problem(p));
+    if (rank < 0 || rank >= c->tp || !c->ranks[rank].local)
+        return fail(FLUX_ERR_DIRECTORY, "rank " + S(rank) + " is not driven by this process");
+    RankState& rs = c->ranks[rank];
+    FLUX_CUDA(cudaSetDevice(rs.device));
+    FLUX_CUDA(cudaDeviceSynchronize());
+    uint32_t n = 0;
+    FLUX_CUDA(cudaMemcpy(&n, rs.heap + kCtrlTraceCursor, 4, cudaMemcpyDeviceToHost));
+    size_t k = std::min<size_t>(std::min<size_t>(n, kTraceBytes / 16), max_records);
+    if (k) FLUX_CUDA(cudaMemcpy(out, rs.heap + layout_for(p).trace_off, k * 16, cudaMemcpyDeviceToHost));
+    if (count) *count = k;
+    return FLUX_OK;
+}
 
 int flux_comm_set_timing(flux_comm* c, int enable) {
     if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");

@@ -32,6 +32,10 @@ constexpr size_t kCtrlReady = 64;       // u32: epoch at which this rank's A sha
 constexpr size_t kCtrlDone = 68;        // u32: epoch whose peer pulls this rank has finished
 constexpr size_t kCtrlKdone = 72;       // u32: epoch whose kernel finished on this rank (push targets)
 constexpr size_t kCtrlFrReady = 76;     // u32: epoch whose FusedReduce accumulator is zeroed (RS FusedReduce)
+constexpr size_t kCtrlTraceCursor = 80; // u32: records written to this rank's trace ring
+constexpr size_t kTraceBytes = size_t(4) << 20;  // trace ring at the end of the data region (16 B records)
+// Trace record kinds (the reference CausalityLog event names, engine.hpp:37-63).
+enum TraceKind : uint32_t { kEvComputeStart = 1, kEvSignalSet = 2, kEvTileWrite = 3, kEvReduce = 4, kEvWait = 5 };
 constexpr size_t kAgFlagOffset = 4096;  // u32[kAgFlagCap]: one flag per comm tile (SignalBoard)
 constexpr size_t kAgFlagCap = 16384;
 // In-kernel AllGather: u32[kAgGroupCap] monotonic piece counters per 128-row
@@ -90,15 +94,19 @@ struct GemmParams {
     const char* agg_src[kMaxRanks];    // per GLOBAL rank: its a_agg (peer pointers; pull source)
     const char* shard_src[kMaxRanks];  // per local slot: its own A shard (local piece source)
     char* a_dst[kMaxRanks];            // per local slot: its a_agg
-    uint32_t* ag_ctr[kMaxRanks];   // per GLOBAL rank: piece counters of this parity (peer pointers)
+    uint32_t* ag_ctr[kMaxRanks];   // per GLOBAL rank: monotonic piece counters (peer pointers)
     int ag_slot_index;             // counter index of "own block copied" (after the group counters)
     uint32_t slot_pieces;          // pieces of one rank's own block
-    uint32_t ag_mult;
+    uint32_t ag_mult;              // operators run on these counters since their last reset (targets scale by it)
     // RS with ownership blocks narrower than a tile: last-arriver reduction
     int rs_last_arriver;
     uint32_t* rs_ctr[kMaxRanks];   // per GLOBAL rank: tile arrival counters (peer pointers)
     uint32_t* rs_done[kMaxRanks];  // per GLOBAL rank: finalised-tile counter (peer pointers)
-    void* c_rank[kMaxRanks];       // per GLOBAL rank: its C (peer pointers)              // operators run on these counters since their last reset (targets scale by it)
+    void* c_rank[kMaxRanks];       // per GLOBAL rank: its C (peer pointers)
+    // Device event trace (reference CausalityLog, engine.hpp:37-63): 16-byte records
+    unsigned long long* trace[kMaxRanks];  // per local slot: ring (nullptr = tracing off)
+    uint32_t* trace_cursor[kMaxRanks];     // per local slot: next record index
+    uint32_t trace_cap;
     float* fr_acc[kMaxRanks];      // per GLOBAL rank: FusedReduce fp32 accumulator [rpr, ld_stage] (this parity)
     const uint32_t* fr_ready[kMaxRanks];  // per GLOBAL rank: control word, accumulator zeroed at epoch
 };

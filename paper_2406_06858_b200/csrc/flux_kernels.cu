@@ -277,6 +277,28 @@ __device__ __forceinline__ uint32_t ag_group_target(const GemmParams& p, int g) 
                             : static_cast<uint32_t>(rows * p.pieces_per_row);
 }
 
+// One 16-byte record of the device event trace: %globaltimer, then
+// kind(4) | rank(4) | target(24) | tile_row(16) | tile_col(16).
+__device__ __forceinline__ void trace_event(const GemmParams& p, int l, uint32_t kind, int rank, int tile_row,
+                                            int tile_col, uint32_t target) {
+    if (p.trace[l] == nullptr) return;
+    const uint64_t ts = globaltimer();
+    const uint32_t i = atomicAdd(p.trace_cursor[l], 1u);
+    if (i >= p.trace_cap) return;
+    unsigned long long* rec = p.trace[l] + 2ull * i;
+    rec[0] = ts;
+    rec[1] = (static_cast<uint64_t>(kind) << 60) | (static_cast<uint64_t>(rank & 0xF) << 56) |
+             (static_cast<uint64_t>(target & 0xFFFFFFu) << 32) | (static_cast<uint64_t>(tile_row & 0xFFFF) << 16) |
+             static_cast<uint64_t>(tile_col & 0xFFFF);
+}
+
+// Publish one landed AG piece (trace timestamp taken before the release).
+__device__ __forceinline__ void ag_signal(const GemmParams& p, uint32_t* ctr, int meta) {
+    const int l = meta >> 16, g = meta & 0xFFFF;
+    trace_event(p, l, kEvSignalSet, p.global_rank[l], g, 0, static_cast<uint32_t>(g));
+    red_release_gpu_add(ctr, 1u);
+}
+
 __device__ __forceinline__ void decode(uint32_t e, int& l, int& tm, int& tn) {
     l = static_cast<int>(e >> 28);
     tm = static_cast<int>((e >> 14) & 0x3FFFu);
@@ -482,6 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     }
                     // Flag acquire (generic proxy) before TMA reads (async proxy).
                     asm volatile("fence.proxy.async.global;" ::: "memory");
+                    trace_event(p, l, kEvComputeStart, p.global_rank[l], row0 / kBM, tn,
+                                static_cast<uint32_t>(p.sm_transfer ? row0 / kBM : row0 / p.rpct));
                 }
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
@@ -551,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             uint32_t phase[2] = {0u, 0u};
             uint32_t* pend[2] = {nullptr, nullptr};
             uint32_t* pend_slot[2] = {nullptr, nullptr};
+            int pend_meta[2] = {0, 0};  // (slot << 16) | group, for the trace
             int it = 0;
             int checked_src = -1;
             for (int j = blockIdx.x; j < p.num_jobs; j += gridDim.x) {
@@ -569,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         bulk_wait_group<0>();
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                         for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) {
-                            if (pend[k2 & 1]) red_release_gpu_add(pend[k2 & 1], 1u);
+                            if (pend[k2 & 1]) ag_signal(p, pend[k2 & 1], pend_meta[k2 & 1]);
                             if (pend_slot[k2 & 1]) red_release_gpu_add(pend_slot[k2 & 1], 1u);
                             pend[k2 & 1] = nullptr;
                             pend_slot[k2 & 1] = nullptr;
@@ -597,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         // The store that last used buffer b is complete: publish its piece.
                         bulk_wait_group<1>();
                         asm volatile("fence.proxy.async.global;" ::: "memory");
-                        if (pend[b]) red_release_gpu_add(pend[b], 1u);
+                        if (pend[b]) ag_signal(p, pend[b], pend_meta[b]);
                         if (pend_slot[b]) red_release_gpu_add(pend_slot[b], 1u);
                     }
                     uint8_t* buf = sComm + b * kPieceBytes;
@@ -608,13 +633,14 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     bulk_store(dst + off, buf, bytes);
                     pend[b] = ctr;
                     pend_slot[b] = slot_ctr;
+                    pend_meta[b] = (l << 16) | g;
                     ++it;
                 }
             }
             bulk_wait_group<0>();
             asm volatile("fence.proxy.async.global;" ::: "memory");
             for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) {
-                if (pend[k2 & 1]) red_release_gpu_add(pend[k2 & 1], 1u);
+                if (pend[k2 & 1]) ag_signal(p, pend[k2 & 1], pend_meta[k2 & 1]);
                 if (pend_slot[k2 & 1]) red_release_gpu_add(pend_slot[k2 & 1], 1u);
             }
         }
@@ -691,8 +717,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 released = true;
                 named_bar_sync(1, 128);
                 if (et == 0) {
+                    trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(row0 / p.rpr));
                     const uint32_t old = atom_add_acq_rel_sys(p.rs_ctr[row0 / p.rpr] + tile_id, 1u);
                     *s_flag = ((old + 1u) % static_cast<uint32_t>(p.tp)) == 0u ? 1u : 0u;
+                    if (*s_flag) trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(row0 / p.rpr));
                 }
                 named_bar_sync(1, 128);
                 if (*s_flag) reduce_tile_coalesced(p, row0, col0, parity, et);
@@ -756,7 +784,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 // Signal each owner in this tile that our partial landed.
                 if (et <= o1 - o0) {
                     const int o = o0 + et;
-                    if (o != me) st_release_sys(p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
+                    if (o != me) {
+                        trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o));
+                        st_release_sys(p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
+                    }
                 }
                 // Phase 2: owned rows = source-ordered sum of all partials.
                 const bool mine_in_tile = (me >= o0 && me <= o1);
@@ -766,6 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                             if (s != me)
                                 wait_flag(p.rs_flags[me] + tile_id * p.tp + s, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
                                           static_cast<uint32_t>(tile_id), static_cast<uint32_t>(s));
+                        trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(me));
                     }
                     named_bar_sync(1, 128);
                     const bool owned = valid && owner == me;

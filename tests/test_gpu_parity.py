@@ -272,3 +272,47 @@ def test_full_size_llama_tp8_row_sampled(pattern):
                 lrows = sorted(int(x) for x in rng.integers(0, rpr, 2))
                 want = O.rs_rows(p.m, p.n, p.k, p.tp, a, b, r, lrows)
                 assert O.max_rel_error(got[r][lrows], want) <= 8e-3
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_causality_from_device_trace_allgather(seed):
+    """Reference acceptance criterion 2 / test_engine.cpp:190-213 on the device:
+    under jitter, every tile's compute_start follows the signal_set of the
+    a_agg group it consumed (both stamped with %globaltimer)."""
+    p = fx.ProblemSpec(1024, 2048, 256, 4, AG)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=3)
+        got = _run(comm, p, True, ag_engine=2, trace=1, interleave_seed=seed)
+        want = _oracle(p, a, b)
+        for r in range(p.tp):
+            assert O.max_rel_error(got[r], want[r]) <= H.tol(True, p.k)
+            ev = fx.comm.read_trace(comm, r, p)
+            sets = {}
+            for e in ev:
+                if e["event"] == "signal_set" and e["rank"] == r:
+                    sets[e["target"]] = max(sets.get(e["target"], -1), e["logical_ts"])
+            starts = [e for e in ev if e["event"] == "compute_start" and e["rank"] == r]
+            assert len(starts) == (p.m // 128) * (p.local_cols() // 256)
+            assert len(sets) == p.m // 128
+            for e in starts:
+                assert e["logical_ts"] > sets[e["target"]], e
+
+
+def test_causality_from_device_trace_reduce_scatter():
+    """Owners reduce a tile only after every source's tile_write for it."""
+    p = fx.ProblemSpec(2048, 512, 512, 8, RS)
+    with H.make_comm(p) as comm:
+        H.upload(comm, p, seed=4)
+        _run(comm, p, True, trace=1, interleave_seed=5)
+        writes, reduces = {}, []
+        for r in range(p.tp):
+            for e in fx.comm.read_trace(comm, r, p):
+                key = (e["tile_row"], e["tile_col"])
+                if e["event"] == "tile_write":
+                    writes.setdefault((e["target"], key), []).append(e["ts"])
+                elif e["event"] == "reduce":
+                    reduces.append((e["rank"], key, e["ts"]))
+        assert len(reduces) == (p.m // 128) * (p.n // 256)
+        for owner, key, t in reduces:  # all ranks share one GPU: one %globaltimer
+            w = writes.get((owner, key), [])
+            assert len(w) == p.tp - 1 and max(w) <= t, (owner, key)
