@@ -189,6 +189,25 @@ int flux_local_gemm(flux_comm* comm, const flux_problem* problem, const flux_opt
  * collective then the same GEMM kernel (or GEMM then serial reduce). */
 int flux_nonoverlap(flux_comm* comm, const flux_problem* problem, const flux_opts* opts,
                     void* const* streams);
+/* Caller-owned operands (e.g. PyTorch tensors): per rank (tp entries in
+ * single-process mode, 1 in IPC mode); NULL ptr fields use the library's
+ * buffers. A = the rank's A shard, B = its weight shard [out, in] (K-major),
+ * C = its output; element (i, j) at ptr + (i*ld + j)*elem_size, ld in elements,
+ * rows 16-byte aligned. Only the symmetric state (a_agg, staging, flags) must
+ * live in the library heap. For GEMM-RS a caller C needs m/tp % 128 == 0. */
+typedef struct {
+    void* ptr;
+    int ld;
+} flux_matrix;
+typedef struct {
+    flux_matrix a, b, c;
+} flux_operands;
+int flux_ag_gemm_ex(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
+                    int rows_per_comm_tile, int transfer, int swizzle_on, const flux_opts* opts,
+                    void* const* streams, const flux_operands* operands);
+int flux_gemm_rs_ex(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
+                    int write_mode, int swizzle_on, const flux_opts* opts, void* const* streams,
+                    const flux_operands* operands);
 /* Joins all work of the last operator; returns FLUX_ERR_DEADLOCK if a device
  * wait timed out (message names the flag, as spin_wait does, engine.cpp:149-162). */
 int flux_sync(flux_comm* comm);

@@ -73,6 +73,14 @@ class CommOpts(C.Structure):
     _fields_ = [("heap_bytes", C.c_size_t)]
 
 
+class Matrix(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("ld", C.c_int)]
+
+
+class Operands(C.Structure):
+    _fields_ = [("a", Matrix), ("b", Matrix), ("c", Matrix)]
+
+
 class BufferDesc(C.Structure):
     _fields_ = [("ptr", C.c_void_p), ("rows", C.c_int), ("cols", C.c_int), ("ld", C.c_int),
                 ("dtype", C.c_int)]
@@ -109,6 +117,10 @@ _SIGS = {
     "flux_ag_gemm": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, C.c_int, C.c_int, _P(Opts),
                                _P(C.c_void_p)]),
     "flux_gemm_rs": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, C.c_int, _P(Opts), _P(C.c_void_p)]),
+    "flux_ag_gemm_ex": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, C.c_int, C.c_int, _P(Opts),
+                                  _P(C.c_void_p), _P(Operands)]),
+    "flux_gemm_rs_ex": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, C.c_int, _P(Opts), _P(C.c_void_p),
+                                  _P(Operands)]),
     "flux_local_gemm": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
     "flux_nonoverlap": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
     "flux_sync": (C.c_int, [C.c_void_p]),

@@ -108,6 +108,21 @@ class _CAI:
         }
 
 
+def _mat(t) -> N.Matrix:
+    if t is None:
+        return N.Matrix(None, 0)
+    assert t.dim() == 2 and t.stride(1) == 1, "operands must be row-major 2-D views"
+    return N.Matrix(t.data_ptr(), t.stride(0))
+
+
+def _operands(per_rank):
+    arr = (N.Operands * len(per_rank))()
+    for i, abc in enumerate(per_rank):
+        a, b, c = abc if abc is not None else (None, None, None)
+        arr[i] = N.Operands(_mat(a), _mat(b), _mat(c))
+    return arr
+
+
 class Communicator:
     """Symmetric-heap communicator over `tp` ranks.
 
@@ -169,6 +184,20 @@ class Communicator:
         o = opts if opts is not None else N.default_opts()
         N.check(N.lib().flux_ag_gemm(self._h, C.byref(problem.c()), C.byref(tile.c()), rows_per_comm_tile,
                                      transfer, int(swizzle), C.byref(o), N.stream_array(streams)))
+
+    def ag_gemm_ex(self, problem: ProblemSpec, tile: TileShape, operands, rows_per_comm_tile: int = 0,
+                   transfer: int = N.PULL, swizzle: bool = True, opts: Optional[N.Opts] = None, streams=None) -> None:
+        """ag_gemm on caller-owned operands: `operands` is a list (one per rank
+        this process drives) of (a, b, c) tensors or None (library buffer)."""
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_ag_gemm_ex(self._h, C.byref(problem.c()), C.byref(tile.c()), rows_per_comm_tile, transfer,
+                                        int(swizzle), C.byref(o), N.stream_array(streams), _operands(operands)))
+
+    def gemm_rs_ex(self, problem: ProblemSpec, tile: TileShape, operands, write_mode: int = N.WRITE_ALLTOALL,
+                   swizzle: bool = True, opts: Optional[N.Opts] = None, streams=None) -> None:
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_gemm_rs_ex(self._h, C.byref(problem.c()), C.byref(tile.c()), write_mode, int(swizzle),
+                                        C.byref(o), N.stream_array(streams), _operands(operands)))
 
     def gemm_rs(self, problem: ProblemSpec, tile: TileShape, write_mode: int = N.WRITE_ALLTOALL,
                 swizzle: bool = True, opts: Optional[N.Opts] = None, streams=None) -> None:

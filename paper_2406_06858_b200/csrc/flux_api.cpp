@@ -513,7 +513,14 @@ struct OpCommon {
     uint64_t timeout_ns;
     int fused_reduce = 0;  // RS FusedReduce in arrival order (red.add into the owner accumulator)
     int rs_last_arriver = 0;  // RS with ownership blocks narrower than a tile
+    const flux_operands* ops = nullptr;  // caller-provided operands (per rank; one entry in IPC mode)
 };
+
+// Caller-provided operand views of rank r (nullptr fields = library buffers).
+const flux_operands* operands_of(flux_comm* c, const OpCommon& oc, int r) {
+    if (!oc.ops) return nullptr;
+    return c->ipc ? &oc.ops[0] : &oc.ops[r];
+}
 
 OpCommon common_opts(const flux_opts* opts) {
     OpCommon oc;
@@ -544,11 +551,24 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         std::memset(&prm, 0, sizeof(prm));
         for (size_t li = 0; li < g.size(); ++li) {
             const RankState& rs = c->ranks[g[li]];
+            const flux_operands* ops = operands_of(c, oc, g[li]);
             const Region& A = (mode == kModeAG || plain_on_agg) ? L.a_agg : L.a_shard;
-            FLUX_TRY(make_tmap(&prm.tma_a[li], rs.heap + A.off, A.rows, lk, A.ld, kBM));
-            FLUX_TRY(make_tmap(&prm.tma_b[li], rs.heap + L.b.off, lc, lk, L.b.ld, kBN / cg));
-            if (plain_f32_to_staging) prm.c[li] = rs.heap + partial_off;  // full [m, n] fp32 partial
-            else prm.c[li] = rs.heap + L.c32.off;
+            if (A.off == L.a_shard.off && ops && ops->a.ptr)
+                FLUX_TRY(make_tmap(&prm.tma_a[li], ops->a.ptr, A.rows, lk, ops->a.ld, kBM));
+            else
+                FLUX_TRY(make_tmap(&prm.tma_a[li], rs.heap + A.off, A.rows, lk, A.ld, kBM));
+            if (ops && ops->b.ptr) FLUX_TRY(make_tmap(&prm.tma_b[li], ops->b.ptr, lc, lk, ops->b.ld, kBN / cg));
+            else FLUX_TRY(make_tmap(&prm.tma_b[li], rs.heap + L.b.off, lc, lk, L.b.ld, kBN / cg));
+            if (plain_f32_to_staging) {
+                prm.c[li] = rs.heap + partial_off;  // full [m, n] partial
+                prm.ldc_l[li] = L.ld_stage;
+            } else if (ops && ops->c.ptr) {
+                prm.c[li] = ops->c.ptr;
+                prm.ldc_l[li] = ops->c.ld;
+            } else {
+                prm.c[li] = rs.heap + L.c32.off;
+                prm.ldc_l[li] = L.c32.ld;
+            }
             prm.global_rank[li] = g[li];
             prm.ag_flags[li] = at<uint32_t>(rs, kAgFlagOffset);
             prm.ctrl[li] = at<uint32_t>(rs, kCtrlErr);
@@ -595,13 +615,8 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.m = m_rows;
         prm.n = lc;
         prm.k = lk;
-        if (plain_f32_to_staging) {
-            prm.ldc = L.ld_stage;
-            prm.out_f32 = oc.o.out_dtype == FLUX_F32 ? 1 : 0;
-        } else {
-            prm.ldc = L.c32.ld;
-            prm.out_f32 = oc.o.out_dtype == FLUX_F32 ? 1 : 0;
-        }
+        prm.ldc = L.c32.ld;
+        prm.out_f32 = oc.o.out_dtype == FLUX_F32 ? 1 : 0;
         prm.tiles_n = (lc + kBN - 1) / kBN;
         prm.tp = p->tp;
         prm.rpr = rows_per_rank(p);
@@ -1002,6 +1017,11 @@ static int check_heap(flux_comm* c, const flux_problem* p) {
 
 int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer, int swizzle_on,
                  const flux_opts* opts, void* const* streams) {
+    return flux_ag_gemm_ex(c, p, tile, rpct, transfer, swizzle_on, opts, streams, nullptr);
+}
+
+int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer, int swizzle_on,
+                    const flux_opts* opts, void* const* streams, const flux_operands* operands) {
     FLUX_TRY(check_comm(c));
     if (p && p->pattern != FLUX_ALLGATHER_GEMM)
         return fail(FLUX_ERR_CONFIG, "run_fused_allgather_gemm requires AllGatherGemm pattern");
@@ -1017,7 +1037,8 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     // Directory check: every peer this rank touches must be mapped (workspace.cpp:56-65).
     for (int r : mine)
         for (int q = 0; q < tp; ++q) FLUX_TRY(check_directory(c, r, q));
-    const OpCommon oc = common_opts(opts);
+    OpCommon oc = common_opts(opts);
+    oc.ops = operands;
     const Layout L = layout_for(p);
     c->last_launches = 0;
     c->kernel_events_used = 0;
@@ -1039,7 +1060,13 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         // Piece geometry: whole contiguous rows up to kPieceBytes, or column splits of long rows.
         const int row_bytes = lk * 2;
         int piece_rows = 1, pieces_per_row = (row_bytes + kPieceBytes - 1) / kPieceBytes;
-        if (row_bytes <= kPieceBytes && L.a_shard.ld == lk && L.a_agg.ld == lk) {
+        // (Every rank must reach the same geometry: SPMD callers pass operands of one shape.)
+        bool contiguous = L.a_agg.ld == lk;
+        for (int r : mine) {
+            const flux_operands* ops = operands_of(c, oc, r);
+            if ((ops && ops->a.ptr ? ops->a.ld : L.a_shard.ld) != lk) contiguous = false;
+        }
+        if (row_bytes <= kPieceBytes && contiguous) {
             pieces_per_row = 1;
             while (piece_rows * 2 <= kBM && piece_rows * 2 * row_bytes <= kPieceBytes && rpr % (piece_rows * 2) == 0)
                 piece_rows *= 2;
@@ -1116,14 +1143,19 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
             prm.ag_slot_index = groups;
             prm.ag_mult = mult;
             prm.slot_pieces = static_cast<uint32_t>((rpr / piece_rows) * (piece_rows > 1 ? 1 : pieces_per_row));
-            prm.src_ld_bytes = static_cast<long long>(L.a_shard.ld) * 2;
+            for (size_t li = 0; li < g.size(); ++li) {
+                const flux_operands* ops = operands_of(c, oc, g[li]);
+                prm.src_ld_l[li] = static_cast<long long>(ops && ops->a.ptr ? ops->a.ld : L.a_shard.ld) * 2;
+            }
             prm.dst_ld_bytes = static_cast<long long>(L.a_agg.ld) * 2;
             for (int q = 0; q < tp; ++q) {
                 prm.agg_src[q] = c->ranks[q].heap + L.a_agg.off;
                 prm.ag_ctr[q] = at<uint32_t>(c->ranks[q], ctr_off);
             }
             for (size_t li = 0; li < g.size(); ++li) {
-                prm.shard_src[li] = c->ranks[g[li]].heap + L.a_shard.off;
+                const flux_operands* ops = operands_of(c, oc, g[li]);
+                prm.shard_src[li] = ops && ops->a.ptr ? static_cast<const char*>(ops->a.ptr)
+                                                      : c->ranks[g[li]].heap + L.a_shard.off;
                 prm.a_dst[li] = c->ranks[g[li]].heap + L.a_agg.off;
             }
             return FLUX_OK;
@@ -1200,8 +1232,11 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
         // Local shard -> own a_agg slot, local flags preset (engine.cpp:469-472).
         for (int r : g) {
             RankState& rs = c->ranks[r];
-            FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes,
-                               rs.heap + L.a_shard.off, shard_pitch, rpr));
+            const flux_operands* ops = operands_of(c, oc, r);
+            const char* shard = ops && ops->a.ptr ? static_cast<const char*>(ops->a.ptr) : rs.heap + L.a_shard.off;
+            const size_t pitch = ops && ops->a.ptr ? static_cast<size_t>(ops->a.ld) * 2 : shard_pitch;
+            FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes, shard,
+                               pitch, rpr));
             FLUX_TRY(write_value(cs, rs.heap + kCtrlReady, e));
             for (int f = r * rpr / rpct; f < (r + 1) * rpr / rpct; ++f)
                 FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + f, e));
@@ -1230,10 +1265,10 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
                         FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
                     } else {
                         if (first && !in_group(q)) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlKdone, e - 1));
+                        // Push reads from my own a_agg slot (already holds my shard).
                         FLUX_TRY(copy_rows(cs, qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
-                                           rowbytes,
-                                           rs.heap + L.a_shard.off + static_cast<size_t>(d.row_begin - r * rpr) * shard_pitch,
-                                           shard_pitch, d.rows));
+                                           rowbytes, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
+                                           rowbytes, d.rows));
                         FLUX_TRY(write_value(cs, at<uint32_t>(qs, kAgFlagOffset) + d.row_begin / rpct, e));
                     }
                 }
@@ -1263,6 +1298,11 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
 
 int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
                  const flux_opts* opts, void* const* streams) {
+    return flux_gemm_rs_ex(c, p, tile, write_mode, swizzle_on, opts, streams, nullptr);
+}
+
+int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
+                    const flux_opts* opts, void* const* streams, const flux_operands* operands) {
     FLUX_TRY(check_comm(c));
     if (p && p->pattern != FLUX_GEMM_REDUCESCATTER)
         return fail(FLUX_ERR_CONFIG, "run_fused_gemm_reducescatter requires GemmReduceScatter pattern");
@@ -1318,6 +1358,12 @@ int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     // waits; the last of the tp arrivals of each tile reduces it (deterministic).
     const int tiles_n = (p->n + kBN - 1) / kBN;
     oc.rs_last_arriver = (rpr % kBM != 0 && !oc.fused_reduce) ? 1 : 0;
+    oc.ops = operands;
+    if (operands && oc.rs_last_arriver)
+        for (int r : mine)
+            if (operands_of(c, oc, r)->c.ptr)
+                return fail(FLUX_ERR_CONFIG,
+                            "caller-provided C needs ownership blocks of whole 128-row tiles (m/tp % 128 == 0)");
     if (oc.rs_last_arriver && static_cast<size_t>(tiles) > kRsCtrCap)
         return fail(FLUX_ERR_CONFIG, "too many output tiles for the arrival counters");
     const int interleave = aligned ? kInterleaveRankTail : (oc.rs_last_arriver ? kInterleaveRank : kInterleaveStep);

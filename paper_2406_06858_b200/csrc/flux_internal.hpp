@@ -71,7 +71,8 @@ struct GemmParams {
     const uint32_t* order;                 // tile schedule (pack_tile entries)
     int num_tiles;
     int m, n, k;                   // per-rank GEMM: A [m, k], B [n, k], C [m, n]
-    int ldc;                       // C row pitch (elements)
+    int ldc;                       // C row pitch (elements) of the library's C buffers (RS peers' C)
+    int ldc_l[kMaxRanks];          // per local slot: C row pitch of the C it writes (caller-provided or library)
     int out_f32;                   // C element type
     int tiles_n;                   // ceil(n / kBN)
     int tp, rpr;                   // TP degree, rows per rank
@@ -90,7 +91,8 @@ struct GemmParams {
     int piece_rows;                // rows per piece chunk (contiguous rows), >= 1
     int pieces_per_row;            // column splits of one row (row bytes > kPieceBytes)
     int row_bytes;                 // k * 2
-    long long src_ld_bytes, dst_ld_bytes;  // A shard / a_agg row pitch in bytes
+    long long dst_ld_bytes;        // a_agg row pitch in bytes
+    long long src_ld_l[kMaxRanks]; // per local slot: A shard row pitch in bytes
     const char* agg_src[kMaxRanks];    // per GLOBAL rank: its a_agg (peer pointers; pull source)
     const char* shard_src[kMaxRanks];  // per local slot: its own A shard (local piece source)
     char* a_dst[kMaxRanks];            // per local slot: its a_agg

@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 const int g = row0 / kBM;
                 const char* src;
                 if (q == me) {
-                    src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_bytes;
+                    src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
                 } else {
                     if (q != checked_src) {
                         // Publish everything in flight before blocking: another CTA may be
@@ -677,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         float v[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                        store_row<32>(p.c[l], static_cast<long long>(row) * p.ldc + col, col, p.n,
+                        store_row<32>(p.c[l], static_cast<long long>(row) * p.ldc_l[l] + col, col, p.n,
                                     p.out_f32, v);
                     }
                 }
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                     acc[j + 2] = v.z + __uint_as_float(r[j + 2]);
                                     acc[j + 3] = v.w + __uint_as_float(r[j + 3]);
                                 }
-                                store_row<32>(p.c[l], static_cast<long long>(row - me * p.rpr) * p.ldc + col, col,
+                                store_row<32>(p.c[l], static_cast<long long>(row - me * p.rpr) * p.ldc_l[l] + col, col,
                                               p.n, p.out_f32, acc);
                             }
                         }
@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                             }
                                         }
                                     }
-                                    store_row<16>(p.c[l], lrow * p.ldc + col + h * 16, col + h * 16, p.n,
+                                    store_row<16>(p.c[l], lrow * p.ldc_l[l] + col + h * 16, col + h * 16, p.n,
                                                   p.out_f32, acc);
                                 }
                             }

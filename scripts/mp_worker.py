@@ -53,6 +53,23 @@ for pat, m, n, k, engine in cases:
     want = O.dense_oracle(pat, m, n, k, world, a_all, b_all)[rank]
     results[f"{pat}-{m}-{n}-{k}-e{engine}"] = (O.max_rel_error(got, want), H.tol(True, k))
     dist.barrier()
+# The PyTorch custom ops on caller-owned tensors (torch.ops.flux_b200.*).
+from paper_2406_06858_b200 import torch_ops  # noqa: E402
+
+cid = torch_ops.register(comm)
+for pat, m, n, k in [(fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384), (fx.GEMM_REDUCESCATTER, 256 * world, 512, 128 * world),
+                     (fx.GEMM_REDUCESCATTER, 8 * world, 512, 128 * world)]:
+    a_bits, bt_bits = O.rank_inputs_bits(pat, m, n, k, world, 11, rank)
+    x = torch.from_numpy(a_bits.view(np.int16)).cuda().view(torch.bfloat16)
+    w = torch.from_numpy(bt_bits.view(np.int16)).cuda().view(torch.bfloat16)
+    dist.barrier()
+    out = (torch.ops.flux_b200.ag_gemm(x, w, cid) if pat == fx.ALLGATHER_GEMM
+           else torch.ops.flux_b200.gemm_rs(x, w, cid))
+    torch.cuda.synchronize()
+    a_all, b_all = zip(*[O.rank_inputs(pat, m, n, k, world, 11, r, True) for r in range(world)])
+    want = O.dense_oracle(pat, m, n, k, world, a_all, b_all)[rank]
+    results[f"torchop-{pat}-{m}-{n}-{k}"] = (O.max_rel_error(out.double().cpu().numpy(), want), H.tol(False, k))
+    dist.barrier()
 comm.close()
 print("RESULT", rank, json.dumps(results), flush=True)
 dist.destroy_process_group()

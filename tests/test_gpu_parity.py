@@ -316,3 +316,36 @@ def test_causality_from_device_trace_reduce_scatter():
         for owner, key, t in reduces:  # all ranks share one GPU: one %globaltimer
             w = writes.get((owner, key), [])
             assert len(w) == p.tp - 1 and max(w) <= t, (owner, key)
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_caller_owned_operands(engine):
+    """flux_ag_gemm_ex / flux_gemm_rs_ex on caller tensors (weights outside the
+    symmetric heap, padded A pitch, caller C) match the library-buffer path."""
+    tp = 4
+    p = fx.ProblemSpec(1024, 2048, 320, tp, AG)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=8)
+        want = _oracle(p, a, b)
+        ops = []
+        for r in range(tp):
+            wide = torch.zeros(p.rows_per_rank(), 384, dtype=torch.bfloat16, device="cuda")
+            wide[:, :p.k].copy_(comm.tensor(r, N.BUF_A_SHARD, p))
+            a_view = wide[:, :p.k]                       # ld 384 != k
+            w = comm.tensor(r, N.BUF_B_SHARD, p).contiguous()
+            c = torch.empty(p.m, p.local_cols(), dtype=torch.float32, device="cuda")
+            ops.append((a_view, w, c))
+        comm.ag_gemm_ex(p, fx.TileShape(256, 256), ops, opts=fx.default_opts(out_dtype=fx.F32, ag_engine=engine))
+        comm.sync()
+        for r in range(tp):
+            assert O.max_rel_error(ops[r][2].double().cpu().numpy(), want[r]) <= H.tol(True, p.k)
+    q = fx.ProblemSpec(1024, 512, 512, tp, RS)
+    with H.make_comm(q) as comm:
+        a, b = H.upload(comm, q, seed=9)
+        want = _oracle(q, a, b)
+        ops = [(comm.tensor(r, N.BUF_A_SHARD, q).contiguous(), comm.tensor(r, N.BUF_B_SHARD, q).contiguous(),
+                torch.empty(q.rows_per_rank(), q.n, dtype=torch.float32, device="cuda")) for r in range(tp)]
+        comm.gemm_rs_ex(q, fx.TileShape(256, 512), ops, opts=fx.default_opts(out_dtype=fx.F32))
+        comm.sync()
+        for r in range(tp):
+            assert O.max_rel_error(ops[r][2].double().cpu().numpy(), want[r]) <= H.tol(True, q.k)

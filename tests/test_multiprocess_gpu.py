@@ -24,6 +24,6 @@ def test_two_processes_ipc_match_oracle():
     assert len(lines) == 2
     for line in lines:
         res = json.loads(line.split(" ", 2)[2])
-        assert len(res) == 4
+        assert len(res) == 7
         for case, (err, tol) in res.items():
             assert err <= tol, (case, err, tol)
