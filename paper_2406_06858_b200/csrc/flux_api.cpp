@@ -479,6 +479,18 @@ cudaStream_t stream_for(flux_comm* c, int rank, void* const* streams) {
 
 // Tile schedules are immutable: upload each distinct table once per device and
 // reuse it (no host sync on the launch path).
+int mark_op_done(flux_comm* c, void* const* streams, uint32_t e) {
+    if (!c->ipc) return FLUX_OK;
+    for (int r = 0; r < c->tp; ++r) {
+        if (!c->ranks[r].local) continue;
+        FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
+        cudaStream_t s = stream_for(c, r, streams);
+        FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlDone, e));
+        FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlKdone, e));
+    }
+    return FLUX_OK;
+}
+
 int upload_order(flux_comm* c, int device, const std::vector<uint32_t>& order, uint32_t** out) {
     auto key = std::make_pair(device, order);
     auto it = c->order_cache.find(key);
@@ -515,6 +527,11 @@ struct OpCommon {
     int rs_last_arriver = 0;  // RS with ownership blocks narrower than a tile
     const flux_operands* ops = nullptr;  // caller-provided operands (per rank; one entry in IPC mode)
 };
+
+// Cross-process operator boundary (IPC mode): every operator stamps `done` and
+// `kdone` with its epoch after its kernel, so a later operator of any kind can
+// wait for "peers finished epoch e-1" regardless of what e-1 was.
+int mark_op_done(flux_comm* c, void* const* streams, uint32_t e);
 
 // Caller-provided operand views of rank r (nullptr fields = library buffers).
 const flux_operands* operands_of(flux_comm* c, const OpCommon& oc, int r) {
@@ -1388,7 +1405,7 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
             (void)other_device;
         }
     }
-    return FLUX_OK;
+    return mark_op_done(c, streams, c->epoch);
 }
 
 int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
@@ -1465,7 +1482,7 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
         }
         FLUX_TRY(launch_groups(c, p, kModePlain, oc, streams, seq, 0,
                                oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, cg, true));
-        return FLUX_OK;
+        return mark_op_done(c, streams, e);
     }
     // GEMM-RS: full fp32 partial into this epoch's staging parity, then the
     // serial source-ordered reduce once every rank's GEMM finished.
@@ -1506,7 +1523,7 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
         ++c->last_launches;
         FLUX_CUDA(cudaEventRecord(rs.kernel_evt, s));
     }
-    return FLUX_OK;
+    return mark_op_done(c, streams, e);
 }
 
 int flux_sync(flux_comm* c) {
