@@ -96,10 +96,20 @@ int write_value(cudaStream_t s, void* addr, uint32_t v) {
     return FLUX_OK;
 }
 
+// Stream-side wait for an epoch-stamped word (wrap-safe >=). The wait is
+// followed by a flush of outstanding remote writes where the device supports
+// it, so data written by peers before they stamped the word is visible to the
+// work queued after the wait.
 int wait_value_geq(cudaStream_t s, const void* addr, uint32_t v) {
     if (v == 0) return FLUX_OK;  // epoch 0 is always satisfied
+    static const unsigned flush = [] {
+        int dev = 0, can = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&can, cudaDevAttrCanFlushRemoteWrites, dev);
+        return can ? static_cast<unsigned>(CU_STREAM_WAIT_VALUE_FLUSH) : 0u;
+    }();
     CUresult r = driver().wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
-                                 CU_STREAM_WAIT_VALUE_GEQ);
+                                 CU_STREAM_WAIT_VALUE_GEQ | flush);
     if (r != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "cuStreamWaitValue32 failed (" + S(r) + ")");
     return FLUX_OK;
 }
