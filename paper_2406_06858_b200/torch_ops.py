@@ -44,7 +44,11 @@ def init_process_group_communicator(max_problem: ProblemSpec, group=None) -> int
 
 
 def _stream():
-    return [torch.cuda.current_stream().cuda_stream]
+    """torch's current stream as a cudaStream_t. torch reports the legacy
+    default stream as 0, which the C ABI reads as "library stream": pass
+    cudaStreamLegacy (0x1) instead so the op is ordered with torch's work."""
+    s = torch.cuda.current_stream().cuda_stream
+    return [s if s != 0 else 1]
 
 
 @torch.library.custom_op("flux_b200::ag_gemm", mutates_args=())
