@@ -168,8 +168,10 @@ def default_opts(**kw) -> Opts:
 
 
 def stream_array(streams):
-    """List of raw cudaStream_t ints (or None) -> void*[] (or NULL)."""
+    """List of raw cudaStream_t ints -> void*[]; None -> NULL (library streams).
+    An explicit 0 (torch's legacy default stream) becomes cudaStreamLegacy (0x1):
+    the C ABI reads a NULL entry as "use the library's stream"."""
     if streams is None:
         return None
-    arr = (C.c_void_p * len(streams))(*[s if s else None for s in streams])
+    arr = (C.c_void_p * len(streams))(*[s if s else 1 for s in streams])
     return arr
