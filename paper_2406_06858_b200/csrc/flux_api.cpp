@@ -290,8 +290,13 @@ std::vector<uint32_t> device_sequence(int m, int ncols, int rpr, const std::vect
             for (int c = 0; c < tiles_n; ++c)
                 for (int r = 0; r < rpb; ++r) seq.push_back(pack_tile(slot, b * rpb + r, c));
     } else {
-        for (int r = 0; r < tiles_m; ++r)
-            for (int c = 0; c < tiles_n; ++c) seq.push_back(pack_tile(slot, r, c));
+        // Grouped raster: bands of kRasterRows tile rows walked column by column,
+        // so one wave of CTAs shares a few A row-panels and B column-panels in L2
+        // (plain row-major re-streams all of B for every tile row).
+        constexpr int kRasterRows = 8;
+        for (int r0 = 0; r0 < tiles_m; r0 += kRasterRows)
+            for (int c = 0; c < tiles_n; ++c)
+                for (int r = r0; r < std::min(tiles_m, r0 + kRasterRows); ++r) seq.push_back(pack_tile(slot, r, c));
     }
     return seq;
 }
