@@ -278,7 +278,7 @@ std::vector<int> ag_block_order(const flux_problem* p, int rank, int transfer, b
 // Device tile sequence of one rank over the kBM x kBN grid. When ownership
 // blocks align with device tile rows the reference's block-then-column-major
 // order is reproduced (swizzle.cpp:51-73); otherwise tiles straddle blocks and
-// the order is row-major (every rank walks the same sequence).
+// the order is a grouped raster (every rank walks the same sequence).
 std::vector<uint32_t> device_sequence(int m, int ncols, int rpr, const std::vector<int>& blocks, int tile_m) {
     const int slot = 0;
     const int tiles_m = (m + tile_m - 1) / tile_m, tiles_n = (ncols + kBN - 1) / kBN;
