@@ -279,16 +279,28 @@ std::vector<int> ag_block_order(const flux_problem* p, int rank, int transfer, b
 // blocks align with device tile rows the reference's block-then-column-major
 // order is reproduced (swizzle.cpp:51-73); otherwise tiles straddle blocks and
 // the order is a grouped raster (every rank walks the same sequence).
-std::vector<uint32_t> device_sequence(int m, int ncols, int rpr, const std::vector<int>& blocks, int tile_m) {
+//
+// Blocks of few tile rows re-stream every column panel of B per block, so
+// `group_blocks` consecutive blocks of the visit order may share one
+// column-major sweep (a super-block); `last_alone` keeps the final block on its
+// own (RS: the owner's local block must stay last).
+std::vector<uint32_t> device_sequence(int m, int ncols, int rpr, const std::vector<int>& blocks, int tile_m,
+                                      int group_blocks = 1, bool last_alone = false) {
     const int slot = 0;
     const int tiles_m = (m + tile_m - 1) / tile_m, tiles_n = (ncols + kBN - 1) / kBN;
     std::vector<uint32_t> seq;
     seq.reserve(static_cast<size_t>(tiles_m) * tiles_n);
     if (!blocks.empty() && rpr % tile_m == 0) {
         const int rpb = rpr / tile_m;
-        for (int b : blocks)
+        const int nb = static_cast<int>(blocks.size());
+        const int grouped = last_alone ? nb - 1 : nb;
+        for (int b0 = 0; b0 < nb;) {
+            const int g = b0 < grouped ? std::min(std::max(1, group_blocks), grouped - b0) : 1;
             for (int c = 0; c < tiles_n; ++c)
-                for (int r = 0; r < rpb; ++r) seq.push_back(pack_tile(slot, b * rpb + r, c));
+                for (int bi = b0; bi < b0 + g; ++bi)
+                    for (int r = 0; r < rpb; ++r) seq.push_back(pack_tile(slot, blocks[bi] * rpb + r, c));
+            b0 += g;
+        }
     } else {
         // Grouped raster: bands of kRasterRows tile rows walked column by column,
         // so one wave of CTAs shares a few A row-panels and B column-panels in L2
@@ -299,6 +311,14 @@ std::vector<uint32_t> device_sequence(int m, int ncols, int rpr, const std::vect
                 for (int r = r0; r < std::min(tiles_m, r0 + kRasterRows); ++r) seq.push_back(pack_tile(slot, r, c));
     }
     return seq;
+}
+
+// Blocks per super-block: sweep at least 4 tile rows per column panel of B
+// (FLUX_GROUP_BLOCKS overrides, 1 = the reference's strict block order).
+int ag_group_blocks(int rpr, int tile_m) {
+    if (const char* env = std::getenv("FLUX_GROUP_BLOCKS")) return std::max(1, std::atoi(env));
+    const int rpb = std::max(1, rpr / tile_m);
+    return std::max(1, 4 / rpb);
 }
 
 // ---------------------------------------------------------------------------
@@ -1145,7 +1165,8 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
             // Pieces always move in arrival order (own block first, then the ring);
             // the swizzle only decides the order the tiles consume them.
             blocks[r] = ag_block_order(p, r, FLUX_PULL, true, rpct);
-            seq[r] = device_sequence(p->m, local_cols(p), rpr, swizzle_on ? blocks[r] : std::vector<int>{}, kBM * cg);
+            seq[r] = device_sequence(p->m, local_cols(p), rpr, swizzle_on ? blocks[r] : std::vector<int>{}, kBM * cg,
+                                     ag_group_blocks(rpr, kBM * cg));
         }
         const bool step_major = oc.o.emulated_order == 1;
         auto extra = [&](const std::vector<int>& g, GemmParams& prm) -> int {
@@ -1227,7 +1248,7 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     std::vector<std::vector<uint32_t>> seq(tp);
     for (int r : mine)
         seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct),
-                                 kBM * cg);
+                                 kBM * cg, ag_group_blocks(rpr, kBM * cg));
     auto launch_kernel = [&]() {
         return launch_groups(c, p, kModeAG, oc, streams, seq, rpct,
                              oc.o.emulated_order == 1 ? kInterleaveStep : kInterleaveRank, cg);
@@ -1377,7 +1398,7 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
         std::vector<int> blocks;
         if (swizzle_on) blocks = block_order(FLUX_SWIZZLE_RANK_SHIFTED, r, tp, oc.o.shift_offset, {});
         else for (int i = 0; i < tp; ++i) blocks.push_back(i);
-        seq[r] = device_sequence(p->m, p->n, rpr, blocks, kBM * cg);
+        seq[r] = device_sequence(p->m, p->n, rpr, blocks, kBM * cg, ag_group_blocks(rpr, kBM * cg), swizzle_on != 0);
     }
     // Deadlock freedom of the single-device multi-rank launch: a tile may only
     // wait on partials scheduled before it. With ownership blocks aligned to
