@@ -349,3 +349,41 @@ def test_caller_owned_operands(engine):
         comm.sync()
         for r in range(tp):
             assert O.max_rel_error(ops[r][2].double().cpu().numpy(), want[r]) <= H.tol(True, q.k)
+
+
+def test_acceptance_randomized_equivalence():
+    """Reference acceptance criterion 1 (acceptance.cpp:67-118) on the GPU: 200
+    randomized cases, tp in {1,2,4,8}, both patterns, every transfer / write
+    mode and both CTA-group variants, against the oracle."""
+    rng = np.random.default_rng(42)
+    worst = 0.0
+    for i in range(200):
+        pat = RS if i % 2 else AG
+        tp = int(rng.choice([1, 2, 4, 8]))
+        rpr = int(rng.choice([8, 16, 40, 128, 256]))
+        m = rpr * tp
+        if pat == AG:
+            n = tp * int(rng.choice([8, 24, 128, 256]))
+            k = int(rng.choice([8, 16, 72, 136, 512]))
+        else:
+            n = int(rng.choice([8, 24, 128, 256, 300]))
+            k = tp * int(rng.choice([8, 16, 72, 128]))
+        p = fx.ProblemSpec(m, n, k, tp, pat)
+        kw = {"cta_group": int(rng.choice([0, 1, 2]))}
+        if pat == AG:
+            kw["ag_engine"] = int(rng.choice([1, 2]))
+            mode = {"transfer": fx.PUSH if (kw["ag_engine"] == 1 and rng.random() < 0.3) else fx.PULL,
+                    "swizzle": bool(rng.random() < 0.8)}
+        else:
+            mode = {"write_mode": int(rng.choice([fx.WRITE_ALLTOALL, fx.FUSED_REDUCE])),
+                    "swizzle": bool(rng.random() < 0.8)}
+            kw["deterministic_reduce"] = int(rng.random() < 0.5)
+        with H.make_comm(p) as comm:
+            a, b = H.upload(comm, p, seed=1000 + i)
+            got = _run(comm, p, True, **mode, **kw)
+            want = _oracle(p, a, b)
+            for r in range(tp):
+                err = O.max_rel_error(got[r], want[r])
+                worst = max(worst, err)
+                assert err <= H.tol(True, p.k), (i, pat, m, n, k, tp, mode, kw, r, err)
+    print("200 randomized cases, worst max_rel_error", worst)
