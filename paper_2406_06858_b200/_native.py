@@ -140,11 +140,12 @@ def lib() -> C.CDLL:
     """Loads libflux_b200.so (raises if it was not built — no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("FLUX_LIB_PATH", LIB_PATH)  # profiling variants only
+        if not os.path.exists(path):
             raise ImportError(
-                f"{LIB_PATH} is missing: build it with `python -m paper_2406_06858_b200.build` "
+                f"{path} is missing: build it with `python -m paper_2406_06858_b200.build` "
                 "(the fused operators have no CPU fallback)")
-        l = C.CDLL(LIB_PATH, mode=C.RTLD_LOCAL)
+        l = C.CDLL(path, mode=C.RTLD_LOCAL)
         for name, (res, args) in _SIGS.items():
             fn = getattr(l, name)
             fn.restype = res

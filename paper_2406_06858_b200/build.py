@@ -33,26 +33,34 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra: list[str] | None = None) -> str:
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
     deps += [os.path.join(ROOT, "include", "flux_b200.h"), os.path.join(ROOT, "include", "flux", "overlap.hpp")]
     deps.append(os.path.abspath(__file__))
-    if not force and not _stale(LIB, deps):
-        return LIB
+    if not force and not _stale(out, deps):
+        return out
     cmd = [
         nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
         "-Xcompiler", "-fvisibility=default", "-cudart", "static",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-        "-o", LIB + ".tmp",
+        *(extra or []),
+        "-o", out + ".tmp",
         *[os.path.join(CSRC, s) for s in SOURCES],
         "-lrt", "-ldl", "-lpthread",
     ]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_2406_06858_b200.build [--force] [--variant NAME -DFLAG ...]  (variants: profiling only)
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, flags = sys.argv[i + 1], sys.argv[i + 2:]
+        os.makedirs(os.path.join(HERE, "variants"), exist_ok=True)
+        print(build(force=True, verbose=True, out=os.path.join(HERE, "variants", f"lib_{name}.so"), extra=flags))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

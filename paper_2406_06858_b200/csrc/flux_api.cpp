@@ -365,7 +365,7 @@ Layout layout_for(const flux_problem* p) {
         place(L.a_shard, p->m, lk, FLUX_BF16, 64);
         place(L.b, lc, lk, FLUX_BF16, 64);
         place(L.c32, rpr, lc, FLUX_F32, 32);
-        L.ld_stage = pad_to(lc, 32);
+        L.ld_stage = pad_to(lc, kBN);  // a plane also holds tile-major 128 x 256 partials (RS mode)
         L.stage_plane = static_cast<long long>(rpr) * L.ld_stage;
         L.stage_parity = L.stage_plane * p->tp;
         L.staging.off = off;
@@ -684,6 +684,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.jitter_seed = oc.o.interleave_seed;
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
         prm.rs_last_arriver = mode == kModeRSLast ? 1 : 0;
+        if (const char* env = std::getenv("FLUX_DEBUG")) prm.dbg = std::atoi(env);  // profiling ablations only
         // Join the other local ranks' streams into the launch stream.
         for (size_t li = 0; li < g.size(); ++li) {
             cudaStream_t s = stream_for(c, g[li], streams);

@@ -111,6 +111,7 @@ struct GemmParams {
     uint32_t trace_cap;
     float* fr_acc[kMaxRanks];      // per GLOBAL rank: FusedReduce fp32 accumulator [rpr, ld_stage] (this parity)
     const uint32_t* fr_ready[kMaxRanks];  // per GLOBAL rank: control word, accumulator zeroed at epoch
+    int dbg;                       // profiling ablations (FLUX_DEBUG): 1 skip RS remote stores, 2 skip RS owner reduce
 };
 
 struct RsReduceParams {

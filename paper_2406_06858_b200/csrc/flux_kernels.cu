@@ -398,6 +398,35 @@ __device__ __forceinline__ void reduce_tile_coalesced(const GemmParams& p, int r
     }
 }
 
+// Epilogue staging through shared memory. Warp q owns a 32-row x 32-column
+// fp32 window (4 KiB) whose 16-byte granules are XOR-swizzled by row, so both
+// the row-per-thread writes (TMEM layout) and the row-contiguous reads are
+// bank-conflict free; the reads turn the epilogue's global traffic from 32 rows
+// x 16 B per warp instruction into 4 rows x 128 B (coalesced).
+constexpr int kEpiWarpBytes = 32 * 32 * 4;
+#ifndef FLUX_EPI_U
+#define FLUX_EPI_U 4
+#endif
+constexpr int kEpiU = FLUX_EPI_U;  // coalesced positions per thread per step (x tp loads in flight)
+__device__ __forceinline__ void epi_stage(uint8_t* wbuf, int lane, const uint32_t (&r)[32]) {
+    __syncwarp();  // the previous chunk's reads of this window are done
+    const uint32_t base = smem_u32(wbuf) + static_cast<uint32_t>(lane) * 128u;
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + ((static_cast<uint32_t>(g ^ (lane & 7))) << 4)),
+                     "r"(r[4 * g]), "r"(r[4 * g + 1]), "r"(r[4 * g + 2]), "r"(r[4 * g + 3])
+                     : "memory");
+    __syncwarp();
+}
+// Tile-major WriteAlltoAll staging: float offset of the 128 x 256 partial of
+// output tile (local row lr0 of the owner's block, column tile tn) in a plane.
+__device__ __forceinline__ long long stage_tile_off(long long lr0, int tn, int tiles_n) {
+    return ((lr0 / kBM) * tiles_n + tn) * static_cast<long long>(kBM * kBN);
+}
+__device__ __forceinline__ float4 epi_read(const uint8_t* wbuf, int i, int g) {
+    return *reinterpret_cast<const float4*>(wbuf + i * 128 + ((g ^ (i & 7)) << 4));
+}
+
 }  // namespace
 
 // Per-variant geometry. CG = CTAs cooperating on one MMA tile: 1 (cta_group::1,
@@ -412,7 +441,8 @@ struct Geo {
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagesN = CG == 2 ? 6 : 4;
     static constexpr int kCommBytes = MODE == kModeAG ? 2 * kPieceBytes : 0;  // in-kernel AG staging
-    static constexpr int kSmem = kStagesN * kStageBytes + kCommBytes + 1024 + 256;
+    static constexpr int kEpiBytes = MODE == kModeRS ? 4 * kEpiWarpBytes : 0;  // RS epilogue windows
+    static constexpr int kSmem = kStagesN * kStageBytes + kCommBytes + kEpiBytes + 1024 + 256;
     static constexpr uint32_t kIdescV = make_idesc(kTileM, kBN);
 };
 
@@ -425,7 +455,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     uint8_t* sA = smem;
     uint8_t* sB = smem + G::kStagesN * G::kABytes;
     uint8_t* sComm = sB + G::kStagesN * G::kBBytes;  // 2 x kPieceBytes (AG only)
-    uint64_t* full = reinterpret_cast<uint64_t*>(sComm + G::kCommBytes);
+    uint8_t* sEpi = sComm + G::kCommBytes;           // 4 x 4 KiB epilogue windows (RS only)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + G::kEpiBytes);
     uint64_t* empty = full + G::kStagesN;
     uint64_t* tfull = empty + G::kStagesN;
     uint64_t* tempty = tfull + 2;
@@ -648,6 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         // ===== epilogue: each CTA drains its own 128 TMEM lanes (rows) =====
         const int q = warp - 4;            // TMEM lane quadrant (warp % 4)
         const int et = threadIdx.x - 128;  // epilogue thread 0..127
+        uint8_t* wbuf = sEpi + q * kEpiWarpBytes;
         const uint32_t tempty_leader = CG == 2 ? mapa(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
         int as = 0;
         uint32_t aphase = 0;
@@ -749,31 +781,40 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 // Phase 1: ship remote rows to their owners (Alg. 1 line 5): plain stores
                 // into the owner's staging plane for this source (WriteAlltoAll), or
                 // vector red.add into the owner's fp32 accumulator (FusedReduce).
-                if (__any_sync(0xffffffffu, remote)) {
-                    float* dst = nullptr;
-                    if (remote)
-                        dst = p.fused_reduce
-                                  ? p.fr_acc[owner] + static_cast<long long>(row - owner * p.rpr) * p.ld_stage
-                                  : p.staging[owner] + parity * p.stage_parity + me * p.stage_plane +
-                                        static_cast<long long>(row - owner * p.rpr) * p.ld_stage;
+                // Each 32-column chunk goes TMEM -> registers -> this warp's smem
+                // window -> coalesced global stores (4 rows x 128 B per instruction).
+                if (__any_sync(0xffffffffu, remote) && !(p.dbg & 1)) {
+                    // RS mode: ownership blocks are whole 128-row tiles, so the owner is
+                    // uniform over this CTA's rows. WriteAlltoAll staging is tile-major:
+                    // each (tile, source) partial is one contiguous 128 KiB run in the
+                    // order the owner reads it back (DRAM-page and NVLink friendly).
+                    // FusedReduce also runs with blocks narrower than a tile: its owner
+                    // is per row.
+                    const long long lr0 = row0 - static_cast<long long>(o0) * p.rpr;
+                    float* wdst = p.fused_reduce ? nullptr
+                                                 : p.staging[o0] + parity * p.stage_parity + me * p.stage_plane +
+                                                       stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
                     for (int c = 0; c < kBN / 32; ++c) {
-                        const int col = col0 + c * 32;
-                        if (col >= p.n) break;
+                        const int colc = col0 + c * 32;
+                        if (colc >= p.n) break;  // warp-uniform
                         uint32_t r[32];
                         tmem_ld32(tbase + c * 32, r);
                         tmem_ld_wait();
-                        if (remote) {
+                        epi_stage(wbuf, lane, r);
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int i = it * 4 + (lane >> 3), g = lane & 7;
+                            const int col = colc + g * 4;
+                            const int grow = row0 + q * 32 + i;
+                            if (grow >= p.m || col >= p.n) continue;
+                            const float4 v = epi_read(wbuf, i, g);
                             if (p.fused_reduce) {
-#pragma unroll
-                                for (int j = 0; j < 32; j += 4)
-                                    red_add_f4(dst + col + j, __uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                               __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                                const int o = grow / p.rpr;
+                                if (o != me)
+                                    red_add_f4(p.fr_acc[o] + (grow - static_cast<long long>(o) * p.rpr) * p.ld_stage + col,
+                                               v.x, v.y, v.z, v.w);
                             } else {
-                                float4* d4 = reinterpret_cast<float4*>(dst + col);
-#pragma unroll
-                                for (int j = 0; j < 32; j += 4)
-                                    d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                                *reinterpret_cast<float4*>(wdst + c * 4096 + it * 128 + lane * 4) = v;
                             }
                         }
                     }
@@ -791,7 +832,24 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 }
                 // Phase 2: owned rows = source-ordered sum of all partials.
                 const bool mine_in_tile = (me >= o0 && me <= o1);
-                if (mine_in_tile) {
+                if (mine_in_tile && (p.dbg & 2)) {
+                    // Ablation: the owner stores only its own accumulator (no waits, no reduce).
+                    const bool owned = valid && owner == me;
+                    for (int c = 0; c < kBN / 32; ++c) {
+                        const int col = col0 + c * 32;
+                        if (col >= p.n) break;
+                        uint32_t r[32];
+                        tmem_ld32(tbase + c * 32, r);
+                        tmem_ld_wait();
+                        if (owned) {
+                            float v[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                            store_row<32>(p.c[l], static_cast<long long>(row - me * p.rpr) * p.ldc_l[l] + col, col,
+                                          p.n, p.out_f32, v);
+                        }
+                    }
+                } else if (mine_in_tile) {
                     if (et == 0) {
                         for (int s = 0; s < p.tp; ++s)
                             if (s != me)
@@ -800,77 +858,69 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(me));
                     }
                     named_bar_sync(1, 128);
-                    const bool owned = valid && owner == me;
-                    if (p.fused_reduce && __any_sync(0xffffffffu, owned)) {
-                        // Remote contributions already summed (arrival order) in the accumulator.
-                        const float* acc_row = p.fr_acc[me] + static_cast<long long>(row - me * p.rpr) * p.ld_stage;
-                        for (int c = 0; c < kBN / 32; ++c) {
-                            const int col = col0 + c * 32;
-                            if (col >= p.n) break;
-                            uint32_t r[32];
-                            tmem_ld32(tbase + c * 32, r);
-                            tmem_ld_wait();
-                            if (owned) {
-                                float acc[32];
+                    // Coalesced source-ordered sum: the own accumulator chunk is staged
+                    // in this warp's smem window; lanes then walk 4 rows x 32 columns
+                    // per step, loading every source's float4 before adding in source
+                    // order 0..tp-1 (deterministic; FusedReduce: accumulator + own).
+                    const long long lr0 = row0 - static_cast<long long>(me) * p.rpr;  // tile's first owned row
+                    const float* src0 = p.fused_reduce
+                                            ? p.fr_acc[me]
+                                            : p.staging[me] + parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) +
+                                                  q * 1024;
+                    for (int c = 0; c < kBN / 32; ++c) {
+                        const int colc = col0 + c * 32;
+                        if (colc >= p.n) break;  // warp-uniform
+                        uint32_t r[32];
+                        tmem_ld32(tbase + c * 32, r);
+                        tmem_ld_wait();
+                        epi_stage(wbuf, lane, r);
 #pragma unroll
-                                for (int j = 0; j < 32; j += 4) {
-                                    const float4 v = ld_cg_f4(acc_row + col + j);
-                                    acc[j] = v.x + __uint_as_float(r[j]);
-                                    acc[j + 1] = v.y + __uint_as_float(r[j + 1]);
-                                    acc[j + 2] = v.z + __uint_as_float(r[j + 2]);
-                                    acc[j + 3] = v.w + __uint_as_float(r[j + 3]);
+                        for (int it0 = 0; it0 < 8; it0 += kEpiU) {
+                            float4 v[kEpiU][kMaxRanks];
+                            bool ok[kEpiU];
+#pragma unroll
+                            for (int u = 0; u < kEpiU; ++u) {
+                                const int i = (it0 + u) * 4 + (lane >> 3), g = lane & 7;
+                                const int col = colc + g * 4;
+                                const long long lr = lr0 + q * 32 + i;  // row within my block
+                                ok[u] = row0 + q * 32 + i < p.m && col < p.n && lr >= 0 && lr < p.rpr;
+                                if (ok[u]) {
+                                    if (p.fused_reduce) {
+                                        v[u][0] = ld_cg_f4(src0 + lr * p.ld_stage + col);
+                                    } else {
+                                        const float* src = src0 + c * 4096 + (it0 + u) * 128 + lane * 4;
+#pragma unroll
+                                        for (int s2 = 0; s2 < kMaxRanks; ++s2)
+                                            if (s2 < p.tp && s2 != me) v[u][s2] = ld_cg_f4(src + s2 * p.stage_plane);
+                                    }
                                 }
-                                store_row<32>(p.c[l], static_cast<long long>(row - me * p.rpr) * p.ldc_l[l] + col, col,
-                                              p.n, p.out_f32, acc);
                             }
-                        }
-                    } else if (__any_sync(0xffffffffu, owned)) {
-                        const long long lrow = row - me * p.rpr;
-                        const float* src0 = p.staging[me] + parity * p.stage_parity + lrow * p.ld_stage;
-                        for (int c = 0; c < kBN / 32; ++c) {
-                            const int col = col0 + c * 32;
-                            if (col >= p.n) break;
-                            uint32_t r[32];
-                            tmem_ld32(tbase + c * 32, r);
-                            tmem_ld_wait();
-                            if (owned) {
-                                // Two 16-column halves; each issues every source's
-                                // loads before summing (memory-level parallelism),
-                                // then adds in source order 0..tp-1 (deterministic).
 #pragma unroll
-                                for (int h = 0; h < 2; ++h) {
-                                    float4 v[kMaxRanks][4];
+                            for (int u = 0; u < kEpiU; ++u) {
+                                if (!ok[u]) continue;
+                                const int i = (it0 + u) * 4 + (lane >> 3), g = lane & 7;
+                                const float4 own = epi_read(wbuf, i, g);
+                                float acc[4];
+                                if (p.fused_reduce) {
+                                    acc[0] = v[u][0].x + own.x;
+                                    acc[1] = v[u][0].y + own.y;
+                                    acc[2] = v[u][0].z + own.z;
+                                    acc[3] = v[u][0].w + own.w;
+                                } else {
+                                    // Source order 0..tp-1 (deterministic, the oracle's rank order).
+                                    acc[0] = acc[1] = acc[2] = acc[3] = 0.0f;
 #pragma unroll
-                                    for (int s = 0; s < kMaxRanks; ++s) {
-                                        if (s < p.tp && s != me) {
-                                            const float* src = src0 + s * p.stage_plane + col + h * 16;
-#pragma unroll
-                                            for (int j = 0; j < 4; ++j) v[s][j] = ld_cg_f4(src + 4 * j);
-                                        }
+                                    for (int s2 = 0; s2 < kMaxRanks; ++s2) {
+                                        if (s2 >= p.tp) break;
+                                        const float4 w = s2 == me ? own : v[u][s2];
+                                        acc[0] += w.x;
+                                        acc[1] += w.y;
+                                        acc[2] += w.z;
+                                        acc[3] += w.w;
                                     }
-                                    float acc[16];
-#pragma unroll
-                                    for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
-#pragma unroll
-                                    for (int s = 0; s < kMaxRanks; ++s) {
-                                        if (s < p.tp) {
-                                            if (s == me) {
-#pragma unroll
-                                                for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(r[h * 16 + j]);
-                                            } else {
-#pragma unroll
-                                                for (int j = 0; j < 4; ++j) {
-                                                    acc[4 * j] += v[s][j].x;
-                                                    acc[4 * j + 1] += v[s][j].y;
-                                                    acc[4 * j + 2] += v[s][j].z;
-                                                    acc[4 * j + 3] += v[s][j].w;
-                                                }
-                                            }
-                                        }
-                                    }
-                                    store_row<16>(p.c[l], lrow * p.ldc_l[l] + col + h * 16, col + h * 16, p.n,
-                                                  p.out_f32, acc);
                                 }
+                                const int col = colc + g * 4;
+                                store_row<4>(p.c[l], (lr0 + q * 32 + i) * p.ldc_l[l] + col, col, p.n, p.out_f32, acc);
                             }
                         }
                     }

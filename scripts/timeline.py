@@ -1,0 +1,56 @@
+"""Device-trace timeline of one fused operator (profiling aid): events per
+time bucket across all emulated ranks, from the kernel's %globaltimer trace.
+
+    python scripts/timeline.py --workload llama70b-down-rs [--bucket-us 25]
+"""
+import argparse
+import collections
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2406_06858_b200 as fx
+from paper_2406_06858_b200 import _native as N
+from paper_2406_06858_b200.comm import read_trace
+from bench import WORKLOADS
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="llama70b-down-rs")
+ap.add_argument("--bucket-us", type=float, default=25.0)
+ap.add_argument("--ag-engine", type=int, default=0)
+args = ap.parse_args()
+pattern, m, n, k, tp, _ = WORKLOADS[args.workload]
+prob = fx.ProblemSpec(m, n, k, tp, pattern)
+torch.cuda.set_stream(torch.cuda.Stream())
+comm = fx.Communicator(tp, [0] * tp, heap_bytes=fx.required_heap_bytes(prob) + (64 << 20))
+for r in range(tp):
+    for kind in (N.BUF_A_SHARD, N.BUF_B_SHARD):
+        t = comm.tensor(r, kind, prob)
+        t.copy_(torch.rand(t.shape, device="cuda").mul_(2).sub_(1))
+torch.cuda.synchronize()
+s = [torch.cuda.current_stream().cuda_stream] * tp
+tile = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
+for trace in (0, 0, 1):
+    opts = fx.default_opts(trace=trace, ag_engine=args.ag_engine)
+    comm.set_timing(True)
+    if pattern == 0:
+        comm.ag_gemm(prob, tile, prob.rows_per_rank(), fx.PULL, True, opts, streams=s)
+    else:
+        comm.gemm_rs(prob, tile, fx.WRITE_ALLTOALL, True, opts, streams=s)
+    comm.sync()
+    print(f"trace={trace} kernel {comm.last_kernel_ms():.4f} ms")
+ev = []
+for r in range(tp):
+    ev += read_trace(comm, r, prob)
+t0 = min(e["ts"] for e in ev)
+b = args.bucket_us * 1000
+hist = collections.defaultdict(collections.Counter)
+for e in ev:
+    hist[int((e["ts"] - t0) // b)][e["event"]] += 1
+kinds = sorted({e["event"] for e in ev})
+print("t_us      " + " ".join(f"{x:>14s}" for x in kinds))
+for i in sorted(hist):
+    print(f"{i * args.bucket_us:8.1f}  " + " ".join(f"{hist[i][x]:14d}" for x in kinds))
+print(f"span {(max(e['ts'] for e in ev) - t0) / 1000:.1f} us, {len(ev)} events")
