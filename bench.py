@@ -274,6 +274,33 @@ def our_arm(args, wl):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item() / steps
 
+    def interleaved(fns, rounds):
+        """Per-variant median device time (max over ranks), one step of every
+        variant per round."""
+        for fn in fns.values():
+            fn()
+            fn()
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        times = {name: [] for name in fns}
+        for _ in range(rounds):
+            for name, fn in fns.items():
+                flush.zero_()
+                barrier()
+                ev0.record()
+                fn()
+                ev1.record()
+                ev1.synchronize()
+                times[name].append(ev0.elapsed_time(ev1))
+        barrier()
+        out = {}
+        for name, ts in times.items():
+            t = torch.tensor([statistics.median(ts)], device=dev)
+            if dist is not None:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            out[name] = t.item()
+        return out
+
     # ---- headline: the fused operator ----
     comm.set_timing(True)
     kernel_ms = []
@@ -286,10 +313,11 @@ def our_arm(args, wl):
     value = flops / (ms_fused * 1e-3) / 1e12
 
     # ---- Eq. 1 / Eq. 2 ingredients ----
+    # Measured round-robin (one step of each variant per round, L2 flushed
+    # before each, medians over the rounds) so clock / power drift during the
+    # run biases no variant; the fused op is re-measured in the same rounds.
     extra = {}
     if not args.quick:
-        ms_local = timed(lambda: comm.local_gemm(prob, opts, streams), max(3, args.steps // 2), 2)
-        ms_nonov = timed(lambda: comm.nonoverlap(prob, opts, streams), max(3, args.steps // 2), 2)
         # cuBLAS + NCCL (or device copies when emulated): B1, and cuBLAS non-split GEMM
         if emulated:
             if pattern == 0:
@@ -309,21 +337,25 @@ def our_arm(args, wl):
                               comm.tensor(rank, N.BUF_B_SHARD, prob).contiguous())
         if pattern == 0:
             b.unfused()  # fills the gathered buffers for gemm_only
-        ms_cublas_gemm = timed(b.gemm_only, max(3, args.steps // 2), 2)
-        ms_b1 = timed(b.unfused, max(3, args.steps // 2), 2)
-        ms_b2 = None
+        variants = {"fused": op, "local": lambda: comm.local_gemm(prob, opts, streams),
+                    "nonoverlap": lambda: comm.nonoverlap(prob, opts, streams),
+                    "cublas_gemm": b.gemm_only, "b1": b.unfused}
         if emulated and pattern == 0:
-            ms_b2 = timed(b.decomposed, max(3, args.steps // 2), 2)
+            variants["b2"] = b.decomposed
+        med = interleaved(variants, max(5, args.steps // 2))
         del b
-        t_gemm = min(ms_local, ms_cublas_gemm)
-        ect_fused = ms_fused - t_gemm
-        ect_b1 = ms_b1 - t_gemm
+        ms_f = med["fused"]
+        t_gemm = min(med["local"], med["cublas_gemm"])
+        ect_fused = ms_f - t_gemm
+        ect_b1 = med["b1"] - t_gemm
         extra = {
-            "t_gemm_nonsplit_ms": t_gemm, "t_gemm_ours_ms": ms_local, "t_gemm_cublas_ms": ms_cublas_gemm,
-            "t_unfused_cublas_ms": ms_b1, "t_decomposed_ms": ms_b2, "t_nonoverlap_ours_ms": ms_nonov,
+            "t_fused_ms": ms_f, "t_gemm_nonsplit_ms": t_gemm, "t_gemm_ours_ms": med["local"],
+            "t_gemm_cublas_ms": med["cublas_gemm"], "t_unfused_cublas_ms": med["b1"], "t_decomposed_ms": med.get("b2"),
+            "t_nonoverlap_ours_ms": med["nonoverlap"],
             "ect_fused_ms": ect_fused, "ect_unfused_ms": ect_b1,
             "overlap_efficiency": (1.0 - ect_fused / ect_b1) if ect_b1 > 0 else None,
-            "speedup_vs_unfused": ms_b1 / ms_fused,
+            "speedup_vs_unfused": med["b1"] / ms_f,
+            "method": "round-robin medians (one step of each variant per round, L2 flushed before each)",
             "unfused_baseline": ("device copies + cuBLAS (ranks emulated on one GPU)" if emulated
                                  else "NCCL + cuBLAS"),
         }
