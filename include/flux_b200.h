@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FLUX_ABI_VERSION 1
+#define FLUX_ABI_VERSION 2
 
 /* Return codes. The reference raises C++ exceptions (errors.hpp:9-31); each
  * maps to one code. The C++ shim (include/flux/overlap.hpp) rethrows them. */
@@ -92,7 +92,20 @@ typedef struct {
     int ag_engine;             /* AllGather transfers: 0 auto, 1 copy engines (stream memcpy + flag
                                   writes), 2 in-kernel (TMA bulk copies by the GEMM's SMs, Pull) */
     int trace;                 /* 1: record the device event trace of the next operators (flux_trace_read) */
+    int activation;            /* flux_activation fused into the AllGather-GEMM / local GEMM epilogue */
+    int activation_grad;       /* flux_activation whose derivative scales C: C = acc * act'(aux) */
 } flux_opts;
+
+/* Epilogue activations (chained MLP; paper Fig. 2). GELU is
+ * the erf form. SWIGLU: the local N columns come in 256-column groups of 128
+ * gate then 128 up columns; C receives silu(gate) * up (N/2 columns). */
+typedef enum {
+    FLUX_ACT_NONE = 0,
+    FLUX_ACT_GELU = 1,
+    FLUX_ACT_RELU = 2,
+    FLUX_ACT_SILU = 3,
+    FLUX_ACT_SWIGLU = 4
+} flux_activation;
 
 typedef struct {
     size_t heap_bytes;         /* per-rank symmetric heap size (0 = 1 GiB) */
@@ -201,6 +214,8 @@ typedef struct {
 } flux_matrix;
 typedef struct {
     flux_matrix a, b, c;
+    flux_matrix aux; /* AG epilogue: pre-activation [m, n/tp] bf16 — written when
+                        opts.activation is set (optional), read when opts.activation_grad is */
 } flux_operands;
 int flux_ag_gemm_ex(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
                     int rows_per_comm_tile, int transfer, int swizzle_on, const flux_opts* opts,
@@ -208,6 +223,35 @@ int flux_ag_gemm_ex(flux_comm* comm, const flux_problem* problem, const flux_til
 int flux_gemm_rs_ex(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
                     int write_mode, int swizzle_on, const flux_opts* opts, void* const* streams,
                     const flux_operands* operands);
+/* ---- chained tensor-parallel MLP (paper Fig. 2, §3) ------
+ * Forward: act = activation(AllGather(x) W_up^T) on every rank (AG-GEMM with
+ * the activation in its epilogue), then out = ReduceScatter(act W_down^T)
+ * (GEMM-RS). Per rank (tp entries single-process, 1 in IPC mode), bf16,
+ * row-major, ld in elements:
+ *   x [m/tp, hidden]; w_up [ffn/tp (x2 for SWIGLU), hidden]; w_down [hidden, ffn/tp];
+ *   pre [m, ffn/tp] (optional: saved pre-activation, not with SWIGLU);
+ *   act [m, ffn/tp] (the intermediate); out [m/tp, hidden] (needs m/tp % 128 == 0).
+ * Backward of the input (the AG <-> RS interchange): dact =
+ * (AllGather(dout) W_down) * act'(pre) (AG-GEMM, derivative in the epilogue),
+ * then dx = ReduceScatter(dact W_up) (GEMM-RS), with the transposed weights
+ * w_down_t [ffn/tp, hidden] and w_up_t [hidden, ffn/tp]. */
+typedef struct {
+    int m, hidden, ffn, tp;
+    int activation; /* flux_activation (backward: GELU / RELU / SILU) */
+} flux_mlp;
+typedef struct {
+    flux_matrix x, w_up, w_down, pre, act, out;
+} flux_mlp_operands;
+typedef struct {
+    flux_matrix dout, w_down_t, w_up_t, pre, dact, dx;
+} flux_mlp_grad_operands;
+int flux_mlp_forward(flux_comm* comm, const flux_mlp* mlp, const flux_opts* opts, void* const* streams,
+                     const flux_mlp_operands* operands);
+int flux_mlp_backward_dx(flux_comm* comm, const flux_mlp* mlp, const flux_opts* opts, void* const* streams,
+                         const flux_mlp_grad_operands* operands);
+/* Heap bytes per rank the MLP calls need (the larger of their two operators). */
+size_t flux_mlp_required_heap_bytes(const flux_mlp* mlp);
+
 /* Joins all work of the last operator; returns FLUX_ERR_DEADLOCK if a device
  * wait timed out (message names the flag, as spin_wait does, engine.cpp:149-162). */
 int flux_sync(flux_comm* comm);

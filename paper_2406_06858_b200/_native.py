@@ -20,6 +20,8 @@ WRITE_ALLTOALL, FUSED_REDUCE = 0, 1
 SWIZZLE_NAIVE, SWIZZLE_RANK_SHIFTED, SWIZZLE_ARRIVAL_ALIGNED = 0, 1, 2
 BF16, F32 = 0, 1
 BUF_A_SHARD, BUF_B_SHARD, BUF_A_AGG, BUF_C_OUT, BUF_STAGING, BUF_C_OUT_F32 = 0, 1, 2, 3, 4, 5
+ACT_NONE, ACT_GELU, ACT_RELU, ACT_SILU, ACT_SWIGLU = 0, 1, 2, 3, 4
+ABI_VERSION = 2
 
 
 class FluxError(RuntimeError):
@@ -66,7 +68,8 @@ class Opts(C.Structure):
     _fields_ = [("workers_per_rank", C.c_int), ("deterministic_reduce", C.c_int),
                 ("poll_budget", C.c_longlong), ("wall_budget_s", C.c_double),
                 ("interleave_seed", C.c_uint64), ("shift_offset", C.c_int), ("out_dtype", C.c_int),
-                ("emulated_order", C.c_int), ("cta_group", C.c_int), ("ag_engine", C.c_int), ("trace", C.c_int)]
+                ("emulated_order", C.c_int), ("cta_group", C.c_int), ("ag_engine", C.c_int), ("trace", C.c_int),
+                ("activation", C.c_int), ("activation_grad", C.c_int)]
 
 
 class CommOpts(C.Structure):
@@ -78,7 +81,21 @@ class Matrix(C.Structure):
 
 
 class Operands(C.Structure):
-    _fields_ = [("a", Matrix), ("b", Matrix), ("c", Matrix)]
+    _fields_ = [("a", Matrix), ("b", Matrix), ("c", Matrix), ("aux", Matrix)]
+
+
+class Mlp(C.Structure):
+    _fields_ = [("m", C.c_int), ("hidden", C.c_int), ("ffn", C.c_int), ("tp", C.c_int), ("activation", C.c_int)]
+
+
+class MlpOperands(C.Structure):
+    _fields_ = [("x", Matrix), ("w_up", Matrix), ("w_down", Matrix), ("pre", Matrix), ("act", Matrix),
+                ("out", Matrix)]
+
+
+class MlpGradOperands(C.Structure):
+    _fields_ = [("dout", Matrix), ("w_down_t", Matrix), ("w_up_t", Matrix), ("pre", Matrix), ("dact", Matrix),
+                ("dx", Matrix)]
 
 
 class BufferDesc(C.Structure):
@@ -128,6 +145,9 @@ _SIGS = {
     "flux_comm_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
     "flux_last_kernel_ms": (C.c_int, [C.c_void_p, _P(C.c_float)]),
     "flux_trace_read": (C.c_int, [C.c_void_p, C.c_int, _P(Problem), C.c_void_p, C.c_size_t, _P(C.c_size_t)]),
+    "flux_mlp_forward": (C.c_int, [C.c_void_p, _P(Mlp), _P(Opts), _P(C.c_void_p), _P(MlpOperands)]),
+    "flux_mlp_backward_dx": (C.c_int, [C.c_void_p, _P(Mlp), _P(Opts), _P(C.c_void_p), _P(MlpGradOperands)]),
+    "flux_mlp_required_heap_bytes": (C.c_size_t, [_P(Mlp)]),
 }
 
 # Symbols include/flux_b200.h declares (tests check the library exports all of them).
@@ -150,6 +170,8 @@ def lib() -> C.CDLL:
             fn = getattr(l, name)
             fn.restype = res
             fn.argtypes = args
+        if l.flux_abi_version() != ABI_VERSION:
+            raise ImportError(f"{path}: ABI version {l.flux_abi_version()} != {ABI_VERSION} (rebuild the library)")
         _lib = l
     return _lib
 

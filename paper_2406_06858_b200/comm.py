@@ -116,11 +116,31 @@ def _mat(t) -> N.Matrix:
 
 
 def _operands(per_rank):
+    """Per rank (a, b, c) or (a, b, c, aux) tensors (None = library buffer)."""
     arr = (N.Operands * len(per_rank))()
     for i, abc in enumerate(per_rank):
-        a, b, c = abc if abc is not None else (None, None, None)
-        arr[i] = N.Operands(_mat(a), _mat(b), _mat(c))
+        t = tuple(abc) if abc is not None else (None, None, None)
+        a, b, c = t[:3]
+        aux = t[3] if len(t) > 3 else None
+        arr[i] = N.Operands(_mat(a), _mat(b), _mat(c), _mat(aux))
     return arr
+
+
+@dataclass(frozen=True)
+class MlpSpec:
+    """Chained tensor-parallel MLP (flux_mlp): x [m/tp, hidden] -> AG-GEMM with
+    W_up + activation -> GEMM-RS with W_down -> out [m/tp, hidden]."""
+    m: int
+    hidden: int
+    ffn: int
+    tp: int
+    activation: int = N.ACT_GELU
+
+    def c(self) -> N.Mlp:
+        return N.Mlp(self.m, self.hidden, self.ffn, self.tp, self.activation)
+
+    def required_heap_bytes(self) -> int:
+        return int(N.lib().flux_mlp_required_heap_bytes(C.byref(self.c())))
 
 
 class Communicator:
@@ -204,6 +224,22 @@ class Communicator:
         o = opts if opts is not None else N.default_opts()
         N.check(N.lib().flux_gemm_rs(self._h, C.byref(problem.c()), C.byref(tile.c()), write_mode, int(swizzle),
                                      C.byref(o), N.stream_array(streams)))
+
+    def mlp_forward(self, mlp: MlpSpec, operands, opts: Optional[N.Opts] = None, streams=None) -> None:
+        """Per rank a dict with x, w_up, w_down, act, out (and optional pre)."""
+        arr = (N.MlpOperands * len(operands))()
+        for i, d in enumerate(operands):
+            arr[i] = N.MlpOperands(*[_mat(d.get(k)) for k in ("x", "w_up", "w_down", "pre", "act", "out")])
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_mlp_forward(self._h, C.byref(mlp.c()), C.byref(o), N.stream_array(streams), arr))
+
+    def mlp_backward_dx(self, mlp: MlpSpec, operands, opts: Optional[N.Opts] = None, streams=None) -> None:
+        """Per rank a dict with dout, w_down_t, w_up_t, pre, dact, dx."""
+        arr = (N.MlpGradOperands * len(operands))()
+        for i, d in enumerate(operands):
+            arr[i] = N.MlpGradOperands(*[_mat(d.get(k)) for k in ("dout", "w_down_t", "w_up_t", "pre", "dact", "dx")])
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_mlp_backward_dx(self._h, C.byref(mlp.c()), C.byref(o), N.stream_array(streams), arr))
 
     def local_gemm(self, problem: ProblemSpec, opts: Optional[N.Opts] = None, streams=None) -> None:
         o = opts if opts is not None else N.default_opts()

@@ -624,6 +624,15 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 prm.c[li] = rs.heap + L.c32.off;
                 prm.ldc_l[li] = L.c32.ld;
             }
+            if (mode == kModePlain || mode == kModeAG) {
+                prm.act = oc.o.activation;
+                prm.act_grad = oc.o.activation_grad;
+                if (ops && ops->aux.ptr) {
+                    prm.aux[li] = ops->aux.ptr;
+                    prm.ld_aux[li] = ops->aux.ld;
+                    prm.aux_save = oc.o.activation_grad == FLUX_ACT_NONE ? 1 : 0;
+                }
+            }
             prm.global_rank[li] = g[li];
             prm.ag_flags[li] = at<uint32_t>(rs, kAgFlagOffset);
             prm.ctrl[li] = at<uint32_t>(rs, kCtrlErr);
@@ -762,6 +771,8 @@ void flux_default_opts(flux_opts* o) {
     o->cta_group = 0;
     o->ag_engine = 0;
     o->trace = 0;
+    o->activation = FLUX_ACT_NONE;
+    o->activation_grad = FLUX_ACT_NONE;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -1071,6 +1082,29 @@ static int check_heap(flux_comm* c, const flux_problem* p) {
     return FLUX_OK;
 }
 
+// Epilogue activation contract (flux_activation, include/flux_b200.h).
+static int check_activation(flux_comm* c, const flux_problem* p, const flux_opts* opts, const flux_operands* ops) {
+    if (!opts) return FLUX_OK;
+    const int a = opts->activation, g = opts->activation_grad;
+    if (a < FLUX_ACT_NONE || a > FLUX_ACT_SWIGLU || g < FLUX_ACT_NONE || g > FLUX_ACT_SILU)
+        return fail(FLUX_ERR_CONFIG, "unknown activation");
+    if (a == FLUX_ACT_NONE && g == FLUX_ACT_NONE) return FLUX_OK;
+    if (a != FLUX_ACT_NONE && g != FLUX_ACT_NONE) return fail(FLUX_ERR_CONFIG, "activation and activation_grad are exclusive");
+    if (p->pattern != FLUX_ALLGATHER_GEMM)
+        return fail(FLUX_ERR_CONFIG, "epilogue activations belong to the AllGather-GEMM (the GEMM-RS partials are pre-reduction)");
+    std::vector<int> mine;
+    local_ranks_only(c, mine);
+    for (size_t i = 0; i < mine.size(); ++i) {
+        const flux_operands* o = ops ? (c->ipc ? ops : ops + mine[i]) : nullptr;
+        const bool aux = o && o->aux.ptr;
+        if (a == FLUX_ACT_SWIGLU && aux) return fail(FLUX_ERR_CONFIG, "SWIGLU does not save a pre-activation");
+        if (g != FLUX_ACT_NONE && !aux) return fail(FLUX_ERR_CONFIG, "activation_grad needs the saved pre-activation (operands.aux)");
+    }
+    if (a == FLUX_ACT_SWIGLU && local_cols(p) % kBN != 0)
+        return fail(FLUX_ERR_SHAPE, "SWIGLU needs n/tp % 256 == 0 (128 gate + 128 up columns per group)");
+    return FLUX_OK;
+}
+
 int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer, int swizzle_on,
                  const flux_opts* opts, void* const* streams) {
     return flux_ag_gemm_ex(c, p, tile, rpct, transfer, swizzle_on, opts, streams, nullptr);
@@ -1083,6 +1117,7 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
         return fail(FLUX_ERR_CONFIG, "run_fused_allgather_gemm requires AllGatherGemm pattern");
     FLUX_TRY(validate_tiling(p, tile));
     FLUX_TRY(check_heap(c, p));
+    FLUX_TRY(check_activation(c, p, opts, operands));
     const int tp = p->tp, rpr = rows_per_rank(p);
     if (rpct <= 0) rpct = rpr;
     if (p->m / rpct > static_cast<int>(kAgFlagCap)) return fail(FLUX_ERR_CONFIG, "too many comm tiles");
@@ -1367,6 +1402,7 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     FLUX_TRY(check_heap(c, p));
     if (write_mode != FLUX_WRITE_ALLTOALL && write_mode != FLUX_FUSED_REDUCE)
         return fail(FLUX_ERR_CONFIG, "unknown write mode");
+    FLUX_TRY(check_activation(c, p, opts, operands));
     const int tp = p->tp, rpr = rows_per_rank(p);
     const int tiles = ((p->m + kBM - 1) / kBM) * ((p->n + kBN - 1) / kBN);
     if (static_cast<size_t>(tiles) * tp > kRsFlagCap) return fail(FLUX_ERR_CONFIG, "too many output tiles for the flag table");
@@ -1453,6 +1489,7 @@ int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
     FLUX_TRY(check_comm(c));
     FLUX_TRY(validate_problem(p));
     FLUX_TRY(check_heap(c, p));
+    FLUX_TRY(check_activation(c, p, opts, nullptr));
     OpCommon oc = common_opts(opts);
     c->last_launches = 0;
     c->kernel_events_used = 0;
@@ -1565,6 +1602,90 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
         FLUX_CUDA(cudaEventRecord(rs.kernel_evt, s));
     }
     return mark_op_done(c, streams, e);
+}
+
+// ---------------------------------------------------------------------------
+// Chained tensor-parallel MLP: AG-GEMM with the activation
+// in its epilogue, then GEMM-RS on the intermediate; backward of the input is
+// the same pair with the roles interchanged.
+// ---------------------------------------------------------------------------
+static int mlp_problems(const flux_mlp* mlp, bool backward, flux_problem* ag, flux_problem* rs) {
+    if (!mlp) return fail(FLUX_ERR_CONFIG, "null mlp");
+    if (mlp->activation < FLUX_ACT_NONE || mlp->activation > FLUX_ACT_SWIGLU)
+        return fail(FLUX_ERR_CONFIG, "unknown activation");
+    if (backward && mlp->activation == FLUX_ACT_SWIGLU)
+        return fail(FLUX_ERR_CONFIG, "flux_mlp_backward_dx supports GELU / RELU / SILU");
+    const int up_cols = mlp->activation == FLUX_ACT_SWIGLU && !backward ? 2 * mlp->ffn : mlp->ffn;
+    *ag = flux_problem{mlp->m, up_cols, mlp->hidden, mlp->tp, FLUX_ALLGATHER_GEMM};
+    *rs = flux_problem{mlp->m, mlp->hidden, mlp->ffn, mlp->tp, FLUX_GEMM_REDUCESCATTER};
+    FLUX_TRY(validate_problem(ag));
+    return validate_problem(rs);
+}
+
+size_t flux_mlp_required_heap_bytes(const flux_mlp* mlp) {
+    flux_problem ag, rs, bag, brs;
+    if (mlp_problems(mlp, false, &ag, &rs) != FLUX_OK) return 0;
+    size_t need = std::max(layout_for(&ag).total, layout_for(&rs).total);
+    if (mlp->activation != FLUX_ACT_SWIGLU && mlp_problems(mlp, true, &bag, &brs) == FLUX_OK)
+        need = std::max(need, std::max(layout_for(&bag).total, layout_for(&brs).total));
+    return need;
+}
+
+static int mlp_pair(flux_comm* c, const flux_problem& ag, const flux_problem& rs, const flux_opts* opts,
+                    void* const* streams, const std::vector<flux_operands>& ag_ops,
+                    const std::vector<flux_operands>& rs_ops, int act, int act_grad) {
+    flux_opts o;
+    if (opts) o = *opts;
+    else flux_default_opts(&o);
+    flux_opts o_ag = o, o_rs = o;
+    o_ag.activation = act;
+    o_ag.activation_grad = act_grad;
+    o_ag.out_dtype = FLUX_BF16;  // the intermediate feeds the next GEMM as bf16
+    o_rs.activation = o_rs.activation_grad = FLUX_ACT_NONE;
+    const flux_tile t_ag{ag.m / ag.tp, ag.n / ag.tp}, t_rs{rs.m / rs.tp, rs.n};
+    FLUX_TRY(flux_ag_gemm_ex(c, &ag, &t_ag, ag.m / ag.tp, FLUX_PULL, 1, &o_ag, streams, ag_ops.data()));
+    const int launches = c->last_launches;
+    FLUX_TRY(flux_gemm_rs_ex(c, &rs, &t_rs, FLUX_WRITE_ALLTOALL, 1, &o_rs, streams, rs_ops.data()));
+    c->last_launches += launches;
+    return FLUX_OK;
+}
+
+int flux_mlp_forward(flux_comm* c, const flux_mlp* mlp, const flux_opts* opts, void* const* streams,
+                     const flux_mlp_operands* ops) {
+    FLUX_TRY(check_comm(c));
+    flux_problem ag, rs;
+    FLUX_TRY(mlp_problems(mlp, false, &ag, &rs));
+    if (!ops) return fail(FLUX_ERR_CONFIG, "flux_mlp_forward needs caller operands");
+    const int n_ops = c->ipc ? 1 : c->tp;
+    std::vector<flux_operands> a(n_ops), r(n_ops);
+    for (int i = 0; i < n_ops; ++i) {
+        const flux_mlp_operands& m = ops[i];
+        if (!m.x.ptr || !m.w_up.ptr || !m.w_down.ptr || !m.act.ptr || !m.out.ptr)
+            return fail(FLUX_ERR_CONFIG, "flux_mlp_forward: x, w_up, w_down, act and out are required");
+        a[i] = flux_operands{m.x, m.w_up, m.act, m.pre};
+        r[i] = flux_operands{m.act, m.w_down, m.out, flux_matrix{nullptr, 0}};
+    }
+    return mlp_pair(c, ag, rs, opts, streams, a, r, mlp->activation, FLUX_ACT_NONE);
+}
+
+int flux_mlp_backward_dx(flux_comm* c, const flux_mlp* mlp, const flux_opts* opts, void* const* streams,
+                         const flux_mlp_grad_operands* ops) {
+    FLUX_TRY(check_comm(c));
+    flux_problem ag, rs;
+    FLUX_TRY(mlp_problems(mlp, true, &ag, &rs));
+    if (!ops) return fail(FLUX_ERR_CONFIG, "flux_mlp_backward_dx needs caller operands");
+    const int n_ops = c->ipc ? 1 : c->tp;
+    std::vector<flux_operands> a(n_ops), r(n_ops);
+    for (int i = 0; i < n_ops; ++i) {
+        const flux_mlp_grad_operands& m = ops[i];
+        if (!m.dout.ptr || !m.w_down_t.ptr || !m.w_up_t.ptr || !m.dact.ptr || !m.dx.ptr ||
+            (mlp->activation != FLUX_ACT_NONE && !m.pre.ptr))
+            return fail(FLUX_ERR_CONFIG, "flux_mlp_backward_dx: dout, w_down_t, w_up_t, pre, dact and dx are required");
+        a[i] = flux_operands{m.dout, m.w_down_t, m.dact,
+                             mlp->activation != FLUX_ACT_NONE ? m.pre : flux_matrix{nullptr, 0}};
+        r[i] = flux_operands{m.dact, m.w_up_t, m.dx, flux_matrix{nullptr, 0}};
+    }
+    return mlp_pair(c, ag, rs, opts, streams, a, r, FLUX_ACT_NONE, mlp->activation);
 }
 
 int flux_sync(flux_comm* c) {

@@ -23,6 +23,7 @@ constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*alig
 constexpr int kMaxRanks = 8;   // TP degree supported by one communicator (one NVSwitch node)
 
 // kModeRSLast: GEMM-RS whose ownership blocks are narrower than a tile (last-arriver reduction).
+enum Activation : int { kActNone = 0, kActGelu = 1, kActRelu = 2, kActSilu = 3, kActSwiGLU = 4 };
 enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2, kModeRSLast = 3 };
 
 // Control block at the start of every rank's symmetric heap. All words are
@@ -111,6 +112,12 @@ struct GemmParams {
     uint32_t trace_cap;
     float* fr_acc[kMaxRanks];      // per GLOBAL rank: FusedReduce fp32 accumulator [rpr, ld_stage] (this parity)
     const uint32_t* fr_ready[kMaxRanks];  // per GLOBAL rank: control word, accumulator zeroed at epoch
+    // Epilogue activation (Plain / AG): act = flux_activation applied to the
+    // accumulator; act_grad = C is acc * act'(aux) (aux = saved pre-activation);
+    // aux_save = also store the pre-activation into aux (forward of a chain).
+    int act, act_grad, aux_save;
+    void* aux[kMaxRanks];          // per local slot: bf16 [m, n] pre-activation
+    int ld_aux[kMaxRanks];
     int dbg;                       // profiling ablations (FLUX_DEBUG): 1 skip RS remote stores, 2 skip RS owner reduce
 };
 

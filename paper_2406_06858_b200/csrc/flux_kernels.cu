@@ -350,6 +350,48 @@ __device__ __forceinline__ void store_row(void* c, long long off, int col, int n
     }
 }
 
+// Epilogue activations (erf GELU, ReLU, SiLU) and their derivatives.
+__device__ __forceinline__ float act_fwd(int a, float x) {
+    switch (a) {
+        case kActGelu: return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+        case kActRelu: return fmaxf(x, 0.0f);
+        case kActSilu: return x / (1.0f + __expf(-x));
+        default: return x;
+    }
+}
+__device__ __forceinline__ float act_bwd(int a, float x) {
+    switch (a) {
+        case kActGelu:
+            return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * 0.3989422804014327f * __expf(-0.5f * x * x);
+        case kActRelu: return x > 0.0f ? 1.0f : 0.0f;
+        case kActSilu: {
+            const float sg = 1.0f / (1.0f + __expf(-x));
+            return sg * (1.0f + x * (1.0f - sg));
+        }
+        default: return 1.0f;
+    }
+}
+// W bf16 values of one row (cols [col, col+W)) as floats; 0 past n.
+template <int W>
+__device__ __forceinline__ void load_row_bf16(const void* base, long long off, int col, int n, float (&x)[W]) {
+    const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(base) + off;
+    if (col + W <= n && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+#pragma unroll
+        for (int j = 0; j < W; j += 8) {
+            const uint4 w = *reinterpret_cast<const uint4*>(src + j);
+            const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                x[j + 2 * t] = __uint_as_float(u[t] << 16);
+                x[j + 2 * t + 1] = __uint_as_float(u[t] & 0xFFFF0000u);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < W; ++j) x[j] = col + j < n ? __bfloat162float(src[j]) : 0.0f;
+    }
+}
+
 // Source-ordered sum of the tp staged partials of one 128 x 256 tile into the
 // owners' C. Consecutive threads take consecutive 4-column groups of a row
 // (coalesced), and every source's float4 is loaded before the sum.
@@ -699,18 +741,53 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             if (row0 >= p.m) {
                 // Fully out-of-range half of a pair tile: nothing to store or signal.
             } else if (MODE != kModeRS && MODE != kModeRSLast) {
-                for (int c = 0; c < kBN / 32; ++c) {
-                    const int col = col0 + c * 32;
-                    if (col >= p.n) break;  // warp-uniform
-                    uint32_t r[32];
-                    tmem_ld32(tbase + c * 32, r);
-                    tmem_ld_wait();
-                    if (valid) {
-                        float v[32];
+                if (p.act == kActSwiGLU) {
+                    // Gated MLP: each 256-column tile holds 128 gate then 128 up
+                    // columns; C gets silu(gate) * up, 128 columns per tile.
+                    for (int c = 0; c < kBN / 64; ++c) {
+                        const int col = col0 + c * 32;
+                        if (col >= p.n) break;  // warp-uniform
+                        uint32_t rg[32], ru[32];
+                        tmem_ld32(tbase + c * 32, rg);
+                        tmem_ld32(tbase + (c + kBN / 64) * 32, ru);
+                        tmem_ld_wait();
+                        if (valid) {
+                            float v[32];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                        store_row<32>(p.c[l], static_cast<long long>(row) * p.ldc_l[l] + col, col, p.n,
-                                    p.out_f32, v);
+                            for (int j = 0; j < 32; ++j)
+                                v[j] = act_fwd(kActSilu, __uint_as_float(rg[j])) * __uint_as_float(ru[j]);
+                            const int ocol = tn * (kBN / 2) + c * 32;
+                            store_row<32>(p.c[l], static_cast<long long>(row) * p.ldc_l[l] + ocol, ocol, p.n / 2,
+                                          p.out_f32, v);
+                        }
+                    }
+                } else {
+                    for (int c = 0; c < kBN / 32; ++c) {
+                        const int col = col0 + c * 32;
+                        if (col >= p.n) break;  // warp-uniform
+                        uint32_t r[32];
+                        tmem_ld32(tbase + c * 32, r);
+                        tmem_ld_wait();
+                        if (valid) {
+                            float v[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                            if (p.act_grad || p.act || p.aux_save) {
+                                const long long aoff = static_cast<long long>(row) * p.ld_aux[l] + col;
+                                if (p.aux_save) store_row<32>(p.aux[l], aoff, col, p.n, 0, v);
+                                if (p.act_grad) {
+                                    float x[32];
+                                    load_row_bf16<32>(p.aux[l], aoff, col, p.n, x);
+#pragma unroll
+                                    for (int j = 0; j < 32; ++j) v[j] *= act_bwd(p.act_grad, x[j]);
+                                } else if (p.act) {
+#pragma unroll
+                                    for (int j = 0; j < 32; ++j) v[j] = act_fwd(p.act, v[j]);
+                                }
+                            }
+                            store_row<32>(p.c[l], static_cast<long long>(row) * p.ldc_l[l] + col, col, p.n,
+                                          p.out_f32, v);
+                        }
                     }
                 }
             } else if (MODE == kModeRSLast) {
