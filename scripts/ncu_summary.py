@@ -31,9 +31,10 @@ def summarise(path):
     # top warp stall reasons (per-instruction-issued ratios)
     stalls = []
     for i, h in enumerate(hdr):
-        if h.startswith("smsp__average_warp_latency_issue_stalled_") and h.endswith(".ratio"):
+        pre = "smsp__average_warps_issue_stalled_"
+        if h.startswith(pre) and h.endswith("_per_issue_active.ratio"):
             try:
-                stalls.append((float(vals[i]), h.replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", "")))
+                stalls.append((float(vals[i]), h[len(pre):-len("_per_issue_active.ratio")]))
             except ValueError:
                 pass
     out["top_stalls"] = [{"reason": r, "ratio": v} for v, r in sorted(stalls, reverse=True)[:6]]
