@@ -186,6 +186,8 @@ def reference_arm(args, wl):
 # our arm
 # ---------------------------------------------------------------------------
 def our_arm(args, wl):
+    import ctypes as C
+
     import torch
 
     import paper_2406_06858_b200 as fx
@@ -300,6 +302,9 @@ def our_arm(args, wl):
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
             out[name] = t.item()
         return out
+
+    ag_transfer = ("copy-engine pull" if N.lib().flux_ag_engine(C.byref(prob.c()), fx.PULL, C.byref(opts)) == 1
+                   else "in-kernel TMA pull (the GEMM's SMs)")
 
     # ---- headline: the fused operator ----
     comm.set_timing(True)
@@ -420,7 +425,7 @@ def our_arm(args, wl):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform[-1,1) bf16)",
             "config": {"workload": wl, "description": desc, "m": m, "n": n, "k": k, "tp": tp,
                        "ranks": "emulated on one GPU" if emulated else "one process per GPU (cudaIpc heaps)",
-                       "parallelism": f"tp{tp}", "transfer": "copy-engine pull" if pattern == 0 else "epilogue P2P",
+                       "parallelism": f"tp{tp}", "transfer": ag_transfer if pattern == 0 else "epilogue P2P",
                        "l2": "flushed between timed steps (256 MiB write outside the events)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "overlap": extra,

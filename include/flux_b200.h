@@ -194,6 +194,9 @@ int flux_ag_gemm(flux_comm* comm, const flux_problem* problem, const flux_tile* 
  * order 0..tp-1 inside its local-tile epilogue (deterministic). */
 int flux_gemm_rs(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
                  int write_mode, int swizzle_on, const flux_opts* opts, void* const* streams);
+/* The AllGather transfer engine flux_ag_gemm uses for this problem: 1 copy
+ * engines, 2 in-kernel (opts.ag_engine, or the automatic choice when 0). */
+int flux_ag_engine(const flux_problem* problem, int transfer, const flux_opts* opts);
 /* Local GEMM only (tp ranks each compute their own C = A_agg B^T / A B^T with no
  * communication): T_gemm_nonsplit of Eq. 1 and the TP=1 path. */
 int flux_local_gemm(flux_comm* comm, const flux_problem* problem, const flux_opts* opts,

@@ -138,6 +138,7 @@ _SIGS = {
                                   _P(C.c_void_p), _P(Operands)]),
     "flux_gemm_rs_ex": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, C.c_int, _P(Opts), _P(C.c_void_p),
                                   _P(Operands)]),
+    "flux_ag_engine": (C.c_int, [_P(Problem), C.c_int, _P(Opts)]),
     "flux_local_gemm": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
     "flux_nonoverlap": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
     "flux_sync": (C.c_int, [C.c_void_p]),

@@ -1082,6 +1082,25 @@ static int check_heap(flux_comm* c, const flux_problem* p) {
     return FLUX_OK;
 }
 
+// AllGather transfer engine: 1 copy engines, 2 in-kernel (the GEMM's SMs).
+static bool ag_sm_engine_ok(const flux_problem* p, int transfer) {
+    return transfer == FLUX_PULL && local_k(p) % 8 == 0 && (p->m + kBM - 1) / kBM < static_cast<int>(kAgGroupCap);
+}
+static int ag_engine_for(const flux_problem* p, int transfer, int requested) {
+    if (requested == 1 || requested == 2) return requested;
+    // Auto: in-kernel transfers up to 32 MiB of gathered A (decode / small
+    // problems: one launch, no host work per comm tile), copy engines above.
+    // Measured on L-AG (64 MiB): within +-5 % of each other, the sign depending
+    // on what runs around them (scripts/ab_engine.py vs bench.py round-robin).
+    const size_t gathered = static_cast<size_t>(p->m) * local_k(p) * 2;
+    return ag_sm_engine_ok(p, transfer) && gathered <= (size_t(32) << 20) ? 2 : 1;
+}
+
+int flux_ag_engine(const flux_problem* p, int transfer, const flux_opts* opts) {
+    if (!p) return fail(FLUX_ERR_CONFIG, "null problem");
+    return ag_engine_for(p, transfer, opts ? opts->ag_engine : 0);
+}
+
 // Epilogue activation contract (flux_activation, include/flux_b200.h).
 static int check_activation(flux_comm* c, const flux_problem* p, const flux_opts* opts, const flux_operands* ops) {
     if (!opts) return FLUX_OK;
@@ -1139,11 +1158,9 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
 
     // ---- transfer engine: copy engines (Alg. 3 on a stream) or the GEMM's own
     // SMs (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies) ----
-    const bool sm_ok = transfer == FLUX_PULL && lk % 8 == 0 && (p->m + kBM - 1) / kBM < static_cast<int>(kAgGroupCap);
-    if (oc.o.ag_engine == 2 && !sm_ok)
+    if (oc.o.ag_engine == 2 && !ag_sm_engine_ok(p, transfer))
         return fail(FLUX_ERR_CONFIG, "in-kernel AllGather transfer needs Pull and k % 8 == 0");
-    const bool use_sm = oc.o.ag_engine == 2 ||
-                        (oc.o.ag_engine == 0 && sm_ok && static_cast<size_t>(p->m) * lk * 2 <= (size_t(32) << 20));
+    const bool use_sm = ag_engine_for(p, transfer, oc.o.ag_engine) == 2;
     if (use_sm) {
         const int cg = choose_cg(p, oc.o);
         const int groups = (p->m + kBM - 1) / kBM;
