@@ -1233,13 +1233,25 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
                 for (int row = b * rpr; row < (b + 1) * rpr; row += piece_rows)
                     jobs.push_back((uint32_t(li) << 28) | (uint32_t(b) << 24) | uint32_t(row));
             };
-            for (size_t li = 0; li < g.size(); ++li) add_block(static_cast<int>(li), g[li]);
-            if (step_major) {
-                for (int step = 1; step < tp; ++step)
-                    for (size_t li = 0; li < g.size(); ++li) add_block(static_cast<int>(li), blocks[g[li]][step]);
+            // Ranks of this launch pull straight from each other's shards, so with
+            // every peer local the table can follow the kernel's consumption order
+            // exactly (rank-major: each slot's own block, then its peers').
+            bool all_local = true;
+            for (int q = 0; q < kMaxRanks; ++q) prm.slot_of[q] = -1;
+            for (size_t li = 0; li < g.size(); ++li) prm.slot_of[g[li]] = static_cast<int>(li);
+            for (int q = 0; q < tp; ++q) all_local = all_local && prm.slot_of[q] >= 0;
+            if (step_major || !all_local) {
+                for (size_t li = 0; li < g.size(); ++li) add_block(static_cast<int>(li), g[li]);
+                if (step_major) {
+                    for (int step = 1; step < tp; ++step)
+                        for (size_t li = 0; li < g.size(); ++li) add_block(static_cast<int>(li), blocks[g[li]][step]);
+                } else {
+                    for (size_t li = 0; li < g.size(); ++li)
+                        for (int step = 1; step < tp; ++step) add_block(static_cast<int>(li), blocks[g[li]][step]);
+                }
             } else {
                 for (size_t li = 0; li < g.size(); ++li)
-                    for (int step = 1; step < tp; ++step) add_block(static_cast<int>(li), blocks[g[li]][step]);
+                    for (int step = 0; step < tp; ++step) add_block(static_cast<int>(li), blocks[g[li]][step]);
             }
             uint32_t* jobs_dev = nullptr;
             FLUX_TRY(upload_order(c, c->ranks[g[0]].device, jobs, &jobs_dev));
@@ -1338,48 +1350,76 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
             for (int r : g)
                 for (int q = 0; q < tp; ++q)
                     if (q != r && !in_group(q)) FLUX_TRY(wait_value_geq(cs, c->ranks[q].heap + kCtrlDone, e - 1));
+        // A rank's own shard: caller operand or library buffer. Ranks sharing
+        // this device (one stream, so no cross-rank hazards) pull straight from
+        // each other's shards instead of from the owner's a_agg slot: nothing
+        // waits for the owners' local copies, which would otherwise serialise
+        // tp local copies ahead of the first remote block.
+        auto shard_of = [&](int q, const char*& ptr, size_t& pitch) {
+            const flux_operands* ops = operands_of(c, oc, q);
+            ptr = ops && ops->a.ptr ? static_cast<const char*>(ops->a.ptr) : c->ranks[q].heap + L.a_shard.off;
+            pitch = ops && ops->a.ptr ? static_cast<size_t>(ops->a.ld) * 2 : shard_pitch;
+        };
         // Local shard -> own a_agg slot, local flags preset (engine.cpp:469-472).
-        for (int r : g) {
+        auto local_copy = [&](int r) -> int {
             RankState& rs = c->ranks[r];
-            const flux_operands* ops = operands_of(c, oc, r);
-            const char* shard = ops && ops->a.ptr ? static_cast<const char*>(ops->a.ptr) : rs.heap + L.a_shard.off;
-            const size_t pitch = ops && ops->a.ptr ? static_cast<size_t>(ops->a.ld) * 2 : shard_pitch;
+            const char* shard;
+            size_t pitch;
+            shard_of(r, shard, pitch);
             FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes, shard,
                                pitch, rpr));
             FLUX_TRY(write_value(cs, rs.heap + kCtrlReady, e));
             for (int f = r * rpr / rpct; f < (r + 1) * rpr / rpct; ++f)
                 FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + f, e));
-        }
+            return FLUX_OK;
+        };
         // Transfers in the order the kernel consumes them: rank-major when the
-        // ranks sharing this device run rank by rank, else ring step by step.
-        std::vector<std::pair<int, int>> jobs;  // (rank, step)
+        // ranks sharing this device run rank by rank (each rank's own block,
+        // then its peers' blocks), else every own block then ring step by step.
+        std::vector<std::pair<int, int>> jobs;  // (rank, step); step -1 = local copy
         const bool rank_major = transfer == FLUX_PULL && oc.o.emulated_order != 1 && g.size() > 1;
-        for (int a = 0; a < (rank_major ? static_cast<int>(g.size()) : tp - 1); ++a)
-            for (int b = 0; b < (rank_major ? tp - 1 : static_cast<int>(g.size())); ++b)
-                jobs.emplace_back(rank_major ? g[a] : g[b], rank_major ? b : a);
+        if (rank_major) {
+            for (int r : g)
+                for (int b = -1; b < tp - 1; ++b) jobs.emplace_back(r, b);
+        } else {
+            for (int r : g) jobs.emplace_back(r, -1);
+            for (int a = 0; a < tp - 1; ++a)
+                for (int r : g) jobs.emplace_back(r, a);
+        }
         for (const auto& job : jobs) {
-            {
-                const int r = job.first, step = job.second;
-                RankState& rs = c->ranks[r];
-                for (int i = step * per_peer; i < (step + 1) * per_peer; ++i) {
-                    const Desc& d = specs[r][i];
-                    const int q = d.peer;
-                    const RankState& qs = c->ranks[q];
-                    const bool first = i == step * per_peer;
-                    if (transfer == FLUX_PULL) {
-                        if (first && !in_group(q)) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlReady, e));
-                        FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
-                                           rowbytes, qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
-                                           rowbytes, d.rows));
-                        FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
+            const int r = job.first, step = job.second;
+            if (step < 0) {
+                FLUX_TRY(local_copy(r));
+                continue;
+            }
+            RankState& rs = c->ranks[r];
+            for (int i = step * per_peer; i < (step + 1) * per_peer; ++i) {
+                const Desc& d = specs[r][i];
+                const int q = d.peer;
+                const RankState& qs = c->ranks[q];
+                const bool first = i == step * per_peer;
+                if (transfer == FLUX_PULL) {
+                    char* dst = rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes;
+                    if (in_group(q)) {
+                        const char* shard;
+                        size_t pitch;
+                        shard_of(q, shard, pitch);
+                        FLUX_TRY(copy_rows(cs, dst, rowbytes, shard + static_cast<size_t>(d.row_begin - q * rpr) * pitch,
+                                           pitch, d.rows));
                     } else {
-                        if (first && !in_group(q)) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlKdone, e - 1));
-                        // Push reads from my own a_agg slot (already holds my shard).
-                        FLUX_TRY(copy_rows(cs, qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
-                                           rowbytes, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
-                                           rowbytes, d.rows));
-                        FLUX_TRY(write_value(cs, at<uint32_t>(qs, kAgFlagOffset) + d.row_begin / rpct, e));
+                        if (first) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlReady, e));
+                        FLUX_TRY(copy_rows(cs, dst, rowbytes,
+                                           qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
+                                           d.rows));
                     }
+                    FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
+                } else {
+                    if (first && !in_group(q)) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlKdone, e - 1));
+                    // Push reads from my own a_agg slot (already holds my shard).
+                    FLUX_TRY(copy_rows(cs, qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
+                                       rowbytes, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
+                                       rowbytes, d.rows));
+                    FLUX_TRY(write_value(cs, at<uint32_t>(qs, kAgFlagOffset) + d.row_begin / rpct, e));
                 }
             }
         }

@@ -96,6 +96,7 @@ struct GemmParams {
     long long src_ld_l[kMaxRanks]; // per local slot: A shard row pitch in bytes
     const char* agg_src[kMaxRanks];    // per GLOBAL rank: its a_agg (peer pointers; pull source)
     const char* shard_src[kMaxRanks];  // per local slot: its own A shard (local piece source)
+    int slot_of[kMaxRanks];        // per GLOBAL rank: its local slot in this launch (same device), else -1
     char* a_dst[kMaxRanks];            // per local slot: its a_agg
     uint32_t* ag_ctr[kMaxRanks];   // per GLOBAL rank: monotonic piece counters (peer pointers)
     int ag_slot_index;             // counter index of "own block copied" (after the group counters)

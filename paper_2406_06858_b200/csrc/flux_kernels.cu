@@ -660,6 +660,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 const char* src;
                 if (q == me) {
                     src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
+                } else if (p.slot_of[q] >= 0) {
+                    // A rank on this device (same launch): pull straight from its shard.
+                    const int sl = p.slot_of[q];
+                    src = p.shard_src[sl] + static_cast<long long>(row0 - q * p.rpr) * p.src_ld_l[sl];
                 } else {
                     if (q != checked_src) {
                         // Publish everything in flight before blocking: another CTA may be
