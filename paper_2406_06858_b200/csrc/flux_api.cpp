@@ -692,6 +692,16 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.timeout_ns = oc.timeout_ns;
         prm.jitter_seed = oc.o.interleave_seed;
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
+        // Chained RS partial sums (see the kernel): every rank in this one
+        // launch, rank-major schedule with the owners' blocks last, so each
+        // chain link waits only on a tile a whole section earlier.
+        {
+            const char* env = std::getenv("FLUX_RS_CHAIN");
+            prm.rs_chain = mode == kModeRS && !oc.fused_reduce && interleave == kInterleaveRankTail &&
+                                   static_cast<int>(g.size()) == c->tp && !(env && std::atoi(env) == 0)
+                               ? 1
+                               : 0;
+        }
         prm.rs_last_arriver = mode == kModeRSLast ? 1 : 0;
         if (const char* env = std::getenv("FLUX_DEBUG")) prm.dbg = std::atoi(env);  // profiling ablations only
         // Join the other local ranks' streams into the launch stream.

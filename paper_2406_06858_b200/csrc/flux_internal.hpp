@@ -119,6 +119,7 @@ struct GemmParams {
     int act, act_grad, aux_save;
     void* aux[kMaxRanks];          // per local slot: bf16 [m, n] pre-activation
     int ld_aux[kMaxRanks];
+    int rs_chain;                  // RS, every rank in this launch: chained partial sums (see kernel)
     int dbg;                       // profiling ablations (FLUX_DEBUG): 1 skip RS remote stores, 2 skip RS owner reduce
 };
 

@@ -392,6 +392,22 @@ __device__ __forceinline__ void load_row_bf16(const void* base, long long off, i
     }
 }
 
+// acc = w (first term, so no 0 + x rounding or -0 sign flip) or acc += w.
+__device__ __forceinline__ void sum_into(float (&acc)[4], const float4& w, bool& first) {
+    if (first) {
+        acc[0] = w.x;
+        acc[1] = w.y;
+        acc[2] = w.z;
+        acc[3] = w.w;
+        first = false;
+    } else {
+        acc[0] += w.x;
+        acc[1] += w.y;
+        acc[2] += w.z;
+        acc[3] += w.w;
+    }
+}
+
 // Source-ordered sum of the tp staged partials of one 128 x 256 tile into the
 // owners' C. Consecutive threads take consecutive 4-column groups of a row
 // (coalesced), and every source's float4 is loaded before the sum.
@@ -424,15 +440,15 @@ __device__ __forceinline__ void reduce_tile_coalesced(const GemmParams& p, int r
             if (pos < npos && col < p.n) {
                 const int grow = row0 + rr;
                 const int o = grow / p.rpr;
-                float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                // Canonical order: the other sources ascending, then the owner's own.
+                float acc[4];
+                bool first = true;
 #pragma unroll
                 for (int s = 0; s < kMaxRanks; ++s)
-                    if (s < p.tp) {
-                        acc[0] += v[u][s].x;
-                        acc[1] += v[u][s].y;
-                        acc[2] += v[u][s].z;
-                        acc[3] += v[u][s].w;
-                    }
+                    if (s < p.tp && s != o) sum_into(acc, v[u][s], first);
+#pragma unroll
+                for (int s = 0; s < kMaxRanks; ++s)
+                    if (s == o) sum_into(acc, v[u][s], first);
                 store_row<4>(p.c_rank[o], static_cast<long long>(grow - o * p.rpr) * p.ldc + col, col, p.n, p.out_f32,
                              acc);
             }
@@ -864,6 +880,19 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 // vector red.add into the owner's fp32 accumulator (FusedReduce).
                 // Each 32-column chunk goes TMEM -> registers -> this warp's smem
                 // window -> coalesced global stores (4 rows x 128 B per instruction).
+                // Chained mode (every rank in this launch, rank-major schedule): the
+                // partials of a tile are summed in a chain in schedule order —
+                // sources ascending, the owner last — each source reading the
+                // running sum its predecessor left in the owner's plane 0, adding its
+                // accumulator and writing it back; the owner then reads one plane
+                // instead of tp-1. Deterministic (fixed order), no extra bytes moved
+                // between ranks, and the owner tail stops being bound by reading
+                // tp-1 planes from HBM.
+                const int chain_pred = p.rs_chain ? (me - 1 == o0 ? me - 2 : me - 1) : -1;
+                if (p.rs_chain && remote && chain_pred >= 0 && et == 0 && !(p.dbg & 1))
+                    wait_flag(p.rs_flags[o0] + tile_id * p.tp + chain_pred, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+                              static_cast<uint32_t>(tile_id), static_cast<uint32_t>(chain_pred));
+                if (p.rs_chain) named_bar_sync(1, 128);
                 if (__any_sync(0xffffffffu, remote) && !(p.dbg & 1)) {
                     // RS mode: ownership blocks are whole 128-row tiles, so the owner is
                     // uniform over this CTA's rows. WriteAlltoAll staging is tile-major:
@@ -873,12 +902,19 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     // is per row.
                     const long long lr0 = row0 - static_cast<long long>(o0) * p.rpr;
                     float* wdst = p.fused_reduce ? nullptr
-                                                 : p.staging[o0] + parity * p.stage_parity + me * p.stage_plane +
+                                                 : p.staging[o0] + parity * p.stage_parity +
+                                                       (p.rs_chain ? 0 : me) * p.stage_plane +
                                                        stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
+                    const bool add_prev = p.rs_chain && chain_pred >= 0;
                     for (int c = 0; c < kBN / 32; ++c) {
                         const int colc = col0 + c * 32;
                         if (colc >= p.n) break;  // warp-uniform
                         uint32_t r[32];
+                        float4 prev[8];
+                        if (add_prev) {  // the running sum, loaded before the TMEM round trip
+#pragma unroll
+                            for (int it = 0; it < 8; ++it) prev[it] = ld_cg_f4(wdst + c * 4096 + it * 128 + lane * 4);
+                        }
                         tmem_ld32(tbase + c * 32, r);
                         tmem_ld_wait();
                         epi_stage(wbuf, lane, r);
@@ -888,7 +924,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                             const int col = colc + g * 4;
                             const int grow = row0 + q * 32 + i;
                             if (grow >= p.m || col >= p.n) continue;
-                            const float4 v = epi_read(wbuf, i, g);
+                            float4 v = epi_read(wbuf, i, g);
+                            if (add_prev) {
+                                v.x = prev[it].x + v.x;
+                                v.y = prev[it].y + v.y;
+                                v.z = prev[it].z + v.z;
+                                v.w = prev[it].w + v.w;
+                            }
                             if (p.fused_reduce) {
                                 const int o = grow / p.rpr;
                                 if (o != me)
@@ -932,8 +974,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     }
                 } else if (mine_in_tile) {
                     if (et == 0) {
+                        const int chain_last = me == p.tp - 1 ? p.tp - 2 : p.tp - 1;
                         for (int s = 0; s < p.tp; ++s)
-                            if (s != me)
+                            if (s != me && (!p.rs_chain || s == chain_last))
                                 wait_flag(p.rs_flags[me] + tile_id * p.tp + s, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
                                           static_cast<uint32_t>(tile_id), static_cast<uint32_t>(s));
                         trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(me));
@@ -941,13 +984,37 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     named_bar_sync(1, 128);
                     // Coalesced source-ordered sum: the own accumulator chunk is staged
                     // in this warp's smem window; lanes then walk 4 rows x 32 columns
-                    // per step, loading every source's float4 before adding in source
-                    // order 0..tp-1 (deterministic; FusedReduce: accumulator + own).
+                    // per step, loading every source's float4 before adding in the
+                    // canonical order (deterministic; chain / FusedReduce: running
+                    // sum + own, the chunk's 8 loads issued before its TMEM load).
                     const long long lr0 = row0 - static_cast<long long>(me) * p.rpr;  // tile's first owned row
                     const float* src0 = p.fused_reduce
                                             ? p.fr_acc[me]
                                             : p.staging[me] + parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) +
                                                   q * 1024;
+                    if (p.rs_chain) {
+                        for (int c = 0; c < kBN / 32; ++c) {
+                            const int colc = col0 + c * 32;
+                            if (colc >= p.n) break;  // warp-uniform
+                            float4 sum[8];
+#pragma unroll
+                            for (int it = 0; it < 8; ++it) sum[it] = ld_cg_f4(src0 + c * 4096 + it * 128 + lane * 4);
+                            uint32_t r[32];
+                            tmem_ld32(tbase + c * 32, r);
+                            tmem_ld_wait();
+                            epi_stage(wbuf, lane, r);
+#pragma unroll
+                            for (int it = 0; it < 8; ++it) {
+                                const int i = it * 4 + (lane >> 3), g = lane & 7;
+                                const int col = colc + g * 4;
+                                if (col >= p.n) continue;
+                                const float4 own = epi_read(wbuf, i, g);
+                                float acc[4] = {sum[it].x + own.x, sum[it].y + own.y, sum[it].z + own.z,
+                                                sum[it].w + own.w};
+                                store_row<4>(p.c[l], (lr0 + q * 32 + i) * p.ldc_l[l] + col, col, p.n, p.out_f32, acc);
+                            }
+                        }
+                    } else
                     for (int c = 0; c < kBN / 32; ++c) {
                         const int colc = col0 + c * 32;
                         if (colc >= p.n) break;  // warp-uniform
@@ -968,6 +1035,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                 if (ok[u]) {
                                     if (p.fused_reduce) {
                                         v[u][0] = ld_cg_f4(src0 + lr * p.ld_stage + col);
+                                    } else if (p.rs_chain) {
+                                        v[u][0] = ld_cg_f4(src0 + c * 4096 + (it0 + u) * 128 + lane * 4);
                                     } else {
                                         const float* src = src0 + c * 4096 + (it0 + u) * 128 + lane * 4;
 #pragma unroll
@@ -982,23 +1051,23 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                 const int i = (it0 + u) * 4 + (lane >> 3), g = lane & 7;
                                 const float4 own = epi_read(wbuf, i, g);
                                 float acc[4];
-                                if (p.fused_reduce) {
+                                if (p.fused_reduce || p.rs_chain) {  // running sum of the others + own
                                     acc[0] = v[u][0].x + own.x;
                                     acc[1] = v[u][0].y + own.y;
                                     acc[2] = v[u][0].z + own.z;
                                     acc[3] = v[u][0].w + own.w;
                                 } else {
-                                    // Source order 0..tp-1 (deterministic, the oracle's rank order).
-                                    acc[0] = acc[1] = acc[2] = acc[3] = 0.0f;
+                                    // The canonical deterministic order (same as the chain and
+                                    // the last-arriver sum): the other sources ascending, then
+                                    // the owner's own partial.
+                                    bool first = true;
 #pragma unroll
                                     for (int s2 = 0; s2 < kMaxRanks; ++s2) {
                                         if (s2 >= p.tp) break;
-                                        const float4 w = s2 == me ? own : v[u][s2];
-                                        acc[0] += w.x;
-                                        acc[1] += w.y;
-                                        acc[2] += w.z;
-                                        acc[3] += w.w;
+                                        if (s2 == me) continue;
+                                        sum_into(acc, v[u][s2], first);
                                     }
+                                    sum_into(acc, own, first);
                                 }
                                 const int col = colc + g * 4;
                                 store_row<4>(p.c[l], (lr0 + q * 32 + i) * p.ldc_l[l] + col, col, p.n, p.out_f32, acc);
