@@ -80,7 +80,7 @@ typedef struct {
 /* overlap::EngineOptions (engine.hpp:65-72) plus the B200 knobs. */
 typedef struct {
     int workers_per_rank;      /* accepted for API parity; the device uses every SM */
-    int deterministic_reduce;  /* 1: WriteAlltoAll-style source-ordered sum */
+    int deterministic_reduce;  /* 1: fixed-order sum (other sources ascending, then the owner's own) */
     long long poll_budget;     /* accepted for API parity (device waits are time-bounded) */
     double wall_budget_s;      /* device spin-wait timeout (default 10 s, engine.hpp:69) */
     uint64_t interleave_seed;  /* nonzero: device jitter (nanosleep) before tiles, race testing */
@@ -190,8 +190,11 @@ int flux_ag_gemm(flux_comm* comm, const flux_problem* problem, const flux_tile* 
                  void* const* streams);
 /* run_fused_gemm_reducescatter (engine.hpp:101-103, engine.cpp:221-352; paper Alg. 1).
  * The epilogue stores each partial tile into the owner's staging plane over
- * NVLink and raises a per-(tile, source) flag; the owner reduces in source
- * order 0..tp-1 inside its local-tile epilogue (deterministic). */
+ * NVLink and raises a per-(tile, source) flag; the owner reduces in a fixed
+ * order (the other sources ascending, then its own partial) inside its
+ * local-tile epilogue (deterministic). When all ranks share one launch the
+ * sources chain the sum in that order instead (each adds its partial to the
+ * running sum its predecessor left), and the owner reads one plane. */
 int flux_gemm_rs(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
                  int write_mode, int swizzle_on, const flux_opts* opts, void* const* streams);
 /* The AllGather transfer engine flux_ag_gemm uses for this problem: 1 copy

@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 // Ownership blocks narrower than a tile (decode-sized M): every source
                 // stores its whole partial tile into the owners' staging planes and
                 // bumps the tile's arrival counter; the last of the tp arrivals sums
-                // the tile in source order 0..tp-1 and writes every owner's rows.
+                // the tile in the canonical order and writes every owner's rows.
                 // Nobody waits, the result stays deterministic.
                 const int me = p.global_rank[l];
                 const uint32_t parity = p.epoch & 1u;
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         st_release_sys(p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
                     }
                 }
-                // Phase 2: owned rows = source-ordered sum of all partials.
+                // Phase 2: owned rows = sum of all partials in the canonical order.
                 const bool mine_in_tile = (me >= o0 && me <= o1);
                 if (mine_in_tile && (p.dbg & 2)) {
                     // Ablation: the owner stores only its own accumulator (no waits, no reduce).
@@ -982,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(me));
                     }
                     named_bar_sync(1, 128);
-                    // Coalesced source-ordered sum: the own accumulator chunk is staged
+                    // Coalesced fixed-order sum: the own accumulator chunk is staged
                     // in this warp's smem window; lanes then walk 4 rows x 32 columns
                     // per step, loading every source's float4 before adding in the
                     // canonical order (deterministic; chain / FusedReduce: running
