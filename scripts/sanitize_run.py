@@ -1,0 +1,69 @@
+"""Small fused runs for compute-sanitizer (memcheck / racecheck / synccheck):
+AG on both transfer engines, RS chained / owner-sum / last-arriver, FusedReduce,
+and the MLP chain, each checked against a cuBLAS product. Usage:
+    compute-sanitizer --tool memcheck python scripts/sanitize_run.py"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2406_06858_b200 as fx
+from paper_2406_06858_b200 import _native as N
+
+
+def fill(comm, p, seed):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    for r in range(p.tp):
+        for kind in (N.BUF_A_SHARD, N.BUF_B_SHARD):
+            t = comm.tensor(r, kind, p)
+            t.copy_((torch.rand(t.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+
+
+def check(comm, p, tag):
+    a = [comm.tensor(r, N.BUF_A_SHARD, p).float() for r in range(p.tp)]
+    b = [comm.tensor(r, N.BUF_B_SHARD, p).float() for r in range(p.tp)]
+    worst = 0.0
+    for r in range(p.tp):
+        got = comm.tensor(r, N.BUF_C_OUT, p).float()
+        if p.pattern == fx.ALLGATHER_GEMM:
+            ref = torch.cat(a) @ b[r].t()
+        else:
+            rpr = p.rows_per_rank()
+            ref = sum(a[s][r * rpr:(r + 1) * rpr] @ b[s].t() for s in range(p.tp))
+        worst = max(worst, ((got - ref).abs().max() / ref.abs().max().clamp(min=1)).item())
+    print(f"{tag}: max err {worst:.2e}", flush=True)
+    assert worst < 1e-2, tag
+
+
+cases = [("AG copy engines", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(ag_engine=1)),
+         ("AG in-kernel", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(ag_engine=2)),
+         ("RS chained (aligned blocks)", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
+         ("RS owner sum (Naive swizzle)", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
+         ("RS last arriver (decode)", fx.ProblemSpec(64, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
+         ("RS FusedReduce", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), dict(deterministic_reduce=0))]
+for tag, p, kw in cases:
+    with fx.Communicator(p.tp, [0] * p.tp, heap_bytes=fx.required_heap_bytes(p)) as comm:
+        fill(comm, p, 1)
+        opts = fx.default_opts(wall_budget_s=120.0, **kw)
+        tile = fx.TileShape(p.rows_per_rank(), p.local_cols())
+        if p.pattern == fx.ALLGATHER_GEMM:
+            comm.ag_gemm(p, tile, opts=opts)
+        else:
+            wm = fx.FUSED_REDUCE if kw.get("deterministic_reduce") == 0 else fx.WRITE_ALLTOALL
+            comm.gemm_rs(p, tile, wm, "Naive" not in tag, opts)
+        comm.sync()
+        check(comm, p, tag)
+spec = fx.MlpSpec(m=512, hidden=256, ffn=1024, tp=2, activation=fx.ACT_GELU)
+x = [torch.randn(256, 256, device="cuda").to(torch.bfloat16) for _ in range(2)]
+wu = [torch.randn(512, 256, device="cuda").mul(0.05).to(torch.bfloat16) for _ in range(2)]
+wd = [torch.randn(256, 512, device="cuda").mul(0.05).to(torch.bfloat16) for _ in range(2)]
+act = [torch.empty(512, 512, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+out = [torch.empty(256, 256, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+with fx.Communicator(2, [0, 0], heap_bytes=spec.required_heap_bytes()) as comm:
+    comm.mlp_forward(spec, [dict(x=x[r], w_up=wu[r], w_down=wd[r], act=act[r], out=out[r]) for r in range(2)],
+                     opts=fx.default_opts(wall_budget_s=120.0))
+    comm.sync()
+print("MLP chain: ok")
+print("SANITIZE-RUN-DONE")
