@@ -86,3 +86,109 @@ def gemm_rs(a: torch.Tensor, weight: torch.Tensor, comm_id: int) -> torch.Tensor
 @gemm_rs.register_fake
 def _(a, weight, comm_id):
     return a.new_empty(a.shape[0] // _REGISTRY[comm_id].tp, weight.shape[0])
+
+
+# ---------------------------------------------------------------------------
+# Chained tensor-parallel MLP as custom ops + autograd.
+# ---------------------------------------------------------------------------
+def _ag_problem(comm, a_shard, n_local):
+    tp = comm.tp
+    return ProblemSpec(a_shard.shape[0] * tp, n_local * tp, a_shard.shape[1], tp, N.ALLGATHER_GEMM)
+
+
+@torch.library.custom_op("flux_b200::ag_gemm_act", mutates_args=())
+def ag_gemm_act(a_shard: torch.Tensor, weight: torch.Tensor, comm_id: int,
+                activation: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """activation(AllGather(a_shard) @ weight^T) with the activation in the
+    GEMM epilogue; also returns the pre-activation (empty for SWIGLU, whose
+    output has half the columns: 128 gate + 128 up rows per 256-row group)."""
+    comm = _REGISTRY[comm_id]
+    p = _ag_problem(comm, a_shard, weight.shape[0])
+    swiglu = activation == N.ACT_SWIGLU
+    out = torch.empty(p.m, weight.shape[0] // (2 if swiglu else 1), dtype=torch.bfloat16, device=a_shard.device)
+    pre = (torch.empty(0, 0, dtype=torch.bfloat16, device=a_shard.device) if swiglu
+           else torch.empty(p.m, weight.shape[0], dtype=torch.bfloat16, device=a_shard.device))
+    opts = N.default_opts(activation=activation)
+    comm.ag_gemm_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a_shard, weight, out, None if swiglu else pre)],
+                    opts=opts, streams=_stream())
+    return out, pre
+
+
+@ag_gemm_act.register_fake
+def _(a_shard, weight, comm_id, activation):
+    m = a_shard.shape[0] * _REGISTRY[comm_id].tp
+    swiglu = activation == N.ACT_SWIGLU
+    return (a_shard.new_empty(m, weight.shape[0] // (2 if swiglu else 1)),
+            a_shard.new_empty(0, 0) if swiglu else a_shard.new_empty(m, weight.shape[0]))
+
+
+@torch.library.custom_op("flux_b200::ag_gemm_dact", mutates_args=())
+def ag_gemm_dact(a_shard: torch.Tensor, weight: torch.Tensor, pre: torch.Tensor, comm_id: int,
+                 activation: int) -> torch.Tensor:
+    """(AllGather(a_shard) @ weight^T) * activation'(pre): the backward of the
+    GEMM-RS + activation, with the derivative in the AG-GEMM epilogue."""
+    comm = _REGISTRY[comm_id]
+    p = _ag_problem(comm, a_shard, weight.shape[0])
+    out = torch.empty(p.m, weight.shape[0], dtype=torch.bfloat16, device=a_shard.device)
+    comm.ag_gemm_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a_shard, weight, out, pre)],
+                    opts=N.default_opts(activation_grad=activation), streams=_stream())
+    return out
+
+
+@ag_gemm_dact.register_fake
+def _(a_shard, weight, pre, comm_id, activation):
+    return a_shard.new_empty(a_shard.shape[0] * _REGISTRY[comm_id].tp, weight.shape[0])
+
+
+def gathered_input(comm_id: int, a_shard: torch.Tensor, n_local: int) -> torch.Tensor:
+    """Copy of this rank's gathered A of the last AG-GEMM (the symmetric a_agg)."""
+    comm = _REGISTRY[comm_id]
+    return comm.tensor(comm.rank, N.BUF_A_AGG, _ag_problem(comm, a_shard, n_local)).clone()
+
+
+class _TPMlpFunction(torch.autograd.Function):
+    """out = ReduceScatter(act(AllGather(x) W_up^T) W_down^T) with the fused
+    operators; backward: dx = ReduceScatter((AllGather(dout) W_down) *
+    act'(pre) W_up) (the AG <-> RS interchange), weight gradients as local
+    GEMMs on the gathered operands read back from the symmetric heap."""
+
+    @staticmethod
+    def forward(ctx, x, w_up, w_down, comm_id, activation):
+        z, pre = torch.ops.flux_b200.ag_gemm_act(x, w_up, comm_id, activation)
+        x_g = gathered_input(comm_id, x, w_up.shape[0]) if w_up.requires_grad else None
+        out = torch.ops.flux_b200.gemm_rs(z, w_down, comm_id)
+        ctx.save_for_backward(w_up, w_down, z, pre, x_g)
+        ctx.comm_id, ctx.activation = comm_id, activation
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        w_up, w_down, z, pre, x_g = ctx.saved_tensors
+        if ctx.activation == N.ACT_SWIGLU:
+            raise NotImplementedError("SWIGLU backward")
+        dout = dout.contiguous().to(torch.bfloat16)
+        dy = torch.ops.flux_b200.ag_gemm_dact(dout, w_down.t().contiguous(), pre, ctx.comm_id, ctx.activation)
+        dout_g = gathered_input(ctx.comm_id, dout, w_down.shape[1]) if w_down.requires_grad else None
+        dx = torch.ops.flux_b200.gemm_rs(dy, w_up.t().contiguous(), ctx.comm_id)
+        d_w_up = (dy.t().float() @ x_g.float()).to(w_up.dtype) if x_g is not None else None
+        d_w_down = (dout_g.t().float() @ z.float()).to(w_down.dtype) if dout_g is not None else None
+        return dx, d_w_up, d_w_down, None, None
+
+
+class TPMlp(torch.nn.Module):
+    """Sequence-parallel tensor-parallel MLP block on the fused operators:
+    x [m/tp, hidden] -> [m/tp, hidden]; w_up [ffn/tp (x2 SWIGLU), hidden],
+    w_down [hidden, ffn/tp] (this rank's shards, nn.Linear layout)."""
+
+    def __init__(self, hidden: int, ffn: int, comm_id: int, activation: int = N.ACT_GELU, device=None):
+        super().__init__()
+        tp = _REGISTRY[comm_id].tp
+        rows = ffn // tp * (2 if activation == N.ACT_SWIGLU else 1)
+        self.w_up = torch.nn.Parameter(torch.empty(rows, hidden, dtype=torch.bfloat16, device=device))
+        self.w_down = torch.nn.Parameter(torch.empty(hidden, ffn // tp, dtype=torch.bfloat16, device=device))
+        torch.nn.init.normal_(self.w_up, std=hidden ** -0.5)
+        torch.nn.init.normal_(self.w_down, std=ffn ** -0.5)
+        self.comm_id, self.activation = comm_id, activation
+
+    def forward(self, x):
+        return _TPMlpFunction.apply(x, self.w_up, self.w_down, self.comm_id, self.activation)

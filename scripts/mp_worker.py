@@ -70,6 +70,49 @@ for pat, m, n, k in [(fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384), (fx.GEM
     want = O.dense_oracle(pat, m, n, k, world, a_all, b_all)[rank]
     results[f"torchop-{pat}-{m}-{n}-{k}"] = (O.max_rel_error(out.double().cpu().numpy(), want), H.tol(False, k))
     dist.barrier()
+# The chained MLP as an autograd module (torch_ops.TPMlp) against fp32 autograd
+# of the same sequence-parallel MLP on the same bf16 values (normwise error).
+M, HID, FFN = 256 * world, 256, 512 * world
+mlp_heap = fx.MlpSpec(M, HID, FFN, world, fx.ACT_GELU).required_heap_bytes()
+assert mlp_heap <= heap, (mlp_heap, heap)
+
+
+def _rand(shape, seed, scale=1.0):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    return ((torch.rand(shape, generator=g, device="cuda") * 2 - 1) * scale).to(torch.bfloat16)
+
+
+xs = [_rand((M // world, HID), 100 + r) for r in range(world)]
+wus = [_rand((FFN // world, HID), 200 + r, 0.1) for r in range(world)]
+wds = [_rand((HID, FFN // world), 300 + r, 0.1) for r in range(world)]
+douts = [_rand((M // world, HID), 400 + r) for r in range(world)]
+mod = torch_ops.TPMlp(HID, FFN, cid, fx.ACT_GELU, device="cuda")
+with torch.no_grad():
+    mod.w_up.copy_(wus[rank])
+    mod.w_down.copy_(wds[rank])
+x = xs[rank].clone().requires_grad_(True)
+dist.barrier()
+y = mod(x)
+y.backward(douts[rank])
+torch.cuda.synchronize()
+xr = torch.cat(xs).float().requires_grad_(True)
+wur = [w.float().requires_grad_(True) for w in wus]
+wdr = [w.float().requires_grad_(True) for w in wds]
+yr = sum(torch.nn.functional.gelu(xr @ wur[r].t()) @ wdr[r].t() for r in range(world))
+yr.backward(torch.cat(douts).float())
+rpr = M // world
+
+
+def _nerr(got, ref):
+    return ((got.float() - ref).abs().max() / ref.abs().max().clamp(min=1.0)).item()
+
+
+results["mlp-out"] = (_nerr(y, yr[rank * rpr:(rank + 1) * rpr].detach()), 3e-2)
+results["mlp-dx"] = (_nerr(x.grad, xr.grad[rank * rpr:(rank + 1) * rpr]), 3e-2)
+results["mlp-dw_up"] = (_nerr(mod.w_up.grad, wur[rank].grad), 3e-2)
+results["mlp-dw_down"] = (_nerr(mod.w_down.grad, wdr[rank].grad), 3e-2)
+dist.barrier()
 comm.close()
 print("RESULT", rank, json.dumps(results), flush=True)
 dist.destroy_process_group()

@@ -1,5 +1,6 @@
 """One process per rank through the IPC communicator (cudaIpc heap mapping,
 cross-process flags, peer stores / copy-engine pulls), launched with torchrun.
+Also runs the chained MLP as a PyTorch autograd module (torch_ops.TPMlp).
 All ranks may share the single GPU of the test box: the kernels of the two
 processes time-slice, and every device wait is bounded, so a missing signal
 fails as DeadlockError instead of hanging."""
@@ -24,6 +25,6 @@ def test_two_processes_ipc_match_oracle():
     assert len(lines) == 2
     for line in lines:
         res = json.loads(line.split(" ", 2)[2])
-        assert len(res) == 7
+        assert len(res) == 11  # 4 operator cases, 3 torch ops, the TPMlp autograd module (out, dx, dW_up, dW_down)
         for case, (err, tol) in res.items():
             assert err <= tol, (case, err, tol)
