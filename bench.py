@@ -167,13 +167,15 @@ def reference_arm(args, wl):
     for _ in range(args.warmup):
         run_cpu_reference(pattern, m, n, k, tp, reps=1)
     vals = []
+    ms, ns, ks = cpu_sample_shape(pattern, m, n, k, tp)
     for _ in range(args.steps):
         base = run_cpu_reference(pattern, m, n, k, tp, reps=1)
         vals.append(base["value"])
     v = statistics.median(vals)
     base["value"] = v
+    ms_step = 2.0 * ms * ns * ks / (v * 1e12) * 1e3  # one bounded sample (sample_m rows) per step
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOPS", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Rng stream)",
             "config": {"workload": wl, "description": desc, "m": m, "n": n, "k": k, "tp": tp,
                        "sample_m": cpu_sample_shape(pattern, m, n, k, tp)[0]},
