@@ -1096,8 +1096,13 @@ static int check_heap(flux_comm* c, const flux_problem* p) {
 static bool ag_sm_engine_ok(const flux_problem* p, int transfer) {
     return transfer == FLUX_PULL && local_k(p) % 8 == 0 && (p->m + kBM - 1) / kBM < static_cast<int>(kAgGroupCap);
 }
-static int ag_engine_for(const flux_problem* p, int transfer, int requested) {
+static int ag_engine_for(const flux_problem* p, int transfer, int requested, int rpct = 0, int ranks_per_device = 1) {
     if (requested == 1 || requested == 2) return requested;
+    // Many small comm tiles on one copy stream cost ~8 us of copy + flag-write
+    // overhead each (measured: L-AG emulated, rpct 64 -> 448 copies, 3x slower):
+    // move them on the SMs instead.
+    const int rpr = rows_per_rank(p);
+    if (rpct > 0 && ag_sm_engine_ok(p, transfer) && (p->tp - 1) * (rpr / rpct) * ranks_per_device > 128) return 2;
     // Auto: in-kernel transfers up to 32 MiB of gathered A (decode / small
     // problems: one launch, no host work per comm tile), copy engines above.
     // Measured on L-AG (64 MiB): within +-5 % of each other, the sign depending
@@ -1170,7 +1175,9 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     // SMs (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies) ----
     if (oc.o.ag_engine == 2 && !ag_sm_engine_ok(p, transfer))
         return fail(FLUX_ERR_CONFIG, "in-kernel AllGather transfer needs Pull and k % 8 == 0");
-    const bool use_sm = ag_engine_for(p, transfer, oc.o.ag_engine) == 2;
+    size_t per_dev = 1;
+    for (const auto& dg : device_groups(c)) per_dev = std::max(per_dev, dg.size());
+    const bool use_sm = ag_engine_for(p, transfer, oc.o.ag_engine, rpct, static_cast<int>(per_dev)) == 2;
     if (use_sm) {
         const int cg = choose_cg(p, oc.o);
         const int groups = (p->m + kBM - 1) / kBM;
@@ -1387,8 +1394,37 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
         // ranks sharing this device run rank by rank (each rank's own block,
         // then its peers' blocks), else every own block then ring step by step.
         std::vector<std::pair<int, int>> jobs;  // (rank, step); step -1 = local copy
+        const bool all_here = static_cast<int>(g.size()) == tp && oc.o.emulated_order != 1 && tp > 1;
+        if (all_here) {
+            // Every rank on this device and stream: Pull and Push move the same
+            // rows (source shard -> destination a_agg), so issue them in exactly
+            // the order the rank-major kernel consumes blocks (its block order
+            // for this transfer mode and swizzle), whoever "owns" the descriptor.
+            for (int cr : g) {
+                FLUX_TRY(local_copy(cr));
+                RankState& rs = c->ranks[cr];
+                const std::vector<int> order = ag_block_order(p, cr, transfer, swizzle_on != 0, rpct);
+                for (int b : order) {
+                    if (b == cr) continue;
+                    const std::vector<Desc>& list = transfer == FLUX_PULL ? specs[cr] : specs[b];
+                    const int want_peer = transfer == FLUX_PULL ? b : cr;
+                    const char* shard;
+                    size_t pitch;
+                    shard_of(b, shard, pitch);
+                    for (const Desc& d : list) {
+                        if (d.peer != want_peer) continue;
+                        FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
+                                           rowbytes, shard + static_cast<size_t>(d.row_begin - b * rpr) * pitch, pitch,
+                                           d.rows));
+                        FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
+                    }
+                }
+            }
+        }
         const bool rank_major = transfer == FLUX_PULL && oc.o.emulated_order != 1 && g.size() > 1;
-        if (rank_major) {
+        if (all_here) {
+            // issued above
+        } else if (rank_major) {
             for (int r : g)
                 for (int b = -1; b < tp - 1; ++b) jobs.emplace_back(r, b);
         } else {
