@@ -563,6 +563,7 @@ struct OpCommon {
     uint64_t timeout_ns;
     int fused_reduce = 0;  // RS FusedReduce in arrival order (red.add into the owner accumulator)
     int rs_last_arriver = 0;  // RS with ownership blocks narrower than a tile
+    int rs_chain = 0;         // RS with every rank in one launch: chained partial sums (kernel)
     const flux_operands* ops = nullptr;  // caller-provided operands (per rank; one entry in IPC mode)
 };
 
@@ -692,16 +693,9 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.timeout_ns = oc.timeout_ns;
         prm.jitter_seed = oc.o.interleave_seed;
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
-        // Chained RS partial sums (see the kernel): every rank in this one
-        // launch, rank-major schedule with the owners' blocks last, so each
-        // chain link waits only on a tile a whole section earlier.
-        {
-            const char* env = std::getenv("FLUX_RS_CHAIN");
-            prm.rs_chain = mode == kModeRS && !oc.fused_reduce && interleave == kInterleaveRankTail &&
-                                   static_cast<int>(g.size()) == c->tp && !(env && std::atoi(env) == 0)
-                               ? 1
-                               : 0;
-        }
+        prm.rs_chain = mode == kModeRS ? oc.rs_chain : 0;
+        for (int q = 0; q < kMaxRanks; ++q) prm.slot_of[q] = -1;
+        for (size_t li = 0; li < g.size(); ++li) prm.slot_of[g[li]] = static_cast<int>(li);
         prm.rs_last_arriver = mode == kModeRSLast ? 1 : 0;
         if (const char* env = std::getenv("FLUX_DEBUG")) prm.dbg = std::atoi(env);  // profiling ablations only
         // Join the other local ranks' streams into the launch stream.
@@ -1563,6 +1557,17 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
                             "caller-provided C needs ownership blocks of whole 128-row tiles (m/tp % 128 == 0)");
     if (oc.rs_last_arriver && static_cast<size_t>(tiles) > kRsCtrCap)
         return fail(FLUX_ERR_CONFIG, "too many output tiles for the arrival counters");
+    // Chained partial sums (kernel, RS branch) when every rank runs in this one
+    // launch (rank-major order, owners' blocks last); every chain link waits only
+    // on an earlier section.
+    {
+        const auto groups = device_groups(c);
+        const char* env = std::getenv("FLUX_RS_CHAIN");
+        oc.rs_chain = aligned && !oc.fused_reduce && !oc.rs_last_arriver && groups.size() == 1 &&
+                              static_cast<int>(groups[0].size()) == tp && !(env && std::atoi(env) == 0)
+                          ? 1
+                          : 0;
+    }
     const int interleave = aligned ? kInterleaveRankTail : (oc.rs_last_arriver ? kInterleaveRank : kInterleaveStep);
     FLUX_TRY(launch_groups(c, p, oc.rs_last_arriver ? kModeRSLast : kModeRS, oc, streams, seq, 0, interleave, cg,
                            false, -1, tail));

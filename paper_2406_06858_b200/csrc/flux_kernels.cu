@@ -867,6 +867,75 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 const int tile_id = tm * p.tiles_n + tn;
                 const int rlast = min(row0 + kBM, p.m) - 1;
                 const int o0 = row0 / p.rpr, o1 = rlast / p.rpr;
+                if (p.rs_chain) {
+                    // Chained partial sums (every rank in this launch, rank-major
+                    // schedule with every owner's block moved behind all other tiles,
+                    // ownership blocks aligned to tiles). The partials of a tile are
+                    // summed in the canonical order — the other sources ascending,
+                    // then the owner — as a chain through the owner's staging plane:
+                    // each source adds its accumulator to the running sum its
+                    // predecessor left (flag (tile, predecessor)) and writes it back;
+                    // the owner adds its own accumulator to that one plane instead of
+                    // reading tp-1 partials. Every wait targets an earlier section.
+                    // (A variant where the last source closes each chain, so the owner
+                    // blocks need no tail, measured no faster: it trades the tail's
+                    // weight re-stream for staging the owners' partials.)
+                    const int o = o0, tp = p.tp;
+                    const int last = o == tp - 1 ? tp - 2 : tp - 1;
+                    const bool own_tile = me == o;
+                    const bool closes = own_tile;
+                    const int pred = own_tile ? last : (me - 1 == o ? me - 2 : me - 1);
+                    const long long lr0 = row0 - static_cast<long long>(o) * p.rpr;
+                    float* plane0 = p.staging[o] + parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
+                    if (et == 0) {
+                        if (pred >= 0)
+                            wait_flag(p.rs_flags[o] + tile_id * tp + pred, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+                                      static_cast<uint32_t>(tile_id), static_cast<uint32_t>(pred));
+                        if (closes) trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(o));
+                    }
+                    named_bar_sync(1, 128);
+                    const int os = p.slot_of[o];
+                    void* cdst = closes ? p.c[os] : nullptr;
+                    const int ldc_o = closes ? p.ldc_l[os] : 0;
+                    float* wdst = plane0;
+                    for (int c = 0; c < kBN / 32; ++c) {
+                        const int colc = col0 + c * 32;
+                        if (colc >= p.n) break;  // warp-uniform
+                        float4 sum[8];
+                        if (pred >= 0) {  // running sum, loaded before the TMEM round trip
+#pragma unroll
+                            for (int it = 0; it < 8; ++it) sum[it] = ld_cg_f4(plane0 + c * 4096 + it * 128 + lane * 4);
+                        }
+                        uint32_t r[32];
+                        tmem_ld32(tbase + c * 32, r);
+                        tmem_ld_wait();
+                        epi_stage(wbuf, lane, r);
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int i = it * 4 + (lane >> 3), g = lane & 7;
+                            const int col = colc + g * 4;
+                            if (col >= p.n) continue;
+                            float4 v = epi_read(wbuf, i, g);
+                            if (pred >= 0) {
+                                v.x = sum[it].x + v.x;
+                                v.y = sum[it].y + v.y;
+                                v.z = sum[it].z + v.z;
+                                v.w = sum[it].w + v.w;
+                            }
+                            if (closes) {
+                                float acc[4] = {v.x, v.y, v.z, v.w};
+                                store_row<4>(cdst, (lr0 + q * 32 + i) * ldc_o + col, col, p.n, p.out_f32, acc);
+                            } else {
+                                *reinterpret_cast<float4*>(wdst + c * 4096 + it * 128 + lane * 4) = v;
+                            }
+                        }
+                    }
+                    named_bar_sync(1, 128);
+                    if (!closes && et == 0) {
+                        trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o));
+                        st_release_sys(p.rs_flags[o] + tile_id * tp + me, p.epoch);
+                    }
+                } else {
                 if (p.fused_reduce) {
                     // FusedReduce: each owner zeroes this parity's accumulator on its
                     // stream before the launch and stamps fr_ready; wait for that once.
@@ -880,19 +949,6 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 // vector red.add into the owner's fp32 accumulator (FusedReduce).
                 // Each 32-column chunk goes TMEM -> registers -> this warp's smem
                 // window -> coalesced global stores (4 rows x 128 B per instruction).
-                // Chained mode (every rank in this launch, rank-major schedule): the
-                // partials of a tile are summed in a chain in schedule order —
-                // sources ascending, the owner last — each source reading the
-                // running sum its predecessor left in the owner's plane 0, adding its
-                // accumulator and writing it back; the owner then reads one plane
-                // instead of tp-1. Deterministic (fixed order), no extra bytes moved
-                // between ranks, and the owner tail stops being bound by reading
-                // tp-1 planes from HBM.
-                const int chain_pred = p.rs_chain ? (me - 1 == o0 ? me - 2 : me - 1) : -1;
-                if (p.rs_chain && remote && chain_pred >= 0 && et == 0 && !(p.dbg & 1))
-                    wait_flag(p.rs_flags[o0] + tile_id * p.tp + chain_pred, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
-                              static_cast<uint32_t>(tile_id), static_cast<uint32_t>(chain_pred));
-                if (p.rs_chain) named_bar_sync(1, 128);
                 if (__any_sync(0xffffffffu, remote) && !(p.dbg & 1)) {
                     // RS mode: ownership blocks are whole 128-row tiles, so the owner is
                     // uniform over this CTA's rows. WriteAlltoAll staging is tile-major:
@@ -902,19 +958,12 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     // is per row.
                     const long long lr0 = row0 - static_cast<long long>(o0) * p.rpr;
                     float* wdst = p.fused_reduce ? nullptr
-                                                 : p.staging[o0] + parity * p.stage_parity +
-                                                       (p.rs_chain ? 0 : me) * p.stage_plane +
+                                                 : p.staging[o0] + parity * p.stage_parity + me * p.stage_plane +
                                                        stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
-                    const bool add_prev = p.rs_chain && chain_pred >= 0;
                     for (int c = 0; c < kBN / 32; ++c) {
                         const int colc = col0 + c * 32;
                         if (colc >= p.n) break;  // warp-uniform
                         uint32_t r[32];
-                        float4 prev[8];
-                        if (add_prev) {  // the running sum, loaded before the TMEM round trip
-#pragma unroll
-                            for (int it = 0; it < 8; ++it) prev[it] = ld_cg_f4(wdst + c * 4096 + it * 128 + lane * 4);
-                        }
                         tmem_ld32(tbase + c * 32, r);
                         tmem_ld_wait();
                         epi_stage(wbuf, lane, r);
@@ -924,13 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                             const int col = colc + g * 4;
                             const int grow = row0 + q * 32 + i;
                             if (grow >= p.m || col >= p.n) continue;
-                            float4 v = epi_read(wbuf, i, g);
-                            if (add_prev) {
-                                v.x = prev[it].x + v.x;
-                                v.y = prev[it].y + v.y;
-                                v.z = prev[it].z + v.z;
-                                v.w = prev[it].w + v.w;
-                            }
+                            const float4 v = epi_read(wbuf, i, g);
                             if (p.fused_reduce) {
                                 const int o = grow / p.rpr;
                                 if (o != me)
@@ -974,9 +1017,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     }
                 } else if (mine_in_tile) {
                     if (et == 0) {
-                        const int chain_last = me == p.tp - 1 ? p.tp - 2 : p.tp - 1;
                         for (int s = 0; s < p.tp; ++s)
-                            if (s != me && (!p.rs_chain || s == chain_last))
+                            if (s != me)
                                 wait_flag(p.rs_flags[me] + tile_id * p.tp + s, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
                                           static_cast<uint32_t>(tile_id), static_cast<uint32_t>(s));
                         trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(me));
@@ -985,36 +1027,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     // Coalesced fixed-order sum: the own accumulator chunk is staged
                     // in this warp's smem window; lanes then walk 4 rows x 32 columns
                     // per step, loading every source's float4 before adding in the
-                    // canonical order (deterministic; chain / FusedReduce: running
-                    // sum + own, the chunk's 8 loads issued before its TMEM load).
+                    // canonical order (deterministic; FusedReduce: the accumulator of
+                    // the others + own).
                     const long long lr0 = row0 - static_cast<long long>(me) * p.rpr;  // tile's first owned row
                     const float* src0 = p.fused_reduce
                                             ? p.fr_acc[me]
                                             : p.staging[me] + parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) +
                                                   q * 1024;
-                    if (p.rs_chain) {
-                        for (int c = 0; c < kBN / 32; ++c) {
-                            const int colc = col0 + c * 32;
-                            if (colc >= p.n) break;  // warp-uniform
-                            float4 sum[8];
-#pragma unroll
-                            for (int it = 0; it < 8; ++it) sum[it] = ld_cg_f4(src0 + c * 4096 + it * 128 + lane * 4);
-                            uint32_t r[32];
-                            tmem_ld32(tbase + c * 32, r);
-                            tmem_ld_wait();
-                            epi_stage(wbuf, lane, r);
-#pragma unroll
-                            for (int it = 0; it < 8; ++it) {
-                                const int i = it * 4 + (lane >> 3), g = lane & 7;
-                                const int col = colc + g * 4;
-                                if (col >= p.n) continue;
-                                const float4 own = epi_read(wbuf, i, g);
-                                float acc[4] = {sum[it].x + own.x, sum[it].y + own.y, sum[it].z + own.z,
-                                                sum[it].w + own.w};
-                                store_row<4>(p.c[l], (lr0 + q * 32 + i) * p.ldc_l[l] + col, col, p.n, p.out_f32, acc);
-                            }
-                        }
-                    } else
                     for (int c = 0; c < kBN / 32; ++c) {
                         const int colc = col0 + c * 32;
                         if (colc >= p.n) break;  // warp-uniform
@@ -1035,8 +1054,6 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                 if (ok[u]) {
                                     if (p.fused_reduce) {
                                         v[u][0] = ld_cg_f4(src0 + lr * p.ld_stage + col);
-                                    } else if (p.rs_chain) {
-                                        v[u][0] = ld_cg_f4(src0 + c * 4096 + (it0 + u) * 128 + lane * 4);
                                     } else {
                                         const float* src = src0 + c * 4096 + (it0 + u) * 128 + lane * 4;
 #pragma unroll
@@ -1051,7 +1068,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                 const int i = (it0 + u) * 4 + (lane >> 3), g = lane & 7;
                                 const float4 own = epi_read(wbuf, i, g);
                                 float acc[4];
-                                if (p.fused_reduce || p.rs_chain) {  // running sum of the others + own
+                                if (p.fused_reduce) {  // arrival-order sum of the others + own
                                     acc[0] = v[u][0].x + own.x;
                                     acc[1] = v[u][0].y + own.y;
                                     acc[2] = v[u][0].z + own.z;
@@ -1075,6 +1092,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         }
                     }
                 }
+                }  // !rs_chain
             }
             if (!released) {
                 tc_fence_before();
