@@ -38,6 +38,11 @@ WORKLOADS = {
     "llama70b-down-rs-tp4": (1, 4096, 8192, 28672, 4, "GEMM-ReduceScatter Llama-2-70B MLP down-proj at TP=4 (M=4096, K=28672, N=8192) bf16"),
     "llama70b-down-rs-tp2": (1, 4096, 8192, 28672, 2, "GEMM-ReduceScatter Llama-2-70B MLP down-proj at TP=2 (M=4096, K=28672, N=8192) bf16"),
     "rs-1024-tp2": (1, 1024, 1024, 1024, 2, "GEMM-ReduceScatter M=N=K=1024 at TP=2 (oracle plumbing config)"),
+    # BASELINE.json configs[4] (decode sweep) representatives; scripts/decode_sweep.py runs the full sweep
+    "decode-ag-up-m16": (0, 16, 28672, 8192, 8, "decode AllGather-GEMM Llama-2-70B MLP up-proj, M=16 tokens, TP=8"),
+    "decode-rs-down-m16": (1, 16, 8192, 28672, 8, "decode GEMM-ReduceScatter Llama-2-70B MLP down-proj, M=16, TP=8"),
+    "decode-rs-attn-m16": (1, 16, 8192, 8192, 8, "decode GEMM-ReduceScatter Llama-2-70B attention-out, M=16, TP=8"),
+    "decode-ag-up-m512": (0, 512, 28672, 8192, 8, "decode AllGather-GEMM Llama-2-70B MLP up-proj, M=512 tokens, TP=8"),
 }
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
 

@@ -288,7 +288,7 @@ def required_heap_bytes(problem: ProblemSpec) -> int:
     return int(N.lib().flux_required_heap_bytes(C.byref(problem.c())))
 
 
-TRACE_KINDS = {1: "compute_start", 2: "signal_set", 3: "tile_write", 4: "reduce", 5: "wait"}
+TRACE_KINDS = {1: "compute_start", 2: "signal_set", 3: "tile_write", 4: "reduce", 5: "wait", 6: "launch"}
 
 
 def read_trace(comm: Communicator, rank: int, problem: ProblemSpec, max_records: int = 1 << 18) -> list[dict]:

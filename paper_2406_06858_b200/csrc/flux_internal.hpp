@@ -36,7 +36,10 @@ constexpr size_t kCtrlFrReady = 76;     // u32: epoch whose FusedReduce accumula
 constexpr size_t kCtrlTraceCursor = 80; // u32: records written to this rank's trace ring
 constexpr size_t kTraceBytes = size_t(4) << 20;  // trace ring at the end of the data region (16 B records)
 // Trace record kinds (the reference CausalityLog event names, engine.hpp:37-63).
-enum TraceKind : uint32_t { kEvComputeStart = 1, kEvSignalSet = 2, kEvTileWrite = 3, kEvReduce = 4, kEvWait = 5 };
+// kEvLaunch (not in the reference schema): a CTA's first (tile_col 0) and last (tile_col 1)
+// instruction, for launch-latency profiling.
+enum TraceKind : uint32_t { kEvComputeStart = 1, kEvSignalSet = 2, kEvTileWrite = 3, kEvReduce = 4, kEvWait = 5,
+                            kEvLaunch = 6 };
 constexpr size_t kAgFlagOffset = 4096;  // u32[kAgFlagCap]: one flag per comm tile (SignalBoard)
 constexpr size_t kAgFlagCap = 16384;
 // In-kernel AllGather: u32[kAgGroupCap] monotonic piece counters per 128-row

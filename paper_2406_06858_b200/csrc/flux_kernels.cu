@@ -530,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     const int num_clusters = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
+        trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 0, 0);
         for (int l = 0; l < kMaxRanks; ++l) {
             if (p.c[l] == nullptr) break;
             tma_prefetch(&p.tma_a[l]);
@@ -1111,6 +1112,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
 
     if (CG == 2) cluster_sync();
     else __syncthreads();
+    if (warp == 0 && lane == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 1, 0);  // CTA done
     if (warp == 2) {
         tc_fence_after();
         if (CG == 2) tmem_dealloc_pair(tmem_base, kTmemCols);

@@ -54,3 +54,8 @@ print("t_us      " + " ".join(f"{x:>14s}" for x in kinds))
 for i in sorted(hist):
     print(f"{i * args.bucket_us:8.1f}  " + " ".join(f"{hist[i][x]:14d}" for x in kinds))
 print(f"span {(max(e['ts'] for e in ev) - t0) / 1000:.1f} us, {len(ev)} events")
+starts = [e["ts"] for e in ev if e["event"] == "launch" and e["tile_col"] == 0]
+ends = [e["ts"] for e in ev if e["event"] == "launch" and e["tile_col"] == 1]
+if starts and ends:
+    print(f"CTAs: first start -> last start {(max(starts) - min(starts)) / 1e3:.1f} us, first start -> last end "
+          f"{(max(ends) - min(starts)) / 1e3:.1f} us (kernel event time above includes launch + teardown)")
