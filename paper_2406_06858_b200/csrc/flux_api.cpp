@@ -339,6 +339,7 @@ struct Region {
 struct Layout {
     Region a_shard, b, a_agg, c, c32, staging;
     size_t trace_off = 0;
+    size_t tail_ws_off = 0;
     long long stage_plane = 0, stage_parity = 0;
     int ld_stage = 0;
     size_t total = 0;
@@ -375,6 +376,8 @@ Layout layout_for(const flux_problem* p) {
         L.staging.dtype = FLUX_F32;
         off = align_up(off + static_cast<size_t>(2) * L.stage_parity * 4, 4096);
     }
+    L.tail_ws_off = off;  // tail-split K-slice partials of one launch (Plain / AG)
+    off = align_up(off + static_cast<size_t>(kTailWsCtas) * kBM * kBN * 4, 4096);
     L.c = L.c32;
     L.c.dtype = FLUX_BF16;
     L.trace_off = off;  // device event trace ring (flux_opts.trace)
@@ -424,6 +427,7 @@ struct flux_comm {
     bool timing = false;                          // bracket fused launches with events
     uint64_t ag_sig = 0;                          // in-kernel AG: piece layout of the counters
     uint32_t ag_mult = 0;                         // in-kernel AG: operators since the counter reset
+    uint32_t launch_seq = 0;                      // fused launches so far (tags the tail-split counters)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel_events;  // per device group
     int kernel_events_used = 0;
     std::map<std::pair<int, std::vector<uint32_t>>, uint32_t*> order_cache;  // (device, schedule) -> table
@@ -716,6 +720,25 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             }
         }
         if (extra) FLUX_TRY(extra(g, prm));
+        // Tail split (Plain / AG): a persistent grid of W clusters runs T tiles in
+        // ceil(T / W) waves; the last T mod W tiles would leave most clusters
+        // idle for a whole tile, so each runs as S <= 8 K-slices instead.
+        prm.tail_splits = 0;
+        if ((mode == kModePlain || mode == kModeAG) && oc.o.activation != FLUX_ACT_SWIGLU) {
+            const char* env = std::getenv("FLUX_TAIL_SPLIT");
+            const int W = std::max(1, sm_count(dev) / cg), T = prm.num_tiles;
+            const int R = T % W, kb = (lk + kBK - 1) / kBK;
+            const int S = R > 0 ? std::min({kTailMaxSplits, W / R, kb}) : 1;
+            if (S >= 2 && R * cg <= kTailCtrCap && R * S * cg <= kTailWsCtas && !(env && std::atoi(env) == 0)) {
+                const RankState& lead_rank = c->ranks[g[0]];
+                prm.tail_base = T - R;
+                prm.tail_splits = S;
+                prm.num_tiles = prm.tail_base + R * S;
+                prm.tail_seq = ++c->launch_seq;
+                prm.tail_ws = reinterpret_cast<float*>(lead_rank.heap + L.tail_ws_off);
+                prm.tail_ctr = at<uint32_t>(lead_rank, kTailCtrOffset);
+            }
+        }
         const int grid = cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
         std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
         if (c->timing) {

@@ -44,6 +44,11 @@ constexpr size_t kAgFlagOffset = 4096;  // u32[kAgFlagCap]: one flag per comm ti
 constexpr size_t kAgFlagCap = 16384;
 // In-kernel AllGather: u32[kAgGroupCap] monotonic piece counters per 128-row
 // group of a_agg (+ one own-block counter), +1 per landed piece, zeroed on layout change.
+// Tail split (Plain / AG): epoch-tagged arrival counters of the split tail tiles.
+constexpr size_t kTailCtrOffset = 72 * 1024;
+constexpr int kTailCtrCap = 256;
+constexpr int kTailMaxSplits = 8;
+constexpr int kTailWsCtas = 160;  // workspace slots (>= CTAs of one launch): 128 x 256 fp32 each
 constexpr size_t kAgCtrOffset = 128 * 1024;
 constexpr size_t kAgGroupCap = 32768;
 constexpr int kPieceBytes = 16384;      // one TMA bulk copy (global -> smem -> global)
@@ -123,6 +128,12 @@ struct GemmParams {
     void* aux[kMaxRanks];          // per local slot: bf16 [m, n] pre-activation
     int ld_aux[kMaxRanks];
     int rs_chain;                  // RS, every rank in this launch: chained partial sums (see kernel)
+    // Tail split (Plain / AG): the last (num tiles mod clusters) tiles run as
+    // tail_splits K-slices each; the last arriving slice sums them in order.
+    int tail_base, tail_splits;    // order[tail_base..] are split; tail_splits <= 1: off
+    uint32_t tail_seq;             // per-launch tag of the tail counters
+    float* tail_ws;                // [tail tile][split][cta of pair][128 x 256] fp32
+    uint32_t* tail_ctr;            // [tail tile][cta of pair]: (tail_seq << 8) | arrivals
     int dbg;                       // profiling ablations (FLUX_DEBUG): 1 skip RS remote stores, 2 skip RS owner reduce
 };
 

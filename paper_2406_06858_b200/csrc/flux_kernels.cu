@@ -350,6 +350,40 @@ __device__ __forceinline__ void store_row(void* c, long long off, int col, int n
     }
 }
 
+// Work unit t of the schedule: a whole tile, or (tail split) K-slice `split`
+// of tail tile order[tail_base + (t - tail_base) / tail_splits].
+__device__ __forceinline__ void tile_unit(const GemmParams& p, int t, int k_blocks, uint32_t& entry, int& kb0, int& kb1,
+                                          int& split) {
+    if (p.tail_splits <= 1 || t < p.tail_base) {
+        entry = p.order[t];
+        kb0 = 0;
+        kb1 = k_blocks;
+        split = -1;
+        return;
+    }
+    const int u = t - p.tail_base, S = p.tail_splits;
+    entry = p.order[p.tail_base + u / S];
+    split = u % S;
+    kb0 = split * k_blocks / S;
+    kb1 = (split + 1) * k_blocks / S;
+}
+
+// Arrival on a tail counter tagged with this launch's sequence number; returns
+// the arrival count (the first arrival of a launch restarts it). acq_rel at gpu
+// scope: orders this CTA's workspace stores (after a CTA barrier) before it.
+__device__ __forceinline__ uint32_t tail_arrive(uint32_t* ctr, uint32_t seq) {
+    const uint32_t tag = seq & 0xFFFFFFu;
+    uint32_t old = *reinterpret_cast<volatile uint32_t*>(ctr);
+    for (;;) {
+        const uint32_t nv = (old >> 8) == tag ? old + 1u : ((tag << 8) | 1u);
+        uint32_t prev;
+        asm volatile("atom.acq_rel.gpu.global.cas.b32 %0, [%1], %2, %3;"
+                     : "=r"(prev) : "l"(ctr), "r"(old), "r"(nv) : "memory");
+        if (prev == old) return nv & 0xFFu;
+        old = prev;
+    }
+}
+
 // Epilogue activations (erf GELU, ReLU, SiLU) and their derivatives.
 __device__ __forceinline__ float act_fwd(int a, float x) {
     switch (a) {
@@ -568,8 +602,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             uint32_t phase = 0;
             uint64_t jit = p.jitter_seed ? p.jitter_seed * 0x9e3779b97f4a7c15ull + blockIdx.x : 0;
             for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-                int l, tm, tn;
-                decode(p.order[t], l, tm, tn);
+                int l, tm, tn, kb0, kb1, split;
+                uint32_t entry;
+                tile_unit(p, t, k_blocks, entry, kb0, kb1, split);
+                decode(entry, l, tm, tn);
                 const int row0 = tm * G::kTileM + static_cast<int>(cta_rank) * kBM;
                 const int bcol0 = tn * kBN + static_cast<int>(cta_rank) * G::kBRows;
                 if (jit) {  // reference Jitter (engine.cpp:116-128): perturb interleavings
@@ -594,10 +630,11 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     }
                     // Flag acquire (generic proxy) before TMA reads (async proxy).
                     asm volatile("fence.proxy.async.global;" ::: "memory");
-                    trace_event(p, l, kEvComputeStart, p.global_rank[l], row0 / kBM, tn,
-                                static_cast<uint32_t>(p.sm_transfer ? row0 / kBM : row0 / p.rpct));
+                    if (split <= 0)
+                        trace_event(p, l, kEvComputeStart, p.global_rank[l], row0 / kBM, tn,
+                                    static_cast<uint32_t>(p.sm_transfer ? row0 / kBM : row0 / p.rpct));
                 }
-                for (int kb = 0; kb < k_blocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     if (CG == 2) {
                         if (leader) mbar_expect_tx(&full[stage], 2 * G::kStageBytes);
@@ -623,10 +660,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             int as = 0;
             uint32_t aphase = 0;
             for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+                int kb0, kb1, split;
+                uint32_t entry;
+                tile_unit(p, t, k_blocks, entry, kb0, kb1, split);
                 mbar_wait(&tempty[as], aphase ^ 1u);
                 tc_fence_after();
                 const uint32_t d = tmem_base + static_cast<uint32_t>(as * kBN);
-                for (int kb = 0; kb < k_blocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t adesc = smem_desc_sw128(sA + stage * G::kABytes);
@@ -635,9 +675,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
                         // +32 B along K inside the 128B swizzle atom = +2 in the >>4 address field.
                         if (CG == 2)
-                            umma_bf16_pair(d, adesc + 2ull * kk, bdesc + 2ull * kk, G::kIdescV, (kb | kk) != 0 ? 1u : 0u);
+                            umma_bf16_pair(d, adesc + 2ull * kk, bdesc + 2ull * kk, G::kIdescV,
+                                           (kb > kb0 || kk != 0) ? 1u : 0u);
                         else
-                            umma_bf16(d, adesc + 2ull * kk, bdesc + 2ull * kk, G::kIdescV, (kb | kk) != 0 ? 1u : 0u);
+                            umma_bf16(d, adesc + 2ull * kk, bdesc + 2ull * kk, G::kIdescV, (kb > kb0 || kk != 0) ? 1u : 0u);
                     }
                     // Frees the smem slot (in both CTAs) when these MMAs retire.
                     if (CG == 2) umma_commit_pair(&empty[stage]);
@@ -747,8 +788,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         int as = 0;
         uint32_t aphase = 0;
         for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
-            int l, tmp, tn;
-            decode(p.order[t], l, tmp, tn);
+            int l, tmp, tn, kb0, kb1, split;
+            uint32_t entry;
+            tile_unit(p, t, k_blocks, entry, kb0, kb1, split);
+            decode(entry, l, tmp, tn);
             const int tm = tmp * CG + static_cast<int>(cta_rank);  // 128-row tile index
             const int row0 = tm * kBM;
             const int col0 = tn * kBN;
@@ -783,16 +826,89 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         }
                     }
                 } else {
-                    for (int c = 0; c < kBN / 32; ++c) {
+                    // Tail split: park this K-slice's accumulator, the last slice to
+                    // arrive sums all of them in slice order and runs the epilogue.
+                    bool do_store = true;
+                    const float* tail_src = nullptr;
+                    if (split >= 0) {
+                        const int ti = (t - p.tail_base) / p.tail_splits;
+                        const long long slot_stride = static_cast<long long>(kBM) * kBN;
+                        // Slot layout [column][row] (row fastest): a warp's 32 rows of one
+                        // column are 128 contiguous bytes, so these stores and the last
+                        // arriver's loads are coalesced without a shared-memory transpose.
+                        float* mine = p.tail_ws + (static_cast<long long>(ti * p.tail_splits + split) * CG + cta_rank) *
+                                                      slot_stride + q * 32 + lane;
+                        for (int c = 0; c < kBN / 32; ++c) {
+                            if (col0 + c * 32 >= p.n) break;  // warp-uniform
+                            uint32_t r[32];
+                            tmem_ld32(tbase + c * 32, r);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) mine[(c * 32 + j) * kBM] = __uint_as_float(r[j]);
+                        }
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (CG == 2) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(as * 8));
+                            else mbar_arrive(&tempty[as]);
+                        }
+                        released = true;
+                        // All slices of this tile run in the same (last) wave: wait for
+                        // every one of them, then each slice sums and stores its share
+                        // of the 32-column chunks (c % slices == slice), so the
+                        // reduction is spread over the slices' CTAs.
+                        named_bar_sync(1, 128);
+                        if (et == 0) {
+                            uint32_t* ctr = p.tail_ctr + ti * CG + cta_rank;
+                            const uint32_t done = ((p.tail_seq & 0xFFFFFFu) << 8) | static_cast<uint32_t>(p.tail_splits);
+                            if (tail_arrive(ctr, p.tail_seq) != static_cast<uint32_t>(p.tail_splits)) {
+                                const uint64_t t0 = globaltimer();
+                                for (;;) {
+                                    uint32_t v;
+                                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                                    if (v == done) break;
+                                    if (globaltimer() - t0 > p.timeout_ns) {
+                                        if (atomicCAS(p.ctrl[l] + 0, 0u, kErrAgFlagTimeout) == 0u) {
+                                            p.ctrl[l][1] = static_cast<uint32_t>(ti);
+                                            p.ctrl[l][2] = 0xFFFE0000u | static_cast<uint32_t>(split);
+                                            p.ctrl[l][3] = done;
+                                        }
+                                        break;
+                                    }
+                                    __nanosleep(64);
+                                }
+                            }
+                        }
+                        named_bar_sync(1, 128);
+                        tail_src = p.tail_ws + (static_cast<long long>(ti * p.tail_splits) * CG + cta_rank) * slot_stride +
+                                   q * 32 + lane;
+                    }
+                    for (int c = 0; do_store && c < kBN / 32; ++c) {
                         const int col = col0 + c * 32;
                         if (col >= p.n) break;  // warp-uniform
+                        if (tail_src && c % p.tail_splits != split) continue;
                         uint32_t r[32];
-                        tmem_ld32(tbase + c * 32, r);
-                        tmem_ld_wait();
+                        if (!tail_src) {
+                            tmem_ld32(tbase + c * 32, r);
+                            tmem_ld_wait();
+                        }
                         if (valid) {
                             float v[32];
+                            if (tail_src) {
+                                const long long slot_stride = static_cast<long long>(CG) * kBM * kBN;
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                                for (int j = 0; j < 32; ++j) v[j] = __ldcg(tail_src + (c * 32 + j) * kBM);
+                                for (int x = 1; x < p.tail_splits; ++x) {
+                                    float w[32];
+#pragma unroll
+                                    for (int j = 0; j < 32; ++j) w[j] = __ldcg(tail_src + x * slot_stride + (c * 32 + j) * kBM);
+#pragma unroll
+                                    for (int j = 0; j < 32; ++j) v[j] += w[j];
+                                }
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                            }
                             if (p.act_grad || p.act || p.aux_save) {
                                 const long long aoff = static_cast<long long>(row) * p.ld_aux[l] + col;
                                 if (p.aux_save) store_row<32>(p.aux[l], aoff, col, p.n, 0, v);

@@ -20,6 +20,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="llama70b-down-rs")
 ap.add_argument("--bucket-us", type=float, default=25.0)
 ap.add_argument("--ag-engine", type=int, default=0)
+ap.add_argument("--local", action="store_true", help="trace the plain local GEMM instead of the fused op")
 args = ap.parse_args()
 pattern, m, n, k, tp, _ = WORKLOADS[args.workload]
 prob = fx.ProblemSpec(m, n, k, tp, pattern)
@@ -35,7 +36,9 @@ tile = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
 for trace in (0, 0, 1):
     opts = fx.default_opts(trace=trace, ag_engine=args.ag_engine)
     comm.set_timing(True)
-    if pattern == 0:
+    if args.local:
+        comm.local_gemm(prob, opts, streams=s)
+    elif pattern == 0:
         comm.ag_gemm(prob, tile, prob.rows_per_rank(), fx.PULL, True, opts, streams=s)
     else:
         comm.gemm_rs(prob, tile, fx.WRITE_ALLTOALL, True, opts, streams=s)
@@ -59,3 +62,6 @@ ends = [e["ts"] for e in ev if e["event"] == "launch" and e["tile_col"] == 1]
 if starts and ends:
     print(f"CTAs: first start -> last start {(max(starts) - min(starts)) / 1e3:.1f} us, first start -> last end "
           f"{(max(ends) - min(starts)) / 1e3:.1f} us (kernel event time above includes launch + teardown)")
+    ends_us = sorted((e - min(starts)) / 1e3 for e in ends)
+    q = [ends_us[int(f * (len(ends_us) - 1))] for f in (0.0, 0.1, 0.5, 0.9, 1.0)]
+    print("CTA end times (us) min/p10/p50/p90/max: " + " / ".join(f"{v:.1f}" for v in q))
