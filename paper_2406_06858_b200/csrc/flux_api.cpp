@@ -1586,8 +1586,14 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     {
         const auto groups = device_groups(c);
         const char* env = std::getenv("FLUX_RS_CHAIN");
+        // Links wait for the previous rank's tile, so each rank's section must
+        // span a few waves (else the sections run concurrently and the chain
+        // serialises them; measured on decode shapes).
+        const long long tiles_per_rank = static_cast<long long>((p->m + kBM * cg - 1) / (kBM * cg)) * tiles_n;
+        const int clusters = std::max(1, sm_count(c->ranks[0].device) / cg);
         oc.rs_chain = aligned && !oc.fused_reduce && !oc.rs_last_arriver && groups.size() == 1 &&
-                              static_cast<int>(groups[0].size()) == tp && !(env && std::atoi(env) == 0)
+                              static_cast<int>(groups[0].size()) == tp && tiles_per_rank >= 2LL * clusters &&
+                              !(env && std::atoi(env) == 0)
                           ? 1
                           : 0;
     }

@@ -387,3 +387,32 @@ def test_acceptance_randomized_equivalence():
                 worst = max(worst, err)
                 assert err <= H.tol(True, p.k), (i, pat, m, n, k, tp, mode, kw, r, err)
     print("200 randomized cases, worst max_rel_error", worst)
+
+
+@pytest.mark.parametrize("tp", [4, 8])
+def test_rs_chain_bit_identical_to_owner_sum(tp, monkeypatch):
+    """Chained partial sums (all ranks in one launch, long rank sections) and the
+    owner-side sum use the same canonical order: bit-identical outputs; and both
+    match fp32 cuBLAS products of the same bf16 operands."""
+    p = fx.ProblemSpec(4096, 4096, 128 * tp, tp, RS)  # 256 CTA-pair tiles per rank: the chain is on
+    with H.make_comm(p) as comm:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(tp)
+        for r in range(tp):
+            for kind in (N.BUF_A_SHARD, N.BUF_B_SHARD):
+                t = comm.tensor(r, kind, p)
+                t.copy_((torch.rand(t.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
+        torch.cuda.synchronize()
+        chained = _run(comm, p, True)
+        monkeypatch.setenv("FLUX_RS_CHAIN", "0")
+        owner_sum = _run(comm, p, True)
+        for r in range(tp):
+            assert np.array_equal(chained[r], owner_sum[r]), r
+        a = [comm.tensor(r, N.BUF_A_SHARD, p).float() for r in range(tp)]
+        b = [comm.tensor(r, N.BUF_B_SHARD, p).float() for r in range(tp)]
+        rpr = p.rows_per_rank()
+        for r in range(tp):
+            rows = torch.arange(r * rpr, (r + 1) * rpr, 97, device="cuda")
+            ref = sum(a[s][rows] @ b[s].t() for s in range(tp)).cpu().numpy()
+            got = chained[r][(rows - r * rpr).cpu().numpy()]
+            assert np.abs(got - ref).max() / max(1.0, np.abs(ref).max()) < 1e-4, r
