@@ -39,7 +39,8 @@ def check(comm, p, tag):
 
 cases = [("AG copy engines", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(ag_engine=1)),
          ("AG in-kernel", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(ag_engine=2)),
-         ("RS chained (aligned blocks)", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
+         ("RS chained (aligned blocks, long sections)", fx.ProblemSpec(4096, 4096, 512, 4, fx.GEMM_REDUCESCATTER), {}),
+         ("AG tail split (K-slices)", fx.ProblemSpec(1024, 2048, 512, 8, fx.ALLGATHER_GEMM), dict(ag_engine=1)),
          ("RS owner sum (Naive swizzle)", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
          ("RS last arriver (decode)", fx.ProblemSpec(64, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
          ("RS FusedReduce", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), dict(deterministic_reduce=0))]
