@@ -416,3 +416,20 @@ def test_rs_chain_bit_identical_to_owner_sum(tp, monkeypatch):
             ref = sum(a[s][rows] @ b[s].t() for s in range(tp)).cpu().numpy()
             got = chained[r][(rows - r * rpr).cpu().numpy()]
             assert np.abs(got - ref).max() / max(1.0, np.abs(ref).max()) < 1e-4, r
+
+
+@pytest.mark.parametrize("tp", [3, 5, 6, 7])
+def test_odd_tp_degrees(tp):
+    """TP degrees that are not powers of two (reference ProblemSpec allows any
+    tp dividing m): AG (both engines), RS aligned and decode-sized blocks."""
+    for pat, m, n, k in [(AG, 128 * tp, 256 * tp, 192), (RS, 256 * tp, 512, 64 * tp), (RS, 8 * tp, 320, 32 * tp)]:
+        p = fx.ProblemSpec(m, n, k, tp, pat)
+        with H.make_comm(p) as comm:
+            a, b = H.upload(comm, p, seed=tp * 13 + m)
+            want = _oracle(p, a, b)
+            engines = (1, 2) if pat == AG else (0,)
+            for engine in engines:
+                for swizzle in (True, False):
+                    got = _run(comm, p, True, swizzle=swizzle, ag_engine=engine)
+                    for r in range(tp):
+                        assert O.max_rel_error(got[r], want[r]) <= H.tol(True, p.k), (pat, m, engine, swizzle, r)
