@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FLUX_ABI_VERSION 2
+#define FLUX_ABI_VERSION 3
 
 /* Return codes. The reference raises C++ exceptions (errors.hpp:9-31); each
  * maps to one code. The C++ shim (include/flux/overlap.hpp) rethrows them. */
@@ -94,6 +94,9 @@ typedef struct {
     int trace;                 /* 1: record the device event trace of the next operators (flux_trace_read) */
     int activation;            /* flux_activation fused into the AllGather-GEMM / local GEMM epilogue */
     int activation_grad;       /* flux_activation whose derivative scales C: C = acc * act'(aux) */
+    int rs_partials;           /* flux_dtype of the GEMM-RS cross-rank partials: F32 (default) or BF16
+                                  (half the NVLink bytes; one bf16 rounding per partial / chain link;
+                                  needs m/tp % 128 == 0 and WriteAlltoAll) */
 } flux_opts;
 
 /* Epilogue activations (chained MLP; paper Fig. 2). GELU is

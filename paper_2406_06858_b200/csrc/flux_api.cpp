@@ -698,6 +698,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.jitter_seed = oc.o.interleave_seed;
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
         prm.rs_chain = mode == kModeRS ? oc.rs_chain : 0;
+        prm.part_bf16 = mode == kModeRS && !oc.fused_reduce && oc.o.rs_partials == FLUX_BF16 ? 1 : 0;
         for (int q = 0; q < kMaxRanks; ++q) prm.slot_of[q] = -1;
         for (size_t li = 0; li < g.size(); ++li) prm.slot_of[g[li]] = static_cast<int>(li);
         prm.rs_last_arriver = mode == kModeRSLast ? 1 : 0;
@@ -800,6 +801,7 @@ void flux_default_opts(flux_opts* o) {
     o->trace = 0;
     o->activation = FLUX_ACT_NONE;
     o->activation_grad = FLUX_ACT_NONE;
+    o->rs_partials = FLUX_F32;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -1578,6 +1580,10 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
             if (operands_of(c, oc, r)->c.ptr)
                 return fail(FLUX_ERR_CONFIG,
                             "caller-provided C needs ownership blocks of whole 128-row tiles (m/tp % 128 == 0)");
+    if (oc.o.rs_partials != FLUX_F32 && oc.o.rs_partials != FLUX_BF16)
+        return fail(FLUX_ERR_CONFIG, "rs_partials must be F32 or BF16");
+    if (oc.o.rs_partials == FLUX_BF16 && (oc.rs_last_arriver || oc.fused_reduce))
+        return fail(FLUX_ERR_CONFIG, "bf16 partials need WriteAlltoAll and ownership blocks of whole 128-row tiles");
     if (oc.rs_last_arriver && static_cast<size_t>(tiles) > kRsCtrCap)
         return fail(FLUX_ERR_CONFIG, "too many output tiles for the arrival counters");
     // Chained partial sums (kernel, RS branch) when every rank runs in this one

@@ -210,6 +210,31 @@ __device__ __forceinline__ float4 ld_cg_f4(const float* p) {
                  : "l"(p));
     return v;
 }
+// Cross-rank partials (RS staging): 4 consecutive elements at element offset e
+// of a plane base, fp32 or (opts.rs_partials = BF16) bf16 — half the bytes over
+// NVLink / HBM, one rounding per stored partial.
+template <int PB>
+__device__ __forceinline__ float4 ld_part4(const float* base, long long e) {
+    if (!PB) return ld_cg_f4(base + e);
+    // Plain (non-volatile) load so the compiler can batch several before the
+    // unpacking that consumes them.
+    const uint2 w = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(base) + e));
+    return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u), __uint_as_float(w.y << 16),
+                       __uint_as_float(w.y & 0xFFFF0000u));
+}
+template <int PB>
+__device__ __forceinline__ void st_part4(float* base, long long e, const float4& v) {
+    if (!PB) {
+        *reinterpret_cast<float4*>(base + e) = v;
+        return;
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t*>(&lo);
+    w.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(base) + e) = w;
+}
+
 // ---- bulk copies (in-kernel AllGather transfer) -----------------------------------
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -538,7 +563,9 @@ struct Geo {
     static constexpr uint32_t kIdescV = make_idesc(kTileM, kBN);
 };
 
-template <int MODE, int CG>
+// PB: RS cross-rank partials stored as bf16 (1) or fp32 (0) — a template
+// parameter so the owner's batched loads stay branch-free.
+template <int MODE, int CG, int PB = 0>
 __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_constant__ GemmParams p) {
     using G = Geo<CG, MODE>;
     extern __shared__ uint8_t smem_raw[];
@@ -1003,7 +1030,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     const bool closes = own_tile;
                     const int pred = own_tile ? last : (me - 1 == o ? me - 2 : me - 1);
                     const long long lr0 = row0 - static_cast<long long>(o) * p.rpr;
-                    float* plane0 = p.staging[o] + parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
+                    float* const sbase = p.staging[o];  // plane 0 of the owner, element offsets below
+                    const long long e0 = parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
                     if (et == 0) {
                         if (pred >= 0)
                             wait_flag(p.rs_flags[o] + tile_id * tp + pred, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
@@ -1014,14 +1042,14 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     const int os = p.slot_of[o];
                     void* cdst = closes ? p.c[os] : nullptr;
                     const int ldc_o = closes ? p.ldc_l[os] : 0;
-                    float* wdst = plane0;
                     for (int c = 0; c < kBN / 32; ++c) {
                         const int colc = col0 + c * 32;
                         if (colc >= p.n) break;  // warp-uniform
                         float4 sum[8];
                         if (pred >= 0) {  // running sum, loaded before the TMEM round trip
 #pragma unroll
-                            for (int it = 0; it < 8; ++it) sum[it] = ld_cg_f4(plane0 + c * 4096 + it * 128 + lane * 4);
+                            for (int it = 0; it < 8; ++it)
+                                sum[it] = ld_part4<PB>(sbase, e0 + c * 4096 + it * 128 + lane * 4);
                         }
                         uint32_t r[32];
                         tmem_ld32(tbase + c * 32, r);
@@ -1043,7 +1071,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                 float acc[4] = {v.x, v.y, v.z, v.w};
                                 store_row<4>(cdst, (lr0 + q * 32 + i) * ldc_o + col, col, p.n, p.out_f32, acc);
                             } else {
-                                *reinterpret_cast<float4*>(wdst + c * 4096 + it * 128 + lane * 4) = v;
+                                st_part4<PB>(sbase, e0 + c * 4096 + it * 128 + lane * 4, v);
                             }
                         }
                     }
@@ -1074,9 +1102,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     // FusedReduce also runs with blocks narrower than a tile: its owner
                     // is per row.
                     const long long lr0 = row0 - static_cast<long long>(o0) * p.rpr;
-                    float* wdst = p.fused_reduce ? nullptr
-                                                 : p.staging[o0] + parity * p.stage_parity + me * p.stage_plane +
-                                                       stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
+                    float* const wbase = p.staging[o0];
+                    const long long we0 = parity * p.stage_parity + me * p.stage_plane +
+                                          stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
                     for (int c = 0; c < kBN / 32; ++c) {
                         const int colc = col0 + c * 32;
                         if (colc >= p.n) break;  // warp-uniform
@@ -1097,7 +1125,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                     red_add_f4(p.fr_acc[o] + (grow - static_cast<long long>(o) * p.rpr) * p.ld_stage + col,
                                                v.x, v.y, v.z, v.w);
                             } else {
-                                *reinterpret_cast<float4*>(wdst + c * 4096 + it * 128 + lane * 4) = v;
+                                st_part4<PB>(wbase, we0 + c * 4096 + it * 128 + lane * 4, v);
                             }
                         }
                     }
@@ -1147,10 +1175,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     // canonical order (deterministic; FusedReduce: the accumulator of
                     // the others + own).
                     const long long lr0 = row0 - static_cast<long long>(me) * p.rpr;  // tile's first owned row
-                    const float* src0 = p.fused_reduce
-                                            ? p.fr_acc[me]
-                                            : p.staging[me] + parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) +
-                                                  q * 1024;
+                    const float* src0 = p.fused_reduce ? p.fr_acc[me] : p.staging[me];
+                    const long long se0 = parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
                     for (int c = 0; c < kBN / 32; ++c) {
                         const int colc = col0 + c * 32;
                         if (colc >= p.n) break;  // warp-uniform
@@ -1172,10 +1198,11 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                     if (p.fused_reduce) {
                                         v[u][0] = ld_cg_f4(src0 + lr * p.ld_stage + col);
                                     } else {
-                                        const float* src = src0 + c * 4096 + (it0 + u) * 128 + lane * 4;
+                                        const long long e = se0 + c * 4096 + (it0 + u) * 128 + lane * 4;
 #pragma unroll
                                         for (int s2 = 0; s2 < kMaxRanks; ++s2)
-                                            if (s2 < p.tp && s2 != me) v[u][s2] = ld_cg_f4(src + s2 * p.stage_plane);
+                                            if (s2 < p.tp && s2 != me)
+                                                v[u][s2] = ld_part4<PB>(src0, e + s2 * p.stage_plane);
                                     }
                                 }
                             }
@@ -1259,10 +1286,10 @@ cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t str
 
 int gemm_tile_rows(int cg) { return kBM * cg; }
 
-template <int MODE, int CG>
+template <int MODE, int CG, int PB = 0>
 static cudaError_t launch_one(const GemmParams& p, int grid, cudaStream_t stream) {
     static bool configured = false;
-    auto fn = flux_gemm_kernel<MODE, CG>;
+    auto fn = flux_gemm_kernel<MODE, CG, PB>;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<CG, MODE>::kSmem);
         if (e != cudaSuccess) return e;
@@ -1290,14 +1317,16 @@ cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStr
         switch (mode) {
             case kModePlain: return launch_one<kModePlain, 2>(p, grid, stream);
             case kModeAG: return launch_one<kModeAG, 2>(p, grid, stream);
-            case kModeRS: return launch_one<kModeRS, 2>(p, grid, stream);
+            case kModeRS:
+                return p.part_bf16 ? launch_one<kModeRS, 2, 1>(p, grid, stream) : launch_one<kModeRS, 2>(p, grid, stream);
             case kModeRSLast: return launch_one<kModeRSLast, 2>(p, grid, stream);
         }
     } else {
         switch (mode) {
             case kModePlain: return launch_one<kModePlain, 1>(p, grid, stream);
             case kModeAG: return launch_one<kModeAG, 1>(p, grid, stream);
-            case kModeRS: return launch_one<kModeRS, 1>(p, grid, stream);
+            case kModeRS:
+                return p.part_bf16 ? launch_one<kModeRS, 1, 1>(p, grid, stream) : launch_one<kModeRS, 1>(p, grid, stream);
             case kModeRSLast: return launch_one<kModeRSLast, 1>(p, grid, stream);
         }
     }
