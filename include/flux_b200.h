@@ -101,7 +101,9 @@ typedef struct {
 
 /* Epilogue activations (chained MLP; paper Fig. 2). GELU is
  * the erf form. SWIGLU: the local N columns come in 256-column groups of 128
- * gate then 128 up columns; C receives silu(gate) * up (N/2 columns). */
+ * gate then 128 up columns; C receives silu(gate) * up (N/2 columns) and aux,
+ * if given, the N pre-activation columns. activation_grad = SWIGLU: C (2N
+ * columns, same grouping) receives dgate, dup from the GEMM's dz and aux. */
 typedef enum {
     FLUX_ACT_NONE = 0,
     FLUX_ACT_GELU = 1,
@@ -243,10 +245,12 @@ int flux_gemm_rs_ex(flux_comm* comm, const flux_problem* problem, const flux_til
  * Backward of the input (the AG <-> RS interchange): dact =
  * (AllGather(dout) W_down) * act'(pre) (AG-GEMM, derivative in the epilogue),
  * then dx = ReduceScatter(dact W_up) (GEMM-RS), with the transposed weights
- * w_down_t [ffn/tp, hidden] and w_up_t [hidden, ffn/tp]. */
+ * w_down_t [ffn/tp, hidden] and w_up_t [hidden, ffn/tp]. SWIGLU: pre and dact
+ * are [m, 2 ffn/tp] in the gate/up grouping (dgate, dup) and w_up_t is
+ * [hidden, 2 ffn/tp]. */
 typedef struct {
     int m, hidden, ffn, tp;
-    int activation; /* flux_activation (backward: GELU / RELU / SILU) */
+    int activation; /* flux_activation */
 } flux_mlp;
 typedef struct {
     flux_matrix x, w_up, w_down, pre, act, out;

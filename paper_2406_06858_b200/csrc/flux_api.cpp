@@ -1139,7 +1139,7 @@ int flux_ag_engine(const flux_problem* p, int transfer, const flux_opts* opts) {
 static int check_activation(flux_comm* c, const flux_problem* p, const flux_opts* opts, const flux_operands* ops) {
     if (!opts) return FLUX_OK;
     const int a = opts->activation, g = opts->activation_grad;
-    if (a < FLUX_ACT_NONE || a > FLUX_ACT_SWIGLU || g < FLUX_ACT_NONE || g > FLUX_ACT_SILU)
+    if (a < FLUX_ACT_NONE || a > FLUX_ACT_SWIGLU || g < FLUX_ACT_NONE || g > FLUX_ACT_SWIGLU)
         return fail(FLUX_ERR_CONFIG, "unknown activation");
     if (a == FLUX_ACT_NONE && g == FLUX_ACT_NONE) return FLUX_OK;
     if (a != FLUX_ACT_NONE && g != FLUX_ACT_NONE) return fail(FLUX_ERR_CONFIG, "activation and activation_grad are exclusive");
@@ -1150,11 +1150,12 @@ static int check_activation(flux_comm* c, const flux_problem* p, const flux_opts
     for (size_t i = 0; i < mine.size(); ++i) {
         const flux_operands* o = ops ? (c->ipc ? ops : ops + mine[i]) : nullptr;
         const bool aux = o && o->aux.ptr;
-        if (a == FLUX_ACT_SWIGLU && aux) return fail(FLUX_ERR_CONFIG, "SWIGLU does not save a pre-activation");
         if (g != FLUX_ACT_NONE && !aux) return fail(FLUX_ERR_CONFIG, "activation_grad needs the saved pre-activation (operands.aux)");
     }
     if (a == FLUX_ACT_SWIGLU && local_cols(p) % kBN != 0)
         return fail(FLUX_ERR_SHAPE, "SWIGLU needs n/tp % 256 == 0 (128 gate + 128 up columns per group)");
+    if (g == FLUX_ACT_SWIGLU && local_cols(p) % (kBN / 2) != 0)
+        return fail(FLUX_ERR_SHAPE, "SWIGLU backward needs n/tp % 128 == 0 (C and aux hold 2n/tp grouped columns)");
     return FLUX_OK;
 }
 
@@ -1756,11 +1757,13 @@ static int mlp_problems(const flux_mlp* mlp, bool backward, flux_problem* ag, fl
     if (!mlp) return fail(FLUX_ERR_CONFIG, "null mlp");
     if (mlp->activation < FLUX_ACT_NONE || mlp->activation > FLUX_ACT_SWIGLU)
         return fail(FLUX_ERR_CONFIG, "unknown activation");
-    if (backward && mlp->activation == FLUX_ACT_SWIGLU)
-        return fail(FLUX_ERR_CONFIG, "flux_mlp_backward_dx supports GELU / RELU / SILU");
-    const int up_cols = mlp->activation == FLUX_ACT_SWIGLU && !backward ? 2 * mlp->ffn : mlp->ffn;
+    // SWIGLU: the up-projection has 2 ffn columns (gate/up groups); its input
+    // gradient is a GEMM-RS over those 2 ffn columns.
+    const bool glu = mlp->activation == FLUX_ACT_SWIGLU;
+    const int up_cols = glu && !backward ? 2 * mlp->ffn : mlp->ffn;
+    const int rs_k = glu && backward ? 2 * mlp->ffn : mlp->ffn;
     *ag = flux_problem{mlp->m, up_cols, mlp->hidden, mlp->tp, FLUX_ALLGATHER_GEMM};
-    *rs = flux_problem{mlp->m, mlp->hidden, mlp->ffn, mlp->tp, FLUX_GEMM_REDUCESCATTER};
+    *rs = flux_problem{mlp->m, mlp->hidden, rs_k, mlp->tp, FLUX_GEMM_REDUCESCATTER};
     FLUX_TRY(validate_problem(ag));
     return validate_problem(rs);
 }
@@ -1769,7 +1772,7 @@ size_t flux_mlp_required_heap_bytes(const flux_mlp* mlp) {
     flux_problem ag, rs, bag, brs;
     if (mlp_problems(mlp, false, &ag, &rs) != FLUX_OK) return 0;
     size_t need = std::max(layout_for(&ag).total, layout_for(&rs).total);
-    if (mlp->activation != FLUX_ACT_SWIGLU && mlp_problems(mlp, true, &bag, &brs) == FLUX_OK)
+    if (mlp_problems(mlp, true, &bag, &brs) == FLUX_OK)
         need = std::max(need, std::max(layout_for(&bag).total, layout_for(&brs).total));
     return need;
 }

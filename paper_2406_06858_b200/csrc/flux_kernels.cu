@@ -842,6 +842,17 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         tmem_ld32(tbase + c * 32, rg);
                         tmem_ld32(tbase + (c + kBN / 64) * 32, ru);
                         tmem_ld_wait();
+                        if (valid && p.aux_save) {  // pre-activation (gate and up) for the backward pass
+                            float g[32], u[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                g[j] = __uint_as_float(rg[j]);
+                                u[j] = __uint_as_float(ru[j]);
+                            }
+                            const long long aoff = static_cast<long long>(row) * p.ld_aux[l];
+                            store_row<32>(p.aux[l], aoff + col, col, p.n, 0, g);
+                            store_row<32>(p.aux[l], aoff + col + kBN / 2, col + kBN / 2, p.n, 0, u);
+                        }
                         if (valid) {
                             float v[32];
 #pragma unroll
@@ -935,6 +946,27 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                             } else {
 #pragma unroll
                                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                            }
+                            if (p.act_grad == kActSwiGLU) {
+                                // Backward of the gated MLP: v = dz for output columns
+                                // [col, col+32) of group col/128; the saved pre-activation
+                                // holds that group's gate and up columns (256-wide groups),
+                                // and C (2n columns, same grouping) receives dgate, dup.
+                                const int gcol = (col / (kBN / 2)) * kBN + col % (kBN / 2), ucol = gcol + kBN / 2;
+                                const long long abase = static_cast<long long>(row) * p.ld_aux[l];
+                                float xg[32], xu[32], dg[32];
+                                load_row_bf16<32>(p.aux[l], abase + gcol, gcol, 2 * p.n, xg);
+                                load_row_bf16<32>(p.aux[l], abase + ucol, ucol, 2 * p.n, xu);
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) {
+                                    const float sg = 1.0f / (1.0f + __expf(-xg[j]));
+                                    dg[j] = v[j] * xu[j] * sg * (1.0f + xg[j] * (1.0f - sg));
+                                    v[j] = v[j] * xg[j] * sg;  // dup = dz * silu(gate)
+                                }
+                                const long long cbase = static_cast<long long>(row) * p.ldc_l[l];
+                                store_row<32>(p.c[l], cbase + gcol, gcol, 2 * p.n, p.out_f32, dg);
+                                store_row<32>(p.c[l], cbase + ucol, ucol, 2 * p.n, p.out_f32, v);
+                                continue;
                             }
                             if (p.act_grad || p.act || p.aux_save) {
                                 const long long aoff = static_cast<long long>(row) * p.ld_aux[l] + col;

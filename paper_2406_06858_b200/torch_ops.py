@@ -100,16 +100,15 @@ def _ag_problem(comm, a_shard, n_local):
 def ag_gemm_act(a_shard: torch.Tensor, weight: torch.Tensor, comm_id: int,
                 activation: int) -> tuple[torch.Tensor, torch.Tensor]:
     """activation(AllGather(a_shard) @ weight^T) with the activation in the
-    GEMM epilogue; also returns the pre-activation (empty for SWIGLU, whose
-    output has half the columns: 128 gate + 128 up rows per 256-row group)."""
+    GEMM epilogue; also returns the pre-activation [m, n/tp] (SWIGLU: the output
+    has half the columns — 128 gate + 128 up rows per 256-row weight group)."""
     comm = _REGISTRY[comm_id]
     p = _ag_problem(comm, a_shard, weight.shape[0])
     swiglu = activation == N.ACT_SWIGLU
     out = torch.empty(p.m, weight.shape[0] // (2 if swiglu else 1), dtype=torch.bfloat16, device=a_shard.device)
-    pre = (torch.empty(0, 0, dtype=torch.bfloat16, device=a_shard.device) if swiglu
-           else torch.empty(p.m, weight.shape[0], dtype=torch.bfloat16, device=a_shard.device))
+    pre = torch.empty(p.m, weight.shape[0], dtype=torch.bfloat16, device=a_shard.device)
     opts = N.default_opts(activation=activation)
-    comm.ag_gemm_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a_shard, weight, out, None if swiglu else pre)],
+    comm.ag_gemm_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a_shard, weight, out, pre)],
                     opts=opts, streams=_stream())
     return out, pre
 
@@ -118,18 +117,19 @@ def ag_gemm_act(a_shard: torch.Tensor, weight: torch.Tensor, comm_id: int,
 def _(a_shard, weight, comm_id, activation):
     m = a_shard.shape[0] * _REGISTRY[comm_id].tp
     swiglu = activation == N.ACT_SWIGLU
-    return (a_shard.new_empty(m, weight.shape[0] // (2 if swiglu else 1)),
-            a_shard.new_empty(0, 0) if swiglu else a_shard.new_empty(m, weight.shape[0]))
+    return a_shard.new_empty(m, weight.shape[0] // (2 if swiglu else 1)), a_shard.new_empty(m, weight.shape[0])
 
 
 @torch.library.custom_op("flux_b200::ag_gemm_dact", mutates_args=())
 def ag_gemm_dact(a_shard: torch.Tensor, weight: torch.Tensor, pre: torch.Tensor, comm_id: int,
                  activation: int) -> torch.Tensor:
     """(AllGather(a_shard) @ weight^T) * activation'(pre): the backward of the
-    GEMM-RS + activation, with the derivative in the AG-GEMM epilogue."""
+    GEMM-RS + activation, with the derivative in the AG-GEMM epilogue (SWIGLU:
+    dgate / dup in the gate/up grouping, twice the columns)."""
     comm = _REGISTRY[comm_id]
     p = _ag_problem(comm, a_shard, weight.shape[0])
-    out = torch.empty(p.m, weight.shape[0], dtype=torch.bfloat16, device=a_shard.device)
+    width = weight.shape[0] * (2 if activation == N.ACT_SWIGLU else 1)
+    out = torch.empty(p.m, width, dtype=torch.bfloat16, device=a_shard.device)
     comm.ag_gemm_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a_shard, weight, out, pre)],
                     opts=N.default_opts(activation_grad=activation), streams=_stream())
     return out
@@ -137,7 +137,8 @@ def ag_gemm_dact(a_shard: torch.Tensor, weight: torch.Tensor, pre: torch.Tensor,
 
 @ag_gemm_dact.register_fake
 def _(a_shard, weight, pre, comm_id, activation):
-    return a_shard.new_empty(a_shard.shape[0] * _REGISTRY[comm_id].tp, weight.shape[0])
+    width = weight.shape[0] * (2 if activation == N.ACT_SWIGLU else 1)
+    return a_shard.new_empty(a_shard.shape[0] * _REGISTRY[comm_id].tp, width)
 
 
 def gathered_input(comm_id: int, a_shard: torch.Tensor, n_local: int) -> torch.Tensor:
@@ -164,8 +165,6 @@ class _TPMlpFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dout):
         w_up, w_down, z, pre, x_g = ctx.saved_tensors
-        if ctx.activation == N.ACT_SWIGLU:
-            raise NotImplementedError("SWIGLU backward")
         dout = dout.contiguous().to(torch.bfloat16)
         dy = torch.ops.flux_b200.ag_gemm_dact(dout, w_down.t().contiguous(), pre, ctx.comm_id, ctx.activation)
         dout_g = gathered_input(ctx.comm_id, dout, w_down.shape[1]) if w_down.requires_grad else None

@@ -73,7 +73,7 @@ for pat, m, n, k in [(fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384), (fx.GEM
 # The chained MLP as an autograd module (torch_ops.TPMlp) against fp32 autograd
 # of the same sequence-parallel MLP on the same bf16 values (normwise error).
 M, HID, FFN = 256 * world, 256, 512 * world
-mlp_heap = fx.MlpSpec(M, HID, FFN, world, fx.ACT_GELU).required_heap_bytes()
+mlp_heap = max(fx.MlpSpec(M, HID, FFN, world, a).required_heap_bytes() for a in (fx.ACT_GELU, fx.ACT_SWIGLU))
 assert mlp_heap <= heap, (mlp_heap, heap)
 
 
@@ -112,6 +112,33 @@ results["mlp-out"] = (_nerr(y, yr[rank * rpr:(rank + 1) * rpr].detach()), 3e-2)
 results["mlp-dx"] = (_nerr(x.grad, xr.grad[rank * rpr:(rank + 1) * rpr]), 3e-2)
 results["mlp-dw_up"] = (_nerr(mod.w_up.grad, wur[rank].grad), 3e-2)
 results["mlp-dw_down"] = (_nerr(mod.w_down.grad, wdr[rank].grad), 3e-2)
+# The gated variant (SwiGLU, Llama MLP): w_up holds 128 gate + 128 up rows per group.
+wus2 = [_rand((2 * FFN // world, HID), 500 + r, 0.1) for r in range(world)]
+mod2 = torch_ops.TPMlp(HID, FFN, cid, fx.ACT_SWIGLU, device="cuda")
+with torch.no_grad():
+    mod2.w_up.copy_(wus2[rank])
+    mod2.w_down.copy_(wds[rank])
+x2 = xs[rank].clone().requires_grad_(True)
+dist.barrier()
+y2 = mod2(x2)
+y2.backward(douts[rank])
+torch.cuda.synchronize()
+
+
+def _glu(y):
+    y4 = y.view(y.shape[0], -1, 2, 128)
+    return (torch.nn.functional.silu(y4[:, :, 0]) * y4[:, :, 1]).reshape(y.shape[0], -1)
+
+
+xr2 = torch.cat(xs).float().requires_grad_(True)
+wur2 = [w.float().requires_grad_(True) for w in wus2]
+wdr2 = [w.float().requires_grad_(True) for w in wds]
+yr2 = sum(_glu(xr2 @ wur2[r].t()) @ wdr2[r].t() for r in range(world))
+yr2.backward(torch.cat(douts).float())
+results["swiglu-out"] = (_nerr(y2, yr2[rank * rpr:(rank + 1) * rpr].detach()), 3e-2)
+results["swiglu-dx"] = (_nerr(x2.grad, xr2.grad[rank * rpr:(rank + 1) * rpr]), 3e-2)
+results["swiglu-dw_up"] = (_nerr(mod2.w_up.grad, wur2[rank].grad), 3e-2)
+results["swiglu-dw_down"] = (_nerr(mod2.w_down.grad, wdr2[rank].grad), 3e-2)
 dist.barrier()
 comm.close()
 print("RESULT", rank, json.dumps(results), flush=True)

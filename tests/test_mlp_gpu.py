@@ -121,20 +121,28 @@ def test_mlp_forward_chain(act):
         assert _err(out[r], total[r * rpr:(r + 1) * rpr]) <= TOL, ("out", r)
 
 
-@pytest.mark.parametrize("act", [fx.ACT_GELU, fx.ACT_RELU, fx.ACT_SILU])
+def _swiglu_ref(y):
+    y4 = y.view(y.shape[0], -1, 2, 128)
+    return (torch.nn.functional.silu(y4[:, :, 0]) * y4[:, :, 1]).reshape(y.shape[0], -1)
+
+
+@pytest.mark.parametrize("act", [fx.ACT_GELU, fx.ACT_RELU, fx.ACT_SILU, fx.ACT_SWIGLU])
 def test_mlp_backward_dx_matches_autograd(act):
     """dx of the TP MLP: AG-GEMM(dout, W_down) * act'(pre) -> GEMM-RS with W_up
-    (the AG <-> RS interchange of the backward pass)."""
+    (the AG <-> RS interchange of the backward pass); SWIGLU:
+    dgate / dup from the saved gate / up pre-activations."""
     spec = fx.MlpSpec(m=512, hidden=256, ffn=1024, tp=2, activation=act)
     tp, f, rpr = spec.tp, spec.ffn // spec.tp, spec.m // spec.tp
-    x, w_up, w_down = _mlp_inputs(spec, 7 + act)
+    glu = act == fx.ACT_SWIGLU
+    x, w_up, w_down = _mlp_inputs(spec, 7 + act, swiglu=glu)
     g = torch.Generator(device="cuda")
     g.manual_seed(99)
     dout = [_bf((rpr, spec.hidden), g) for _ in range(tp)]
-    pre = [torch.empty(spec.m, f, dtype=torch.bfloat16, device="cuda") for _ in range(tp)]
+    wide = 2 * f if glu else f
+    pre = [torch.empty(spec.m, wide, dtype=torch.bfloat16, device="cuda") for _ in range(tp)]
     inter = [torch.empty(spec.m, f, dtype=torch.bfloat16, device="cuda") for _ in range(tp)]
     out = [torch.empty(rpr, spec.hidden, dtype=torch.bfloat16, device="cuda") for _ in range(tp)]
-    dact = [torch.empty(spec.m, f, dtype=torch.bfloat16, device="cuda") for _ in range(tp)]
+    dact = [torch.empty(spec.m, wide, dtype=torch.bfloat16, device="cuda") for _ in range(tp)]
     dx = [torch.empty(rpr, spec.hidden, dtype=torch.bfloat16, device="cuda") for _ in range(tp)]
     with fx.Communicator(tp, [0] * tp, heap_bytes=spec.required_heap_bytes()) as comm:
         opts = fx.default_opts(wall_budget_s=5.0)
@@ -146,7 +154,8 @@ def test_mlp_backward_dx_matches_autograd(act):
         comm.sync()
     # fp32 autograd reference of the same TP MLP on the same bf16 inputs
     xa = torch.cat(x).float().requires_grad_(True)
-    y = sum(ACTS[act](xa @ w_up[r].float().t()) @ w_down[r].float().t() for r in range(tp))
+    fn = _swiglu_ref if glu else ACTS[act]
+    y = sum(fn(xa @ w_up[r].float().t()) @ w_down[r].float().t() for r in range(tp))
     y.backward(torch.cat(dout).float())
     for r in range(tp):
         assert _err(dx[r], xa.grad[r * rpr:(r + 1) * rpr]) <= 2 * TOL, r
