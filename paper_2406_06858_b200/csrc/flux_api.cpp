@@ -1576,11 +1576,22 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     const int tiles_n = (p->n + kBN - 1) / kBN;
     oc.rs_last_arriver = (rpr % kBM != 0 && !oc.fused_reduce) ? 1 : 0;
     oc.ops = operands;
-    if (operands && oc.rs_last_arriver)
-        for (int r : mine)
-            if (operands_of(c, oc, r)->c.ptr)
-                return fail(FLUX_ERR_CONFIG,
-                            "caller-provided C needs ownership blocks of whole 128-row tiles (m/tp % 128 == 0)");
+    // Decode-sized blocks: the last arrivers write every owner's rows into the
+    // library C (peer-addressable); a caller C then receives a copy of its rows.
+    std::vector<flux_operands> ops_lib;
+    std::vector<std::pair<int, flux_matrix>> caller_c;
+    if (operands && oc.rs_last_arriver) {
+        const int n_ops = c->ipc ? 1 : tp;
+        ops_lib.assign(operands, operands + n_ops);
+        for (int r : mine) {
+            flux_operands& o = c->ipc ? ops_lib[0] : ops_lib[r];
+            if (o.c.ptr) {
+                caller_c.emplace_back(r, o.c);
+                o.c = flux_matrix{nullptr, 0};
+            }
+        }
+        oc.ops = ops_lib.data();
+    }
     if (oc.o.rs_partials != FLUX_F32 && oc.o.rs_partials != FLUX_BF16)
         return fail(FLUX_ERR_CONFIG, "rs_partials must be F32 or BF16");
     if (oc.o.rs_partials == FLUX_BF16 && (oc.rs_last_arriver || oc.fused_reduce))
@@ -1624,6 +1635,15 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
             }
             if (remote_peer) FLUX_TRY(wait_value_geq(s, c->ranks[r].heap + kRsDoneOffset, c->ranks[r].rs_done_cum));
             (void)other_device;
+        }
+        const Layout L = layout_for(p);
+        const size_t esz = oc.o.out_dtype == FLUX_F32 ? 4 : 2;
+        for (const auto& rc : caller_c) {
+            const RankState& rs = c->ranks[rc.first];
+            FLUX_CUDA(cudaSetDevice(rs.device));
+            FLUX_CUDA(cudaMemcpy2DAsync(rc.second.ptr, static_cast<size_t>(rc.second.ld) * esz, rs.heap + L.c32.off,
+                                        static_cast<size_t>(L.c32.ld) * esz, static_cast<size_t>(p->n) * esz, rpr,
+                                        cudaMemcpyDeviceToDevice, stream_for(c, rc.first, streams)));
         }
     }
     return mark_op_done(c, streams, c->epoch);

@@ -75,11 +75,8 @@ def gemm_rs(a: torch.Tensor, weight: torch.Tensor, comm_id: int) -> torch.Tensor
     comm = _REGISTRY[comm_id]
     tp = comm.tp
     p = ProblemSpec(a.shape[0], weight.shape[0], a.shape[1] * tp, tp, N.GEMM_REDUCESCATTER)
-    aligned = p.rows_per_rank() % 128 == 0
-    out = torch.empty(p.rows_per_rank(), p.n, dtype=torch.bfloat16, device=a.device) if aligned else None
+    out = torch.empty(p.rows_per_rank(), p.n, dtype=torch.bfloat16, device=a.device)
     comm.gemm_rs_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a, weight, out)], streams=_stream())
-    if out is None:  # decode-sized blocks: the result lives in the symmetric heap
-        out = comm.tensor(comm.rank, N.BUF_C_OUT, p).clone()
     return out
 
 

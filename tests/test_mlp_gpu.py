@@ -94,9 +94,12 @@ def _mlp_inputs(spec, seed, swiglu=False):
     return x, w_up, w_down
 
 
-@pytest.mark.parametrize("act", [fx.ACT_GELU, fx.ACT_SILU, fx.ACT_SWIGLU])
-def test_mlp_forward_chain(act):
-    spec = fx.MlpSpec(m=1024, hidden=512, ffn=2048, tp=4, activation=act)
+@pytest.mark.parametrize("act,m", [(fx.ACT_GELU, 1024), (fx.ACT_SILU, 1024), (fx.ACT_SWIGLU, 1024),
+                                   (fx.ACT_SWIGLU, 64), (fx.ACT_GELU, 40)])
+def test_mlp_forward_chain(act, m):
+    """m = 64 / 40: decode-sized ownership blocks (last-arriver GEMM-RS into the
+    caller's output)."""
+    spec = fx.MlpSpec(m=m, hidden=512, ffn=2048, tp=4, activation=act)
     tp, f = spec.tp, spec.ffn // spec.tp
     x, w_up, w_down = _mlp_inputs(spec, 21 + act, swiglu=act == fx.ACT_SWIGLU)
     inter = [torch.empty(spec.m, f, dtype=torch.bfloat16, device="cuda") for _ in range(tp)]
