@@ -22,6 +22,7 @@ ap.add_argument("--workload", default="llama70b-up-ag")
 ap.add_argument("--rounds", type=int, default=20)
 ap.add_argument("--cfg", action="append", default=[])
 ap.add_argument("--local", action="store_true", help="also time the plain local GEMM each round")
+ap.add_argument("--op", default="fused", choices=["fused", "local"], help="what each --cfg runs")
 args = ap.parse_args()
 pattern, m, n, k, tp, _ = WORKLOADS[args.workload]
 p = fx.ProblemSpec(m, n, k, tp, pattern)
@@ -51,7 +52,9 @@ def make(cfg):
         saved = {key: os.environ.get(key) for key in env}
         os.environ.update(env)
         o = fx.default_opts(**opt)
-        if pattern == fx.ALLGATHER_GEMM:
+        if args.op == "local":
+            comm.local_gemm(p, o, st)
+        elif pattern == fx.ALLGATHER_GEMM:
             comm.ag_gemm(p, tile, p.rows_per_rank(), fx.PULL, True, o, st)
         else:
             comm.gemm_rs(p, tile, fx.WRITE_ALLTOALL, True, o, st)
