@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FLUX_ABI_VERSION 3
+#define FLUX_ABI_VERSION 4
 
 /* Return codes. The reference raises C++ exceptions (errors.hpp:9-31); each
  * maps to one code. The C++ shim (include/flux/overlap.hpp) rethrows them. */
@@ -97,7 +97,12 @@ typedef struct {
     int rs_partials;           /* flux_dtype of the GEMM-RS cross-rank partials: F32 (default) or BF16
                                   (half the NVLink bytes; one bf16 rounding per partial / chain link;
                                   needs m/tp % 128 == 0 and WriteAlltoAll) */
+    int b_layout;              /* flux_b_layout of caller-provided B (operands.b): NK = [n/tp or n, k]
+                                  (nn.Linear.weight, default) or KN = [k, n] row-major (the reference's
+                                  b_shard; no transposed copy needed, e.g. for the backward pass) */
 } flux_opts;
+
+typedef enum { FLUX_B_NK = 0, FLUX_B_KN = 1 } flux_b_layout;
 
 /* Epilogue activations (chained MLP; paper Fig. 2). GELU is
  * the erf form. SWIGLU: the local N columns come in 256-column groups of 128
@@ -247,7 +252,8 @@ int flux_gemm_rs_ex(flux_comm* comm, const flux_problem* problem, const flux_til
  * then dx = ReduceScatter(dact W_up) (GEMM-RS), with the transposed weights
  * w_down_t [ffn/tp, hidden] and w_up_t [hidden, ffn/tp]. SWIGLU: pre and dact
  * are [m, 2 ffn/tp] in the gate/up grouping (dgate, dup) and w_up_t is
- * [hidden, 2 ffn/tp]. */
+ * [hidden, 2 ffn/tp]. With opts.b_layout = KN the *_t fields take the forward
+ * weights untransposed (w_down [hidden, ffn/tp], w_up [ffn/tp, hidden]). */
 typedef struct {
     int m, hidden, ffn, tp;
     int activation; /* flux_activation */

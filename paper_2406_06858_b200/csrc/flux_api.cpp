@@ -617,7 +617,9 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 FLUX_TRY(make_tmap(&prm.tma_a[li], ops->a.ptr, A.rows, lk, ops->a.ld, kBM));
             else
                 FLUX_TRY(make_tmap(&prm.tma_a[li], rs.heap + A.off, A.rows, lk, A.ld, kBM));
-            if (ops && ops->b.ptr) FLUX_TRY(make_tmap(&prm.tma_b[li], ops->b.ptr, lc, lk, ops->b.ld, kBN / cg));
+            if (ops && ops->b.ptr && oc.o.b_layout == FLUX_B_KN)  // [k, n]: 64 (N) x 64 (K) boxes, MN-major
+                FLUX_TRY(make_tmap(&prm.tma_b[li], ops->b.ptr, lk, lc, ops->b.ld, kBK));
+            else if (ops && ops->b.ptr) FLUX_TRY(make_tmap(&prm.tma_b[li], ops->b.ptr, lc, lk, ops->b.ld, kBN / cg));
             else FLUX_TRY(make_tmap(&prm.tma_b[li], rs.heap + L.b.off, lc, lk, L.b.ld, kBN / cg));
             if (plain_f32_to_staging) {
                 prm.c[li] = rs.heap + partial_off;  // full [m, n] partial
@@ -698,6 +700,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.jitter_seed = oc.o.interleave_seed;
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
         prm.rs_chain = mode == kModeRS ? oc.rs_chain : 0;
+        prm.b_mn = oc.o.b_layout == FLUX_B_KN ? 1 : 0;
         prm.part_bf16 = mode == kModeRS && !oc.fused_reduce && oc.o.rs_partials == FLUX_BF16 ? 1 : 0;
         for (int q = 0; q < kMaxRanks; ++q) prm.slot_of[q] = -1;
         for (size_t li = 0; li < g.size(); ++li) prm.slot_of[g[li]] = static_cast<int>(li);
@@ -802,6 +805,7 @@ void flux_default_opts(flux_opts* o) {
     o->activation = FLUX_ACT_NONE;
     o->activation_grad = FLUX_ACT_NONE;
     o->rs_partials = FLUX_F32;
+    o->b_layout = FLUX_B_NK;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -1135,6 +1139,21 @@ int flux_ag_engine(const flux_problem* p, int transfer, const flux_opts* opts) {
     return ag_engine_for(p, transfer, opts ? opts->ag_engine : 0);
 }
 
+// B layout contract: KN needs caller-provided B on every local rank (the
+// library's B buffer is [n, k]) and whole 64-column atoms.
+static int check_b_layout(flux_comm* c, const flux_problem* p, const flux_opts* opts, const flux_operands* ops) {
+    if (!opts || opts->b_layout == FLUX_B_NK) return FLUX_OK;
+    if (opts->b_layout != FLUX_B_KN) return fail(FLUX_ERR_CONFIG, "unknown b_layout");
+    std::vector<int> mine;
+    local_ranks_only(c, mine);
+    for (int r : mine) {
+        const flux_operands* o = ops ? (c->ipc ? ops : ops + r) : nullptr;
+        if (!o || !o->b.ptr) return fail(FLUX_ERR_CONFIG, "b_layout KN needs caller-provided B ([k, n] row-major)");
+    }
+    if (local_cols(p) % 64 != 0) return fail(FLUX_ERR_SHAPE, "b_layout KN needs the local n to be a multiple of 64");
+    return FLUX_OK;
+}
+
 // Epilogue activation contract (flux_activation, include/flux_b200.h).
 static int check_activation(flux_comm* c, const flux_problem* p, const flux_opts* opts, const flux_operands* ops) {
     if (!opts) return FLUX_OK;
@@ -1172,6 +1191,7 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     FLUX_TRY(validate_tiling(p, tile));
     FLUX_TRY(check_heap(c, p));
     FLUX_TRY(check_activation(c, p, opts, operands));
+    FLUX_TRY(check_b_layout(c, p, opts, operands));
     const int tp = p->tp, rpr = rows_per_rank(p);
     if (rpct <= 0) rpct = rpr;
     if (p->m / rpct > static_cast<int>(kAgFlagCap)) return fail(FLUX_ERR_CONFIG, "too many comm tiles");
@@ -1526,6 +1546,7 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     if (write_mode != FLUX_WRITE_ALLTOALL && write_mode != FLUX_FUSED_REDUCE)
         return fail(FLUX_ERR_CONFIG, "unknown write mode");
     FLUX_TRY(check_activation(c, p, opts, operands));
+    FLUX_TRY(check_b_layout(c, p, opts, operands));
     const int tp = p->tp, rpr = rows_per_rank(p);
     const int tiles = ((p->m + kBM - 1) / kBM) * ((p->n + kBN - 1) / kBN);
     if (static_cast<size_t>(tiles) * tp > kRsFlagCap) return fail(FLUX_ERR_CONFIG, "too many output tiles for the flag table");
@@ -1654,6 +1675,7 @@ int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
     FLUX_TRY(validate_problem(p));
     FLUX_TRY(check_heap(c, p));
     FLUX_TRY(check_activation(c, p, opts, nullptr));
+    FLUX_TRY(check_b_layout(c, p, opts, nullptr));
     OpCommon oc = common_opts(opts);
     c->last_launches = 0;
     c->kernel_events_used = 0;

@@ -128,6 +128,7 @@ struct GemmParams {
     void* aux[kMaxRanks];          // per local slot: bf16 [m, n] pre-activation
     int ld_aux[kMaxRanks];
     int rs_chain;                  // RS, every rank in this launch: chained partial sums (see kernel)
+    int b_mn;                      // B operand given as [k, n] row-major (MN-major), else [n, k]
     int part_bf16;                 // RS staging partials stored as bf16 (opts.rs_partials)
     // Tail split (Plain / AG): the last (num tiles mod clusters) tiles run as
     // tail_splits K-slices each; the last arriving slice sums them in order.

@@ -184,6 +184,16 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
     return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
            (2ull << 61);
 }
+// MN-major 128B-swizzled operand (B given as [k, n] row-major): 64-element MN
+// atoms of 8 K-rows x 128 B; K groups of 8 rows 1 KiB apart (SBO), MN atoms
+// (one 64 x 64 TMA box each) 8 KiB apart (LBO).
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
+    const uint64_t addr = smem_u32(p);
+    return ((addr >> 4) & 0x3FFFull) | (uint64_t(8192 >> 4) << 16) | (uint64_t(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+constexpr int kMnBoxBytes = 64 * kBK * 2;  // one 64 (N) x 64 (K) bf16 TMA box
+
 // Instruction descriptor: D f32, A/B bf16, both K-major, M x N.
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
@@ -666,11 +676,23 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     if (CG == 2) {
                         if (leader) mbar_expect_tx(&full[stage], 2 * G::kStageBytes);
                         tma_load_2d_pair(sA + stage * G::kABytes, &p.tma_a[l], &full[stage], kb * kBK, row0);
-                        tma_load_2d_pair(sB + stage * G::kBBytes, &p.tma_b[l], &full[stage], kb * kBK, bcol0);
+                        if (p.b_mn) {  // [k, n] weights: kBRows / 64 boxes of 64 (N) x 64 (K)
+                            for (int j = 0; j < G::kBRows / 64; ++j)
+                                tma_load_2d_pair(sB + stage * G::kBBytes + j * kMnBoxBytes, &p.tma_b[l], &full[stage],
+                                                 bcol0 + j * 64, kb * kBK);
+                        } else {
+                            tma_load_2d_pair(sB + stage * G::kBBytes, &p.tma_b[l], &full[stage], kb * kBK, bcol0);
+                        }
                     } else {
                         mbar_expect_tx(&full[stage], G::kStageBytes);
                         tma_load_2d(sA + stage * G::kABytes, &p.tma_a[l], &full[stage], kb * kBK, row0);
-                        tma_load_2d(sB + stage * G::kBBytes, &p.tma_b[l], &full[stage], kb * kBK, bcol0);
+                        if (p.b_mn) {
+                            for (int j = 0; j < G::kBRows / 64; ++j)
+                                tma_load_2d(sB + stage * G::kBBytes + j * kMnBoxBytes, &p.tma_b[l], &full[stage],
+                                            bcol0 + j * 64, kb * kBK);
+                        } else {
+                            tma_load_2d(sB + stage * G::kBBytes, &p.tma_b[l], &full[stage], kb * kBK, bcol0);
+                        }
                     }
                     if (++stage == G::kStagesN) {
                         stage = 0;
@@ -697,15 +719,18 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t adesc = smem_desc_sw128(sA + stage * G::kABytes);
-                    const uint64_t bdesc = smem_desc_sw128(sB + stage * G::kBBytes);
+                    const uint64_t bdesc = p.b_mn ? smem_desc_mn_sw128(sB + stage * G::kBBytes)
+                                                  : smem_desc_sw128(sB + stage * G::kBBytes);
+                    // K-major: +32 B along K inside the 128B atom = +2 in the >>4 address
+                    // field; MN-major: +16 K-rows = +2 KiB = +128.
+                    const uint64_t bstep = p.b_mn ? 128ull : 2ull;
+                    const uint32_t idesc = G::kIdescV | (p.b_mn ? (1u << 16) : 0u);
 #pragma unroll
                     for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
-                        // +32 B along K inside the 128B swizzle atom = +2 in the >>4 address field.
                         if (CG == 2)
-                            umma_bf16_pair(d, adesc + 2ull * kk, bdesc + 2ull * kk, G::kIdescV,
-                                           (kb > kb0 || kk != 0) ? 1u : 0u);
+                            umma_bf16_pair(d, adesc + 2ull * kk, bdesc + bstep * kk, idesc, (kb > kb0 || kk != 0) ? 1u : 0u);
                         else
-                            umma_bf16(d, adesc + 2ull * kk, bdesc + 2ull * kk, G::kIdescV, (kb > kb0 || kk != 0) ? 1u : 0u);
+                            umma_bf16(d, adesc + 2ull * kk, bdesc + bstep * kk, idesc, (kb > kb0 || kk != 0) ? 1u : 0u);
                     }
                     // Frees the smem slot (in both CTAs) when these MMAs retire.
                     if (CG == 2) umma_commit_pair(&empty[stage]);

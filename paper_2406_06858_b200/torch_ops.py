@@ -69,20 +69,23 @@ def _(a_shard, weight, comm_id):
 
 
 @torch.library.custom_op("flux_b200::gemm_rs", mutates_args=())
-def gemm_rs(a: torch.Tensor, weight: torch.Tensor, comm_id: int) -> torch.Tensor:
+def gemm_rs(a: torch.Tensor, weight: torch.Tensor, comm_id: int, b_kn: bool = False) -> torch.Tensor:
     """ReduceScatter(a @ weight^T) over rows. a [m, k/tp] bf16, weight [n, k/tp]
-    bf16; returns this rank's [m/tp, n] bf16 rows (source-ordered fp32 sum)."""
+    bf16 (b_kn: weight given as [k/tp, n], used as a @ weight); returns this
+    rank's [m/tp, n] bf16 rows (fixed-order fp32 sum)."""
     comm = _REGISTRY[comm_id]
     tp = comm.tp
-    p = ProblemSpec(a.shape[0], weight.shape[0], a.shape[1] * tp, tp, N.GEMM_REDUCESCATTER)
+    n = weight.shape[1] if b_kn else weight.shape[0]
+    p = ProblemSpec(a.shape[0], n, a.shape[1] * tp, tp, N.GEMM_REDUCESCATTER)
     out = torch.empty(p.rows_per_rank(), p.n, dtype=torch.bfloat16, device=a.device)
-    comm.gemm_rs_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a, weight, out)], streams=_stream())
+    comm.gemm_rs_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a, weight, out)],
+                    opts=N.default_opts(b_layout=N.B_KN if b_kn else N.B_NK), streams=_stream())
     return out
 
 
 @gemm_rs.register_fake
-def _(a, weight, comm_id):
-    return a.new_empty(a.shape[0] // _REGISTRY[comm_id].tp, weight.shape[0])
+def _(a, weight, comm_id, b_kn=False):
+    return a.new_empty(a.shape[0] // _REGISTRY[comm_id].tp, weight.shape[1] if b_kn else weight.shape[0])
 
 
 # ---------------------------------------------------------------------------
@@ -119,22 +122,26 @@ def _(a_shard, weight, comm_id, activation):
 
 @torch.library.custom_op("flux_b200::ag_gemm_dact", mutates_args=())
 def ag_gemm_dact(a_shard: torch.Tensor, weight: torch.Tensor, pre: torch.Tensor, comm_id: int,
-                 activation: int) -> torch.Tensor:
+                 activation: int, b_kn: bool = False) -> torch.Tensor:
     """(AllGather(a_shard) @ weight^T) * activation'(pre): the backward of the
     GEMM-RS + activation, with the derivative in the AG-GEMM epilogue (SWIGLU:
-    dgate / dup in the gate/up grouping, twice the columns)."""
+    dgate / dup in the gate/up grouping, twice the columns). b_kn: weight given
+    as [k, n/tp] (e.g. the forward's W_down itself), used as AllGather(a) @ weight."""
     comm = _REGISTRY[comm_id]
-    p = _ag_problem(comm, a_shard, weight.shape[0])
-    width = weight.shape[0] * (2 if activation == N.ACT_SWIGLU else 1)
+    n_local = weight.shape[1] if b_kn else weight.shape[0]
+    p = _ag_problem(comm, a_shard, n_local)
+    width = n_local * (2 if activation == N.ACT_SWIGLU else 1)
     out = torch.empty(p.m, width, dtype=torch.bfloat16, device=a_shard.device)
     comm.ag_gemm_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a_shard, weight, out, pre)],
-                    opts=N.default_opts(activation_grad=activation), streams=_stream())
+                    opts=N.default_opts(activation_grad=activation, b_layout=N.B_KN if b_kn else N.B_NK),
+                    streams=_stream())
     return out
 
 
 @ag_gemm_dact.register_fake
-def _(a_shard, weight, pre, comm_id, activation):
-    width = weight.shape[0] * (2 if activation == N.ACT_SWIGLU else 1)
+def _(a_shard, weight, pre, comm_id, activation, b_kn=False):
+    n_local = weight.shape[1] if b_kn else weight.shape[0]
+    width = n_local * (2 if activation == N.ACT_SWIGLU else 1)
     return a_shard.new_empty(a_shard.shape[0] * _REGISTRY[comm_id].tp, width)
 
 
@@ -163,9 +170,11 @@ class _TPMlpFunction(torch.autograd.Function):
     def backward(ctx, dout):
         w_up, w_down, z, pre, x_g = ctx.saved_tensors
         dout = dout.contiguous().to(torch.bfloat16)
-        dy = torch.ops.flux_b200.ag_gemm_dact(dout, w_down.t().contiguous(), pre, ctx.comm_id, ctx.activation)
+        # The backward GEMMs read the forward weights as [k, n] (MN-major B
+        # operand): no transposed copies.
+        dy = torch.ops.flux_b200.ag_gemm_dact(dout, w_down, pre, ctx.comm_id, ctx.activation, True)
         dout_g = gathered_input(ctx.comm_id, dout, w_down.shape[1]) if w_down.requires_grad else None
-        dx = torch.ops.flux_b200.gemm_rs(dy, w_up.t().contiguous(), ctx.comm_id)
+        dx = torch.ops.flux_b200.gemm_rs(dy, w_up, ctx.comm_id, True)
         d_w_up = (dy.t().float() @ x_g.float()).to(w_up.dtype) if x_g is not None else None
         d_w_down = (dout_g.t().float() @ z.float()).to(w_down.dtype) if dout_g is not None else None
         return dx, d_w_up, d_w_down, None, None

@@ -463,3 +463,31 @@ def test_rs_bf16_partials_normwise(case):
     with H.make_comm(q) as comm:
         with pytest.raises(fx.ConfigError, match="bf16 partials"):
             _run(comm, q, True, rs_partials=fx.BF16)
+
+
+@pytest.mark.parametrize("cta_group", [1, 2])
+@pytest.mark.parametrize("case", [(AG, 1024, 2048, 512, 4), (RS, 1024, 512, 768, 4), (AG, 512, 1536, 200, 2),
+                                  (RS, 2048, 1024, 1024, 8), (RS, 64, 256, 256, 4)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_b_layout_kn(case, cta_group):
+    """Caller B given as [k, n] row-major (the reference's b_shard layout,
+    opts.b_layout = KN): MN-major tcgen05 B operand, no transposed copy."""
+    pat, m, n, k, tp = case
+    p = fx.ProblemSpec(m, n, k, tp, pat)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=19 + m)
+        want = _oracle(p, a, b)
+        b_kn = [comm.tensor(r, N.BUF_B_SHARD, p).t().contiguous() for r in range(tp)]  # [k_local, n_local]
+        opts = fx.default_opts(out_dtype=fx.F32, wall_budget_s=5.0, b_layout=fx.B_KN, cta_group=cta_group)
+        ops = [(None, b_kn[r], None) for r in range(tp)]
+        tile = fx.TileShape(p.rows_per_rank(), p.local_cols())
+        if pat == AG:
+            comm.ag_gemm_ex(p, tile, ops, opts=opts)
+        else:
+            comm.gemm_rs_ex(p, tile, ops, opts=opts)
+        comm.sync()
+        got = H.outputs(comm, p, True)
+        for r in range(tp):
+            assert O.max_rel_error(got[r], want[r]) <= H.tol(True, p.k), r
+        with pytest.raises(fx.ConfigError, match="caller-provided B"):
+            comm.ag_gemm(p, tile, opts=opts) if pat == AG else comm.gemm_rs(p, tile, opts=opts)
