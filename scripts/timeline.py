@@ -21,6 +21,7 @@ ap.add_argument("--workload", default="llama70b-down-rs")
 ap.add_argument("--bucket-us", type=float, default=25.0)
 ap.add_argument("--ag-engine", type=int, default=0)
 ap.add_argument("--local", action="store_true", help="trace the plain local GEMM instead of the fused op")
+ap.add_argument("--cta-ends", action="store_true", help="print the earliest / latest CTA end times with their ids")
 args = ap.parse_args()
 pattern, m, n, k, tp, _ = WORKLOADS[args.workload]
 prob = fx.ProblemSpec(m, n, k, tp, pattern)
@@ -65,3 +66,8 @@ if starts and ends:
     ends_us = sorted((e - min(starts)) / 1e3 for e in ends)
     q = [ends_us[int(f * (len(ends_us) - 1))] for f in (0.0, 0.1, 0.5, 0.9, 1.0)]
     print("CTA end times (us) min/p10/p50/p90/max: " + " / ".join(f"{v:.1f}" for v in q))
+    if args.cta_ends:
+        t00 = min(starts)
+        by = sorted(((e["ts"] - t00) / 1e3, e["tile_row"]) for e in ev if e["event"] == "launch" and e["tile_col"] == 1)
+        print("earliest CTA ends (us, blockIdx):", [(round(t), b) for t, b in by[:16]])
+        print("latest CTA ends (us, blockIdx):", [(round(t), b) for t, b in by[-16:]])
