@@ -1,26 +1,34 @@
 // Fused tensor-parallel GEMM kernels for sm_100a (B200).
 //
-// One persistent, warp-specialised tcgen05 GEMM serves three roles
+// One persistent, warp-specialised tcgen05 GEMM serves every role
 // (KernelMode):
-//   Plain — C = A B^T, no communication (TP=1 and the Eq. 1 "non-split GEMM").
-//   AG    — paper Alg. 2 (reference engine.cpp:516-547): before the TMA
-//           producer loads the A rows of a tile it spins on the per-comm-tile
-//           flags covering those rows (reference spin_wait on SignalBoard,
-//           engine.cpp:529-539); flags are raised by the copy-engine transfer
-//           loop (Alg. 3, engine.cpp:367-423) running on a side stream.
-//   RS    — paper Alg. 1 (reference engine.cpp:265-341): the epilogue routes
-//           every accumulator row to its owner (owner_of_row, problem.hpp:37),
-//           storing fp32 partials into the owner's staging plane for this
-//           source over NVLink (WriteAlltoAll, engine.cpp:285-292) and raising
-//           a per-(tile, source) flag; the owner reduces its own rows in source
-//           order 0..tp-1 inside its local-tile epilogue, replacing the
-//           reference's discrete reduce agent (engine.cpp:324-341).
+//   Plain  — C = A B^T, no communication (TP=1 and the Eq. 1 "non-split GEMM").
+//   AG     — paper Alg. 2 (reference engine.cpp:516-547): before the TMA
+//            producer loads the A rows of a tile it spins on the per-comm-tile
+//            flags covering those rows (reference spin_wait on SignalBoard,
+//            engine.cpp:529-539); flags are raised by the copy-engine transfer
+//            loop (Alg. 3, engine.cpp:367-423) on a side stream, or by warp 3
+//            of every CTA pulling a_agg pieces with TMA bulk copies.
+//   RS     — paper Alg. 1 (reference engine.cpp:265-341): the epilogue routes
+//            every accumulator row to its owner (owner_of_row, problem.hpp:37)
+//            as tile-major partials (WriteAlltoAll, engine.cpp:285-292) or
+//            red.add (FusedReduce, :304-319) and raises a per-(tile, source)
+//            flag; the owner reduces its rows inside its local-tile epilogue
+//            in a fixed order, replacing the reference's reduce agent
+//            (engine.cpp:324-341); with every rank in one launch the partials
+//            are chained instead (each source adds to its predecessor's sum).
+//   RSLast — RS with ownership blocks narrower than a tile (decode): the last
+//            of the tp arrivals of a tile reduces it.
+// Epilogue options: activations (GELU / ReLU / SiLU / SwiGLU), pre-activation
+// save, derivative scaling (MLP backward); tail split of the last wave
+// (Plain / AG); B operand K-major or MN-major; bf16 RS partials (PB).
 //
 // Roles: warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one lane),
-// warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM lane quadrants 0..3).
-// Pipelines: kStages smem ring (TMA -> MMA), two TMEM accumulators
-// (MMA -> epilogue). The tile schedule is a host-built table (reference
-// tile_order, swizzle.cpp:75-80) walked with a static stride of gridDim.x.
+// warp 2 = TMEM allocator, warp 3 = in-kernel AllGather transfer (AG),
+// warps 4..7 = epilogue (TMEM lane quadrants 0..3). Pipelines: a smem ring
+// (TMA -> MMA), two TMEM accumulators (MMA -> epilogue). The tile schedule is
+// a host-built table (reference tile_order, swizzle.cpp:75-80) walked with a
+// static stride of the cluster count.
 #include <cuda_bf16.h>
 
 #include "flux_internal.hpp"
