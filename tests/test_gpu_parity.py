@@ -491,3 +491,39 @@ def test_b_layout_kn(case, cta_group):
             assert O.max_rel_error(got[r], want[r]) <= H.tol(True, p.k), r
         with pytest.raises(fx.ConfigError, match="caller-provided B"):
             comm.ag_gemm(p, tile, opts=opts) if pat == AG else comm.gemm_rs(p, tile, opts=opts)
+
+
+@pytest.mark.parametrize("pattern", [AG, RS])
+def test_acceptance_wallclock_ratio(pattern):
+    """Reference acceptance criterion 7 (acceptance.cpp:323-371): fused /
+    non-overlapped wall-clock ratio <= 1.5 (there non-gating, on CPU threads);
+    here on the GPU with device time, medians of 5 after warm-up."""
+    p = fx.ProblemSpec(2048, 8192, 2048, 8, pattern) if pattern == AG else fx.ProblemSpec(2048, 2048, 8192, 8, pattern)
+    with H.make_comm(p) as comm:
+        for r in range(p.tp):
+            for kind in (N.BUF_A_SHARD, N.BUF_B_SHARD):
+                t = comm.tensor(r, kind, p)
+                t.copy_((torch.rand(t.shape, device="cuda") * 2 - 1).to(torch.bfloat16))
+        tile = fx.TileShape(p.rows_per_rank(), p.local_cols())
+
+        def fused():
+            comm.ag_gemm(p, tile) if pattern == AG else comm.gemm_rs(p, tile)
+
+        def nonoverlap():
+            comm.nonoverlap(p)
+
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        times = {"fused": [], "nonoverlap": []}
+        for fn in (fused, nonoverlap, fused, nonoverlap):
+            fn()
+        comm.sync()
+        for _ in range(5):
+            for name, fn in (("fused", fused), ("nonoverlap", nonoverlap)):
+                e0.record()
+                fn()
+                e1.record()
+                comm.sync()
+                times[name].append(e0.elapsed_time(e1))
+        ratio = float(np.median(times["fused"]) / np.median(times["nonoverlap"]))
+        print(f"fused / non-overlapped wall-clock ratio ({'AG' if pattern == AG else 'RS'}): {ratio:.3f}")
+        assert ratio <= 1.5
