@@ -744,6 +744,13 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             }
         }
         const int grid = cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
+        // Dynamic tile scheduler (FLUX_DYN_SCHED=1): clusters fetch tiles from a
+        // counter in the lead rank's control block instead of a static stride.
+        if (const char* env = std::getenv("FLUX_DYN_SCHED"); env && std::atoi(env) != 0 && grid / cg > 1) {
+            const RankState& lead_rank = c->ranks[g[0]];
+            prm.dyn_ctr = at<uint32_t>(lead_rank, kCtrlDynCtr);
+            prm.dyn_exit = at<uint32_t>(lead_rank, kCtrlDynExit);
+        }
         std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
         if (c->timing) {
             if (static_cast<int>(c->kernel_events.size()) <= c->kernel_events_used) {
@@ -1898,6 +1905,7 @@ int flux_sync(flux_comm* c) {
             }
             const uint32_t zero[4] = {0, 0, 0, 0};
             FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlErr, zero, sizeof(zero), cudaMemcpyHostToDevice));
+            FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlDynCtr, zero, 8, cudaMemcpyHostToDevice));
         }
     }
     if (!deadlock.empty()) return fail(FLUX_ERR_DEADLOCK, deadlock);

@@ -34,6 +34,8 @@ constexpr size_t kCtrlDone = 68;        // u32: epoch whose peer pulls this rank
 constexpr size_t kCtrlKdone = 72;       // u32: epoch whose kernel finished on this rank (push targets)
 constexpr size_t kCtrlFrReady = 76;     // u32: epoch whose FusedReduce accumulator is zeroed (RS FusedReduce)
 constexpr size_t kCtrlTraceCursor = 80; // u32: records written to this rank's trace ring
+constexpr size_t kCtrlDynCtr = 88;      // u32: dynamic tile scheduler — next tile (zeroed by the last cluster out)
+constexpr size_t kCtrlDynExit = 92;     // u32: dynamic tile scheduler — clusters finished
 constexpr size_t kTraceBytes = size_t(4) << 20;  // trace ring at the end of the data region (16 B records)
 // Trace record kinds (the reference CausalityLog event names, engine.hpp:37-63).
 // kEvLaunch (not in the reference schema): a CTA's first (tile_col 0) and last (tile_col 1)
@@ -128,6 +130,11 @@ struct GemmParams {
     void* aux[kMaxRanks];          // per local slot: bf16 [m, n] pre-activation
     int ld_aux[kMaxRanks];
     int rs_chain;                  // RS, every rank in this launch: chained partial sums (see kernel)
+    // Dynamic tile scheduler: the pair leader's producer fetches tiles from a
+    // global counter (tail-split units stay statically one per cluster) and
+    // hands them to its pair through a shared-memory queue.
+    uint32_t* dyn_ctr;             // nullptr: static stride
+    uint32_t* dyn_exit;
     int b_mn;                      // B operand given as [k, n] row-major (MN-major), else [n, k]
     int part_bf16;                 // RS staging partials stored as bf16 (opts.rs_partials)
     // Tail split (Plain / AG): the last (num tiles mod clusters) tiles run as

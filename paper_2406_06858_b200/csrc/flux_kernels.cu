@@ -185,6 +185,21 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAITC:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONEC;\n\t"
+        "bra LAB_WAITC;\n"
+        "DONEC:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void st_shared_cluster_s32(uint32_t cluster_addr, int v) {
+    asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+
 // Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row core groups
 // 1024 B apart (SBO), version 1 (sm_100).
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
@@ -581,6 +596,73 @@ struct Geo {
     static constexpr uint32_t kIdescV = make_idesc(kTileM, kBN);
 };
 
+constexpr int kTileQ = 4;  // dynamic scheduler: tile-queue depth
+
+// The sequence of work units a CTA processes. Static: cluster_id, +clusters,
+// ... Dynamic: the pair leader's producer fetches from a global counter (tiles
+// below `dyn_end`, then at most one statically assigned tail-split unit per
+// cluster, so all slices of a tail tile stay co-resident) and publishes each
+// unit in a kTileQ-slot queue to the other roles of both CTAs; -1 ends it.
+struct TileSeq {
+    const GemmParams* p;
+    int cluster_id, num_clusters, cta_rank, qi = 0;
+    uint32_t qph = 0;
+    bool fetcher, dyn_done = false, tail_done = false;
+    int t = -1;       // static cursor
+    int pend = -1;    // dynamic: the next fetch, issued one unit ahead so its latency hides
+    __device__ int fetch() {
+        const int dyn_end = p->tail_splits > 1 ? p->tail_base : p->num_tiles;
+        if (!dyn_done) {
+            const int v = pend < 0 ? static_cast<int>(atomicAdd(p->dyn_ctr, 1u)) : pend;
+            if (v < dyn_end) {
+                pend = static_cast<int>(atomicAdd(p->dyn_ctr, 1u));
+                return v;
+            }
+            dyn_done = true;
+        }
+        if (!tail_done) {
+            tail_done = true;
+            const int u = dyn_end + cluster_id;
+            if (p->tail_splits > 1 && u < p->num_tiles) return u;
+        }
+        return -1;
+    }
+    // Next unit; the fetcher also publishes it (producer warp of the pair leader).
+    template <int CG>
+    __device__ int next(uint64_t* qfull, uint64_t* qempty, int* qtile) {
+        if (p->dyn_ctr == nullptr) {
+            t = t < 0 ? cluster_id : t + num_clusters;
+            return t < p->num_tiles ? t : -1;
+        }
+        int v;
+        if (fetcher) {
+            v = fetch();
+            mbar_wait_acq_cluster(&qempty[qi], qph ^ 1u);
+            qtile[qi] = v;
+            if (CG == 2) st_shared_cluster_s32(mapa(smem_u32(&qtile[qi]), 1), v);
+            mbar_arrive(&qfull[qi]);
+            if (CG == 2) mbar_arrive_cluster(mapa(smem_u32(&qfull[qi]), 1));
+        } else {
+            mbar_wait_acq_cluster(&qfull[qi], qph);
+            v = qtile[qi];
+        }
+        return v;
+    }
+    // Consumers release the slot they read (lane 0 of each consuming warp).
+    template <int CG>
+    __device__ void release(uint64_t* qempty, bool arrive) {
+        if (p->dyn_ctr == nullptr) return;
+        if (!fetcher && arrive) {
+            if (CG == 2 && cta_rank != 0) mbar_arrive_cluster(mapa(smem_u32(&qempty[qi]), 0));
+            else mbar_arrive(&qempty[qi]);
+        }
+        if (++qi == kTileQ) {
+            qi = 0;
+            qph ^= 1u;
+        }
+    }
+};
+
 // PB: RS cross-rank partials stored as bf16 (1) or fp32 (0) — a template
 // parameter so the owner's batched loads stay branch-free.
 template <int MODE, int CG, int PB = 0>
@@ -598,8 +680,12 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     uint64_t* tfull = empty + G::kStagesN;
     uint64_t* tempty = tfull + 2;
     uint64_t* cbar = tempty + 2;  // 2 comm-piece barriers (AG)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 2);
+    uint64_t* qfull = cbar + 2;    // dynamic scheduler: tile queue slots full / empty
+    uint64_t* qempty = qfull + kTileQ;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qempty + kTileQ);
     uint32_t* s_flag = tmem_slot + 1;  // epilogue broadcast (RS last arriver)
+    int* qtile = reinterpret_cast<int*>(s_flag + 1);
+    static_assert((2 * G::kStagesN + 6 + 2 * kTileQ) * 8 + 8 + 4 * kTileQ <= 256, "barrier region");
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -626,6 +712,11 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             mbar_init(&tempty[a], 4 * CG);  // every epilogue warp of the pair drains it
             mbar_init(&cbar[a], 1);
         }
+        for (int i = 0; i < kTileQ; ++i) {
+            mbar_init(&qfull[i], 1);
+            // leader: MMA lane + its 4 epilogue warps (+ the peer's producer and 4 epilogue warps)
+            mbar_init(&qempty[i], CG == 2 ? 10 : 5);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -646,7 +737,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             int stage = 0;
             uint32_t phase = 0;
             uint64_t jit = p.jitter_seed ? p.jitter_seed * 0x9e3779b97f4a7c15ull + blockIdx.x : 0;
-            for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            TileSeq seq{&p, cluster_id, num_clusters, static_cast<int>(cta_rank)};
+            seq.fetcher = leader;
+            for (int t = seq.next<CG>(qfull, qempty, qtile); t >= 0; t = seq.next<CG>(qfull, qempty, qtile)) {
+                seq.release<CG>(qempty, true);
                 int l, tm, tn, kb0, kb1, split;
                 uint32_t entry;
                 tile_unit(p, t, k_blocks, entry, kb0, kb1, split);
@@ -708,6 +802,15 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     }
                 }
             }
+            if (p.dyn_ctr != nullptr && leader) {
+                // Every fetch of this cluster precedes its exit count; the last
+                // cluster out re-arms the counter for the next launch.
+                __threadfence();
+                if (atomicAdd(p.dyn_exit, 1u) == static_cast<uint32_t>(num_clusters - 1)) {
+                    atomicExch(p.dyn_ctr, 0u);
+                    atomicExch(p.dyn_exit, 0u);
+                }
+            }
         }
     } else if (warp == 1) {
         // ===== MMA issuer (the pair leader issues for both CTAs) =====
@@ -716,7 +819,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             uint32_t phase = 0;
             int as = 0;
             uint32_t aphase = 0;
-            for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+            TileSeq seq{&p, cluster_id, num_clusters, static_cast<int>(cta_rank)};
+            seq.fetcher = false;
+            for (int t = seq.next<CG>(qfull, qempty, qtile); t >= 0; t = seq.next<CG>(qfull, qempty, qtile)) {
+                seq.release<CG>(qempty, true);
                 int kb0, kb1, split;
                 uint32_t entry;
                 tile_unit(p, t, k_blocks, entry, kb0, kb1, split);
@@ -847,7 +953,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         const uint32_t tempty_leader = CG == 2 ? mapa(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
         int as = 0;
         uint32_t aphase = 0;
-        for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+        TileSeq seq{&p, cluster_id, num_clusters, static_cast<int>(cta_rank)};
+        seq.fetcher = false;
+        for (int t = seq.next<CG>(qfull, qempty, qtile); t >= 0; t = seq.next<CG>(qfull, qempty, qtile)) {
+            seq.release<CG>(qempty, lane == 0);
             int l, tmp, tn, kb0, kb1, split;
             uint32_t entry;
             tile_unit(p, t, k_blocks, entry, kb0, kb1, split);
