@@ -398,7 +398,6 @@ struct RankState {
     cudaStream_t copy_stream = nullptr;  // copy-engine transfer loop
     cudaEvent_t start_evt = nullptr, kernel_evt = nullptr, copy_evt = nullptr;
     bool kernel_evt_valid = false;
-    uint32_t rs_done_cum = 0;  // tiles of mine finalised by last arrivers, cumulative (RS)
 };
 
 constexpr uint32_t kIpcMagic = 0xF1u << 24 | 0xB200u;
@@ -550,7 +549,7 @@ int upload_order(flux_comm* c, int device, const std::vector<uint32_t>& order, u
     return FLUX_OK;
 }
 
-enum { kInterleaveStep = 0, kInterleaveRank = 1, kInterleaveRankTail = 2 };
+enum { kInterleaveStep = 0, kInterleaveRank = 1, kInterleaveRankTail = 2, kInterleaveBlock = 3 };
 
 // CTAs per MMA tile: CTA pairs (256-row tiles, cta_group::2) unless ownership
 // blocks only align with 128-row tiles; opts.cta_group forces 1 or 2.
@@ -651,9 +650,6 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 prm.fr_acc[r] = reinterpret_cast<float*>(c->ranks[r].heap + L.staging.off +
                                                          static_cast<size_t>(c->epoch & 1u) * L.stage_parity * 4);
                 prm.fr_ready[r] = at<uint32_t>(c->ranks[r], kCtrlFrReady);
-                prm.rs_ctr[r] = at<uint32_t>(c->ranks[r], kRsCtrOffset);
-                prm.rs_done[r] = at<uint32_t>(c->ranks[r], kRsDoneOffset);
-                prm.c_rank[r] = c->ranks[r].heap + L.c32.off;
             }
         }
         // Interleave the per-rank sequences into one device schedule.
@@ -669,7 +665,19 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             const uint32_t e = seq_of_rank[g[li]][i];
             order.push_back((e & 0x0FFFFFFFu) | (uint32_t(li) << 28));
         };
-        if (interleave == kInterleaveStep || g.size() == 1) {
+        if (interleave == kInterleaveBlock && g.size() > 1) {
+            // Blocks of positions, every rank's tiles of a block in turn: a
+            // position's partials are complete after its block instead of after
+            // the last rank's whole GEMM, so the owners' reduction (decode RS)
+            // runs concurrently with later blocks. ~One wave per block.
+            const char* env = std::getenv("FLUX_RS_BLOCK");
+            const int clusters = std::max(1, sm_count(dev) / cg);
+            size_t bs = std::max<size_t>(1, static_cast<size_t>(clusters) / g.size());
+            if (env) bs = std::atoi(env) > 0 ? static_cast<size_t>(std::atoi(env)) : T;
+            for (size_t i0 = 0; i0 < T; i0 += bs)
+                for (size_t li = 0; li < g.size(); ++li)
+                    for (size_t i = i0; i < std::min(T, i0 + bs); ++i) push(li, i);
+        } else if (interleave == kInterleaveStep || g.size() == 1) {
             for (size_t i = 0; i < T; ++i)
                 for (size_t li = 0; li < g.size(); ++li) push(li, i);
         } else {
@@ -705,6 +713,8 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         for (int q = 0; q < kMaxRanks; ++q) prm.slot_of[q] = -1;
         for (size_t li = 0; li < g.size(); ++li) prm.slot_of[g[li]] = static_cast<int>(li);
         prm.rs_last_arriver = mode == kModeRSLast ? 1 : 0;
+        prm.red_ctr = at<uint32_t>(c->ranks[g[0]], kCtrlRedCtr);
+        prm.red_exit = at<uint32_t>(c->ranks[g[0]], kCtrlRedExit);
         if (const char* env = std::getenv("FLUX_DEBUG")) prm.dbg = std::atoi(env);  // profiling ablations only
         // Join the other local ranks' streams into the launch stream.
         for (size_t li = 0; li < g.size(); ++li) {
@@ -1599,33 +1609,15 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     // operands L2-resident); otherwise fall back to position-major.
     const bool aligned = swizzle_on && rpr % (kBM * cg) == 0 && oc.o.emulated_order != 1;
     const int tail = aligned ? (rpr / (kBM * cg)) * ((p->n + kBN - 1) / kBN) : 0;
-    // Ownership blocks narrower than a device tile (decode-sized M): no owner
-    // waits; the last of the tp arrivals of each tile reduces it (deterministic).
+    // Ownership blocks narrower than a device tile (decode-sized M): sources
+    // stage whole tiles, owners sum their rows at the end of the kernel.
     const int tiles_n = (p->n + kBN - 1) / kBN;
     oc.rs_last_arriver = (rpr % kBM != 0 && !oc.fused_reduce) ? 1 : 0;
     oc.ops = operands;
-    // Decode-sized blocks: the last arrivers write every owner's rows into the
-    // library C (peer-addressable); a caller C then receives a copy of its rows.
-    std::vector<flux_operands> ops_lib;
-    std::vector<std::pair<int, flux_matrix>> caller_c;
-    if (operands && oc.rs_last_arriver) {
-        const int n_ops = c->ipc ? 1 : tp;
-        ops_lib.assign(operands, operands + n_ops);
-        for (int r : mine) {
-            flux_operands& o = c->ipc ? ops_lib[0] : ops_lib[r];
-            if (o.c.ptr) {
-                caller_c.emplace_back(r, o.c);
-                o.c = flux_matrix{nullptr, 0};
-            }
-        }
-        oc.ops = ops_lib.data();
-    }
     if (oc.o.rs_partials != FLUX_F32 && oc.o.rs_partials != FLUX_BF16)
         return fail(FLUX_ERR_CONFIG, "rs_partials must be F32 or BF16");
     if (oc.o.rs_partials == FLUX_BF16 && (oc.rs_last_arriver || oc.fused_reduce))
         return fail(FLUX_ERR_CONFIG, "bf16 partials need WriteAlltoAll and ownership blocks of whole 128-row tiles");
-    if (oc.rs_last_arriver && static_cast<size_t>(tiles) > kRsCtrCap)
-        return fail(FLUX_ERR_CONFIG, "too many output tiles for the arrival counters");
     // Chained partial sums (kernel, RS branch) when every rank runs in this one
     // launch (rank-major order, owners' blocks last); every chain link waits only
     // on an earlier section.
@@ -1643,37 +1635,9 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
                           ? 1
                           : 0;
     }
-    const int interleave = aligned ? kInterleaveRankTail : (oc.rs_last_arriver ? kInterleaveRank : kInterleaveStep);
+    const int interleave = aligned ? kInterleaveRankTail : (oc.rs_last_arriver ? kInterleaveBlock : kInterleaveStep);
     FLUX_TRY(launch_groups(c, p, oc.rs_last_arriver ? kModeRSLast : kModeRS, oc, streams, seq, 0, interleave, cg,
                            false, -1, tail));
-    if (oc.rs_last_arriver) {
-        // Other ranks finalise my rows: I am done once every tile holding my rows is.
-        for (int r : mine) {
-            const int t0 = (r * rpr) / kBM, t1 = ((r + 1) * rpr - 1) / kBM;
-            c->ranks[r].rs_done_cum += static_cast<uint32_t>((t1 - t0 + 1) * tiles_n);
-            FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
-            cudaStream_t s = stream_for(c, r, streams);
-            bool remote_peer = false, other_device = false;
-            for (int q = 0; q < tp; ++q) {
-                if (!c->ranks[q].local) remote_peer = true;
-                else if (c->ranks[q].device != c->ranks[r].device) {
-                    other_device = true;
-                    FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[q].kernel_evt, 0));
-                }
-            }
-            if (remote_peer) FLUX_TRY(wait_value_geq(s, c->ranks[r].heap + kRsDoneOffset, c->ranks[r].rs_done_cum));
-            (void)other_device;
-        }
-        const Layout L = layout_for(p);
-        const size_t esz = oc.o.out_dtype == FLUX_F32 ? 4 : 2;
-        for (const auto& rc : caller_c) {
-            const RankState& rs = c->ranks[rc.first];
-            FLUX_CUDA(cudaSetDevice(rs.device));
-            FLUX_CUDA(cudaMemcpy2DAsync(rc.second.ptr, static_cast<size_t>(rc.second.ld) * esz, rs.heap + L.c32.off,
-                                        static_cast<size_t>(L.c32.ld) * esz, static_cast<size_t>(p->n) * esz, rpr,
-                                        cudaMemcpyDeviceToDevice, stream_for(c, rc.first, streams)));
-        }
-    }
     return mark_op_done(c, streams, c->epoch);
 }
 
@@ -1905,7 +1869,7 @@ int flux_sync(flux_comm* c) {
             }
             const uint32_t zero[4] = {0, 0, 0, 0};
             FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlErr, zero, sizeof(zero), cudaMemcpyHostToDevice));
-            FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlDynCtr, zero, 8, cudaMemcpyHostToDevice));
+            FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlDynCtr, zero, 16, cudaMemcpyHostToDevice));  // + reduction counters
         }
     }
     if (!deadlock.empty()) return fail(FLUX_ERR_DEADLOCK, deadlock);

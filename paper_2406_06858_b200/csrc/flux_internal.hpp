@@ -22,12 +22,15 @@ constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*alig
 
 constexpr int kMaxRanks = 8;   // TP degree supported by one communicator (one NVSwitch node)
 
-// kModeRSLast: GEMM-RS whose ownership blocks are narrower than a tile (last-arriver reduction).
+// kModeRSLast: GEMM-RS whose ownership blocks are narrower than a tile (sources stage whole
+//   tiles; the owners' rows are summed by reduction units running alongside the GEMM).
 enum Activation : int { kActNone = 0, kActGelu = 1, kActRelu = 2, kActSilu = 3, kActSwiGLU = 4 };
 enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2, kModeRSLast = 3 };
 
-// Control block at the start of every rank's symmetric heap. All words are
-// epoch-stamped (monotonic), so nothing needs resetting between operators.
+// Control block at the start of every rank's symmetric heap. The flags are
+// epoch-stamped (monotonic), so nothing needs resetting between operators; the
+// two launch-scoped work counters (dynamic tiles, reduction units) are re-armed
+// by the last CTA / group of the launch that used them.
 constexpr size_t kCtrlErr = 0;          // u32[4]: code, info0, info1, info2
 constexpr size_t kCtrlReady = 64;       // u32: epoch at which this rank's A shard is staged (AG pull source ready)
 constexpr size_t kCtrlDone = 68;        // u32: epoch whose peer pulls this rank has finished
@@ -36,6 +39,8 @@ constexpr size_t kCtrlFrReady = 76;     // u32: epoch whose FusedReduce accumula
 constexpr size_t kCtrlTraceCursor = 80; // u32: records written to this rank's trace ring
 constexpr size_t kCtrlDynCtr = 88;      // u32: dynamic tile scheduler — next tile (zeroed by the last cluster out)
 constexpr size_t kCtrlDynExit = 92;     // u32: dynamic tile scheduler — clusters finished
+constexpr size_t kCtrlRedCtr = 96;      // u32: decode RS reduction — next unit (zeroed by the last group out)
+constexpr size_t kCtrlRedExit = 100;    // u32: decode RS reduction — groups finished
 constexpr size_t kTraceBytes = size_t(4) << 20;  // trace ring at the end of the data region (16 B records)
 // Trace record kinds (the reference CausalityLog event names, engine.hpp:37-63).
 // kEvLaunch (not in the reference schema): a CTA's first (tile_col 0) and last (tile_col 1)
@@ -56,9 +61,6 @@ constexpr size_t kAgGroupCap = 32768;
 constexpr int kPieceBytes = 16384;      // one TMA bulk copy (global -> smem -> global)
 constexpr size_t kRsFlagOffset = 256 * 1024;  // u32[tile][src]: partial of tile from src landed
 constexpr size_t kRsFlagCap = (512 * 1024) / 4;
-constexpr size_t kRsCtrOffset = 768 * 1024;   // u32[tile]: monotonic arrival count (RS last arriver)
-constexpr size_t kRsCtrCap = 60 * 1024;
-constexpr size_t kRsDoneOffset = kRsCtrOffset + kRsCtrCap * 4;  // u32: tiles of mine finalised (monotonic)
 constexpr size_t kDataOffset = 1 << 20;
 
 // Error codes written by device waits into the control block.
@@ -112,11 +114,10 @@ struct GemmParams {
     int ag_slot_index;             // counter index of "own block copied" (after the group counters)
     uint32_t slot_pieces;          // pieces of one rank's own block
     uint32_t ag_mult;              // operators run on these counters since their last reset (targets scale by it)
-    // RS with ownership blocks narrower than a tile: last-arriver reduction
+    // RS with ownership blocks narrower than a tile: owners reduce during the GEMM
     int rs_last_arriver;
-    uint32_t* rs_ctr[kMaxRanks];   // per GLOBAL rank: tile arrival counters (peer pointers)
-    uint32_t* rs_done[kMaxRanks];  // per GLOBAL rank: finalised-tile counter (peer pointers)
-    void* c_rank[kMaxRanks];       // per GLOBAL rank: its C (peer pointers)
+    uint32_t* red_ctr;             // reduction unit counter (lead rank's control block)
+    uint32_t* red_exit;
     // Device event trace (reference CausalityLog, engine.hpp:37-63): 16-byte records
     unsigned long long* trace[kMaxRanks];  // per local slot: ring (nullptr = tracing off)
     uint32_t* trace_cursor[kMaxRanks];     // per local slot: next record index

@@ -285,14 +285,6 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_group() {
     asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ uint32_t atom_add_acq_rel_sys(uint32_t* p, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-    return old;
-}
-__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
-    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -503,47 +495,86 @@ __device__ __forceinline__ void sum_into(float (&acc)[4], const float4& w, bool&
 // Source-ordered sum of the tp staged partials of one 128 x 256 tile into the
 // owners' C. Consecutive threads take consecutive 4-column groups of a row
 // (coalesced), and every source's float4 is loaded before the sum.
-__device__ __forceinline__ void reduce_tile_coalesced(const GemmParams& p, int row0, int col0, uint32_t parity,
-                                                   int et) {
-    constexpr int kU = 4;  // positions per thread per iteration: kU x tp loads in flight
-    const int rows_valid = min(kBM, p.m - row0);
-    const int npos = rows_valid * (kBN / 4);
-    for (int base = et; base < npos; base += 128 * kU) {
-        float4 v[kU][kMaxRanks];
+// Decode-sized RS, owner side. The rows each local rank owns are cut into
+// units of kRedRows rows x one 256-column tile, ordered column tile first (the
+// order in which the blocked schedule completes them). Two otherwise idle warps
+// of every CTA (2 and 3) take units from a launch-wide counter while the GEMM
+// runs; the four epilogue warps join once their CTA's GEMM units are done. A
+// unit waits for the tp flags (tile, source) of the tile(s) its rows lie in,
+// then each thread keeps kU positions x tp sources in flight and sums them in
+// the canonical order (other sources ascending, then the owner) into the
+// owner's C. The GEMM never waits on a reduction, so these waits cannot
+// deadlock. The last group out re-arms the counter for the next launch.
+constexpr int kRedRows = 16;
+__device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr, int bar_id, int* slot) {
+    constexpr int kU = 4;
+    const int tp = p.tp, tiles_n = p.tiles_n, rpr = p.rpr, n = p.n, out_f32 = p.out_f32;
+    const long long ld_stage = p.ld_stage, stage_plane = p.stage_plane;
+    const uint32_t epoch = p.epoch, parity = p.epoch & 1u;
+    const bool no_wait = (p.dbg & 32) != 0;  // dbg 32: profiling ablation, no waits
+    const int nch = (rpr + kRedRows - 1) / kRedRows;
+    int nl = 0;
+    while (nl < kMaxRanks && p.c[nl] != nullptr) ++nl;
+    const int per_tn = nl * nch;
+    const int units = per_tn * tiles_n;
+    for (;;) {
+        if (tid == 0) *slot = static_cast<int>(atomicAdd(p.red_ctr, 1u));
+        named_bar_sync(bar_id, nthr);
+        const int u = *slot;
+        if (u >= units) break;
+        const int tn = u / per_tn, rem = u % per_tn;
+        const int l = rem / nch;
+        const int me = p.global_rank[l];
+        const int r0 = me * rpr + (rem % nch) * kRedRows, r1 = min(r0 + kRedRows, (me + 1) * rpr);
+        const int tm0 = r0 / kBM, tm1 = (r1 - 1) / kBM;
+        if (tid < (tm1 - tm0 + 1) * tp && !no_wait) {
+            const int tile_id = (tm0 + tid / tp) * tiles_n + tn;
+            wait_flag(p.rs_flags[me] + tile_id * tp + tid % tp, epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+                      static_cast<uint32_t>(tile_id), static_cast<uint32_t>(tid % tp));
+            if (tid == 0) trace_event(p, l, kEvReduce, me, tm0, tn, static_cast<uint32_t>(me));
+        }
+        named_bar_sync(bar_id, nthr);  // flags acquired; everyone has read *slot
+        const int npos = (r1 - r0) * (kBN / 4);
+        const float* base = p.staging[me] + parity * p.stage_parity + static_cast<long long>(r0 - me * rpr) * ld_stage;
+        void* const cl = p.c[l];
+        const long long ldc = p.ldc_l[l];
+        for (int b = tid; b < npos; b += nthr * kU) {
+            float4 v[kU][kMaxRanks];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int pos = base + u * 128;
-            const int rr = pos / (kBN / 4);
-            const int col = col0 + (pos % (kBN / 4)) * 4;
-            if (pos < npos && col < p.n) {
-                const int grow = row0 + rr;
-                const int o = grow / p.rpr;
-                const float* src = p.staging[o] + parity * p.stage_parity + (grow - o * p.rpr) * p.ld_stage + col;
+            for (int i = 0; i < kU; ++i) {
+                const int pos = b + i * nthr;
+                const int col = tn * kBN + (pos % (kBN / 4)) * 4;
+                if (pos < npos && col < n) {
+                    const float* src = base + (pos / (kBN / 4)) * ld_stage + col;
 #pragma unroll
-                for (int s = 0; s < kMaxRanks; ++s)
-                    if (s < p.tp) v[u][s] = ld_cg_f4(src + s * p.stage_plane);
+                    for (int s = 0; s < kMaxRanks; ++s)
+                        if (s < tp) v[i][s] = ld_cg_f4(src + s * stage_plane);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kU; ++i) {
+                const int pos = b + i * nthr;
+                const int col = tn * kBN + (pos % (kBN / 4)) * 4;
+                if (pos < npos && col < n) {
+                    float acc[4];
+                    bool first = true;
+#pragma unroll
+                    for (int s = 0; s < kMaxRanks; ++s)
+                        if (s < tp && s != me) sum_into(acc, v[i][s], first);
+#pragma unroll
+                    for (int s = 0; s < kMaxRanks; ++s)
+                        if (s == me) sum_into(acc, v[i][s], first);
+                    const long long lr = r0 - me * rpr + pos / (kBN / 4);
+                    store_row<4>(cl, lr * ldc + col, col, n, out_f32, acc);
+                }
             }
         }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int pos = base + u * 128;
-            const int rr = pos / (kBN / 4);
-            const int col = col0 + (pos % (kBN / 4)) * 4;
-            if (pos < npos && col < p.n) {
-                const int grow = row0 + rr;
-                const int o = grow / p.rpr;
-                // Canonical order: the other sources ascending, then the owner's own.
-                float acc[4];
-                bool first = true;
-#pragma unroll
-                for (int s = 0; s < kMaxRanks; ++s)
-                    if (s < p.tp && s != o) sum_into(acc, v[u][s], first);
-#pragma unroll
-                for (int s = 0; s < kMaxRanks; ++s)
-                    if (s == o) sum_into(acc, v[u][s], first);
-                store_row<4>(p.c_rank[o], static_cast<long long>(grow - o * p.rpr) * p.ldc + col, col, p.n, p.out_f32,
-                             acc);
-            }
+    }
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(p.red_exit, 1u) == 2u * gridDim.x - 1u) {
+            atomicExch(p.red_ctr, 0u);
+            atomicExch(p.red_exit, 0u);
         }
     }
 }
@@ -582,6 +613,7 @@ __device__ __forceinline__ float4 epi_read(const uint8_t* wbuf, int i, int g) {
 // Per-variant geometry. CG = CTAs cooperating on one MMA tile: 1 (cta_group::1,
 // 128 x 256 tile per CTA) or 2 (cta_group::2 CTA pair, 256 x 256 tile; each CTA
 // stages half of A (128 rows) and half of B (128 of the 256 N rows)).
+constexpr int kBarRegion = 512;  // mbarriers + TMEM slot + tile queue
 template <int CG, int MODE = kModePlain>
 struct Geo {
     static constexpr int kTileM = kBM * CG;                 // rows of one scheduled tile
@@ -591,8 +623,8 @@ struct Geo {
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagesN = CG == 2 ? 6 : 4;
     static constexpr int kCommBytes = MODE == kModeAG ? 2 * kPieceBytes : 0;  // in-kernel AG staging
-    static constexpr int kEpiBytes = MODE == kModeRS ? 4 * kEpiWarpBytes : 0;  // RS epilogue windows
-    static constexpr int kSmem = kStagesN * kStageBytes + kCommBytes + kEpiBytes + 1024 + 256;
+    static constexpr int kEpiBytes = MODE == kModeRS || MODE == kModeRSLast ? 4 * kEpiWarpBytes : 0;  // RS epilogue windows
+    static constexpr int kSmem = kStagesN * kStageBytes + kCommBytes + kEpiBytes + 1024 + kBarRegion;
     static constexpr uint32_t kIdescV = make_idesc(kTileM, kBN);
 };
 
@@ -683,9 +715,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     uint64_t* qfull = cbar + 2;    // dynamic scheduler: tile queue slots full / empty
     uint64_t* qempty = qfull + kTileQ;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qempty + kTileQ);
-    uint32_t* s_flag = tmem_slot + 1;  // epilogue broadcast (RS last arriver)
-    int* qtile = reinterpret_cast<int*>(s_flag + 1);
-    static_assert((2 * G::kStagesN + 6 + 2 * kTileQ) * 8 + 8 + 4 * kTileQ <= 256, "barrier region");
+    int* qtile = reinterpret_cast<int*>(tmem_slot + 2);
+    int* red_slot = qtile + kTileQ;  // decode RS reduction: unit broadcast per group
+    static_assert((2 * G::kStagesN + 6 + 2 * kTileQ) * 8 + 8 + 4 * kTileQ + 8 <= kBarRegion, "barrier region");
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -862,6 +894,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 }
             }
         }
+    } else if (MODE == kModeRSLast && (warp == 2 || warp == 3)) {
+        // ===== decode RS: owners' reduction, concurrent with the GEMM =====
+        owner_reduce(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
     } else if (warp == 3) {
         // ===== in-kernel AllGather transfer (Alg. 3 on the SMs) =====
         // Lane 0 walks this CTA's share of the piece table: TMA bulk copy
@@ -1131,27 +1166,47 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             } else if (MODE == kModeRSLast) {
                 // Ownership blocks narrower than a tile (decode-sized M): every source
                 // stores its whole partial tile into the owners' staging planes and
-                // bumps the tile's arrival counter; the last of the tp arrivals sums
-                // the tile in the canonical order and writes every owner's rows.
-                // Nobody waits, the result stays deterministic.
+                // stamps flag (tile, source) of each owner in the tile. The owners
+                // sum their rows after their own GEMM work (owner_reduce_phase).
+                // Through the warp's smem window, so each store instruction writes
+                // 4 rows x 128 contiguous bytes.
                 const int me = p.global_rank[l];
                 const uint32_t parity = p.epoch & 1u;
-                const int owner = valid ? row / p.rpr : 0;
-                const long long lrow = row - owner * p.rpr;
                 const int tile_id = tm * p.tiles_n + tn;
-                float* dst = p.staging[owner] + parity * p.stage_parity + me * p.stage_plane + lrow * p.ld_stage;
+                const int rpr = p.rpr;
+                const long long ld_stage = p.ld_stage;
                 for (int c = 0; c < kBN / 32; ++c) {
-                    const int col = col0 + c * 32;
-                    if (col >= p.n) break;
+                    const int colc = col0 + c * 32;
+                    if (colc >= p.n) break;  // warp-uniform
                     uint32_t r[32];
                     tmem_ld32(tbase + c * 32, r);
                     tmem_ld_wait();
-                    if (valid) {
-                        float4* d4 = reinterpret_cast<float4*>(dst + col);
+                    if (p.dbg & 8) continue;  // dbg 8: profiling ablation, no staging stores
+                    if (row0 + q * 32 >= p.m) continue;  // no rows of this warp in range
+                    // A partly valid warp (decode M) stores its rows directly.
+                    if (row0 + q * 32 + 32 > p.m || (p.dbg & 64)) {  // dbg 64: ablation, always direct
+                        if (valid) {
+                            const int o = row / rpr;
+                            float4* d4 = reinterpret_cast<float4*>(p.staging[o] + parity * p.stage_parity + me * p.stage_plane +
+                                                                   (row - static_cast<long long>(o) * rpr) * ld_stage + colc);
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                    __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                            for (int j = 0; j < 32; j += 4)
+                                d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                        }
+                        continue;
+                    }
+                    epi_stage(wbuf, lane, r);
+#pragma unroll
+                    for (int it = 0; it < 8; ++it) {
+                        const int i = it * 4 + (lane >> 3), g = lane & 7;
+                        const int col = colc + g * 4;
+                        const int grow = row0 + q * 32 + i;
+                        if (grow >= p.m || col >= p.n) continue;
+                        const int o = grow / rpr;
+                        float* dst = p.staging[o] + parity * p.stage_parity + me * p.stage_plane +
+                                     (grow - static_cast<long long>(o) * rpr) * ld_stage + col;
+                        *reinterpret_cast<float4*>(dst) = epi_read(wbuf, i, g);
                     }
                 }
                 // The accumulator is in staging now: hand TMEM back to the MMA warp.
@@ -1163,20 +1218,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 }
                 released = true;
                 named_bar_sync(1, 128);
-                if (et == 0) {
-                    trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(row0 / p.rpr));
-                    const uint32_t old = atom_add_acq_rel_sys(p.rs_ctr[row0 / p.rpr] + tile_id, 1u);
-                    *s_flag = ((old + 1u) % static_cast<uint32_t>(p.tp)) == 0u ? 1u : 0u;
-                    if (*s_flag) trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(row0 / p.rpr));
-                }
-                named_bar_sync(1, 128);
-                if (*s_flag) reduce_tile_coalesced(p, row0, col0, parity, et);
-                // Tell each owner in the tile one more of its tiles is final.
-                if (*s_flag) {
-                    named_bar_sync(1, 128);
-                    const int o0 = row0 / p.rpr, o1 = (min(row0 + kBM, p.m) - 1) / p.rpr;
-                    if (et <= o1 - o0) red_release_sys_add(p.rs_done[o0 + et], 1u);
-                }
+                const int o0 = row0 / p.rpr, o1 = (min(row0 + kBM, p.m) - 1) / p.rpr;
+                if (et == 0) trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o0));
+                for (int o = o0 + et; o <= o1; o += 128)
+                    st_release_sys(p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
             } else {
                 const int me = p.global_rank[l];
                 const uint32_t parity = p.epoch & 1u;
@@ -1425,6 +1470,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 aphase ^= 1u;
             }
         }
+        if (MODE == kModeRSLast) owner_reduce(p, et, 128, 4, &red_slot[1]);
     }
 
     if (CG == 2) cluster_sync();

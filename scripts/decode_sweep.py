@@ -70,9 +70,10 @@ for name, (pat, n, k) in shapes.items():
         comm.set_timing(False)
         comm.sync()
         t_b1 = timed(b.unfused)
+        t_local = timed(lambda: comm.local_gemm(p, None, streams))  # the same GEMMs, no communication
         wbytes = 2.0 * n * k  # all ranks' weight shards, streamed once
         row = {"shape": name, "m": m, "tp": tp, "fused_ms": t_fused, "kernel_ms": sorted(kms)[len(kms) // 2],
-               "unfused_ms": t_b1,
+               "unfused_ms": t_b1, "local_gemm_ms": t_local, "overhead_vs_local": t_fused / t_local - 1.0,
                "speedup": t_b1 / t_fused, "hbm_roofline_ms": wbytes / (HBM * 1e9) * 1e3,
                "roofline_frac": (wbytes / (HBM * 1e9) * 1e3) / t_fused}
         rows.append(row)
