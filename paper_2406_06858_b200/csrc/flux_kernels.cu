@@ -684,6 +684,7 @@ struct TileSeq {
     template <int CG>
     __device__ void release(uint64_t* qempty, bool arrive) {
         if (p->dyn_ctr == nullptr) return;
+        __syncwarp(__activemask());  // every lane's read of the slot precedes lane 0's release
         if (!fetcher && arrive) {
             if (CG == 2 && cta_rank != 0) mbar_arrive_cluster(mapa(smem_u32(&qempty[qi]), 0));
             else mbar_arrive(&qempty[qi]);

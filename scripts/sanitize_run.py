@@ -1,5 +1,6 @@
 """Small fused runs for compute-sanitizer (memcheck / racecheck / synccheck):
-AG on both transfer engines, RS chained / owner-sum / last-arriver, FusedReduce,
+AG on both transfer engines, RS chained / owner-sum / decode owner units,
+FusedReduce, the dynamic tile scheduler,
 and the MLP chain, each checked against a cuBLAS product. Usage:
     compute-sanitizer --tool memcheck python scripts/sanitize_run.py"""
 import os
@@ -42,9 +43,18 @@ cases = [("AG copy engines", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM
          ("RS chained (aligned blocks, long sections)", fx.ProblemSpec(4096, 4096, 512, 4, fx.GEMM_REDUCESCATTER), {}),
          ("AG tail split (K-slices)", fx.ProblemSpec(1024, 2048, 512, 8, fx.ALLGATHER_GEMM), dict(ag_engine=1)),
          ("RS owner sum (Naive swizzle)", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
-         ("RS last arriver (decode)", fx.ProblemSpec(64, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
+         ("RS decode (owner reduction units)", fx.ProblemSpec(64, 512, 512, 4, fx.GEMM_REDUCESCATTER), {}),
+         ("RS decode, blocks straddling tiles", fx.ProblemSpec(360, 515, 96, 8, fx.GEMM_REDUCESCATTER), {}),
+         ("AG dynamic scheduler", fx.ProblemSpec(1024, 2048, 512, 8, fx.ALLGATHER_GEMM), dict(env="FLUX_DYN_SCHED")),
+         ("RS dynamic scheduler", fx.ProblemSpec(4096, 4096, 512, 4, fx.GEMM_REDUCESCATTER), dict(env="FLUX_DYN_SCHED")),
          ("RS FusedReduce", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), dict(deterministic_reduce=0))]
 for tag, p, kw in cases:
+    kw = dict(kw)
+    env = kw.pop("env", None)
+    if env:
+        os.environ[env] = "1"
+    else:
+        os.environ.pop("FLUX_DYN_SCHED", None)
     with fx.Communicator(p.tp, [0] * p.tp, heap_bytes=fx.required_heap_bytes(p)) as comm:
         fill(comm, p, 1)
         opts = fx.default_opts(wall_budget_s=120.0, **kw)

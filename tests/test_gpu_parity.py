@@ -66,6 +66,8 @@ CASES = [
     (AG, 8, 8, 8, 1), (AG, 1000, 600, 200, 1),
     (RS, 1024, 512, 256, 4), (RS, 512, 768, 1024, 2), (RS, 40, 24, 72, 4), (RS, 2048, 1024, 512, 8),
     (RS, 192, 300, 96, 2), (RS, 64, 64, 64, 1),
+    # columns not a multiple of 4 / of the tile; decode-sized blocks straddling tiles
+    (RS, 24, 301, 40, 4), (RS, 200, 257, 64, 8), (RS, 360, 515, 96, 8), (AG, 96, 300, 136, 4),
 ]
 
 
