@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FLUX_ABI_VERSION 4
+#define FLUX_ABI_VERSION 5
 
 /* Return codes. The reference raises C++ exceptions (errors.hpp:9-31); each
  * maps to one code. The C++ shim (include/flux/overlap.hpp) rethrows them. */
@@ -100,6 +100,11 @@ typedef struct {
     int b_layout;              /* flux_b_layout of caller-provided B (operands.b): NK = [n/tp or n, k]
                                   (nn.Linear.weight, default) or KN = [k, n] row-major (the reference's
                                   b_shard; no transposed copy needed, e.g. for the backward pass) */
+    int graph_safe;            /* 1: the operator may be captured in a CUDA graph and replayed: it
+                                  zeroes the flags / counters it uses before and after its kernel
+                                  (one small kernel each), so every replay starts from a clean
+                                  state. Single-process communicators; AllGather uses the in-kernel
+                                  transfer engine (no host stream memops); not with FusedReduce. */
 } flux_opts;
 
 typedef enum { FLUX_B_NK = 0, FLUX_B_KN = 1 } flux_b_layout;

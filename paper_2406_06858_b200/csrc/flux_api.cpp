@@ -823,6 +823,7 @@ void flux_default_opts(flux_opts* o) {
     o->activation_grad = FLUX_ACT_NONE;
     o->rs_partials = FLUX_F32;
     o->b_layout = FLUX_B_NK;
+    o->graph_safe = 0;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -1195,13 +1196,108 @@ static int check_activation(flux_comm* c, const flux_problem* p, const flux_opts
     return FLUX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// CUDA-graph-safe operators (flux_opts.graph_safe). Between operators the host
+// tracks device state: epoch-stamped flags, the in-kernel AllGather's monotonic
+// piece counters (targets scale with the operators run since their reset) and
+// the tail-split counters' launch tags. A replayed graph repeats the epoch and
+// targets it was captured with, so a graph-safe operator zeroes the words it
+// uses before its kernel: flags stamped by eager operators since the capture
+// carry later epochs and would satisfy the replay's waits. Nothing is needed
+// afterwards: its stamps carry an epoch older than any later eager operator's,
+// the in-kernel AllGather runs on a separate counter set (kAgCtrGraphOffset,
+// target = one operator's pieces), tail-split tags differ per eager launch and
+// the work counters re-arm themselves. No host stream memops are issued:
+// AllGather runs on the in-kernel transfer engine.
+// ---------------------------------------------------------------------------
+static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
+                        int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands);
+static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
+                        const flux_opts* opts, void* const* streams, const flux_operands* operands);
+static int local_gemm_impl(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams);
+
+static int graph_zero(flux_comm* c, const flux_problem* p, void* const* streams) {
+    ZeroParams z;
+    std::memset(&z, 0, sizeof(z));
+    auto add = [&](size_t off, size_t bytes) {
+        z.off[z.nranges] = static_cast<uint32_t>(off);
+        z.bytes[z.nranges] = static_cast<uint32_t>(bytes);
+        ++z.nranges;
+    };
+    add(kCtrlReady, kCtrlRedExit + 4 - kCtrlReady);  // ready / done / kdone / fr_ready / trace / work counters
+    add(kAgFlagOffset, std::min<size_t>(kAgFlagCap, static_cast<size_t>(p->m)) * 4);
+    add(kAgCtrGraphOffset, (static_cast<size_t>((p->m + kBM - 1) / kBM) + 1) * 4);
+    add(kTailCtrOffset, static_cast<size_t>(kTailCtrCap) * 4);
+    if (p->pattern == FLUX_GEMM_REDUCESCATTER) {
+        const size_t tiles = static_cast<size_t>((p->m + kBM - 1) / kBM) * ((p->n + kBN - 1) / kBN);
+        add(kRsFlagOffset, std::min(kRsFlagCap, tiles * p->tp) * 4);
+    }
+    for (const auto& g : device_groups(c)) {
+        ZeroParams zg = z;
+        for (size_t li = 0; li < g.size(); ++li) zg.heap[li] = c->ranks[g[li]].heap;
+        FLUX_CUDA(cudaSetDevice(c->ranks[g[0]].device));
+        FLUX_CUDA(launch_zero_ranges(zg, static_cast<int>(g.size()), stream_for(c, g[0], streams)));
+    }
+    return FLUX_OK;
+}
+
+// Validates a graph-safe request and returns the options the operator runs with.
+static int graph_opts(flux_comm* c, const flux_problem* p, const flux_opts* opts, int transfer, flux_opts* out) {
+    if (opts) *out = *opts;
+    else flux_default_opts(out);
+    if (!out->graph_safe) return FLUX_OK;
+    FLUX_TRY(check_comm(c));
+    if (!p) return fail(FLUX_ERR_CONFIG, "null problem");
+    if (c->ipc) return fail(FLUX_ERR_CONFIG, "graph_safe operators need every rank in this process");
+    if (p->pattern == FLUX_ALLGATHER_GEMM && transfer >= 0) {
+        if (out->ag_engine == 1 || !ag_sm_engine_ok(p, transfer))
+            return fail(FLUX_ERR_CONFIG, "graph_safe AllGather needs the in-kernel transfer engine (Pull, k % 8 == 0)");
+        out->ag_engine = 2;
+    }
+    return FLUX_OK;
+}
+
+int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer, int swizzle_on,
+                    const flux_opts* opts, void* const* streams, const flux_operands* operands) {
+    flux_opts o;
+    FLUX_TRY(graph_opts(c, p, opts, transfer, &o));
+    if (!o.graph_safe) return ag_gemm_impl(c, p, tile, rpct, transfer, swizzle_on, &o, streams, operands);
+    FLUX_TRY(validate_tiling(p, tile));
+    FLUX_TRY(check_heap(c, p));
+    FLUX_TRY(graph_zero(c, p, streams));
+    return ag_gemm_impl(c, p, tile, rpct, transfer, swizzle_on, &o, streams, operands);
+}
+
+int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
+                    const flux_opts* opts, void* const* streams, const flux_operands* operands) {
+    flux_opts o;
+    FLUX_TRY(graph_opts(c, p, opts, -1, &o));
+    if (!o.graph_safe) return gemm_rs_impl(c, p, tile, write_mode, swizzle_on, &o, streams, operands);
+    if (write_mode == FLUX_FUSED_REDUCE && !o.deterministic_reduce)
+        return fail(FLUX_ERR_CONFIG, "graph_safe is not available with the arrival-order FusedReduce");
+    FLUX_TRY(validate_tiling(p, tile));
+    FLUX_TRY(check_heap(c, p));
+    FLUX_TRY(graph_zero(c, p, streams));
+    return gemm_rs_impl(c, p, tile, write_mode, swizzle_on, &o, streams, operands);
+}
+
+int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
+    flux_opts o;
+    FLUX_TRY(graph_opts(c, p, opts, -1, &o));
+    if (!o.graph_safe) return local_gemm_impl(c, p, &o, streams);
+    FLUX_TRY(validate_problem(p));
+    FLUX_TRY(check_heap(c, p));
+    FLUX_TRY(graph_zero(c, p, streams));
+    return local_gemm_impl(c, p, &o, streams);
+}
+
 int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer, int swizzle_on,
                  const flux_opts* opts, void* const* streams) {
     return flux_ag_gemm_ex(c, p, tile, rpct, transfer, swizzle_on, opts, streams, nullptr);
 }
 
-int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer, int swizzle_on,
-                    const flux_opts* opts, void* const* streams, const flux_operands* operands) {
+static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
+                        int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands) {
     FLUX_TRY(check_comm(c));
     if (p && p->pattern != FLUX_ALLGATHER_GEMM)
         return fail(FLUX_ERR_CONFIG, "run_fused_allgather_gemm requires AllGatherGemm pattern");
@@ -1238,7 +1334,7 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     if (use_sm) {
         const int cg = choose_cg(p, oc.o);
         const int groups = (p->m + kBM - 1) / kBM;
-        const size_t ctr_off = kAgCtrOffset;
+        const size_t ctr_off = oc.o.graph_safe ? kAgCtrGraphOffset : kAgCtrOffset;
         // Piece geometry: whole contiguous rows up to kPieceBytes, or column splits of long rows.
         const int row_bytes = lk * 2;
         int piece_rows = 1, pieces_per_row = (row_bytes + kPieceBytes - 1) / kPieceBytes;
@@ -1259,7 +1355,8 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
         const uint64_t sig = (static_cast<uint64_t>(p->m) << 40) ^ (static_cast<uint64_t>(lk) << 16) ^
                              (static_cast<uint64_t>(piece_rows) << 8) ^ static_cast<uint64_t>(pieces_per_row) ^
                              (static_cast<uint64_t>(tp) << 60);
-        const bool reset = c->ag_sig != sig || c->ag_mult > (1u << 30) / std::max(1, kBM * pieces_per_row);
+        const bool graph = oc.o.graph_safe != 0;  // own counter set, zeroed by graph_zero: target x1
+        const bool reset = !graph && (c->ag_sig != sig || c->ag_mult > (1u << 30) / std::max(1, kBM * pieces_per_row));
         for (int r : mine) {
             RankState& rs = c->ranks[r];
             FLUX_CUDA(cudaSetDevice(rs.device));
@@ -1288,7 +1385,7 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
             c->ag_sig = sig;
             c->ag_mult = 0;
         }
-        const uint32_t mult = ++c->ag_mult;
+        const uint32_t mult = graph ? 1u : ++c->ag_mult;
         std::vector<std::vector<uint32_t>> seq(tp);
         std::vector<std::vector<int>> blocks(tp);
         for (int r : mine) {
@@ -1553,8 +1650,8 @@ int flux_gemm_rs(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
     return flux_gemm_rs_ex(c, p, tile, write_mode, swizzle_on, opts, streams, nullptr);
 }
 
-int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
-                    const flux_opts* opts, void* const* streams, const flux_operands* operands) {
+static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
+                        const flux_opts* opts, void* const* streams, const flux_operands* operands) {
     FLUX_TRY(check_comm(c));
     if (p && p->pattern != FLUX_GEMM_REDUCESCATTER)
         return fail(FLUX_ERR_CONFIG, "run_fused_gemm_reducescatter requires GemmReduceScatter pattern");
@@ -1641,7 +1738,7 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     return mark_op_done(c, streams, c->epoch);
 }
 
-int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
+static int local_gemm_impl(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
     FLUX_TRY(check_comm(c));
     FLUX_TRY(validate_problem(p));
     FLUX_TRY(check_heap(c, p));
@@ -1664,6 +1761,7 @@ int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
 
 int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
     FLUX_TRY(check_comm(c));
+    if (opts && opts->graph_safe) return fail(FLUX_ERR_CONFIG, "graph_safe applies to the fused operators and the local GEMM");
     FLUX_TRY(validate_problem(p));
     FLUX_TRY(check_heap(c, p));
     const int tp = p->tp, rpr = rows_per_rank(p), lk = local_k(p);

@@ -57,7 +57,10 @@ constexpr int kTailCtrCap = 256;
 constexpr int kTailMaxSplits = 8;
 constexpr int kTailWsCtas = 160;  // workspace slots (>= CTAs of one launch): 128 x 256 fp32 each
 constexpr size_t kAgCtrOffset = 128 * 1024;
-constexpr size_t kAgGroupCap = 32768;
+constexpr size_t kAgGroupCap = 16384;  // per counter set
+// Graph-safe operators use their own counter set (zeroed by each of them), so
+// replays never disturb the eager operators' monotonic counters.
+constexpr size_t kAgCtrGraphOffset = kAgCtrOffset + kAgGroupCap * 4;
 constexpr int kPieceBytes = 16384;      // one TMA bulk copy (global -> smem -> global)
 constexpr size_t kRsFlagOffset = 256 * 1024;  // u32[tile][src]: partial of tile from src landed
 constexpr size_t kRsFlagCap = (512 * 1024) / 4;
@@ -158,5 +161,16 @@ struct RsReduceParams {
 cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStream_t stream);
 int gemm_tile_rows(int cg);
 cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t stream);
+
+// Graph-safe operators: zero byte ranges (4-byte multiples) of several heaps,
+// one CTA per heap.
+constexpr int kZeroMaxRanges = 8;
+struct ZeroParams {
+    char* heap[kMaxRanks];
+    uint32_t off[kZeroMaxRanges];
+    uint32_t bytes[kZeroMaxRanges];
+    int nranges;
+};
+cudaError_t launch_zero_ranges(const ZeroParams& p, int nheaps, cudaStream_t stream);
 
 }  // namespace fluxb200

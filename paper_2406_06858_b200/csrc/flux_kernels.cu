@@ -1500,6 +1500,19 @@ __global__ void rs_reduce_kernel(RsReduceParams p) {
     }
 }
 
+__global__ void zero_ranges_kernel(ZeroParams p) {
+    char* h = p.heap[blockIdx.x];
+    for (int r = 0; r < p.nranges; ++r) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(h + p.off[r]);
+        for (uint32_t i = threadIdx.x; i < p.bytes[r] / 4; i += blockDim.x) w[i] = 0u;
+    }
+}
+
+cudaError_t launch_zero_ranges(const ZeroParams& p, int nheaps, cudaStream_t stream) {
+    zero_ranges_kernel<<<nheaps, 512, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t stream) {
     rs_reduce_kernel<<<grid, 256, 0, stream>>>(p);
     return cudaGetLastError();
