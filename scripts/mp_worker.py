@@ -35,7 +35,8 @@ results = {}
 cases = [(fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 1), (fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 2),
          (fx.ALLGATHER_GEMM, 16 * world, 256 * world, 1024, 0), (fx.GEMM_REDUCESCATTER, 512 * world, 768, 256 * world, 0),
          (fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 3), (fx.GEMM_REDUCESCATTER, 512 * world, 768, 256 * world, 1),
-         (fx.GEMM_REDUCESCATTER, 512 * world, 768, 256 * world, 2)]
+         (fx.GEMM_REDUCESCATTER, 512 * world, 768, 256 * world, 2),
+         (fx.GEMM_REDUCESCATTER, 40 * world, 300, 64 * world, 0)]  # decode-sized blocks: owner reduction units
 heap = max(fx.required_heap_bytes(fx.ProblemSpec(m, n, k, world, pat)) for pat, m, n, k, _ in cases) + (8 << 20)
 comm = fx.Communicator.ipc(rank, world, dev, heap, gather)
 for pat, m, n, k, engine in cases:
