@@ -901,15 +901,55 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     } else if (warp == 3) {
         // ===== in-kernel AllGather transfer (Alg. 3 on the SMs) =====
         // Lane 0 walks this CTA's share of the piece table: TMA bulk copy
-        // global -> smem -> global (two buffers in flight), then a release
-        // increment of the destination group's counter. Remote pieces first
-        // wait until the source rank's own slot of a_agg is complete.
+        // global -> smem -> global through two buffers, then a release
+        // increment of the destination group's counter. Two loads are in
+        // flight: piece i+1 is loaded while piece i is stored (a buffer is
+        // reloaded once the store that used it has read it), and a piece is
+        // published once its store has completed. Remote pieces first wait until
+        // the source rank's own slot of a_agg is complete.
         if (MODE == kModeAG && p.sm_transfer && lane == 0) {
+            struct Piece {
+                const char* src;
+                char* dst;
+                uint32_t bytes;
+                uint32_t* ctr;
+                uint32_t* slot_ctr;
+                int meta;  // (slot << 16) | group, for the trace
+                int buf;
+            };
             uint32_t phase[2] = {0u, 0u};
-            uint32_t* pend[2] = {nullptr, nullptr};
-            uint32_t* pend_slot[2] = {nullptr, nullptr};
-            int pend_meta[2] = {0, 0};  // (slot << 16) | group, for the trace
-            int it = 0;
+            Piece ld[2] = {};  // loads in flight, oldest first
+            int nld = 0;
+            Piece st[2] = {};  // stored, awaiting completion + publication, oldest first
+            int nst = 0;
+            int nb = 0;   // buffer of the next load
+            auto publish = [&](const Piece& P) {
+                if (P.ctr) ag_signal(p, P.ctr, P.meta);
+                if (P.slot_ctr) red_release_gpu_add(P.slot_ctr, 1u);
+            };
+            auto store_oldest = [&]() {  // wait for the oldest load, store it
+                const Piece P = ld[0];
+                mbar_wait(&cbar[P.buf], phase[P.buf]);
+                phase[P.buf] ^= 1u;
+                bulk_store(P.dst, sComm + P.buf * kPieceBytes, P.bytes);
+                ld[0] = ld[1];
+                --nld;
+                if (nst == 2) {  // keep at most two stores outstanding: publish the older
+                    bulk_wait_group<1>();
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    publish(st[0]);
+                    st[0] = st[1];
+                    nst = 1;
+                }
+                st[nst++] = P;
+            };
+            auto drain = [&]() {  // everything in flight stored, completed and published
+                while (nld > 0) store_oldest();
+                bulk_wait_group<0>();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                for (int i = 0; i < nst; ++i) publish(st[i]);
+                nst = 0;
+            };
             int checked_src = -1;
             for (int j = blockIdx.x; j < p.num_jobs; j += gridDim.x) {
                 const uint32_t e = p.jobs[j];
@@ -928,14 +968,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     if (q != checked_src) {
                         // Publish everything in flight before blocking: another CTA may be
                         // waiting for our own-block pieces (no wait may hold a signal).
-                        bulk_wait_group<0>();
-                        asm volatile("fence.proxy.async.global;" ::: "memory");
-                        for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) {
-                            if (pend[k2 & 1]) ag_signal(p, pend[k2 & 1], pend_meta[k2 & 1]);
-                            if (pend_slot[k2 & 1]) red_release_gpu_add(pend_slot[k2 & 1], 1u);
-                            pend[k2 & 1] = nullptr;
-                            pend_slot[k2 & 1] = nullptr;
-                        }
+                        drain();
                         // The source's own slot (its shard copied into its a_agg) is complete.
                         wait_flag(p.ag_ctr[q] + p.ag_slot_index, p.ag_mult * p.slot_pieces, p, p.ctrl[l],
                                   kErrAgFlagTimeout, static_cast<uint32_t>(p.ag_slot_index),
@@ -946,40 +979,28 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     src = p.agg_src[q] + static_cast<long long>(row0) * p.dst_ld_bytes;
                 }
                 char* dst = p.a_dst[l] + static_cast<long long>(row0) * p.dst_ld_bytes;
-                uint32_t* ctr = p.ag_ctr[me] + g;
-                uint32_t* slot_ctr = q == me ? p.ag_ctr[me] + p.ag_slot_index : nullptr;
                 const int npieces = p.piece_rows > 1 ? 1 : p.pieces_per_row;
                 for (int c = 0; c < npieces; ++c) {
                     const int off = c * kPieceBytes;
-                    const uint32_t bytes = p.piece_rows > 1
-                                               ? static_cast<uint32_t>(p.piece_rows * p.row_bytes)
+                    Piece P;
+                    P.src = src + off;
+                    P.dst = dst + off;
+                    P.bytes = p.piece_rows > 1 ? static_cast<uint32_t>(p.piece_rows * p.row_bytes)
                                                : static_cast<uint32_t>(min(kPieceBytes, p.row_bytes - off));
-                    const int b = it & 1;
-                    if (it >= 2) {
-                        // The store that last used buffer b is complete: publish its piece.
-                        bulk_wait_group<1>();
-                        asm volatile("fence.proxy.async.global;" ::: "memory");
-                        if (pend[b]) ag_signal(p, pend[b], pend_meta[b]);
-                        if (pend_slot[b]) red_release_gpu_add(pend_slot[b], 1u);
-                    }
-                    uint8_t* buf = sComm + b * kPieceBytes;
-                    mbar_expect_tx(&cbar[b], bytes);
-                    bulk_load(buf, src + off, bytes, &cbar[b]);
-                    mbar_wait(&cbar[b], phase[b]);
-                    phase[b] ^= 1u;
-                    bulk_store(dst + off, buf, bytes);
-                    pend[b] = ctr;
-                    pend_slot[b] = slot_ctr;
-                    pend_meta[b] = (l << 16) | g;
-                    ++it;
+                    P.ctr = p.ag_ctr[me] + g;
+                    P.slot_ctr = q == me ? p.ag_ctr[me] + p.ag_slot_index : nullptr;
+                    P.meta = (l << 16) | g;
+                    P.buf = nb;
+                    if (nld == 2) store_oldest();  // frees nothing yet: its buffer is read by the store
+                    // The last store that used this buffer has read it.
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    mbar_expect_tx(&cbar[nb], P.bytes);
+                    bulk_load(sComm + nb * kPieceBytes, P.src, P.bytes, &cbar[nb]);
+                    ld[nld++] = P;
+                    nb ^= 1;
                 }
             }
-            bulk_wait_group<0>();
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            for (int k2 = (it >= 2 ? it - 2 : 0); k2 < it; ++k2) {
-                if (pend[k2 & 1]) ag_signal(p, pend[k2 & 1], pend_meta[k2 & 1]);
-                if (pend_slot[k2 & 1]) red_release_gpu_add(pend_slot[k2 & 1], 1u);
-            }
+            drain();
         }
     } else if (warp >= 4) {
         // ===== epilogue: each CTA drains its own 128 TMEM lanes (rows) =====
