@@ -251,21 +251,22 @@ def test_shape_and_config_errors():
             comm.ag_gemm(fx.ProblemSpec(8192, 8192, 8192, 4, AG), fx.TileShape(16, 16))
 
 
-FULL_SIZE = {  # BASELINE.json configs (TP=8): Llama-2-70B MLP, GPT-3 175B MLP, decode M=16 / 512
-    "llama-ag": (AG, 4096, 28672, 8192), "llama-rs": (RS, 4096, 8192, 28672),
-    "gpt3-ag": (AG, 8192, 49152, 12288), "gpt3-rs": (RS, 8192, 12288, 49152),
-    "decode-ag-m16": (AG, 16, 28672, 8192), "decode-rs-m512": (RS, 512, 8192, 28672),
+FULL_SIZE = {  # BASELINE.json configs: Llama-2-70B MLP (TP=8, RS also TP=2/4), GPT-3 175B MLP, decode M=16 / 512
+    "llama-ag": (AG, 4096, 28672, 8192, 8), "llama-rs": (RS, 4096, 8192, 28672, 8),
+    "llama-rs-tp4": (RS, 4096, 8192, 28672, 4), "llama-rs-tp2": (RS, 4096, 8192, 28672, 2),
+    "gpt3-ag": (AG, 8192, 49152, 12288, 8), "gpt3-rs": (RS, 8192, 12288, 49152, 8),
+    "decode-ag-m16": (AG, 16, 28672, 8192, 8), "decode-rs-m512": (RS, 512, 8192, 28672, 8),
 }
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name", list(FULL_SIZE))
 def test_full_size_tp8_row_sampled(name):
-    """BASELINE configs at full size (TP=8 emulated on one GPU), checked on
+    """BASELINE configs at full size (ranks emulated on one GPU), checked on
     sampled rows: >= 1 row per (rank, row block) for AG, 2 owned rows per rank
     for RS, against the fp64 oracle on the same bf16 inputs."""
-    pattern, m, n, k = FULL_SIZE[name]
-    p = fx.ProblemSpec(m, n, k, 8, pattern)
+    pattern, m, n, k, tp = FULL_SIZE[name]
+    p = fx.ProblemSpec(m, n, k, tp, pattern)
     with H.make_comm(p) as comm:
         a, b = H.upload(comm, p, seed=42)
         got = _run(comm, p, False)
