@@ -90,7 +90,7 @@ typedef struct {
                                   RS own blocks last), 1 position-major across ranks */
     int cta_group;             /* 0 auto, 1 = 128x256 tiles per CTA, 2 = CTA pairs (256x256, cta_group::2) */
     int ag_engine;             /* AllGather transfers: 0 auto, 1 copy engines (stream memcpy + flag
-                                  writes), 2 in-kernel (TMA bulk copies by the GEMM's SMs, Pull) */
+                                  writes), 2 in-kernel (TMA bulk copies by the GEMM's SMs, Pull or Push) */
     int trace;                 /* 1: record the device event trace of the next operators (flux_trace_read) */
     int activation;            /* flux_activation fused into the AllGather-GEMM / local GEMM epilogue */
     int activation_grad;       /* flux_activation whose derivative scales C: C = acc * act'(aux) */

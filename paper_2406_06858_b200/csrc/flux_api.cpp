@@ -734,6 +734,8 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             }
         }
         if (extra) FLUX_TRY(extra(g, prm));
+        // Flag producers all on this GPU's SMs (not the copy engines): gpu-scope acquires.
+        prm.all_local = static_cast<int>(g.size()) == p->tp && (mode != kModeAG || prm.sm_transfer) ? 1 : 0;
         // Tail split (Plain / AG): a persistent grid of W clusters runs T tiles in
         // ceil(T / W) waves; the last T mod W tiles would leave most clusters
         // idle for a whole tile, so each runs as S <= 8 K-slices instead.
@@ -1135,7 +1137,8 @@ static int check_heap(flux_comm* c, const flux_problem* p) {
 
 // AllGather transfer engine: 1 copy engines, 2 in-kernel (the GEMM's SMs).
 static bool ag_sm_engine_ok(const flux_problem* p, int transfer) {
-    return transfer == FLUX_PULL && local_k(p) % 8 == 0 && (p->m + kBM - 1) / kBM < static_cast<int>(kAgGroupCap);
+    return (transfer == FLUX_PULL || transfer == FLUX_PUSH) && local_k(p) % 8 == 0 &&
+           (p->m + kBM - 1) / kBM < static_cast<int>(kAgGroupCap);
 }
 static int ag_engine_for(const flux_problem* p, int transfer, int requested, int rpct = 0, int ranks_per_device = 1) {
     if (requested == 1 || requested == 2) return requested;
@@ -1251,7 +1254,7 @@ static int graph_opts(flux_comm* c, const flux_problem* p, const flux_opts* opts
     if (c->ipc) return fail(FLUX_ERR_CONFIG, "graph_safe operators need every rank in this process");
     if (p->pattern == FLUX_ALLGATHER_GEMM && transfer >= 0) {
         if (out->ag_engine == 1 || !ag_sm_engine_ok(p, transfer))
-            return fail(FLUX_ERR_CONFIG, "graph_safe AllGather needs the in-kernel transfer engine (Pull, k % 8 == 0)");
+            return fail(FLUX_ERR_CONFIG, "graph_safe AllGather needs the in-kernel transfer engine (k % 8 == 0)");
         out->ag_engine = 2;
     }
     return FLUX_OK;
@@ -1327,7 +1330,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     // ---- transfer engine: copy engines (Alg. 3 on a stream) or the GEMM's own
     // SMs (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies) ----
     if (oc.o.ag_engine == 2 && !ag_sm_engine_ok(p, transfer))
-        return fail(FLUX_ERR_CONFIG, "in-kernel AllGather transfer needs Pull and k % 8 == 0");
+        return fail(FLUX_ERR_CONFIG, "in-kernel AllGather transfer needs Pull or Push and k % 8 == 0");
     size_t per_dev = 1;
     for (const auto& dg : device_groups(c)) per_dev = std::max(per_dev, dg.size());
     const bool use_sm = ag_engine_for(p, transfer, oc.o.ag_engine, rpct, static_cast<int>(per_dev)) == 2;
@@ -1396,6 +1399,10 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
                                      group_blocks(rpr, kBM * cg, /*ag=*/true));
         }
         const bool step_major = oc.o.emulated_order == 1;
+        const bool push = transfer == FLUX_PUSH;
+        std::vector<std::vector<int>> blocks_all(tp);  // every rank's consumption order (Push tables)
+        if (push)
+            for (int q = 0; q < tp; ++q) blocks_all[q] = ag_block_order(p, q, FLUX_PULL, true, rpct);
         auto extra = [&](const std::vector<int>& g, GemmParams& prm) -> int {
             // Piece table in consumption order: every slot's own block first (peers
             // copy from it), then the others in the order the tiles need them.
@@ -1411,7 +1418,23 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
             for (int q = 0; q < kMaxRanks; ++q) prm.slot_of[q] = -1;
             for (size_t li = 0; li < g.size(); ++li) prm.slot_of[g[li]] = static_cast<int>(li);
             for (int q = 0; q < tp; ++q) all_local = all_local && prm.slot_of[q] >= 0;
-            if (step_major || !all_local) {
+            if (push) {
+                // Push: each local source copies its own block into every destination.
+                auto add_push = [&](int src_rank, int q) {
+                    for (int row = src_rank * rpr; row < (src_rank + 1) * rpr; row += piece_rows)
+                        jobs.push_back((uint32_t(prm.slot_of[src_rank]) << 28) | (uint32_t(q) << 24) | uint32_t(row));
+                };
+                if (all_local) {
+                    // Every source in this launch: follow the kernel's consumption order
+                    // (destinations rank-major, each in its own block order).
+                    for (size_t li = 0; li < g.size(); ++li)
+                        for (int step = 0; step < tp; ++step) add_push(blocks_all[g[li]][step], g[li]);
+                } else {
+                    // The ring (reference push order, engine.cpp:86-95): own a_agg first.
+                    for (size_t li = 0; li < g.size(); ++li)
+                        for (int k2 = 0; k2 < tp; ++k2) add_push(g[li], (g[li] + k2) % tp);
+                }
+            } else if (step_major || !all_local) {
                 for (size_t li = 0; li < g.size(); ++li) add_block(static_cast<int>(li), g[li]);
                 if (step_major) {
                     for (int step = 1; step < tp; ++step)
@@ -1427,6 +1450,8 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
             uint32_t* jobs_dev = nullptr;
             FLUX_TRY(upload_order(c, c->ranks[g[0]].device, jobs, &jobs_dev));
             prm.sm_transfer = 1;
+            prm.ag_push = push ? 1 : 0;
+            for (int q = 0; q < tp; ++q) prm.kdone[q] = at<uint32_t>(c->ranks[q], kCtrlKdone);
             prm.jobs = jobs_dev;
             prm.num_jobs = static_cast<int>(jobs.size());
             prm.piece_rows = piece_rows;

@@ -112,11 +112,18 @@ struct GemmParams {
     const char* agg_src[kMaxRanks];    // per GLOBAL rank: its a_agg (peer pointers; pull source)
     const char* shard_src[kMaxRanks];  // per local slot: its own A shard (local piece source)
     int slot_of[kMaxRanks];        // per GLOBAL rank: its local slot in this launch (same device), else -1
+    int all_local;                 // every rank runs in this launch: flag producers are on this GPU
     char* a_dst[kMaxRanks];            // per local slot: its a_agg
     uint32_t* ag_ctr[kMaxRanks];   // per GLOBAL rank: monotonic piece counters (peer pointers)
     int ag_slot_index;             // counter index of "own block copied" (after the group counters)
     uint32_t slot_pieces;          // pieces of one rank's own block
     uint32_t ag_mult;              // operators run on these counters since their last reset (targets scale by it)
+    // Push (engine.cpp:406-419 on the SMs): jobs carry (source slot, DESTINATION rank,
+    // rows); a source copies its own block into every destination's a_agg and
+    // bumps the destination's counter. A destination in another process is
+    // written only after its previous operator's kernel finished (kdone).
+    int ag_push;
+    const uint32_t* kdone[kMaxRanks];  // per GLOBAL rank: kernel-done epoch word (peer pointers)
     // RS with ownership blocks narrower than a tile: owners reduce during the GEMM
     int rs_last_arriver;
     uint32_t* red_ctr;             // reduction unit counter (lead rank's control block)

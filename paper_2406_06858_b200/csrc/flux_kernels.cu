@@ -231,6 +231,15 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// RS partial-landed flag of owner `o`: gpu scope when the owner runs in this
+// launch (same device), system scope for a peer GPU.
+__device__ __forceinline__ void rs_flag_set(const GemmParams& p, int o, uint32_t* f, uint32_t v) {
+    if (p.slot_of[o] >= 0 && !(p.dbg & 512)) st_release_gpu(f, v);  // dbg 512: ablation, always sys
+    else st_release_sys(f, v);
+}
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -285,6 +294,9 @@ template <int N>
 __device__ __forceinline__ void bulk_wait_group() {
     asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -298,15 +310,25 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 
 // Bounded spin (reference spin_wait, engine.cpp:149-162): epoch-stamped flag
 // reaches `target`, or the timeout records an error naming the flag.
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Every producer of this launch's flags on this GPU (all ranks in one launch):
+// gpu-scope acquires suffice.
+__device__ __forceinline__ uint32_t ld_acquire_flag(const GemmParams& p, const uint32_t* f) {
+    return p.all_local && !(p.dbg & 512) ? ld_acquire_gpu(f) : ld_acquire_sys(f);
+}
 __device__ bool wait_flag(const uint32_t* flag, uint32_t target, const GemmParams& p,
                           uint32_t* ctrl, uint32_t code, uint32_t info0, uint32_t info1) {
-    if (static_cast<int32_t>(ld_acquire_sys(flag) - target) >= 0) return true;
+    if (static_cast<int32_t>(ld_acquire_flag(p, flag) - target) >= 0) return true;
     const uint64_t t0 = globaltimer();
     uint32_t ns = 32;
     for (;;) {
         __nanosleep(ns);
         if (ns < 2048) ns <<= 1;
-        if (static_cast<int32_t>(ld_acquire_sys(flag) - target) >= 0) return true;
+        if (static_cast<int32_t>(ld_acquire_flag(p, flag) - target) >= 0) return true;
         if (globaltimer() - t0 > p.timeout_ns) {
             if (atomicCAS(ctrl + 0, 0u, code) == 0u) {
                 ctrl[1] = info0;
@@ -915,6 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 uint32_t* ctr;
                 uint32_t* slot_ctr;
                 int meta;  // (slot << 16) | group, for the trace
+                int dest;  // Push: the destination rank (the reference's signal_set target)
                 int buf;
             };
             uint32_t phase[2] = {0u, 0u};
@@ -924,7 +947,16 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             int nst = 0;
             int nb = 0;   // buffer of the next load
             auto publish = [&](const Piece& P) {
-                if (P.ctr) ag_signal(p, P.ctr, P.meta);
+                if (P.ctr) {
+                    if (p.ag_push) {  // the destination's counter, possibly on another GPU
+                        trace_event(p, P.meta >> 16, kEvSignalSet, p.global_rank[P.meta >> 16], P.meta & 0xFFFF, 0,
+                                    static_cast<uint32_t>(P.dest));
+                        if (p.slot_of[P.dest] >= 0) red_release_gpu_add(P.ctr, 1u);
+                        else red_release_sys_add(P.ctr, 1u);
+                    } else {
+                        ag_signal(p, P.ctr, P.meta);
+                    }
+                }
                 if (P.slot_ctr) red_release_gpu_add(P.slot_ctr, 1u);
             };
             auto store_oldest = [&]() {  // wait for the oldest load, store it
@@ -958,6 +990,26 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 const int me = p.global_rank[l];
                 const int g = row0 / kBM;
                 const char* src;
+                char* dst;
+                uint32_t* ctr;
+                uint32_t* slot_ctr = nullptr;
+                if (p.ag_push) {
+                    // q = destination: my own rows go to its a_agg and count there.
+                    if (p.slot_of[q] < 0 && q != checked_src) {
+                        drain();  // (no wait may hold a signal)
+                        wait_flag(p.kdone[q], p.epoch - 1u, p, p.ctrl[l], kErrAgFlagTimeout,
+                                  static_cast<uint32_t>(p.ag_slot_index), 0xFFFE0000u | static_cast<uint32_t>(q));
+                        checked_src = q;
+                    }
+                    src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
+                    dst = const_cast<char*>(p.agg_src[q]) + static_cast<long long>(row0) * p.dst_ld_bytes;
+                    ctr = p.ag_ctr[q] + g;
+                    // Keep the own-slot counter in step with Pull operators' targets.
+                    if (q == me) slot_ctr = p.ag_ctr[me] + p.ag_slot_index;
+                } else {
+                dst = p.a_dst[l] + static_cast<long long>(row0) * p.dst_ld_bytes;
+                ctr = p.ag_ctr[me] + g;
+                slot_ctr = q == me ? p.ag_ctr[me] + p.ag_slot_index : nullptr;
                 if (q == me) {
                     src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
                 } else if (p.slot_of[q] >= 0) {
@@ -978,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     }
                     src = p.agg_src[q] + static_cast<long long>(row0) * p.dst_ld_bytes;
                 }
-                char* dst = p.a_dst[l] + static_cast<long long>(row0) * p.dst_ld_bytes;
+                }  // pull
                 const int npieces = p.piece_rows > 1 ? 1 : p.pieces_per_row;
                 for (int c = 0; c < npieces; ++c) {
                     const int off = c * kPieceBytes;
@@ -987,9 +1039,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     P.dst = dst + off;
                     P.bytes = p.piece_rows > 1 ? static_cast<uint32_t>(p.piece_rows * p.row_bytes)
                                                : static_cast<uint32_t>(min(kPieceBytes, p.row_bytes - off));
-                    P.ctr = p.ag_ctr[me] + g;
-                    P.slot_ctr = q == me ? p.ag_ctr[me] + p.ag_slot_index : nullptr;
+                    P.ctr = ctr;
+                    P.slot_ctr = slot_ctr;
                     P.meta = (l << 16) | g;
+                    P.dest = q;
                     P.buf = nb;
                     if (nld == 2) store_oldest();  // frees nothing yet: its buffer is read by the store
                     // The last store that used this buffer has read it.
@@ -1243,7 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 const int o0 = row0 / p.rpr, o1 = (min(row0 + kBM, p.m) - 1) / p.rpr;
                 if (et == 0) trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o0));
                 for (int o = o0 + et; o <= o1; o += 128)
-                    st_release_sys(p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
+                    rs_flag_set(p, o, p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
             } else {
                 const int me = p.global_rank[l];
                 const uint32_t parity = p.epoch & 1u;
@@ -1319,7 +1372,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     named_bar_sync(1, 128);
                     if (!closes && et == 0) {
                         trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o));
-                        st_release_sys(p.rs_flags[o] + tile_id * tp + me, p.epoch);
+                        rs_flag_set(p, o, p.rs_flags[o] + tile_id * tp + me, p.epoch);
                     }
                 } else {
                 if (p.fused_reduce) {
@@ -1379,7 +1432,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     const int o = o0 + et;
                     if (o != me) {
                         trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o));
-                        st_release_sys(p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
+                        rs_flag_set(p, o, p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
                     }
                 }
                 // Phase 2: owned rows = sum of all partials in the canonical order.

@@ -133,8 +133,6 @@ def enumerate_knobs(problem: ProblemSpec, knobs: KnobSpace) -> List[TuneConfig]:
                     for sw in knobs.swizzle_policies:
                         for cg in knobs.cta_groups:
                             for eng in knobs.ag_engines:
-                                if eng == 2 and tm != N.PULL:
-                                    continue  # the in-kernel engine pulls
                                 grid.append(TuneConfig(tile, sw, c, tm, N.FUSED_REDUCE, cg, eng))
         else:
             for wm in knobs.write_modes:

@@ -3,7 +3,7 @@
 configuration per round, L2 flushed before each, medians over the rounds — so
 clock / power drift biases no configuration (profiling aid).
 
-    python scripts/ab_env.py --workload llama70b-up-ag --cfg "" --cfg FLUX_GROUP_BLOCKS=2 --cfg opt:ag_engine=2
+    python scripts/ab_env.py --workload llama70b-up-ag --cfg "" --cfg FLUX_GROUP_BLOCKS=2 --cfg opt:ag_engine=2,push=1
 """
 import argparse
 import os
@@ -41,9 +41,12 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 
 def make(cfg):
     env, opt = {}, {}
+    push = False
     for kv in filter(None, cfg.split(",")):
         key, val = kv.split("=", 1)
-        if key.startswith("opt:"):
+        if key == "push":  # AllGather transfer mode
+            push = val == "1"
+        elif key.startswith("opt:"):
             opt[key[4:]] = int(val)
         else:
             env[key] = val
@@ -55,7 +58,7 @@ def make(cfg):
         if args.op == "local":
             comm.local_gemm(p, o, st)
         elif pattern == fx.ALLGATHER_GEMM:
-            comm.ag_gemm(p, tile, p.rows_per_rank(), fx.PULL, True, o, st)
+            comm.ag_gemm(p, tile, p.rows_per_rank(), fx.PUSH if push else fx.PULL, True, o, st)
         else:
             comm.gemm_rs(p, tile, fx.WRITE_ALLTOALL, True, o, st)
         for key, old in saved.items():

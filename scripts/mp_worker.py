@@ -30,13 +30,15 @@ def gather(blob):
 
 
 results = {}
-# (pattern, m, n, k, variant): AG variant = engine (0 auto, 1 copy engines, 2 in-kernel, 3 copy-engine Push);
+# (pattern, m, n, k, variant): AG variant = engine (0 auto, 1 copy engines, 2 in-kernel, 3 copy-engine Push,
+# 4 in-kernel Push);
 # RS variant = 0 WriteAlltoAll, 1 FusedReduce (arrival order), 2 WriteAlltoAll with bf16 partials
 cases = [(fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 1), (fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 2),
          (fx.ALLGATHER_GEMM, 16 * world, 256 * world, 1024, 0), (fx.GEMM_REDUCESCATTER, 512 * world, 768, 256 * world, 0),
          (fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 3), (fx.GEMM_REDUCESCATTER, 512 * world, 768, 256 * world, 1),
          (fx.GEMM_REDUCESCATTER, 512 * world, 768, 256 * world, 2),
-         (fx.GEMM_REDUCESCATTER, 40 * world, 300, 64 * world, 0)]  # decode-sized blocks: owner reduction units
+         (fx.GEMM_REDUCESCATTER, 40 * world, 300, 64 * world, 0),  # decode-sized blocks: owner reduction units
+         (fx.ALLGATHER_GEMM, 256 * world, 512 * world, 384, 4)]  # in-kernel Push into the peers' a_agg
 heap = max(fx.required_heap_bytes(fx.ProblemSpec(m, n, k, world, pat)) for pat, m, n, k, _ in cases) + (8 << 20)
 comm = fx.Communicator.ipc(rank, world, dev, heap, gather)
 for pat, m, n, k, engine in cases:
@@ -47,12 +49,13 @@ for pat, m, n, k, engine in cases:
     torch.cuda.synchronize()
     dist.barrier()
     ag = pat == fx.ALLGATHER_GEMM
-    opts = fx.default_opts(out_dtype=fx.F32, wall_budget_s=20.0, ag_engine=(1 if engine == 3 else engine) if ag else 0,
+    opts = fx.default_opts(out_dtype=fx.F32, wall_budget_s=20.0,
+                           ag_engine={3: 1, 4: 2}.get(engine, engine) if ag else 0,
                            deterministic_reduce=0 if (not ag and engine == 1) else 1,
                            rs_partials=fx.BF16 if (not ag and engine == 2) else fx.F32)
     for it in range(3):
         if ag:
-            comm.ag_gemm(p, fx.TileShape(p.rows_per_rank(), p.local_cols()), 0, fx.PUSH if engine == 3 else fx.PULL,
+            comm.ag_gemm(p, fx.TileShape(p.rows_per_rank(), p.local_cols()), 0, fx.PUSH if engine >= 3 else fx.PULL,
                          True, opts)
         else:
             comm.gemm_rs(p, fx.TileShape(p.rows_per_rank(), p.local_cols()),

@@ -132,15 +132,17 @@ def test_allgather_comm_tile_sizes_and_transfer_modes(tp, rpct):
         a, b = H.upload(comm, p, seed=7)
         want = _oracle(p, a, b)
         outs = {}
-        for transfer in (fx.PULL, fx.PUSH):
-            for swizzle in (True, False):
-                got = _run(comm, p, True, transfer=transfer, swizzle=swizzle, rpct=rpct)
-                outs[(transfer, swizzle)] = got
-                for r in range(tp):
-                    assert O.max_rel_error(got[r], want[r]) <= H.tol(True, p.k)
-        # push == pull bitwise (test_engine.cpp:63-74): same GEMM, same inputs
+        for engine in (1, 2):  # copy engines, in-kernel (SM) transfers
+            for transfer in (fx.PULL, fx.PUSH):
+                for swizzle in (True, False):
+                    got = _run(comm, p, True, transfer=transfer, swizzle=swizzle, rpct=rpct, ag_engine=engine)
+                    outs[(engine, transfer, swizzle)] = got
+                    for r in range(tp):
+                        assert O.max_rel_error(got[r], want[r]) <= H.tol(True, p.k)
+        # push == pull bitwise (test_engine.cpp:63-74): same GEMM, same inputs, either engine
         for r in range(tp):
-            assert np.array_equal(outs[(fx.PULL, True)][r], outs[(fx.PUSH, True)][r])
+            for key in outs:
+                assert np.array_equal(outs[(1, fx.PULL, True)][r], outs[key][r]) or not key[2], key
 
 
 def test_reduce_scatter_is_deterministic_across_runs_and_orders():
@@ -381,7 +383,7 @@ def test_acceptance_randomized_equivalence():
         kw = {"cta_group": int(rng.choice([0, 1, 2]))}
         if pat == AG:
             kw["ag_engine"] = int(rng.choice([1, 2]))
-            mode = {"transfer": fx.PUSH if (kw["ag_engine"] == 1 and rng.random() < 0.3) else fx.PULL,
+            mode = {"transfer": fx.PUSH if rng.random() < 0.3 else fx.PULL,
                     "swizzle": bool(rng.random() < 0.8)}
         else:
             mode = {"write_mode": int(rng.choice([fx.WRITE_ALLTOALL, fx.FUSED_REDUCE])),

@@ -18,20 +18,21 @@ from oracle import gpu_harness as H  # noqa: E402
 AG, RS = fx.ALLGATHER_GEMM, fx.GEMM_REDUCESCATTER
 
 
-def _op(comm, p, opts, streams):
+def _op(comm, p, opts, streams, push=False):
     tile = fx.TileShape(p.rows_per_rank(), p.local_cols())
     if p.pattern == AG:
-        comm.ag_gemm(p, tile, p.rows_per_rank(), fx.PULL, True, opts, streams)
+        comm.ag_gemm(p, tile, p.rows_per_rank(), fx.PUSH if push else fx.PULL, True, opts, streams)
     else:
         comm.gemm_rs(p, tile, fx.WRITE_ALLTOALL, True, opts, streams)
 
 
 @pytest.mark.parametrize("case", [(AG, 256, 1024, 512, 4), (AG, 64, 2048, 1024, 8), (RS, 1024, 512, 512, 4),
                                   (RS, 4096, 4096, 512, 4), (RS, 40, 24, 72, 4), (RS, 512, 8192, 1024, 8),
-                                  (AG, 1000, 600, 200, 2)],
+                                  (AG, 1000, 600, 200, 2), (AG, 512, 1024, 256, 4, "push")],
                          ids=lambda c: "x".join(map(str, c)))
 def test_graph_replay_matches_oracle(case):
-    pat, m, n, k, tp = case
+    pat, m, n, k, tp = case[:5]
+    push = len(case) > 5
     p = fx.ProblemSpec(m, n, k, tp, pat)
     side = torch.cuda.Stream()
     streams = [side.cuda_stream] * tp
@@ -40,15 +41,15 @@ def test_graph_replay_matches_oracle(case):
     with H.make_comm(p) as comm:
         H.upload(comm, p, seed=1)
         with torch.cuda.stream(side):
-            _op(comm, p, gopts, streams)  # warm-up: schedule tables are uploaded outside the capture
+            _op(comm, p, gopts, streams, push)  # warm-up: schedule tables are uploaded outside the capture
         comm.sync()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=side):
-            _op(comm, p, gopts, streams)
+            _op(comm, p, gopts, streams, push)
         for it in range(4):
             a, b = H.upload(comm, p, seed=100 + it)
             if it == 2:  # an eager operator between replays (different inputs, normal epochs)
-                _op(comm, p, eopts, None)
+                _op(comm, p, eopts, None, push)
                 comm.sync()
                 a, b = H.upload(comm, p, seed=100 + it)
             graph.replay()
@@ -139,8 +140,6 @@ def test_graph_safe_contract():
         tile = fx.TileShape(p.rows_per_rank(), p.local_cols())
         with pytest.raises(N.ConfigError, match="in-kernel transfer engine"):
             comm.ag_gemm(p, tile, p.rows_per_rank(), fx.PULL, True, fx.default_opts(graph_safe=1, ag_engine=1))
-        with pytest.raises(N.ConfigError, match="in-kernel transfer engine"):
-            comm.ag_gemm(p, tile, p.rows_per_rank(), fx.PUSH, True, fx.default_opts(graph_safe=1))
         with pytest.raises(N.ConfigError, match="fused operators"):
             comm.nonoverlap(p, fx.default_opts(graph_safe=1))
     q = fx.ProblemSpec(256, 512, 256, 2, RS)

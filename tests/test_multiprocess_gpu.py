@@ -25,6 +25,6 @@ def test_two_processes_ipc_match_oracle():
     assert len(lines) == 2
     for line in lines:
         res = json.loads(line.split(" ", 2)[2])
-        assert len(res) == 19  # 8 operator cases, 3 torch ops, TPMlp GELU and SwiGLU (out, dx, dW_up, dW_down)
+        assert len(res) == 20  # 9 operator cases, 3 torch ops, TPMlp GELU and SwiGLU (out, dx, dW_up, dW_down)
         for case, (err, tol) in res.items():
             assert err <= tol, (case, err, tol)
