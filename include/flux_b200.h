@@ -96,7 +96,7 @@ typedef struct {
     int activation_grad;       /* flux_activation whose derivative scales C: C = acc * act'(aux) */
     int rs_partials;           /* flux_dtype of the GEMM-RS cross-rank partials: F32 (default) or BF16
                                   (half the NVLink bytes; one bf16 rounding per partial / chain link;
-                                  needs m/tp % 128 == 0 and WriteAlltoAll) */
+                                  WriteAlltoAll only) */
     int b_layout;              /* flux_b_layout of caller-provided B (operands.b): NK = [n/tp or n, k]
                                   (nn.Linear.weight, default) or KN = [k, n] row-major (the reference's
                                   b_shard; no transposed copy needed, e.g. for the backward pass) */

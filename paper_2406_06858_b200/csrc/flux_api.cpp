@@ -709,7 +709,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
         prm.rs_chain = mode == kModeRS ? oc.rs_chain : 0;
         prm.b_mn = oc.o.b_layout == FLUX_B_KN ? 1 : 0;
-        prm.part_bf16 = mode == kModeRS && !oc.fused_reduce && oc.o.rs_partials == FLUX_BF16 ? 1 : 0;
+        prm.part_bf16 = (mode == kModeRS || mode == kModeRSLast) && !oc.fused_reduce && oc.o.rs_partials == FLUX_BF16 ? 1 : 0;
         for (int q = 0; q < kMaxRanks; ++q) prm.slot_of[q] = -1;
         for (size_t li = 0; li < g.size(); ++li) prm.slot_of[g[li]] = static_cast<int>(li);
         prm.rs_last_arriver = mode == kModeRSLast ? 1 : 0;
@@ -1738,8 +1738,8 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     oc.ops = operands;
     if (oc.o.rs_partials != FLUX_F32 && oc.o.rs_partials != FLUX_BF16)
         return fail(FLUX_ERR_CONFIG, "rs_partials must be F32 or BF16");
-    if (oc.o.rs_partials == FLUX_BF16 && (oc.rs_last_arriver || oc.fused_reduce))
-        return fail(FLUX_ERR_CONFIG, "bf16 partials need WriteAlltoAll and ownership blocks of whole 128-row tiles");
+    if (oc.o.rs_partials == FLUX_BF16 && oc.fused_reduce)
+        return fail(FLUX_ERR_CONFIG, "bf16 partials need WriteAlltoAll");
     // Chained partial sums (kernel, RS branch) when every rank runs in this one
     // launch (rank-major order, owners' blocks last); every chain link waits only
     // on an earlier section.

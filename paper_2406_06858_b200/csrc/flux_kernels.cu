@@ -528,6 +528,7 @@ __device__ __forceinline__ void sum_into(float (&acc)[4], const float4& w, bool&
 // owner's C. The GEMM never waits on a reduction, so these waits cannot
 // deadlock. The last group out re-arms the counter for the next launch.
 constexpr int kRedRows = 16;
+template <int PB>
 __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr, int bar_id, int* slot) {
     constexpr int kU = 4;
     const int tp = p.tp, tiles_n = p.tiles_n, rpr = p.rpr, n = p.n, out_f32 = p.out_f32;
@@ -557,7 +558,8 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
         }
         named_bar_sync(bar_id, nthr);  // flags acquired; everyone has read *slot
         const int npos = (r1 - r0) * (kBN / 4);
-        const float* base = p.staging[me] + parity * p.stage_parity + static_cast<long long>(r0 - me * rpr) * ld_stage;
+        const float* const sbase = p.staging[me];  // element offsets below (fp32 or bf16 elements, PB)
+        const long long e0 = parity * p.stage_parity + static_cast<long long>(r0 - me * rpr) * ld_stage;
         void* const cl = p.c[l];
         const long long ldc = p.ldc_l[l];
         for (int b = tid; b < npos; b += nthr * kU) {
@@ -567,10 +569,10 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
                 const int pos = b + i * nthr;
                 const int col = tn * kBN + (pos % (kBN / 4)) * 4;
                 if (pos < npos && col < n) {
-                    const float* src = base + (pos / (kBN / 4)) * ld_stage + col;
+                    const long long e = e0 + (pos / (kBN / 4)) * ld_stage + col;
 #pragma unroll
                     for (int s = 0; s < kMaxRanks; ++s)
-                        if (s < tp) v[i][s] = ld_cg_f4(src + s * stage_plane);
+                        if (s < tp) v[i][s] = ld_part4<PB>(sbase, e + s * stage_plane);
                 }
             }
 #pragma unroll
@@ -919,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         }
     } else if (MODE == kModeRSLast && (warp == 2 || warp == 3)) {
         // ===== decode RS: owners' reduction, concurrent with the GEMM =====
-        owner_reduce(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
+        owner_reduce<PB>(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
     } else if (warp == 3) {
         // ===== in-kernel AllGather transfer (Alg. 3 on the SMs) =====
         // Lane 0 walks this CTA's share of the piece table: TMA bulk copy
@@ -1262,12 +1264,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     if (row0 + q * 32 + 32 > p.m || (p.dbg & 64)) {  // dbg 64: ablation, always direct
                         if (valid) {
                             const int o = row / rpr;
-                            float4* d4 = reinterpret_cast<float4*>(p.staging[o] + parity * p.stage_parity + me * p.stage_plane +
-                                                                   (row - static_cast<long long>(o) * rpr) * ld_stage + colc);
+                            const long long e = parity * p.stage_parity + me * p.stage_plane +
+                                                (row - static_cast<long long>(o) * rpr) * ld_stage + colc;
 #pragma unroll
                             for (int j = 0; j < 32; j += 4)
-                                d4[j / 4] = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                                st_part4<PB>(p.staging[o], e + j,
+                                             make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                         __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
                         }
                         continue;
                     }
@@ -1279,9 +1282,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         const int grow = row0 + q * 32 + i;
                         if (grow >= p.m || col >= p.n) continue;
                         const int o = grow / rpr;
-                        float* dst = p.staging[o] + parity * p.stage_parity + me * p.stage_plane +
-                                     (grow - static_cast<long long>(o) * rpr) * ld_stage + col;
-                        *reinterpret_cast<float4*>(dst) = epi_read(wbuf, i, g);
+                        st_part4<PB>(p.staging[o],
+                                     parity * p.stage_parity + me * p.stage_plane +
+                                         (grow - static_cast<long long>(o) * rpr) * ld_stage + col,
+                                     epi_read(wbuf, i, g));
                     }
                 }
                 // The accumulator is in staging now: hand TMEM back to the MMA warp.
@@ -1545,7 +1549,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 aphase ^= 1u;
             }
         }
-        if (MODE == kModeRSLast) owner_reduce(p, et, 128, 4, &red_slot[1]);
+        if (MODE == kModeRSLast) owner_reduce<PB>(p, et, 128, 4, &red_slot[1]);
     }
 
     if (CG == 2) cluster_sync();
@@ -1627,7 +1631,9 @@ cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStr
             case kModeAG: return launch_one<kModeAG, 2>(p, grid, stream);
             case kModeRS:
                 return p.part_bf16 ? launch_one<kModeRS, 2, 1>(p, grid, stream) : launch_one<kModeRS, 2>(p, grid, stream);
-            case kModeRSLast: return launch_one<kModeRSLast, 2>(p, grid, stream);
+            case kModeRSLast:
+                return p.part_bf16 ? launch_one<kModeRSLast, 2, 1>(p, grid, stream)
+                                   : launch_one<kModeRSLast, 2>(p, grid, stream);
         }
     } else {
         switch (mode) {
@@ -1635,7 +1641,9 @@ cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStr
             case kModeAG: return launch_one<kModeAG, 1>(p, grid, stream);
             case kModeRS:
                 return p.part_bf16 ? launch_one<kModeRS, 1, 1>(p, grid, stream) : launch_one<kModeRS, 1>(p, grid, stream);
-            case kModeRSLast: return launch_one<kModeRSLast, 1>(p, grid, stream);
+            case kModeRSLast:
+                return p.part_bf16 ? launch_one<kModeRSLast, 1, 1>(p, grid, stream)
+                                   : launch_one<kModeRSLast, 1>(p, grid, stream);
         }
     }
     return cudaErrorInvalidValue;

@@ -450,13 +450,14 @@ def _normwise(got, want):
     return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
 
 
-@pytest.mark.parametrize("case", [(1024, 512, 768, 4), (2048, 1024, 1024, 8), (4096, 4096, 512, 4)],
+@pytest.mark.parametrize("case", [(1024, 512, 768, 4), (2048, 1024, 1024, 8), (4096, 4096, 512, 4),
+                                  (40, 24, 72, 4), (512, 8192, 1024, 8), (360, 515, 96, 8)],
                          ids=lambda c: "x".join(map(str, c)))
 def test_rs_bf16_partials_normwise(case):
     """opts.rs_partials = BF16 (half the cross-rank bytes): one bf16 rounding per
-    partial (owner sum) or per chain link (4096x4096: chained); checked
-    normwise <= 5e-3, and it must differ from the fp32 path only
-    by that rounding. Other RS modes reject it."""
+    partial (owner sum, decode owner units) or per chain link (4096x4096:
+    chained); checked normwise <= 5e-3, and it must differ from
+    the fp32 path only by that rounding. FusedReduce rejects it."""
     m, n, k, tp = case
     p = fx.ProblemSpec(m, n, k, tp, RS)
     with H.make_comm(p) as comm:
@@ -470,10 +471,10 @@ def test_rs_bf16_partials_normwise(case):
         for r in range(tp):
             assert _normwise(bf[r], want[r]) <= 5e-3, r
             assert _normwise(bf[r], f32[r]) <= 5e-3, r
-    q = fx.ProblemSpec(40, 24, 72, 4, RS)  # decode-sized blocks: last-arriver mode keeps fp32 partials
+    q = fx.ProblemSpec(1024, 512, 768, 4, RS)  # arrival-order FusedReduce accumulates in fp32
     with H.make_comm(q) as comm:
         with pytest.raises(fx.ConfigError, match="bf16 partials"):
-            _run(comm, q, True, rs_partials=fx.BF16)
+            _run(comm, q, True, rs_partials=fx.BF16, write_mode=fx.FUSED_REDUCE, deterministic_reduce=0)
 
 
 @pytest.mark.parametrize("cta_group", [1, 2])
