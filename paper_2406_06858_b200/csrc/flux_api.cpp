@@ -755,7 +755,9 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 prm.tail_ctr = at<uint32_t>(lead_rank, kTailCtrOffset);
             }
         }
-        const int grid = cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
+        // Decode RS: every SM runs reduction units, also those without a GEMM tile.
+        const int grid = mode == kModeRSLast ? cg * std::max(1, sm_count(dev) / cg)
+                                             : cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
         // Dynamic tile scheduler (FLUX_DYN_SCHED=1): clusters fetch tiles from a
         // counter in the lead rank's control block instead of a static stride.
         if (const char* env = std::getenv("FLUX_DYN_SCHED"); env && std::atoi(env) != 0 && grid / cg > 1) {
@@ -1757,9 +1759,26 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
                           ? 1
                           : 0;
     }
-    const int interleave = aligned ? kInterleaveRankTail : (oc.rs_last_arriver ? kInterleaveBlock : kInterleaveStep);
+    // Whole-tile blocks of a problem smaller than one wave are summed by the
+    // owners' reduction units (the decode path) on every SM, the idle ones
+    // included, instead of in the owners' tiles (C1: 67 -> 50 us). Larger
+    // problems keep the tail / chain (units measured slower there).
+    // FLUX_RS_UNITS=0/1 overrides (profiling).
+    if (!oc.rs_chain && !oc.fused_reduce && !oc.rs_last_arriver) {
+        const auto groups = device_groups(c);
+        size_t per_dev = 1;
+        for (const auto& dg : groups) per_dev = std::max(per_dev, dg.size());
+        const long long tiles_launch = static_cast<long long>((p->m + kBM * cg - 1) / (kBM * cg)) * tiles_n *
+                                       static_cast<long long>(per_dev);
+        const int clusters = std::max(1, sm_count(c->ranks[mine.empty() ? 0 : mine[0]].device) / cg);
+        bool units = tiles_launch < clusters;
+        if (const char* env = std::getenv("FLUX_RS_UNITS")) units = std::atoi(env) != 0;
+        if (units) oc.rs_last_arriver = 1;
+    }
+    const int interleave =
+        oc.rs_last_arriver ? kInterleaveBlock : (aligned ? kInterleaveRankTail : kInterleaveStep);
     FLUX_TRY(launch_groups(c, p, oc.rs_last_arriver ? kModeRSLast : kModeRS, oc, streams, seq, 0, interleave, cg,
-                           false, -1, tail));
+                           false, -1, oc.rs_last_arriver ? 0 : tail));
     return mark_op_done(c, streams, c->epoch);
 }
 
