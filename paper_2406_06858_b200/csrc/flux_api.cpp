@@ -755,9 +755,12 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 prm.tail_ctr = at<uint32_t>(lead_rank, kTailCtrOffset);
             }
         }
-        // Decode RS: every SM runs reduction units, also those without a GEMM tile.
-        const int grid = mode == kModeRSLast ? cg * std::max(1, sm_count(dev) / cg)
-                                             : cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
+        // Every SM takes part even without a GEMM tile of its own: decode RS runs
+        // reduction units, the in-kernel AllGather moves pieces (decode AG M=128:
+        // 124 -> 116 us).
+        const bool full = mode == kModeRSLast || (mode == kModeAG && prm.sm_transfer);
+        const int grid = full ? cg * std::max(1, sm_count(dev) / cg)
+                              : cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
         // Dynamic tile scheduler (FLUX_DYN_SCHED=1): clusters fetch tiles from a
         // counter in the lead rank's control block instead of a static stride.
         if (const char* env = std::getenv("FLUX_DYN_SCHED"); env && std::atoi(env) != 0 && grid / cg > 1) {
