@@ -565,7 +565,7 @@ struct OpCommon {
     flux_opts o;
     uint64_t timeout_ns;
     int fused_reduce = 0;  // RS FusedReduce in arrival order (red.add into the owner accumulator)
-    int rs_last_arriver = 0;  // RS with ownership blocks narrower than a tile
+    int rs_units = 0;  // RS summed by the owners' reduction units (decode-sized blocks, sub-wave problems)
     int rs_chain = 0;         // RS with every rank in one launch: chained partial sums (kernel)
     const flux_operands* ops = nullptr;  // caller-provided operands (per rank; one entry in IPC mode)
 };
@@ -643,7 +643,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             prm.ag_flags[li] = at<uint32_t>(rs, kAgFlagOffset);
             prm.ctrl[li] = at<uint32_t>(rs, kCtrlErr);
         }
-        if (mode == kModeRS || mode == kModeRSLast) {
+        if (mode == kModeRS || mode == kModeRSUnits) {
             for (int r = 0; r < c->tp; ++r) {
                 prm.staging[r] = reinterpret_cast<float*>(c->ranks[r].heap + L.staging.off);
                 prm.rs_flags[r] = at<uint32_t>(c->ranks[r], kRsFlagOffset);
@@ -709,10 +709,10 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.fused_reduce = mode == kModeRS ? oc.fused_reduce : 0;
         prm.rs_chain = mode == kModeRS ? oc.rs_chain : 0;
         prm.b_mn = oc.o.b_layout == FLUX_B_KN ? 1 : 0;
-        prm.part_bf16 = (mode == kModeRS || mode == kModeRSLast) && !oc.fused_reduce && oc.o.rs_partials == FLUX_BF16 ? 1 : 0;
+        prm.part_bf16 = (mode == kModeRS || mode == kModeRSUnits) && !oc.fused_reduce && oc.o.rs_partials == FLUX_BF16 ? 1 : 0;
         for (int q = 0; q < kMaxRanks; ++q) prm.slot_of[q] = -1;
         for (size_t li = 0; li < g.size(); ++li) prm.slot_of[g[li]] = static_cast<int>(li);
-        prm.rs_last_arriver = mode == kModeRSLast ? 1 : 0;
+        prm.rs_units = mode == kModeRSUnits ? 1 : 0;
         prm.red_ctr = at<uint32_t>(c->ranks[g[0]], kCtrlRedCtr);
         prm.red_exit = at<uint32_t>(c->ranks[g[0]], kCtrlRedExit);
         if (const char* env = std::getenv("FLUX_DEBUG")) prm.dbg = std::atoi(env);  // profiling ablations only
@@ -758,7 +758,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         // Every SM takes part even without a GEMM tile of its own: decode RS runs
         // reduction units, the in-kernel AllGather moves pieces (decode AG M=128:
         // 124 -> 116 us).
-        const bool full = mode == kModeRSLast || (mode == kModeAG && prm.sm_transfer);
+        const bool full = mode == kModeRSUnits || (mode == kModeAG && prm.sm_transfer);
         const int grid = full ? cg * std::max(1, sm_count(dev) / cg)
                               : cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
         // Dynamic tile scheduler (FLUX_DYN_SCHED=1): clusters fetch tiles from a
@@ -1739,7 +1739,7 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     // Ownership blocks narrower than a device tile (decode-sized M): sources
     // stage whole tiles, owners sum their rows at the end of the kernel.
     const int tiles_n = (p->n + kBN - 1) / kBN;
-    oc.rs_last_arriver = (rpr % kBM != 0 && !oc.fused_reduce) ? 1 : 0;
+    oc.rs_units = (rpr % kBM != 0 && !oc.fused_reduce) ? 1 : 0;
     oc.ops = operands;
     if (oc.o.rs_partials != FLUX_F32 && oc.o.rs_partials != FLUX_BF16)
         return fail(FLUX_ERR_CONFIG, "rs_partials must be F32 or BF16");
@@ -1756,7 +1756,7 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         // serialises them; measured on decode shapes).
         const long long tiles_per_rank = static_cast<long long>((p->m + kBM * cg - 1) / (kBM * cg)) * tiles_n;
         const int clusters = std::max(1, sm_count(c->ranks[0].device) / cg);
-        oc.rs_chain = aligned && !oc.fused_reduce && !oc.rs_last_arriver && groups.size() == 1 &&
+        oc.rs_chain = aligned && !oc.fused_reduce && !oc.rs_units && groups.size() == 1 &&
                               static_cast<int>(groups[0].size()) == tp && tiles_per_rank >= 2LL * clusters &&
                               !(env && std::atoi(env) == 0)
                           ? 1
@@ -1767,7 +1767,7 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     // included, instead of in the owners' tiles (C1: 67 -> 50 us). Larger
     // problems keep the tail / chain (units measured slower there).
     // FLUX_RS_UNITS=0/1 overrides (profiling).
-    if (!oc.rs_chain && !oc.fused_reduce && !oc.rs_last_arriver) {
+    if (!oc.rs_chain && !oc.fused_reduce && !oc.rs_units) {
         const auto groups = device_groups(c);
         size_t per_dev = 1;
         for (const auto& dg : groups) per_dev = std::max(per_dev, dg.size());
@@ -1776,12 +1776,12 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         const int clusters = std::max(1, sm_count(c->ranks[mine.empty() ? 0 : mine[0]].device) / cg);
         bool units = tiles_launch < clusters;
         if (const char* env = std::getenv("FLUX_RS_UNITS")) units = std::atoi(env) != 0;
-        if (units) oc.rs_last_arriver = 1;
+        if (units) oc.rs_units = 1;
     }
     const int interleave =
-        oc.rs_last_arriver ? kInterleaveBlock : (aligned ? kInterleaveRankTail : kInterleaveStep);
-    FLUX_TRY(launch_groups(c, p, oc.rs_last_arriver ? kModeRSLast : kModeRS, oc, streams, seq, 0, interleave, cg,
-                           false, -1, oc.rs_last_arriver ? 0 : tail));
+        oc.rs_units ? kInterleaveBlock : (aligned ? kInterleaveRankTail : kInterleaveStep);
+    FLUX_TRY(launch_groups(c, p, oc.rs_units ? kModeRSUnits : kModeRS, oc, streams, seq, 0, interleave, cg,
+                           false, -1, oc.rs_units ? 0 : tail));
     return mark_op_done(c, streams, c->epoch);
 }
 

@@ -22,10 +22,10 @@ constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*alig
 
 constexpr int kMaxRanks = 8;   // TP degree supported by one communicator (one NVSwitch node)
 
-// kModeRSLast: GEMM-RS whose ownership blocks are narrower than a tile (sources stage whole
+// kModeRSUnits: GEMM-RS whose ownership blocks are narrower than a tile (sources stage whole
 //   tiles; the owners' rows are summed by reduction units running alongside the GEMM).
 enum Activation : int { kActNone = 0, kActGelu = 1, kActRelu = 2, kActSilu = 3, kActSwiGLU = 4 };
-enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2, kModeRSLast = 3 };
+enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2, kModeRSUnits = 3 };
 
 // Control block at the start of every rank's symmetric heap. The flags are
 // epoch-stamped (monotonic), so nothing needs resetting between operators; the
@@ -125,7 +125,7 @@ struct GemmParams {
     int ag_push;
     const uint32_t* kdone[kMaxRanks];  // per GLOBAL rank: kernel-done epoch word (peer pointers)
     // RS with ownership blocks narrower than a tile: owners reduce during the GEMM
-    int rs_last_arriver;
+    int rs_units;
     uint32_t* red_ctr;             // reduction unit counter (lead rank's control block)
     uint32_t* red_exit;
     // Device event trace (reference CausalityLog, engine.hpp:37-63): 16-byte records

@@ -17,18 +17,21 @@
 //            in a fixed order, replacing the reference's reduce agent
 //            (engine.cpp:324-341); with every rank in one launch the partials
 //            are chained instead (each source adds to its predecessor's sum).
-//   RSLast — RS with ownership blocks narrower than a tile (decode): the last
-//            of the tp arrivals of a tile reduces it.
+//   RSUnits — RS with ownership blocks narrower than a tile (decode) or a
+//            problem smaller than one wave: sources stage whole tiles and stamp
+//            per-(tile, source) flags; the owners' rows are summed by reduction
+//            units on warps 2-3 during the GEMM (and the epilogue warps after).
 // Epilogue options: activations (GELU / ReLU / SiLU / SwiGLU), pre-activation
 // save, derivative scaling (MLP backward); tail split of the last wave
 // (Plain / AG); B operand K-major or MN-major; bf16 RS partials (PB).
 //
 // Roles: warp 0 = TMA producer (one lane), warp 1 = MMA issuer (one lane),
 // warp 2 = TMEM allocator, warp 3 = in-kernel AllGather transfer (AG),
-// warps 4..7 = epilogue (TMEM lane quadrants 0..3). Pipelines: a smem ring
-// (TMA -> MMA), two TMEM accumulators (MMA -> epilogue). The tile schedule is
-// a host-built table (reference tile_order, swizzle.cpp:75-80) walked with a
-// static stride of the cluster count.
+// warps 2-3 = reduction units (RSUnits), warps 4..7 = epilogue (TMEM lane
+// quadrants 0..3). Pipelines: a smem ring (TMA -> MMA), two TMEM accumulators
+// (MMA -> epilogue). The tile schedule is a host-built table (reference
+// tile_order, swizzle.cpp:75-80) walked with a static stride of the cluster
+// count (or fetched from a counter: FLUX_DYN_SCHED, ablation).
 #include <cuda_bf16.h>
 
 #include "flux_internal.hpp"
@@ -647,7 +650,7 @@ struct Geo {
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kStagesN = CG == 2 ? 6 : 4;
     static constexpr int kCommBytes = MODE == kModeAG ? 2 * kPieceBytes : 0;  // in-kernel AG staging
-    static constexpr int kEpiBytes = MODE == kModeRS || MODE == kModeRSLast ? 4 * kEpiWarpBytes : 0;  // RS epilogue windows
+    static constexpr int kEpiBytes = MODE == kModeRS || MODE == kModeRSUnits ? 4 * kEpiWarpBytes : 0;  // RS epilogue windows
     static constexpr int kSmem = kStagesN * kStageBytes + kCommBytes + kEpiBytes + 1024 + kBarRegion;
     static constexpr uint32_t kIdescV = make_idesc(kTileM, kBN);
 };
@@ -919,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 }
             }
         }
-    } else if (MODE == kModeRSLast && (warp == 2 || warp == 3)) {
+    } else if (MODE == kModeRSUnits && (warp == 2 || warp == 3)) {
         // ===== decode RS: owners' reduction, concurrent with the GEMM =====
         owner_reduce<PB>(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
     } else if (warp == 3) {
@@ -1085,7 +1088,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                    static_cast<uint32_t>(as * kBN);
             if (row0 >= p.m) {
                 // Fully out-of-range half of a pair tile: nothing to store or signal.
-            } else if (MODE != kModeRS && MODE != kModeRSLast) {
+            } else if (MODE != kModeRS && MODE != kModeRSUnits) {
                 if (p.act == kActSwiGLU) {
                     // Gated MLP: each 256-column tile holds 128 gate then 128 up
                     // columns; C gets silu(gate) * up, 128 columns per tile.
@@ -1240,7 +1243,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         }
                     }
                 }
-            } else if (MODE == kModeRSLast) {
+            } else if (MODE == kModeRSUnits) {
                 // Ownership blocks narrower than a tile (decode-sized M): every source
                 // stores its whole partial tile into the owners' staging planes and
                 // stamps flag (tile, source) of each owner in the tile. The owners
@@ -1517,7 +1520,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                     acc[3] = v[u][0].w + own.w;
                                 } else {
                                     // The canonical deterministic order (same as the chain and
-                                    // the last-arriver sum): the other sources ascending, then
+                                    // the decode owner units): the other sources ascending, then
                                     // the owner's own partial.
                                     bool first = true;
 #pragma unroll
@@ -1549,7 +1552,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 aphase ^= 1u;
             }
         }
-        if (MODE == kModeRSLast) owner_reduce<PB>(p, et, 128, 4, &red_slot[1]);
+        if (MODE == kModeRSUnits) owner_reduce<PB>(p, et, 128, 4, &red_slot[1]);
     }
 
     if (CG == 2) cluster_sync();
@@ -1631,9 +1634,9 @@ cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStr
             case kModeAG: return launch_one<kModeAG, 2>(p, grid, stream);
             case kModeRS:
                 return p.part_bf16 ? launch_one<kModeRS, 2, 1>(p, grid, stream) : launch_one<kModeRS, 2>(p, grid, stream);
-            case kModeRSLast:
-                return p.part_bf16 ? launch_one<kModeRSLast, 2, 1>(p, grid, stream)
-                                   : launch_one<kModeRSLast, 2>(p, grid, stream);
+            case kModeRSUnits:
+                return p.part_bf16 ? launch_one<kModeRSUnits, 2, 1>(p, grid, stream)
+                                   : launch_one<kModeRSUnits, 2>(p, grid, stream);
         }
     } else {
         switch (mode) {
@@ -1641,9 +1644,9 @@ cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStr
             case kModeAG: return launch_one<kModeAG, 1>(p, grid, stream);
             case kModeRS:
                 return p.part_bf16 ? launch_one<kModeRS, 1, 1>(p, grid, stream) : launch_one<kModeRS, 1>(p, grid, stream);
-            case kModeRSLast:
-                return p.part_bf16 ? launch_one<kModeRSLast, 1, 1>(p, grid, stream)
-                                   : launch_one<kModeRSLast, 1>(p, grid, stream);
+            case kModeRSUnits:
+                return p.part_bf16 ? launch_one<kModeRSUnits, 1, 1>(p, grid, stream)
+                                   : launch_one<kModeRSUnits, 1>(p, grid, stream);
         }
     }
     return cudaErrorInvalidValue;

@@ -97,7 +97,7 @@ def _mlp_inputs(spec, seed, swiglu=False):
 @pytest.mark.parametrize("act,m", [(fx.ACT_GELU, 1024), (fx.ACT_SILU, 1024), (fx.ACT_SWIGLU, 1024),
                                    (fx.ACT_SWIGLU, 64), (fx.ACT_GELU, 40)])
 def test_mlp_forward_chain(act, m):
-    """m = 64 / 40: decode-sized ownership blocks (last-arriver GEMM-RS into the
+    """m = 64 / 40: decode-sized ownership blocks (owner-unit GEMM-RS into the
     caller's output)."""
     spec = fx.MlpSpec(m=m, hidden=512, ffn=2048, tp=4, activation=act)
     tp, f = spec.tp, spec.ffn // spec.tp
