@@ -126,6 +126,7 @@ struct GemmParams {
     const uint32_t* kdone[kMaxRanks];  // per GLOBAL rank: kernel-done epoch word (peer pointers)
     // RS with ownership blocks narrower than a tile: owners reduce during the GEMM
     int rs_units;
+    int red_rows;                  // owner rows per reduction unit (8 or 16)
     uint32_t* red_ctr;             // reduction unit counter (lead rank's control block)
     uint32_t* red_exit;
     // Device event trace (reference CausalityLog, engine.hpp:37-63): 16-byte records

@@ -521,7 +521,7 @@ __device__ __forceinline__ void sum_into(float (&acc)[4], const float4& w, bool&
 // owners' C. Consecutive threads take consecutive 4-column groups of a row
 // (coalesced), and every source's float4 is loaded before the sum.
 // Decode-sized RS, owner side. The rows each local rank owns are cut into
-// units of kRedRows rows x one 256-column tile, ordered column tile first (the
+// units of p.red_rows rows x one 256-column tile, ordered column tile first (the
 // order in which the blocked schedule completes them). Two otherwise idle warps
 // of every CTA (2 and 3) take units from a launch-wide counter while the GEMM
 // runs; the four epilogue warps join once their CTA's GEMM units are done. A
@@ -530,7 +530,6 @@ __device__ __forceinline__ void sum_into(float (&acc)[4], const float4& w, bool&
 // the canonical order (other sources ascending, then the owner) into the
 // owner's C. The GEMM never waits on a reduction, so these waits cannot
 // deadlock. The last group out re-arms the counter for the next launch.
-constexpr int kRedRows = 16;
 template <int PB>
 __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr, int bar_id, int* slot) {
     constexpr int kU = 4;
@@ -538,7 +537,8 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
     const long long ld_stage = p.ld_stage, stage_plane = p.stage_plane;
     const uint32_t epoch = p.epoch, parity = p.epoch & 1u;
     const bool no_wait = (p.dbg & 32) != 0;  // dbg 32: profiling ablation, no waits
-    const int nch = (rpr + kRedRows - 1) / kRedRows;
+    const int red_rows = p.red_rows;
+    const int nch = (rpr + red_rows - 1) / red_rows;
     int nl = 0;
     while (nl < kMaxRanks && p.c[nl] != nullptr) ++nl;
     const int per_tn = nl * nch;
@@ -551,7 +551,7 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
         const int tn = u / per_tn, rem = u % per_tn;
         const int l = rem / nch;
         const int me = p.global_rank[l];
-        const int r0 = me * rpr + (rem % nch) * kRedRows, r1 = min(r0 + kRedRows, (me + 1) * rpr);
+        const int r0 = me * rpr + (rem % nch) * red_rows, r1 = min(r0 + red_rows, (me + 1) * rpr);
         const int tm0 = r0 / kBM, tm1 = (r1 - 1) / kBM;
         if (tid < (tm1 - tm0 + 1) * tp && !no_wait) {
             const int tile_id = (tm0 + tid / tp) * tiles_n + tn;
