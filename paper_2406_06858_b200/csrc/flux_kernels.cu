@@ -599,7 +599,7 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
     }
     if (tid == 0) {
         __threadfence();
-        if (atomicAdd(p.red_exit, 1u) == 2u * gridDim.x - 1u) {
+        if (atomicAdd(p.red_exit, 1u) == 3u * gridDim.x - 1u) {  // three groups per CTA
             atomicExch(p.red_ctr, 0u);
             atomicExch(p.red_exit, 0u);
         }
@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qempty + kTileQ);
     int* qtile = reinterpret_cast<int*>(tmem_slot + 2);
     int* red_slot = qtile + kTileQ;  // decode RS reduction: unit broadcast per group
-    static_assert((2 * G::kStagesN + 6 + 2 * kTileQ) * 8 + 8 + 4 * kTileQ + 8 <= kBarRegion, "barrier region");
+    static_assert((2 * G::kStagesN + 6 + 2 * kTileQ) * 8 + 8 + 4 * kTileQ + 12 <= kBarRegion, "barrier region");
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -1553,6 +1553,12 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             }
         }
         if (MODE == kModeRSUnits) owner_reduce<PB>(p, et, 128, 4, &red_slot[1]);
+    }
+    if (MODE == kModeRSUnits && warp < 2) {
+        // The producer and MMA warps are done with the GEMM: a third group of
+        // reduction units (shortens the last block's exposed sums).
+        __syncwarp();
+        owner_reduce<PB>(p, threadIdx.x, 64, 5, &red_slot[2]);
     }
 
     if (CG == 2) cluster_sync();
