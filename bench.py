@@ -148,7 +148,8 @@ def run_cpu_reference(pattern, m, n, k, tp, reps=1):
             times.append(secs)
         kind, used = "reference", tp * workers + (tp if pattern == 0 else tp)
         what = (f"reference {'run_fused_allgather_gemm (Pull, swizzle)' if pattern == 0 else 'run_fused_gemm_reducescatter (WriteAlltoAll, swizzle)'}"
-                f" fp64, oracle/_ref built from /root/reference, {workers} workers/rank")
+                f" fp64, oracle/_ref built from /root/reference, {workers} workers/rank + 1 transfer/reduce agent per rank"
+                f" = {tp * workers + tp} threads")
     else:
         import numpy as np
 
