@@ -22,7 +22,7 @@ def fill(comm, p, seed):
             t.copy_((torch.rand(t.shape, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16))
 
 
-def check(comm, p, tag):
+def check(comm, p, tag, bf16_partials=False):
     a = [comm.tensor(r, N.BUF_A_SHARD, p).float() for r in range(p.tp)]
     b = [comm.tensor(r, N.BUF_B_SHARD, p).float() for r in range(p.tp)]
     worst = 0.0
@@ -35,7 +35,7 @@ def check(comm, p, tag):
             ref = sum(a[s][r * rpr:(r + 1) * rpr] @ b[s].t() for s in range(p.tp))
         worst = max(worst, ((got - ref).abs().max() / ref.abs().max().clamp(min=1)).item())
     print(f"{tag}: max err {worst:.2e}", flush=True)
-    assert worst < 1e-2, tag
+    assert worst < (3e-2 if bf16_partials else 1e-2), tag
 
 
 cases = [("AG copy engines", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(ag_engine=1)),
@@ -47,10 +47,15 @@ cases = [("AG copy engines", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM
          ("RS decode, blocks straddling tiles", fx.ProblemSpec(360, 515, 96, 8, fx.GEMM_REDUCESCATTER), {}),
          ("AG dynamic scheduler", fx.ProblemSpec(1024, 2048, 512, 8, fx.ALLGATHER_GEMM), dict(env="FLUX_DYN_SCHED")),
          ("RS dynamic scheduler", fx.ProblemSpec(4096, 4096, 512, 4, fx.GEMM_REDUCESCATTER), dict(env="FLUX_DYN_SCHED")),
-         ("RS FusedReduce", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), dict(deterministic_reduce=0))]
+         ("RS FusedReduce", fx.ProblemSpec(1024, 512, 512, 4, fx.GEMM_REDUCESCATTER), dict(deterministic_reduce=0)),
+         ("AG in-kernel Push", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(ag_engine=2, push=1)),
+         ("RS smaller than a wave (owner units)", fx.ProblemSpec(1024, 1024, 512, 2, fx.GEMM_REDUCESCATTER), {}),
+         ("RS decode, bf16 partials", fx.ProblemSpec(64, 512, 512, 4, fx.GEMM_REDUCESCATTER), dict(rs_partials=fx.BF16)),
+         ("AG graph-safe", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(graph_safe=1))]
 for tag, p, kw in cases:
     kw = dict(kw)
     env = kw.pop("env", None)
+    push = kw.pop("push", 0)
     if env:
         os.environ[env] = "1"
     else:
@@ -60,12 +65,12 @@ for tag, p, kw in cases:
         opts = fx.default_opts(wall_budget_s=120.0, **kw)
         tile = fx.TileShape(p.rows_per_rank(), p.local_cols())
         if p.pattern == fx.ALLGATHER_GEMM:
-            comm.ag_gemm(p, tile, opts=opts)
+            comm.ag_gemm(p, tile, p.rows_per_rank(), fx.PUSH if push else fx.PULL, True, opts)
         else:
             wm = fx.FUSED_REDUCE if kw.get("deterministic_reduce") == 0 else fx.WRITE_ALLTOALL
             comm.gemm_rs(p, tile, wm, "Naive" not in tag, opts)
         comm.sync()
-        check(comm, p, tag)
+        check(comm, p, tag, kw.get("rs_partials") == fx.BF16)
 spec = fx.MlpSpec(m=512, hidden=256, ffn=1024, tp=2, activation=fx.ACT_GELU)
 x = [torch.randn(256, 256, device="cuda").to(torch.bfloat16) for _ in range(2)]
 wu = [torch.randn(512, 256, device="cuda").mul(0.05).to(torch.bfloat16) for _ in range(2)]
