@@ -208,4 +208,25 @@ EngineResult run_fused_allgather_gemm(const ProblemSpec& problem, ShardedWorkspa
                                       std::vector<std::vector<TransferRecord>>* traces = nullptr);
 std::vector<Matrix> run_nonoverlap(const ProblemSpec& problem, ShardedWorkspace& workspace, const TileShape& tile);
 
+// Medium-grained (decomposed) baseline, reference engine.hpp:129-145. The
+// schedule is the reference's (chunk GEMM / transfer / add steps with their
+// dependencies); the outputs come from the device's unfused path — the
+// reference itself executes the schedule serially, so its values do not
+// depend on it. The timed decomposed baseline (B2) is
+// paper_2406_06858_b200/baselines.py.
+struct MediumStep {
+    enum class Kind { ChunkGemm, ChunkTransfer, ChunkAdd };
+    int rank = 0;
+    Kind kind = Kind::ChunkGemm;
+    int chunk = 0;
+    std::vector<int> deps;  // indices into the schedule, topologically ordered
+};
+std::vector<MediumStep> medium_schedule(const ProblemSpec& problem, int partitions);
+struct MediumResult {
+    std::vector<Matrix> outputs;
+    std::vector<MediumStep> trace;
+};
+MediumResult run_medium_grained(const ProblemSpec& problem, ShardedWorkspace& workspace, const TileShape& tile,
+                                int partitions);
+
 }  // namespace overlap

@@ -186,6 +186,43 @@ EngineResult collect(flux_comm* c, const ProblemSpec& p, ShardedWorkspace& ws) {
     return res;
 }
 
+// EngineResult::log from the device event trace (CausalityLog schema,
+// engine.hpp:37-63): every rank's records ordered by %globaltimer, logical
+// timestamps 1..n in that order, wall_ns relative to the first event. The
+// launch-latency records (kind 6) are not part of the reference schema.
+std::vector<CausalityEvent> device_log(flux_comm* c, const ProblemSpec& p) {
+    static const char* kKinds[] = {"", "compute_start", "signal_set", "tile_write", "reduce", "wait"};
+    const flux_problem cp = cprob(p);
+    std::vector<std::pair<uint64_t, CausalityEvent>> all;
+    std::vector<uint64_t> buf(2u << 18);
+    for (int r = 0; r < p.tp; ++r) {
+        size_t n = 0;
+        ok(flux_trace_read(c, r, &cp, buf.data(), buf.size() / 2, &n));
+        for (size_t i = 0; i < n; ++i) {
+            const uint64_t ts = buf[2 * i], w = buf[2 * i + 1];
+            const unsigned kind = static_cast<unsigned>(w >> 60);
+            if (kind == 0 || kind > 5) continue;
+            CausalityEvent e;
+            e.kind = kKinds[kind];
+            e.rank = static_cast<int>((w >> 56) & 0xF);
+            e.target = static_cast<int>((w >> 32) & 0xFFFFFF);
+            e.tile_row = static_cast<int>((w >> 16) & 0xFFFF);
+            e.tile_col = static_cast<int>(w & 0xFFFF);
+            all.emplace_back(ts, e);
+        }
+    }
+    std::stable_sort(all.begin(), all.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<CausalityEvent> log;
+    log.reserve(all.size());
+    for (size_t i = 0; i < all.size(); ++i) {
+        CausalityEvent e = all[i].second;
+        e.logical_ts = i + 1;
+        e.wall_ns = static_cast<int64_t>(all[i].first - all.front().first);
+        log.push_back(e);
+    }
+    return log;
+}
+
 }  // namespace
 
 // ---- matrix helpers ----------------------------------------------------------------
@@ -426,11 +463,14 @@ EngineResult run_fused_gemm_reducescatter(const ProblemSpec& p, ShardedWorkspace
     upload_inputs(c, p, ws);
     const flux_problem cp = cprob(p);
     const flux_tile ct{tile.tm, tile.tn};
-    const flux_opts o = copts(opts);
+    flux_opts o = copts(opts);
+    o.trace = 1;  // EngineResult::log
     ok(flux_gemm_rs(c, &cp, &ct, write_mode == WriteMode::WriteAlltoAll ? FLUX_WRITE_ALLTOALL : FLUX_FUSED_REDUCE,
                     swizzle_on ? 1 : 0, &o, nullptr));
     ok(flux_sync(c));
-    return collect(c, p, ws);
+    EngineResult res = collect(c, p, ws);
+    res.log = device_log(c, p);
+    return res;
 }
 
 EngineResult run_fused_allgather_gemm(const ProblemSpec& p, ShardedWorkspace& ws, const TileShape& tile,
@@ -452,7 +492,8 @@ EngineResult run_fused_allgather_gemm(const ProblemSpec& p, ShardedWorkspace& ws
     upload_inputs(c, p, ws);
     const flux_problem cp = cprob(p);
     const flux_tile ct{tile.tm, tile.tn};
-    const flux_opts o = copts(opts);
+    flux_opts o = copts(opts);
+    o.trace = 1;  // EngineResult::log
     ok(flux_ag_gemm(c, &cp, &ct, rpct, transfer == TransferMode::Pull ? FLUX_PULL : FLUX_PUSH, swizzle_on ? 1 : 0, &o,
                     nullptr));
     ok(flux_sync(c));
@@ -461,7 +502,9 @@ EngineResult run_fused_allgather_gemm(const ProblemSpec& p, ShardedWorkspace& ws
         for (int r = 0; r < p.tp; ++r)
             for (const TransferDesc& d : comm[r].order) (*traces)[r].push_back(TransferRecord{d, 0, 0, 0, 0});
     }
-    return collect(c, p, ws);
+    EngineResult res = collect(c, p, ws);
+    res.log = device_log(c, p);
+    return res;
 }
 
 std::vector<Matrix> run_nonoverlap(const ProblemSpec& p, ShardedWorkspace& ws, const TileShape& tile) {
@@ -479,6 +522,55 @@ std::vector<Matrix> run_nonoverlap(const ProblemSpec& p, ShardedWorkspace& ws, c
     ok(flux_nonoverlap(c, &cp, &o, nullptr));
     ok(flux_sync(c));
     return collect(c, p, ws).outputs;
+}
+
+// Reference medium_schedule (engine.cpp:607-651): a partition count of tp or
+// 2*tp (or 1 at tp=1) dividing m. RS, per rank and chunk: the chunk GEMM and the
+// chunk transfer both follow the previous chunk's add, and the add joins them.
+// AG, per rank: the transfers of the chunks owned by other ranks first, then
+// one GEMM per chunk gated on its own chunk's transfer.
+std::vector<MediumStep> medium_schedule(const ProblemSpec& p, int partitions) {
+    p.validate();
+    const bool valid = partitions == p.tp || partitions == 2 * p.tp || (p.tp == 1 && partitions == 1);
+    if (!valid)
+        throw ConfigError("partitions=" + std::to_string(partitions) + " must be tp or 2*tp (tp=" +
+                          std::to_string(p.tp) + ")");
+    if (p.m % partitions != 0) throw ConfigError("m must be divisible by the partition count");
+    const int rows = p.m / partitions;
+    std::vector<MediumStep> steps;
+    auto step = [&](int r, MediumStep::Kind kind, int chunk, std::vector<int> deps) {
+        MediumStep s;
+        s.rank = r;
+        s.kind = kind;
+        s.chunk = chunk;
+        s.deps = std::move(deps);
+        steps.push_back(std::move(s));
+        return static_cast<int>(steps.size()) - 1;
+    };
+    for (int r = 0; r < p.tp; ++r) {
+        if (p.pattern == Pattern::GemmReduceScatter) {
+            std::vector<int> after_add;
+            for (int chunk = 0; chunk < partitions; ++chunk) {
+                const int g = step(r, MediumStep::Kind::ChunkGemm, chunk, after_add);
+                const int x = step(r, MediumStep::Kind::ChunkTransfer, chunk, after_add);
+                after_add = {step(r, MediumStep::Kind::ChunkAdd, chunk, {g, x})};
+            }
+        } else {
+            std::vector<std::vector<int>> gate(partitions);
+            for (int chunk = 0; chunk < partitions; ++chunk)
+                if (p.owner_of_row(chunk * rows) != r) gate[chunk] = {step(r, MediumStep::Kind::ChunkTransfer, chunk, {})};
+            for (int chunk = 0; chunk < partitions; ++chunk) step(r, MediumStep::Kind::ChunkGemm, chunk, gate[chunk]);
+        }
+    }
+    return steps;
+}
+
+MediumResult run_medium_grained(const ProblemSpec& p, ShardedWorkspace& ws, const TileShape& tile, int partitions) {
+    validate_tiling(p, tile);
+    MediumResult res;
+    res.trace = medium_schedule(p, partitions);
+    res.outputs = run_nonoverlap(p, ws, tile);
+    return res;
 }
 
 }  // namespace overlap

@@ -100,6 +100,28 @@ static void host_checks() {
     auto specs = make_comm_specs(ag, Topology{}, 1, TransferMode::Push);
     check(specs.size() == 8 && specs[2].order.size() == 7, "push comm specs carry the local tile to 7 peers");
     check(throws<BoundsError>([] { map_tile({}, 99, GridDims{2, 2, 1}); }), "map_tile out of range raises BoundsError");
+    // test_engine.cpp:141-156: medium-grained schedule shape
+    {
+        ProblemSpec p{8, 4, 4, 2, Pattern::GemmReduceScatter};
+        auto steps = medium_schedule(p, 2);
+        bool shape = steps.size() == 12;
+        for (int r = 0; r < 2 && shape; ++r) {
+            const int base = r * 6;
+            shape = steps[base + 0].kind == MediumStep::Kind::ChunkGemm &&
+                    steps[base + 2].kind == MediumStep::Kind::ChunkAdd &&
+                    steps[base + 3].kind == MediumStep::Kind::ChunkGemm &&
+                    steps[base + 5].kind == MediumStep::Kind::ChunkAdd && steps[base + 3].deps.size() == 1 &&
+                    steps[base + 3].deps[0] == base + 2;
+        }
+        check(shape, "medium schedule tp=2 partitions=2 alternates chunk gemm and add");
+        ProblemSpec q{16, 8, 8, 4, Pattern::GemmReduceScatter};
+        check(throws<ConfigError>([&] { medium_schedule(q, 3); }), "invalid partition count raises ConfigError");
+        ProblemSpec ag{16, 8, 8, 4, Pattern::AllGatherGemm};
+        auto a = medium_schedule(ag, 4);
+        int xfers = 0;
+        for (const MediumStep& s : a) xfers += s.rank == 0 && s.kind == MediumStep::Kind::ChunkTransfer;
+        check(a.size() == 4 * 7 && xfers == 3, "medium schedule AG: 3 remote chunk transfers + 4 chunk GEMMs per rank");
+    }
 }
 
 static void device_checks() {
@@ -117,6 +139,11 @@ static void device_checks() {
             check(worst(res.outputs, want) <= 1e-4, "fused all-gather golden config within 1e-4");
         }
         check(worst(run_nonoverlap(p, ws, {2, 2}), want) <= 1e-4, "nonoverlap golden config within 1e-4");
+        // test_golden.cpp:70 / acceptance.cpp:102: the medium-grained baseline
+        auto med = run_medium_grained(p, ws, {2, 2}, 8);
+        int gemms = 0;
+        for (const MediumStep& s : med.trace) gemms += s.rank == 0 && s.kind == MediumStep::Kind::ChunkGemm;
+        check(gemms == 8 && worst(med.outputs, want) <= 1e-4, "medium-grained (8 chunks) golden config within 1e-4");
     }
     // test_engine.cpp:63-74 push == pull bitwise
     ProblemSpec p{64, 32, 48, 4, Pattern::AllGatherGemm};
@@ -128,6 +155,22 @@ static void device_checks() {
     bool same = true;
     for (int r = 0; r < p.tp; ++r) same = same && bitwise_equal(pull.outputs[r], push.outputs[r]);
     check(same, "push and pull transfers produce identical outputs");
+    // test_engine.cpp:190-213 on EngineResult::log (the device event trace): every
+    // compute_start follows the signal_set of the group it consumed.
+    {
+        bool causal = !pull.log.empty();
+        int starts = 0;
+        for (const CausalityEvent& e : pull.log) {
+            if (e.kind != "compute_start") continue;
+            ++starts;
+            bool seen = false;
+            for (const CausalityEvent& f : pull.log)
+                seen = seen || (f.kind == "signal_set" && f.rank == e.rank && f.target == e.target &&
+                                f.logical_ts < e.logical_ts);
+            causal = causal && seen;
+        }
+        check(causal && starts > 0, "EngineResult::log: compute_start after its group's signal_set");
+    }
     check(worst(pull.outputs, oracle(p, ws)) <= 1e-4, "all-gather 64x32x48 tp=4 within 1e-4");
     // acceptance.cpp criterion 1 style: random shapes, every tp
     Rng rng(42);
