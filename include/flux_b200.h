@@ -101,10 +101,11 @@ typedef struct {
                                   (nn.Linear.weight, default) or KN = [k, n] row-major (the reference's
                                   b_shard; no transposed copy needed, e.g. for the backward pass) */
     int graph_safe;            /* 1: the operator may be captured in a CUDA graph and replayed: it
-                                  zeroes the flags / counters it uses before and after its kernel
-                                  (one small kernel each), so every replay starts from a clean
-                                  state. Single-process communicators; AllGather uses the in-kernel
-                                  transfer engine (no host stream memops); not with FusedReduce. */
+                                  zeroes the flags / counters it uses before its kernel (one small
+                                  kernel) and runs the in-kernel AllGather on its own counter set,
+                                  so every replay starts from a clean state. Single-process
+                                  communicators; AllGather uses the in-kernel transfer engine (no
+                                  host stream memops); not with the arrival-order FusedReduce. */
 } flux_opts;
 
 typedef enum { FLUX_B_NK = 0, FLUX_B_KN = 1 } flux_b_layout;
