@@ -208,12 +208,10 @@ EngineResult run_fused_allgather_gemm(const ProblemSpec& problem, ShardedWorkspa
                                       std::vector<std::vector<TransferRecord>>* traces = nullptr);
 std::vector<Matrix> run_nonoverlap(const ProblemSpec& problem, ShardedWorkspace& workspace, const TileShape& tile);
 
-// Medium-grained (decomposed) baseline, reference engine.hpp:129-145. The
-// schedule is the reference's (chunk GEMM / transfer / add steps with their
-// dependencies); the outputs come from the device's unfused path — the
-// reference itself executes the schedule serially, so its values do not
-// depend on it. The timed decomposed baseline (B2) is
-// paper_2406_06858_b200/baselines.py.
+// Medium-grained (decomposed) baseline, reference engine.hpp:129-145: the
+// reference's schedule (chunk GEMM / transfer / add steps with their
+// dependencies) as the trace; the outputs from the device's chunked execution
+// (flux_medium_grained: per-chunk copy-engine transfers / GEMMs / reduces).
 struct MediumStep {
     enum class Kind { ChunkGemm, ChunkTransfer, ChunkAdd };
     int rank = 0;

@@ -224,6 +224,14 @@ int flux_local_gemm(flux_comm* comm, const flux_problem* problem, const flux_opt
  * collective then the same GEMM kernel (or GEMM then serial reduce). */
 int flux_nonoverlap(flux_comm* comm, const flux_problem* problem, const flux_opts* opts,
                     void* const* streams);
+/* run_medium_grained (engine.hpp:144-145, schedule engine.cpp:607-651): the
+ * decomposed (B2) baseline — m split into `partitions` (tp or 2*tp; 1 at tp=1)
+ * row chunks; AG: every chunk's copy-engine transfers are issued up front and
+ * each chunk's GEMM (this library's kernel) waits for its chunk; RS: chunk
+ * GEMMs into fp32 partials, each chunk's source-ordered reduce on a side
+ * stream overlapping the next chunk's GEMM. Single-process communicators. */
+int flux_medium_grained(flux_comm* comm, const flux_problem* problem, const flux_tile* tile, int partitions,
+                        const flux_opts* opts, void* const* streams);
 /* Caller-owned operands (e.g. PyTorch tensors): per rank (tp entries in
  * single-process mode, 1 in IPC mode); NULL ptr fields use the library's
  * buffers. A = the rank's A shard, B = its weight shard [out, in] (K-major),

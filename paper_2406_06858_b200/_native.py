@@ -143,6 +143,7 @@ _SIGS = {
     "flux_ag_engine": (C.c_int, [_P(Problem), C.c_int, _P(Opts)]),
     "flux_local_gemm": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
     "flux_nonoverlap": (C.c_int, [C.c_void_p, _P(Problem), _P(Opts), _P(C.c_void_p)]),
+    "flux_medium_grained": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, _P(Opts), _P(C.c_void_p)]),
     "flux_sync": (C.c_int, [C.c_void_p]),
     "flux_last_launch_count": (C.c_int, [C.c_void_p]),
     "flux_comm_set_timing": (C.c_int, [C.c_void_p, C.c_int]),

@@ -249,6 +249,13 @@ class Communicator:
         o = opts if opts is not None else N.default_opts()
         N.check(N.lib().flux_nonoverlap(self._h, C.byref(problem.c()), C.byref(o), N.stream_array(streams)))
 
+    def medium_grained(self, problem: ProblemSpec, tile: TileShape, partitions: int, opts: Optional[N.Opts] = None,
+                       streams=None) -> None:
+        """run_medium_grained (engine.hpp:144-145): the decomposed (B2) baseline on the device."""
+        o = opts if opts is not None else N.default_opts()
+        N.check(N.lib().flux_medium_grained(self._h, C.byref(problem.c()), C.byref(tile.c()), partitions, C.byref(o),
+                                            N.stream_array(streams)))
+
     def sync(self) -> None:
         N.check(N.lib().flux_sync(self._h))
 

@@ -1902,16 +1902,147 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
         rp.c = rs.heap + L.c32.off;
         rp.ldc = L.c32.ld;
         rp.out_f32 = oc.o.out_dtype == FLUX_F32;
-        rp.rpr = rpr;
+        rp.rows = rpr;
         rp.n = p->n;
         rp.ld_src = L.ld_stage;
-        rp.owner = r;
+        rp.src_row0 = r * rpr;
+        rp.dst_row0 = 0;
         rp.tp = tp;
         FLUX_CUDA(launch_rs_reduce(rp, std::max(1, sm_count(rs.device)) * 4, s));
         ++c->last_launches;
         FLUX_CUDA(cudaEventRecord(rs.kernel_evt, s));
     }
     return mark_op_done(c, streams, e);
+}
+
+// run_medium_grained (engine.cpp:653-728) on the device: the decomposed (B2)
+// baseline. Chunks of m / partitions rows; AG: the copy stream issues every
+// chunk's transfers up front (one event per chunk) and each chunk's GEMM — the
+// plain kernel over the tiles holding the chunk's rows — waits for its event;
+// RS: each chunk's GEMM writes fp32 partials, then the owner's source-ordered
+// reduce of those rows runs on the copy stream while the next chunk computes.
+int flux_medium_grained(flux_comm* c, const flux_problem* p, const flux_tile* tile, int partitions,
+                        const flux_opts* opts, void* const* streams) {
+    FLUX_TRY(check_comm(c));
+    if (c->ipc) return fail(FLUX_ERR_CONFIG, "the medium-grained baseline runs on single-process communicators");
+    if (opts && opts->graph_safe) return fail(FLUX_ERR_CONFIG, "graph_safe applies to the fused operators and the local GEMM");
+    FLUX_TRY(validate_tiling(p, tile));
+    FLUX_TRY(check_heap(c, p));
+    const int tp = p->tp;
+    if (!(partitions == tp || partitions == 2 * tp || (tp == 1 && partitions == 1)))
+        return fail(FLUX_ERR_CONFIG, "partitions=" + S(partitions) + " must be tp or 2*tp (tp=" + S(tp) + ")");
+    if (p->m % partitions != 0) return fail(FLUX_ERR_CONFIG, "m must be divisible by the partition count");
+    std::vector<int> mine;
+    local_ranks_only(c, mine);
+    for (int r : mine)
+        for (int q = 0; q < tp; ++q) FLUX_TRY(check_directory(c, r, q));
+    OpCommon oc = common_opts(opts);
+    const Layout L = layout_for(p);
+    c->last_launches = 0;
+    c->kernel_events_used = 0;
+    const uint32_t e = ++c->epoch;
+    const int rpr = rows_per_rank(p), lk = local_k(p), chunk = p->m / partitions;
+    const int cg = choose_cg(p, oc.o), tile_m = kBM * cg;
+    const int ncols = p->pattern == FLUX_ALLGATHER_GEMM ? local_cols(p) : p->n;
+    const int tiles_n = (ncols + kBN - 1) / kBN;
+    auto chunk_seq = [&](int cc) {
+        std::vector<std::vector<uint32_t>> seq(tp);
+        const int t0 = (cc * chunk) / tile_m, t1 = ((cc + 1) * chunk - 1) / tile_m;
+        for (int r : mine)
+            for (int tn = 0; tn < tiles_n; ++tn)
+                for (int tm = t0; tm <= t1; ++tm) seq[r].push_back(pack_tile(0, tm, tn));
+        return seq;
+    };
+    const auto groups = device_groups(c);
+    std::vector<std::vector<cudaEvent_t>> ev(groups.size());
+    auto cleanup = [&]() {
+        for (auto& v : ev)
+            for (cudaEvent_t x : v) cudaEventDestroy(x);
+    };
+    auto fail_clean = [&](int rc) {
+        cleanup();
+        return rc;
+    };
+    // The copy stream of every device group starts after the callers' prior work
+    // (inputs) and after every kernel of the previous operator (WAR).
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        RankState& lead = c->ranks[groups[gi][0]];
+        FLUX_CUDA(cudaSetDevice(lead.device));
+        for (int r : groups[gi]) {
+            RankState& rs = c->ranks[r];
+            FLUX_CUDA(cudaEventRecord(rs.start_evt, stream_for(c, r, streams)));
+            FLUX_CUDA(cudaStreamWaitEvent(lead.copy_stream, rs.start_evt, 0));
+        }
+        for (int q = 0; q < tp; ++q)
+            if (c->ranks[q].kernel_evt_valid) FLUX_CUDA(cudaStreamWaitEvent(lead.copy_stream, c->ranks[q].kernel_evt, 0));
+        ev[gi].resize(partitions);
+        for (auto& x : ev[gi]) FLUX_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    }
+    if (p->pattern == FLUX_ALLGATHER_GEMM) {
+        const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
+        for (size_t gi = 0; gi < groups.size(); ++gi) {
+            RankState& lead = c->ranks[groups[gi][0]];
+            FLUX_CUDA(cudaSetDevice(lead.device));
+            for (int cc = 0; cc < partitions; ++cc) {
+                const int o = (cc * chunk) / rpr, lr = cc * chunk - o * rpr;
+                for (int r : groups[gi])
+                    FLUX_CUDA(cudaMemcpy2DAsync(c->ranks[r].heap + L.a_agg.off + static_cast<size_t>(cc) * chunk * rowbytes,
+                                                rowbytes,
+                                                c->ranks[o].heap + L.a_shard.off +
+                                                    static_cast<size_t>(lr) * L.a_shard.ld * 2,
+                                                static_cast<size_t>(L.a_shard.ld) * 2, lk * 2, chunk,
+                                                cudaMemcpyDeviceToDevice, lead.copy_stream));
+                FLUX_CUDA(cudaEventRecord(ev[gi][cc], lead.copy_stream));
+            }
+        }
+        for (int cc = 0; cc < partitions; ++cc) {
+            for (size_t gi = 0; gi < groups.size(); ++gi) {
+                FLUX_CUDA(cudaSetDevice(c->ranks[groups[gi][0]].device));
+                FLUX_CUDA(cudaStreamWaitEvent(stream_for(c, groups[gi][0], streams), ev[gi][cc], 0));
+            }
+            const int rc = launch_groups(c, p, kModePlain, oc, streams, chunk_seq(cc), 0, kInterleaveRank, cg, true);
+            if (rc != FLUX_OK) return fail_clean(rc);
+        }
+        cleanup();
+        return FLUX_OK;
+    }
+    const size_t parity_off = L.staging.off + static_cast<size_t>(e & 1u) * L.stage_parity * 4;
+    OpCommon oc32 = oc;
+    oc32.o.out_dtype = FLUX_F32;  // fp32 partials, reduced in source order
+    for (int cc = 0; cc < partitions; ++cc) {
+        const int rc = launch_groups(c, p, kModePlain, oc32, streams, chunk_seq(cc), 0, kInterleaveRank, cg, false,
+                                     static_cast<long long>(parity_off));
+        if (rc != FLUX_OK) return fail_clean(rc);
+        const int o = (cc * chunk) / rpr, lr = cc * chunk - o * rpr;
+        if (!c->ranks[o].local) continue;
+        RankState& rs = c->ranks[o];
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        for (int q = 0; q < tp; ++q) FLUX_CUDA(cudaStreamWaitEvent(rs.copy_stream, c->ranks[q].kernel_evt, 0));
+        RsReduceParams rp;
+        std::memset(&rp, 0, sizeof(rp));
+        for (int q = 0; q < tp; ++q) rp.partials[q] = reinterpret_cast<const float*>(c->ranks[q].heap + parity_off);
+        rp.c = rs.heap + L.c32.off;
+        rp.ldc = L.c32.ld;
+        rp.out_f32 = oc.o.out_dtype == FLUX_F32;
+        rp.rows = chunk;
+        rp.n = p->n;
+        rp.ld_src = L.ld_stage;
+        rp.src_row0 = cc * chunk;
+        rp.dst_row0 = lr;
+        rp.tp = tp;
+        FLUX_CUDA(launch_rs_reduce(rp, std::max(1, sm_count(rs.device)) * 2, rs.copy_stream));
+        ++c->last_launches;
+    }
+    // Every rank's stream continues after its owner's reduces.
+    for (int r : mine) {
+        RankState& rs = c->ranks[r];
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        FLUX_CUDA(cudaEventRecord(rs.copy_evt, rs.copy_stream));
+        FLUX_CUDA(cudaStreamWaitEvent(stream_for(c, r, streams), rs.copy_evt, 0));
+        FLUX_CUDA(cudaEventRecord(rs.kernel_evt, stream_for(c, r, streams)));
+    }
+    cleanup();
+    return FLUX_OK;
 }
 
 // ---------------------------------------------------------------------------

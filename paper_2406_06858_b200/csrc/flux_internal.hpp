@@ -161,7 +161,9 @@ struct GemmParams {
 struct RsReduceParams {
     const float* partials[kMaxRanks];  // per source rank: full [m, n] fp32 partial (peer pointers)
     void* c;
-    int ldc, out_f32, rpr, n, ld_src, owner, tp;
+    int ldc, out_f32, rows, n, ld_src, tp;
+    int src_row0;  // first partial row summed (global row)
+    int dst_row0;  // its row in C (the owner's local row)
 };
 
 // Host launchers (flux_kernels.cu).

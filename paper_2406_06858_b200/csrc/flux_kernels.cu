@@ -1575,15 +1575,16 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
 // run_nonoverlap RS branch, engine.cpp:595-602, and the WriteAlltoAll reduce
 // agent, engine.cpp:335-339): C[i, j] = sum_{s=0..tp-1} P_s[owner*rpr + i, j].
 __global__ void rs_reduce_kernel(RsReduceParams p) {
-    const long long total = static_cast<long long>(p.rpr) * p.n;
+    const long long total = static_cast<long long>(p.rows) * p.n;
     for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(idx / p.n), j = static_cast<int>(idx % p.n);
-        const long long src = (static_cast<long long>(p.owner) * p.rpr + i) * p.ld_src + j;
+        const long long src = (static_cast<long long>(p.src_row0) + i) * p.ld_src + j;
+        const long long dst = (static_cast<long long>(p.dst_row0) + i) * p.ldc + j;
         float acc = 0.0f;
         for (int s = 0; s < p.tp; ++s) acc += __ldcg(p.partials[s] + src);
-        if (p.out_f32) static_cast<float*>(p.c)[static_cast<long long>(i) * p.ldc + j] = acc;
-        else static_cast<__nv_bfloat16*>(p.c)[static_cast<long long>(i) * p.ldc + j] = __float2bfloat16_rn(acc);
+        if (p.out_f32) static_cast<float*>(p.c)[dst] = acc;
+        else static_cast<__nv_bfloat16*>(p.c)[dst] = __float2bfloat16_rn(acc);
     }
 }
 

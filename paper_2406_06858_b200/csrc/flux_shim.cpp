@@ -569,7 +569,20 @@ MediumResult run_medium_grained(const ProblemSpec& p, ShardedWorkspace& ws, cons
     validate_tiling(p, tile);
     MediumResult res;
     res.trace = medium_schedule(p, partitions);
-    res.outputs = run_nonoverlap(p, ws, tile);
+    ws.validate(p);
+    check_directory(ws);
+    ws.clear_outputs();
+    std::lock_guard<std::mutex> g(g_mu);
+    flux_comm* c = session_for(p);
+    upload_inputs(c, p, ws);
+    const flux_problem cp = cprob(p);
+    const flux_tile ct{tile.tm, tile.tn};
+    flux_opts o;
+    flux_default_opts(&o);
+    o.out_dtype = FLUX_F32;
+    ok(flux_medium_grained(c, &cp, &ct, partitions, &o, nullptr));
+    ok(flux_sync(c));
+    res.outputs = collect(c, p, ws).outputs;
     return res;
 }
 

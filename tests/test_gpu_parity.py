@@ -559,3 +559,28 @@ def test_dynamic_scheduler_bit_identical(pat, m, n, k, tp, monkeypatch):
         want = _oracle(p, a, b)
         for r in range(tp):
             np.testing.assert_allclose(dyn[r], want[r], rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("case", [(AG, 1024, 1024, 512, 4, 4), (AG, 1024, 768, 256, 4, 8), (AG, 64, 256, 128, 2, 4),
+                                  (RS, 1024, 512, 512, 4, 4), (RS, 2048, 1024, 256, 8, 16), (RS, 40, 24, 72, 4, 8),
+                                  (RS, 64, 64, 64, 1, 1)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_medium_grained_baseline(case):
+    """run_medium_grained (engine.hpp:144-145) on the device — chunked
+    transfers / GEMMs / reduces (B2) — matches the oracle; invalid partition
+    counts raise the reference's ConfigError."""
+    pat, m, n, k, tp, parts = case
+    p = fx.ProblemSpec(m, n, k, tp, pat)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=m + parts)
+        want = _oracle(p, a, b)
+        tile = fx.TileShape(p.rows_per_rank(), p.local_cols())
+        for f32 in (True, False):
+            comm.medium_grained(p, tile, parts, fx.default_opts(out_dtype=fx.F32 if f32 else fx.BF16))
+            comm.sync()
+            got = H.outputs(comm, p, f32)
+            for r in range(tp):
+                assert O.max_rel_error(got[r], want[r]) <= H.tol(f32, p.k), (f32, r)
+        if tp > 1:
+            with pytest.raises(fx.ConfigError, match="must be tp or 2\\*tp"):
+                comm.medium_grained(p, tile, 3 * tp)
