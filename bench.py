@@ -358,6 +358,9 @@ def our_arm(args, wl):
                     "cublas_gemm": b.gemm_only, "b1": b.unfused}
         if emulated and pattern == 0:
             variants["b2"] = b.decomposed
+        if emulated:  # the device decomposed baseline (flux_medium_grained, tp chunks)
+            tile_b2 = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
+            variants["b2_ours"] = lambda: comm.medium_grained(prob, tile_b2, tp, opts, streams)
         med = interleaved(variants, max(5, args.steps // 2))
         del b
         ms_f = med["fused"]
@@ -367,6 +370,7 @@ def our_arm(args, wl):
         extra = {
             "t_fused_ms": ms_f, "t_gemm_nonsplit_ms": t_gemm, "t_gemm_ours_ms": med["local"],
             "t_gemm_cublas_ms": med["cublas_gemm"], "t_unfused_cublas_ms": med["b1"], "t_decomposed_ms": med.get("b2"),
+            "t_decomposed_ours_ms": med.get("b2_ours"),
             "t_nonoverlap_ours_ms": med["nonoverlap"],
             "ect_fused_ms": ect_fused, "ect_unfused_ms": ect_b1,
             "overlap_efficiency": (1.0 - ect_fused / ect_b1) if ect_b1 > 0 else None,
