@@ -43,6 +43,7 @@ WORKLOADS = {
     "decode-rs-down-m16": (1, 16, 8192, 28672, 8, "decode GEMM-ReduceScatter Llama-2-70B MLP down-proj, M=16, TP=8"),
     "decode-rs-attn-m16": (1, 16, 8192, 8192, 8, "decode GEMM-ReduceScatter Llama-2-70B attention-out, M=16, TP=8"),
     "decode-ag-up-m128": (0, 128, 28672, 8192, 8, "decode AllGather-GEMM Llama-2-70B MLP up-proj, M=128 tokens, TP=8"),
+    "decode-ag-up-m256": (0, 256, 28672, 8192, 8, "decode AllGather-GEMM Llama-2-70B MLP up-proj, M=256 tokens, TP=8"),
     "decode-ag-up-m512": (0, 512, 28672, 8192, 8, "decode AllGather-GEMM Llama-2-70B MLP up-proj, M=512 tokens, TP=8"),
     "decode-rs-down-m256": (1, 256, 8192, 28672, 8, "decode GEMM-ReduceScatter Llama-2-70B MLP down-proj, M=256, TP=8"),
     "decode-rs-down-m512": (1, 512, 8192, 28672, 8, "decode GEMM-ReduceScatter Llama-2-70B MLP down-proj, M=512, TP=8"),
