@@ -210,11 +210,19 @@ def our_arm(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    # FLUX_BENCH_SHARE_GPU=1 (tests only): every rank on the visible GPUs modulo
+    # their count, gloo for the plumbing — runs the N>1 (IPC) path on a one-GPU box.
+    share = os.environ.get("FLUX_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = local_rank % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     # A real (non-legacy) stream: the library runs on it and the CUDA events
@@ -480,7 +488,7 @@ def our_arm(args, wl):
     achieved = flops_per_launch / (kms * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and emulated:  # captured at N=1 (every rank in one launch)
         try:
             with open(prof) as f:
                 traffic = json.load(f).get(wl)

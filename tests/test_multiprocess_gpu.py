@@ -28,3 +28,22 @@ def test_two_processes_ipc_match_oracle():
         assert len(res) == 20  # 9 operator cases, 3 torch ops, TPMlp GELU and SwiGLU (out, dx, dW_up, dW_down)
         for case, (err, tol) in res.items():
             assert err <= tol, (case, err, tol)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["llama70b-up-ag", "llama70b-down-rs"])
+def test_bench_two_ranks_ipc_path(workload):
+    """bench.py's N>1 path (one process per rank, IPC communicator, max-over-ranks
+    timing, rank 0 prints one JSON line), with both ranks sharing this box's GPU
+    (FLUX_BENCH_SHARE_GPU=1: gloo plumbing instead of NCCL)."""
+    env = dict(os.environ, FLUX_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29541", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--quick", "--no-cpu-baseline", "--workload", workload]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    print(out.stdout[-3000:], out.stderr[-3000:])
+    assert out.returncode == 0
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["tp"] == 2 and d["value"] > 0
