@@ -170,6 +170,9 @@ def run_cpu_reference(pattern, m, n, k, tp, reps=1):
 
 def reference_arm(args, wl):
     pattern, m, n, k, tp, desc = WORKLOADS[wl]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        tp = world  # the same TP = N problem as our arm's N>1 run
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
