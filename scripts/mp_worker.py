@@ -157,5 +157,9 @@ results["swiglu-dw_up"] = (_nerr(mod2.w_up.grad, wur2[rank].grad), 3e-2)
 results["swiglu-dw_down"] = (_nerr(mod2.w_down.grad, wdr2[rank].grad), 3e-2)
 dist.barrier()
 comm.close()
-print("RESULT", rank, json.dumps(results), flush=True)
+for turn in range(world):  # one rank at a time: the two lines must not interleave on the shared stdout
+    if turn == rank:
+        sys.stdout.write("RESULT %d %s\n" % (rank, json.dumps(results)))
+        sys.stdout.flush()
+    dist.barrier()
 dist.destroy_process_group()
