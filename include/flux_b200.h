@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FLUX_ABI_VERSION 5
+#define FLUX_ABI_VERSION 6
 
 /* Return codes. The reference raises C++ exceptions (errors.hpp:9-31); each
  * maps to one code. The C++ shim (include/flux/overlap.hpp) rethrows them. */
@@ -42,7 +42,9 @@ typedef enum {
     FLUX_ERR_DIRECTORY = 3, /* overlap::DirectoryError (peer mapping missing) */
     FLUX_ERR_DEADLOCK = 4,  /* overlap::DeadlockError (device wait timed out) */
     FLUX_ERR_BOUNDS = 5,    /* overlap::BoundsError   */
-    FLUX_ERR_CUDA = 6       /* CUDA runtime / driver failure */
+    FLUX_ERR_CUDA = 6,      /* CUDA runtime / driver failure */
+    FLUX_ERR_RUNTIME = 7    /* std::runtime_error: a signal flag set twice in one operator
+                               (SignalBoard::set -> false, engine.cpp:401-403) */
 } flux_status;
 
 /* overlap::Pattern (problem.hpp:10) */
@@ -301,6 +303,26 @@ int flux_comm_set_timing(flux_comm* comm, int enable);
 int flux_trace_read(flux_comm* comm, int rank, const flux_problem* problem, void* out,
                     size_t max_records, size_t* count);
 int flux_last_kernel_ms(flux_comm* comm, float* ms);
+
+/* ---- fault injection and checking (tests; reference acceptance.cpp:121-158,
+ * spin_wait engine.cpp:149-162, SignalBoard signal_board.hpp:25-28) ---------
+ * Arms a fault for the NEXT operator only: DROP_SIGNAL never raises signal
+ * `index` of rank `rank`'s flag table, so the waiter times out after
+ * opts.wall_budget_s and flux_sync returns FLUX_ERR_DEADLOCK naming the flag;
+ * DOUBLE_SIGNAL raises it twice. Signal index per table: AllGather copy-engine
+ * flags: comm tile (row / rows_per_comm_tile); AllGather in-kernel transfer:
+ * 128-row group of a_agg; GEMM-RS: output tile * tp + source rank (tile =
+ * 128-row tile row * ceil(n / 256) + 256-column tile). A device failure is also
+ * reported by the next operator call (FLUX_ERR_DEADLOCK / FLUX_ERR_RUNTIME,
+ * without synchronising) until flux_sync clears it. */
+typedef enum { FLUX_FAULT_NONE = 0, FLUX_FAULT_DROP_SIGNAL = 1, FLUX_FAULT_DOUBLE_SIGNAL = 2 } flux_fault_kind;
+int flux_comm_inject_fault(flux_comm* comm, int kind, int rank, int index);
+/* Double-set detector for the device-stamped GEMM-RS flags (an exchange that
+ * checks the previous stamp instead of a plain store): a second stamp in one
+ * operator makes flux_sync return FLUX_ERR_RUNTIME "flag i on rank r set
+ * twice". Copy-engine AllGather flags are always checked on the host (the
+ * operator call itself returns FLUX_ERR_RUNTIME). */
+int flux_comm_set_check_double_set(flux_comm* comm, int enable);
 
 #ifdef __cplusplus
 } /* extern "C" */

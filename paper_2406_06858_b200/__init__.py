@@ -7,8 +7,9 @@ reference's operator API over that ABI.
 from . import _native
 from ._native import (ALLGATHER_GEMM, GEMM_REDUCESCATTER, PULL, PUSH, WRITE_ALLTOALL, FUSED_REDUCE,
                       SWIZZLE_NAIVE, SWIZZLE_RANK_SHIFTED, SWIZZLE_ARRIVAL_ALIGNED, BF16, F32,
-                      ConfigError, ShapeError, DirectoryError, DeadlockError, BoundsError, CudaError,
-                      FluxError, default_opts, ACT_NONE, ACT_GELU, ACT_RELU, ACT_SILU, ACT_SWIGLU, B_NK, B_KN)
+                      ConfigError, ShapeError, DirectoryError, DeadlockError, BoundsError, CudaError, SignalError,
+                      FluxError, default_opts, ACT_NONE, ACT_GELU, ACT_RELU, ACT_SILU, ACT_SWIGLU, B_NK, B_KN,
+                      FAULT_NONE, FAULT_DROP_SIGNAL, FAULT_DOUBLE_SIGNAL)
 from .comm import (Communicator, MlpSpec, ProblemSpec, TileShape, comm_order, grid_for, make_comm_spec,
                    required_heap_bytes, tile_order, validate_tiling)
 

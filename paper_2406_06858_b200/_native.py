@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libflux_b200.so")
 
 # Return codes (flux_status) -> reference exception taxonomy (errors.hpp:9-31).
-OK, ERR_CONFIG, ERR_SHAPE, ERR_DIRECTORY, ERR_DEADLOCK, ERR_BOUNDS, ERR_CUDA = range(7)
+OK, ERR_CONFIG, ERR_SHAPE, ERR_DIRECTORY, ERR_DEADLOCK, ERR_BOUNDS, ERR_CUDA, ERR_RUNTIME = range(8)
 ALLGATHER_GEMM, GEMM_REDUCESCATTER = 0, 1
 PULL, PUSH = 0, 1
 WRITE_ALLTOALL, FUSED_REDUCE = 0, 1
@@ -21,7 +21,8 @@ SWIZZLE_NAIVE, SWIZZLE_RANK_SHIFTED, SWIZZLE_ARRIVAL_ALIGNED = 0, 1, 2
 BF16, F32 = 0, 1
 BUF_A_SHARD, BUF_B_SHARD, BUF_A_AGG, BUF_C_OUT, BUF_STAGING, BUF_C_OUT_F32 = 0, 1, 2, 3, 4, 5
 ACT_NONE, ACT_GELU, ACT_RELU, ACT_SILU, ACT_SWIGLU = 0, 1, 2, 3, 4
-ABI_VERSION = 5
+ABI_VERSION = 6
+FAULT_NONE, FAULT_DROP_SIGNAL, FAULT_DOUBLE_SIGNAL = 0, 1, 2
 B_NK, B_KN = 0, 1
 
 
@@ -53,8 +54,13 @@ class CudaError(FluxError):
     code = ERR_CUDA
 
 
+class SignalError(FluxError):
+    """std::runtime_error of the reference: a flag set twice (engine.cpp:401-403)."""
+    code = ERR_RUNTIME
+
+
 _EXC = {ERR_CONFIG: ConfigError, ERR_SHAPE: ShapeError, ERR_DIRECTORY: DirectoryError,
-        ERR_DEADLOCK: DeadlockError, ERR_BOUNDS: BoundsError, ERR_CUDA: CudaError}
+        ERR_DEADLOCK: DeadlockError, ERR_BOUNDS: BoundsError, ERR_CUDA: CudaError, ERR_RUNTIME: SignalError}
 
 
 class Problem(C.Structure):
@@ -152,6 +158,8 @@ _SIGS = {
     "flux_mlp_forward": (C.c_int, [C.c_void_p, _P(Mlp), _P(Opts), _P(C.c_void_p), _P(MlpOperands)]),
     "flux_mlp_backward_dx": (C.c_int, [C.c_void_p, _P(Mlp), _P(Opts), _P(C.c_void_p), _P(MlpGradOperands)]),
     "flux_mlp_required_heap_bytes": (C.c_size_t, [_P(Mlp)]),
+    "flux_comm_inject_fault": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int]),
+    "flux_comm_set_check_double_set": (C.c_int, [C.c_void_p, C.c_int]),
 }
 
 # Symbols include/flux_b200.h declares (tests check the library exports all of them).

@@ -150,13 +150,17 @@ class Communicator:
     emulated on one GPU). IPC mode: one process per GPU, see `Communicator.ipc`.
     """
 
-    def __init__(self, tp: int, devices: Optional[Sequence[int]] = None, heap_bytes: int = 0, *, _handle=None):
+    def __init__(self, tp: int, devices: Optional[Sequence[int]] = None, heap_bytes: int = 0, *, _handle=None,
+                 device: Optional[int] = None):
         self.tp = tp
         self._h = C.c_void_p(_handle) if _handle is not None else C.c_void_p()
         if _handle is None:
             devs = (C.c_int * tp)(*(devices if devices is not None else [0] * tp))
             N.check(N.lib().flux_comm_create(tp, devs, C.byref(N.CommOpts(heap_bytes)), C.byref(self._h)))
         self.rank = N.lib().flux_comm_rank(self._h)
+        # The device this process drives (single device or IPC mode), else None.
+        devs_l = list(devices) if devices is not None else [0] * tp
+        self.device = device if device is not None else (devs_l[0] if len(set(devs_l)) == 1 else None)
 
     @classmethod
     def ipc(cls, rank: int, tp: int, device: int, heap_bytes: int,
@@ -172,7 +176,7 @@ class Communicator:
         blobs = all_gather_bytes(blob.raw)
         joined = C.create_string_buffer(b"".join(blobs), nb * tp)
         N.check(N.lib().flux_comm_ipc_connect(h, joined))
-        return cls(tp, _handle=h.value)
+        return cls(tp, _handle=h.value, device=device)
 
     # ---- buffers -------------------------------------------------------------
     def buffer(self, rank: int, kind: int, problem: ProblemSpec) -> N.BufferDesc:
@@ -269,6 +273,14 @@ class Communicator:
         v = C.c_float()
         N.check(N.lib().flux_last_kernel_ms(self._h, C.byref(v)))
         return float(v.value)
+
+    def inject_fault(self, kind: int, rank: int = 0, index: int = 0) -> None:
+        """Arm a fault for the next operator (flux_comm_inject_fault): drop or
+        double one signal of `rank`'s flag table."""
+        N.check(N.lib().flux_comm_inject_fault(self._h, kind, rank, index))
+
+    def set_check_double_set(self, enable: bool = True) -> None:
+        N.check(N.lib().flux_comm_set_check_double_set(self._h, int(enable)))
 
     def drop_peer(self, from_rank: int, peer_rank: int) -> None:
         N.check(N.lib().flux_comm_drop_peer(self._h, from_rank, peer_rank))

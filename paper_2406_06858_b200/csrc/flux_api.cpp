@@ -8,6 +8,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -102,12 +103,26 @@ int write_value(cudaStream_t s, void* addr, uint32_t v) {
 // work queued after the wait.
 int wait_value_geq(cudaStream_t s, const void* addr, uint32_t v) {
     if (v == 0) return FLUX_OK;  // epoch 0 is always satisfied
-    static const unsigned flush = [] {
-        int dev = 0, can = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&can, cudaDevAttrCanFlushRemoteWrites, dev);
-        return can ? static_cast<unsigned>(CU_STREAM_WAIT_VALUE_FLUSH) : 0u;
-    }();
+    // The flush capability is a property of the device the stream belongs to
+    // (callers set it current): cached per device, -1 = not probed yet.
+    static std::atomic<int> flush_cap[64] = {};
+    static std::once_flag init;
+    std::call_once(init, [] {
+        for (auto& f : flush_cap) f.store(-1);
+    });
+    int dev = 0;
+    cudaGetDevice(&dev);
+    unsigned flush = 0;
+    if (dev >= 0 && dev < 64) {
+        int cap = flush_cap[dev].load(std::memory_order_acquire);
+        if (cap < 0) {
+            int can = 0;
+            cudaDeviceGetAttribute(&can, cudaDevAttrCanFlushRemoteWrites, dev);
+            cap = can ? 1 : 0;
+            flush_cap[dev].store(cap, std::memory_order_release);
+        }
+        flush = cap ? static_cast<unsigned>(CU_STREAM_WAIT_VALUE_FLUSH) : 0u;
+    }
     CUresult r = driver().wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
                                  CU_STREAM_WAIT_VALUE_GEQ | flush);
     if (r != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "cuStreamWaitValue32 failed (" + S(r) + ")");
@@ -429,7 +444,27 @@ struct flux_comm {
     uint32_t launch_seq = 0;                      // fused launches so far (tags the tail-split counters)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernel_events;  // per device group
     int kernel_events_used = 0;
-    std::map<std::pair<int, std::vector<uint32_t>>, uint32_t*> order_cache;  // (device, schedule) -> table
+    // Device copies of tile schedules / piece tables, keyed by (device, content
+    // hash), bounded (least recently used evicted; tables a CUDA graph captured
+    // are kept for the communicator's lifetime).
+    struct OrderEntry {
+        int device = 0;
+        uint64_t hash = 0;
+        std::vector<uint32_t> table;
+        uint32_t* dev = nullptr;     // device copy
+        uint32_t* staged = nullptr;  // pinned host copy the asynchronous upload reads
+        uint64_t last_use = 0;
+        bool captured = false;
+    };
+    std::vector<OrderEntry> order_cache;
+    uint64_t order_clock = 0;
+    uint32_t* err_host = nullptr;  // host-mapped error mirror [tp][4] (device waits write it on timeout)
+    // Fault injection (flux_comm_inject_fault): armed for the next operator,
+    // active while that operator enqueues its work.
+    int fault_kind = 0, fault_rank = 0, fault_index = 0;
+    int act_fault_kind = 0, act_fault_rank = 0, act_fault_index = 0;
+    bool check_double = false;      // flux_comm_set_check_double_set
+    std::string host_error;         // host-detected failure of the last operator (flag set twice)
 };
 
 namespace {
@@ -437,6 +472,53 @@ namespace {
 int check_comm(flux_comm* c) {
     if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
     if (c->ipc && !c->connected) return fail(FLUX_ERR_DIRECTORY, "IPC communicator not connected");
+    return FLUX_OK;
+}
+
+// Message of a device error record {code, info0, info1, info2} of rank r
+// (the reference's DeadlockError / "set twice" texts, engine.cpp:149-162,401-403).
+std::string error_text(const uint32_t* err, int r) {
+    if (err[0] == kErrAgFlagTimeout)
+        return "deadlock budget exhausted waiting for signal " + S(err[1]) + " for tile (" + S(err[2] >> 16) + "," +
+               S(err[2] & 0xFFFF) + ") on rank " + S(r);
+    if (err[0] == kErrDoubleSet) return "flag " + S(err[1]) + " on rank " + S(err[2]) + " set twice";
+    return "deadlock budget exhausted waiting for partial of tile " + S(err[1]) + " from source " + S(err[2]) +
+           " on rank " + S(r);
+}
+
+int code_of(uint32_t device_code) { return device_code == kErrDoubleSet ? FLUX_ERR_RUNTIME : FLUX_ERR_DEADLOCK; }
+
+// Operator entry: the communicator is usable and no earlier operator left a
+// device failure behind. Device waits that time out write their record into a
+// host-mapped mirror as well, so this check needs no synchronisation; the
+// failure stays reported until flux_sync clears it. Also activates a fault
+// armed by flux_comm_inject_fault for this operator.
+int begin_op(flux_comm* c) {
+    FLUX_TRY(check_comm(c));
+    if (c->err_host) {
+        for (int r = 0; r < c->tp; ++r) {
+            if (!c->ranks[r].local) continue;
+            const volatile uint32_t* h = c->err_host + 4 * r;
+            if (h[0] != 0) {
+                const uint32_t e[4] = {h[0], h[1], h[2], h[3]};
+                return fail(code_of(e[0]), "a previous operator failed on the device (" + error_text(e, r) +
+                                               "); flux_sync reports and clears it");
+            }
+        }
+    }
+    c->act_fault_kind = c->fault_kind;
+    c->act_fault_rank = c->fault_rank;
+    c->act_fault_index = c->fault_index;
+    c->fault_kind = 0;
+    c->host_error.clear();
+    return FLUX_OK;
+}
+
+// Operator exit: a host-detected failure (a copy-engine flag the transfer loop
+// set twice, engine.cpp:401-403) is raised once every piece of work is enqueued.
+int end_op(flux_comm* c) {
+    c->act_fault_kind = 0;
+    if (!c->host_error.empty()) return fail(FLUX_ERR_RUNTIME, c->host_error);
     return FLUX_OK;
 }
 
@@ -467,6 +549,16 @@ int alloc_heap(RankState& r, size_t bytes) {
     FLUX_CUDA(cudaDeviceSynchronize());
     r.heap = static_cast<char*>(p);
     r.owned = true;
+    return FLUX_OK;
+}
+
+// Host-mapped, zeroed error mirror ([tp][4] u32; UVA: the host pointer is the
+// device address).
+int alloc_err_host(flux_comm* c) {
+    void* h = nullptr;
+    FLUX_CUDA(cudaHostAlloc(&h, sizeof(uint32_t) * 4 * kMaxRanks, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(h, 0, sizeof(uint32_t) * 4 * kMaxRanks);
+    c->err_host = static_cast<uint32_t*>(h);
     return FLUX_OK;
 }
 
@@ -532,20 +624,67 @@ int mark_op_done(flux_comm* c, void* const* streams, uint32_t e) {
     return FLUX_OK;
 }
 
-int upload_order(flux_comm* c, int device, const std::vector<uint32_t>& order, uint32_t** out) {
-    auto key = std::make_pair(device, order);
-    auto it = c->order_cache.find(key);
-    if (it != c->order_cache.end()) {
-        *out = it->second;
-        return FLUX_OK;
+constexpr size_t kOrderCacheCap = 256;
+
+uint64_t fnv1a(const std::vector<uint32_t>& v) {
+    uint64_t h = 1469598103934665603ull ^ v.size();
+    for (uint32_t x : v) {
+        h ^= x;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+void free_order_entry(flux_comm::OrderEntry& e) {
+    cudaSetDevice(e.device);
+    if (e.dev) cudaFree(e.dev);  // synchronises the device: no enqueued kernel still reads it
+    if (e.staged) cudaFreeHost(e.staged);
+    e.dev = nullptr;
+    e.staged = nullptr;
+}
+
+// Device copy of a schedule table for `device`, uploaded asynchronously on
+// `stream` (from a pinned copy that lives as long as the entry) on first use.
+// A miss costs one cudaMalloc; no host synchronisation on the launch path, and
+// a miss during CUDA-graph capture becomes a memcpy node of the graph (the
+// entry is then never evicted).
+int upload_order(flux_comm* c, int device, const std::vector<uint32_t>& order, uint32_t** out, cudaStream_t stream) {
+    const uint64_t h = fnv1a(order);
+    ++c->order_clock;
+    for (auto& e : c->order_cache) {
+        if (e.device == device && e.hash == h && e.table == order) {
+            e.last_use = c->order_clock;
+            *out = e.dev;
+            return FLUX_OK;
+        }
+    }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (stream) FLUX_CUDA(cudaStreamIsCapturing(stream, &cap));
+    if (c->order_cache.size() >= kOrderCacheCap && cap == cudaStreamCaptureStatusNone) {
+        size_t victim = c->order_cache.size();
+        for (size_t i = 0; i < c->order_cache.size(); ++i)
+            if (!c->order_cache[i].captured &&
+                (victim == c->order_cache.size() || c->order_cache[i].last_use < c->order_cache[victim].last_use))
+                victim = i;
+        if (victim < c->order_cache.size()) {
+            free_order_entry(c->order_cache[victim]);
+            c->order_cache.erase(c->order_cache.begin() + static_cast<long>(victim));
+        }
     }
     FLUX_CUDA(cudaSetDevice(device));
-    uint32_t* d = nullptr;
-    const size_t bytes = order.size() * sizeof(uint32_t);
-    FLUX_CUDA(cudaMalloc(&d, bytes));
-    FLUX_CUDA(cudaMemcpy(d, order.data(), bytes, cudaMemcpyHostToDevice));
-    c->order_cache.emplace(std::move(key), d);
-    *out = d;
+    flux_comm::OrderEntry e;
+    e.device = device;
+    e.hash = h;
+    e.table = order;
+    e.last_use = c->order_clock;
+    e.captured = cap != cudaStreamCaptureStatusNone;
+    const size_t bytes = std::max<size_t>(1, order.size()) * sizeof(uint32_t);
+    FLUX_CUDA(cudaMalloc(&e.dev, bytes));
+    FLUX_CUDA(cudaHostAlloc(&e.staged, bytes, cudaHostAllocPortable));
+    if (!order.empty()) std::memcpy(e.staged, order.data(), order.size() * sizeof(uint32_t));
+    FLUX_CUDA(cudaMemcpyAsync(e.dev, e.staged, bytes, cudaMemcpyHostToDevice, stream));
+    *out = e.dev;
+    c->order_cache.push_back(std::move(e));
     return FLUX_OK;
 }
 
@@ -688,7 +827,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 for (size_t i = T - tail; i < T; ++i) push(li, i);
         }
         uint32_t* order_dev = nullptr;
-        FLUX_TRY(upload_order(c, dev, order, &order_dev));
+        FLUX_TRY(upload_order(c, dev, order, &order_dev, lead));
         prm.order = order_dev;
         prm.num_tiles = static_cast<int>(order.size());
         prm.m = m_rows;
@@ -724,6 +863,11 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         prm.red_ctr = at<uint32_t>(c->ranks[g[0]], kCtrlRedCtr);
         prm.red_exit = at<uint32_t>(c->ranks[g[0]], kCtrlRedExit);
         if (const char* env = std::getenv("FLUX_DEBUG")) prm.dbg = std::atoi(env);  // profiling ablations only
+        prm.err_host = c->err_host;
+        prm.fault_kind = c->act_fault_kind;
+        prm.fault_rank = c->act_fault_rank;
+        prm.fault_index = c->act_fault_index;
+        prm.check_double = c->check_double ? 1 : 0;
         // Join the other local ranks' streams into the launch stream.
         for (size_t li = 0; li < g.size(); ++li) {
             cudaStream_t s = stream_for(c, g[li], streams);
@@ -933,6 +1077,7 @@ int flux_comm_create(int tp, const int* devices, const flux_comm_opts* opts, flu
         rs.device = devices ? devices[r] : 0;
         rs.local = true;
         int rc = alloc_heap(rs, c->heap_bytes);
+        if (rc == FLUX_OK && r == 0) rc = alloc_err_host(c);
         if (rc == FLUX_OK) rc = init_rank_streams(rs);
         if (rc != FLUX_OK) {
             std::string msg = g_last_error;
@@ -978,6 +1123,7 @@ int flux_comm_create_ipc(int rank, int tp, int device, const flux_comm_opts* opt
     me.device = device;
     me.local = true;
     int rc = alloc_heap(me, c->heap_bytes);
+    if (rc == FLUX_OK) rc = alloc_err_host(c);
     if (rc == FLUX_OK) rc = init_rank_streams(me);
     if (rc != FLUX_OK) {
         std::string msg = g_last_error;
@@ -1064,14 +1210,12 @@ int flux_comm_destroy(flux_comm* c) {
         if (rs.kernel_evt) cudaEventDestroy(rs.kernel_evt);
         if (rs.copy_evt) cudaEventDestroy(rs.copy_evt);
     }
-    for (auto& kv : c->order_cache) {
-        cudaSetDevice(kv.first.first);
-        cudaFree(kv.second);
-    }
+    for (auto& e : c->order_cache) free_order_entry(e);
     for (auto& pr : c->kernel_events) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);
     }
+    if (c->err_host) cudaFreeHost(c->err_host);
     delete c;
     return FLUX_OK;
 }
@@ -1273,8 +1417,48 @@ static int graph_opts(flux_comm* c, const flux_problem* p, const flux_opts* opts
     return FLUX_OK;
 }
 
+// Every operator runs between begin_op (pending device failure check, fault
+// activation) and end_op (host-detected failures).
+static int run_op(flux_comm* c, const std::function<int()>& body) {
+    FLUX_TRY(begin_op(c));
+    const int rc = body();
+    if (rc != FLUX_OK) {
+        c->act_fault_kind = 0;
+        return rc;
+    }
+    return end_op(c);
+}
+
+static int ag_gemm_ex_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
+                           int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands);
+static int gemm_rs_ex_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
+                           const flux_opts* opts, void* const* streams, const flux_operands* operands);
+static int local_gemm_body(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams);
+static int nonoverlap_body(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams);
+static int medium_grained_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int partitions,
+                               const flux_opts* opts, void* const* streams);
+
 int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer, int swizzle_on,
                     const flux_opts* opts, void* const* streams, const flux_operands* operands) {
+    return run_op(c, [&] { return ag_gemm_ex_body(c, p, tile, rpct, transfer, swizzle_on, opts, streams, operands); });
+}
+int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
+                    const flux_opts* opts, void* const* streams, const flux_operands* operands) {
+    return run_op(c, [&] { return gemm_rs_ex_body(c, p, tile, write_mode, swizzle_on, opts, streams, operands); });
+}
+int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
+    return run_op(c, [&] { return local_gemm_body(c, p, opts, streams); });
+}
+int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
+    return run_op(c, [&] { return nonoverlap_body(c, p, opts, streams); });
+}
+int flux_medium_grained(flux_comm* c, const flux_problem* p, const flux_tile* tile, int partitions,
+                        const flux_opts* opts, void* const* streams) {
+    return run_op(c, [&] { return medium_grained_body(c, p, tile, partitions, opts, streams); });
+}
+
+static int ag_gemm_ex_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
+                           int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands) {
     flux_opts o;
     FLUX_TRY(graph_opts(c, p, opts, transfer, &o));
     if (!o.graph_safe) return ag_gemm_impl(c, p, tile, rpct, transfer, swizzle_on, &o, streams, operands);
@@ -1284,8 +1468,8 @@ int flux_ag_gemm_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     return ag_gemm_impl(c, p, tile, rpct, transfer, swizzle_on, &o, streams, operands);
 }
 
-int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
-                    const flux_opts* opts, void* const* streams, const flux_operands* operands) {
+static int gemm_rs_ex_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
+                           const flux_opts* opts, void* const* streams, const flux_operands* operands) {
     flux_opts o;
     FLUX_TRY(graph_opts(c, p, opts, -1, &o));
     if (!o.graph_safe) return gemm_rs_impl(c, p, tile, write_mode, swizzle_on, &o, streams, operands);
@@ -1297,7 +1481,7 @@ int flux_gemm_rs_ex(flux_comm* c, const flux_problem* p, const flux_tile* tile, 
     return gemm_rs_impl(c, p, tile, write_mode, swizzle_on, &o, streams, operands);
 }
 
-int flux_local_gemm(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
+static int local_gemm_body(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
     flux_opts o;
     FLUX_TRY(graph_opts(c, p, opts, -1, &o));
     if (!o.graph_safe) return local_gemm_impl(c, p, &o, streams);
@@ -1461,7 +1645,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
                     for (int step = 0; step < tp; ++step) add_block(static_cast<int>(li), blocks[g[li]][step]);
             }
             uint32_t* jobs_dev = nullptr;
-            FLUX_TRY(upload_order(c, c->ranks[g[0]].device, jobs, &jobs_dev));
+            FLUX_TRY(upload_order(c, c->ranks[g[0]].device, jobs, &jobs_dev, stream_for(c, g[0], streams)));
             prm.sm_transfer = 1;
             prm.ag_push = push ? 1 : 0;
             for (int q = 0; q < tp; ++q) prm.kdone[q] = at<uint32_t>(c->ranks[q], kCtrlKdone);
@@ -1548,6 +1732,21 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         return FLUX_OK;
     };
     const int per_peer = rpr / rpct;
+    // SignalBoard::set semantics (signal_board.hpp:25-28, engine.cpp:401-403):
+    // every comm-tile flag is raised once per operator; a second set is an
+    // error (the transfer loop enqueues every flag write, so the host checks).
+    // Fault injection drops or doubles one flag write.
+    std::vector<std::vector<uint8_t>> raised(tp, std::vector<uint8_t>(static_cast<size_t>(p->m / rpct), 0));
+    auto set_flag = [&](cudaStream_t cs, int r, int f) -> int {
+        const bool hit = c->act_fault_kind != 0 && c->act_fault_rank == r && c->act_fault_index == f;
+        if (hit && c->act_fault_kind == FLUX_FAULT_DROP_SIGNAL) return FLUX_OK;
+        for (int rep = 0; rep < (hit ? 2 : 1); ++rep) {
+            if (++raised[r][f] > 1 && c->host_error.empty())
+                c->host_error = "flag " + S(f) + " on rank " + S(r) + " set twice";
+            FLUX_TRY(write_value(cs, at<uint32_t>(c->ranks[r], kAgFlagOffset) + f, e));
+        }
+        return FLUX_OK;
+    };
     for (const auto& g : groups) {
         RankState& lead = c->ranks[g[0]];
         FLUX_CUDA(cudaSetDevice(lead.device));
@@ -1578,8 +1777,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
             FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(r) * rpr * rowbytes, rowbytes, shard,
                                pitch, rpr));
             FLUX_TRY(write_value(cs, rs.heap + kCtrlReady, e));
-            for (int f = r * rpr / rpct; f < (r + 1) * rpr / rpct; ++f)
-                FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + f, e));
+            for (int f = r * rpr / rpct; f < (r + 1) * rpr / rpct; ++f) FLUX_TRY(set_flag(cs, r, f));
             return FLUX_OK;
         };
         // Transfers in the order the kernel consumes them: rank-major when the
@@ -1608,7 +1806,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
                         FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
                                            rowbytes, shard + static_cast<size_t>(d.row_begin - b * rpr) * pitch, pitch,
                                            d.rows));
-                        FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
+                        FLUX_TRY(set_flag(cs, cr, d.row_begin / rpct));
                     }
                 }
             }
@@ -1650,14 +1848,14 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
                                            qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
                                            d.rows));
                     }
-                    FLUX_TRY(write_value(cs, at<uint32_t>(rs, kAgFlagOffset) + d.row_begin / rpct, e));
+                    FLUX_TRY(set_flag(cs, r, d.row_begin / rpct));
                 } else {
                     if (first && !in_group(q)) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlKdone, e - 1));
                     // Push reads from my own a_agg slot (already holds my shard).
                     FLUX_TRY(copy_rows(cs, qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
                                        rowbytes, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
                                        rowbytes, d.rows));
-                    FLUX_TRY(write_value(cs, at<uint32_t>(qs, kAgFlagOffset) + d.row_begin / rpct, e));
+                    FLUX_TRY(set_flag(cs, q, d.row_begin / rpct));
                 }
             }
         }
@@ -1814,8 +2012,7 @@ static int local_gemm_impl(flux_comm* c, const flux_problem* p, const flux_opts*
                          static_cast<long long>(layout_for(p).staging.off));
 }
 
-int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
-    FLUX_TRY(check_comm(c));
+static int nonoverlap_body(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams) {
     if (opts && opts->graph_safe) return fail(FLUX_ERR_CONFIG, "graph_safe applies to the fused operators and the local GEMM");
     FLUX_TRY(validate_problem(p));
     FLUX_TRY(check_heap(c, p));
@@ -1921,9 +2118,8 @@ int flux_nonoverlap(flux_comm* c, const flux_problem* p, const flux_opts* opts, 
 // plain kernel over the tiles holding the chunk's rows — waits for its event;
 // RS: each chunk's GEMM writes fp32 partials, then the owner's source-ordered
 // reduce of those rows runs on the copy stream while the next chunk computes.
-int flux_medium_grained(flux_comm* c, const flux_problem* p, const flux_tile* tile, int partitions,
-                        const flux_opts* opts, void* const* streams) {
-    FLUX_TRY(check_comm(c));
+static int medium_grained_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int partitions,
+                               const flux_opts* opts, void* const* streams) {
     if (c->ipc) return fail(FLUX_ERR_CONFIG, "the medium-grained baseline runs on single-process communicators");
     if (opts && opts->graph_safe) return fail(FLUX_ERR_CONFIG, "graph_safe applies to the fused operators and the local GEMM");
     FLUX_TRY(validate_tiling(p, tile));
@@ -2134,6 +2330,7 @@ int flux_mlp_backward_dx(flux_comm* c, const flux_mlp* mlp, const flux_opts* opt
 int flux_sync(flux_comm* c) {
     if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
     std::string deadlock;
+    int code = FLUX_ERR_DEADLOCK;
     for (int r = 0; r < c->tp; ++r) {
         RankState& rs = c->ranks[r];
         if (!rs.local) continue;
@@ -2144,19 +2341,19 @@ int flux_sync(flux_comm* c) {
         FLUX_CUDA(cudaMemcpy(err, rs.heap + kCtrlErr, sizeof(err), cudaMemcpyDeviceToHost));
         if (err[0] != 0) {
             if (deadlock.empty()) {
-                if (err[0] == kErrAgFlagTimeout)
-                    deadlock = "deadlock budget exhausted waiting for signal " + S(err[1]) + " for tile (" +
-                               S(err[2] >> 16) + "," + S(err[2] & 0xFFFF) + ") on rank " + S(r);
-                else
-                    deadlock = "deadlock budget exhausted waiting for partial of tile " + S(err[1]) + " from source " +
-                               S(err[2]) + " on rank " + S(r);
+                deadlock = error_text(err, r);
+                code = code_of(err[0]);
             }
-            const uint32_t zero[4] = {0, 0, 0, 0};
-            FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlErr, zero, sizeof(zero), cudaMemcpyHostToDevice));
+            // Clean state for the next operator: the error record and epoch,
+            // the launch-scoped work counters a failed launch may have left
+            // armed (dynamic tiles, reduction units), the host mirror.
+            const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlErr, zero, 20, cudaMemcpyHostToDevice));
             FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlDynCtr, zero, 16, cudaMemcpyHostToDevice));  // + reduction counters
         }
+        if (c->err_host) std::memset(c->err_host + 4 * r, 0, 16);
     }
-    if (!deadlock.empty()) return fail(FLUX_ERR_DEADLOCK, deadlock);
+    if (!deadlock.empty()) return fail(code, deadlock);
     return FLUX_OK;
 }
 
@@ -2175,6 +2372,23 @@ int flux_trace_read(flux_comm* c, int rank, const flux_problem* p, void* out, si
     size_t k = std::min<size_t>(std::min<size_t>(n, kTraceBytes / 16), max_records);
     if (k) FLUX_CUDA(cudaMemcpy(out, rs.heap + layout_for(p).trace_off, k * 16, cudaMemcpyDeviceToHost));
     if (count) *count = k;
+    return FLUX_OK;
+}
+
+int flux_comm_inject_fault(flux_comm* c, int kind, int rank, int index) {
+    if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
+    if (kind < FLUX_FAULT_NONE || kind > FLUX_FAULT_DOUBLE_SIGNAL) return fail(FLUX_ERR_CONFIG, "unknown fault kind");
+    if (kind != FLUX_FAULT_NONE && (rank < 0 || rank >= c->tp || index < 0))
+        return fail(FLUX_ERR_CONFIG, "fault target out of range");
+    c->fault_kind = kind;
+    c->fault_rank = rank;
+    c->fault_index = index;
+    return FLUX_OK;
+}
+
+int flux_comm_set_check_double_set(flux_comm* c, int enable) {
+    if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
+    c->check_double = enable != 0;
     return FLUX_OK;
 }
 

@@ -32,6 +32,7 @@ enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2, kModeRSUnits =
 // two launch-scoped work counters (dynamic tiles, reduction units) are re-armed
 // by the last CTA / group of the launch that used them.
 constexpr size_t kCtrlErr = 0;          // u32[4]: code, info0, info1, info2
+constexpr size_t kCtrlErrEpoch = 16;    // u32: epoch of the operator whose wait recorded the error
 constexpr size_t kCtrlReady = 64;       // u32: epoch at which this rank's A shard is staged (AG pull source ready)
 constexpr size_t kCtrlDone = 68;        // u32: epoch whose peer pulls this rank has finished
 constexpr size_t kCtrlKdone = 72;       // u32: epoch whose kernel finished on this rank (push targets)
@@ -69,6 +70,11 @@ constexpr size_t kDataOffset = 1 << 20;
 // Error codes written by device waits into the control block.
 constexpr uint32_t kErrAgFlagTimeout = 1;
 constexpr uint32_t kErrRsFlagTimeout = 2;
+constexpr uint32_t kErrDoubleSet = 3;   // a flag stamped twice in one operator (signal_board.hpp:25-28)
+
+// Fault injection (tests: the reference's deadlock / double-set paths,
+// acceptance.cpp:121-158, engine.cpp:401-403): armed for one operator.
+enum FaultKind : int { kFaultNone = 0, kFaultDropSignal = 1, kFaultDoubleSignal = 2 };
 
 // Tile order entry: local rank (4 bits) | tile row (14 bits) | tile col (14 bits).
 __host__ __device__ inline uint32_t pack_tile(int l, int tm, int tn) {
@@ -156,6 +162,15 @@ struct GemmParams {
     float* tail_ws;                // [tail tile][split][cta of pair][128 x 256] fp32
     uint32_t* tail_ctr;            // [tail tile][cta of pair]: (tail_seq << 8) | arrivals
     int dbg;                       // profiling ablations (FLUX_DEBUG): 1 skip RS remote stores, 2 skip RS owner reduce
+    // Error reporting: a timed-out wait also writes its record into this
+    // host-mapped mirror ([global rank][4] u32), which the host reads at the
+    // start of the next operator without synchronising (nullptr: off).
+    uint32_t* err_host;
+    // Fault injection (one operator): drop / double the signal `fault_index` of
+    // rank `fault_rank`'s flag table (AG in-kernel: 128-row group counter;
+    // RS: tile * tp + source).
+    int fault_kind, fault_rank, fault_index;
+    int check_double;              // RS flags: exchange-and-check instead of store (double-set detector)
 };
 
 struct RsReduceParams {

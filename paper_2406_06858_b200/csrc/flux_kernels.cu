@@ -34,6 +34,8 @@
 // count (or fetched from a counter: FLUX_DYN_SCHED, ablation).
 #include <cuda_bf16.h>
 
+#include <atomic>
+
 #include "flux_internal.hpp"
 
 namespace fluxb200 {
@@ -237,12 +239,6 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// RS partial-landed flag of owner `o`: gpu scope when the owner runs in this
-// launch (same device), system scope for a peer GPU.
-__device__ __forceinline__ void rs_flag_set(const GemmParams& p, int o, uint32_t* f, uint32_t v) {
-    if (p.slot_of[o] >= 0 && !(p.dbg & 512)) st_release_gpu(f, v);  // dbg 512: ablation, always sys
-    else st_release_sys(f, v);
-}
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -323,25 +319,81 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 __device__ __forceinline__ uint32_t ld_acquire_flag(const GemmParams& p, const uint32_t* f) {
     return p.all_local && !(p.dbg & 512) ? ld_acquire_gpu(f) : ld_acquire_sys(f);
 }
-__device__ bool wait_flag(const uint32_t* flag, uint32_t target, const GemmParams& p,
-                          uint32_t* ctrl, uint32_t code, uint32_t info0, uint32_t info1) {
+// First failure of local slot l in this operator: the control block's error
+// record (read by flux_sync) plus the host-mapped mirror the host checks at the
+// start of the next operator (so a failure cannot go unnoticed when the caller
+// never synchronises through flux_sync, e.g. the PyTorch ops).
+__device__ void record_error(const GemmParams& p, int l, uint32_t code, uint32_t info0, uint32_t info1,
+                             uint32_t info2) {
+    uint32_t* ctrl = p.ctrl[l];
+    if (atomicCAS(ctrl + 0, 0u, code) != 0u) return;
+    ctrl[1] = info0;
+    ctrl[2] = info1;
+    ctrl[3] = info2;
+    ctrl[kCtrlErrEpoch / 4] = p.epoch;
+    if (p.err_host != nullptr) {
+        volatile uint32_t* h = p.err_host + 4 * p.global_rank[l];
+        h[1] = info0;
+        h[2] = info1;
+        h[3] = info2;
+        __threadfence_system();
+        h[0] = code;
+    }
+    __threadfence_system();
+}
+
+// Bounded spin of local slot l on an epoch-stamped flag / monotonic counter.
+// Waits of this operator abort early once a sibling wait of the SAME operator
+// failed (the error record carries its epoch); an error left over from an
+// earlier operator does not short-circuit later waits.
+__device__ bool wait_flag(const uint32_t* flag, uint32_t target, const GemmParams& p, int l, uint32_t code,
+                          uint32_t info0, uint32_t info1) {
     if (static_cast<int32_t>(ld_acquire_flag(p, flag) - target) >= 0) return true;
     const uint64_t t0 = globaltimer();
     uint32_t ns = 32;
+    const volatile uint32_t* ctrl = p.ctrl[l];
     for (;;) {
         __nanosleep(ns);
-        if (ns < 2048) ns <<= 1;
+        if (ns < 256) ns <<= 1;
         if (static_cast<int32_t>(ld_acquire_flag(p, flag) - target) >= 0) return true;
         if (globaltimer() - t0 > p.timeout_ns) {
-            if (atomicCAS(ctrl + 0, 0u, code) == 0u) {
-                ctrl[1] = info0;
-                ctrl[2] = info1;
-                ctrl[3] = target;
-                __threadfence_system();
-            }
+            record_error(p, l, code, info0, info1, target);
             return false;
         }
-        if (*reinterpret_cast<volatile uint32_t*>(ctrl) != 0u) return false;  // sibling failed
+        if (ctrl[0] != 0u && ctrl[kCtrlErrEpoch / 4] == p.epoch) return false;  // sibling failed
+    }
+}
+
+__device__ __forceinline__ bool fault_hit(const GemmParams& p, int rank, int index) {
+    return p.fault_kind != kFaultNone && p.fault_rank == rank && p.fault_index == index;
+}
+
+// Stamp RS flag (tile, src) of owner o with this operator's epoch (local slot l
+// sets it): gpu scope when the owner runs in this launch, system scope for a
+// peer GPU. With the double-set detector on, the stamp is an exchange and a
+// previous stamp of the same epoch is an error (SignalBoard::set returning
+// false, signal_board.hpp:25-28 / engine.cpp:401-403).
+__device__ void rs_flag_set(const GemmParams& p, int l, int o, int tile_id, int src) {
+    const int idx = tile_id * p.tp + src;
+    uint32_t* f = p.rs_flags[o] + idx;
+    const bool hit = fault_hit(p, o, idx);
+    if (hit && p.fault_kind == kFaultDropSignal) return;
+    const bool gpu = p.slot_of[o] >= 0 && !(p.dbg & 512);  // dbg 512: ablation, always sys
+    for (int rep = 0; rep < (hit ? 2 : 1); ++rep) {
+        if (p.check_double) {
+            uint32_t old;
+            if (gpu)
+                asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(f), "r"(p.epoch) : "memory");
+            else
+                asm volatile("atom.release.sys.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(f), "r"(p.epoch) : "memory");
+            if (old == p.epoch)
+                record_error(p, l, kErrDoubleSet, static_cast<uint32_t>(idx), static_cast<uint32_t>(o),
+                             static_cast<uint32_t>(tile_id));
+        } else if (gpu) {
+            st_release_gpu(f, p.epoch);
+        } else {
+            st_release_sys(f, p.epoch);
+        }
     }
 }
 
@@ -370,8 +422,10 @@ __device__ __forceinline__ void trace_event(const GemmParams& p, int l, uint32_t
 // Publish one landed AG piece (trace timestamp taken before the release).
 __device__ __forceinline__ void ag_signal(const GemmParams& p, uint32_t* ctr, int meta) {
     const int l = meta >> 16, g = meta & 0xFFFF;
+    const bool hit = fault_hit(p, p.global_rank[l], g);
+    if (hit && p.fault_kind == kFaultDropSignal) return;
     trace_event(p, l, kEvSignalSet, p.global_rank[l], g, 0, static_cast<uint32_t>(g));
-    red_release_gpu_add(ctr, 1u);
+    red_release_gpu_add(ctr, hit ? 2u : 1u);
 }
 
 __device__ __forceinline__ void decode(uint32_t e, int& l, int& tm, int& tn) {
@@ -555,7 +609,7 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
         const int tm0 = r0 / kBM, tm1 = (r1 - 1) / kBM;
         if (tid < (tm1 - tm0 + 1) * tp && !no_wait) {
             const int tile_id = (tm0 + tid / tp) * tiles_n + tn;
-            wait_flag(p.rs_flags[me] + tile_id * tp + tid % tp, epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+            wait_flag(p.rs_flags[me] + tile_id * tp + tid % tp, epoch, p, l, kErrRsFlagTimeout,
                       static_cast<uint32_t>(tile_id), static_cast<uint32_t>(tid % tp));
             if (tid == 0) trace_event(p, l, kEvReduce, me, tm0, tn, static_cast<uint32_t>(me));
         }
@@ -817,14 +871,14 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         // In-kernel transfer: every piece of this 128-row group landed.
                         const int g = row0 / kBM;
                         wait_flag(p.ag_ctr[p.global_rank[l]] + g, p.ag_mult * ag_group_target(p, g), p,
-                                  p.ctrl[l], kErrAgFlagTimeout, static_cast<uint32_t>(g),
+                                  l, kErrAgFlagTimeout, static_cast<uint32_t>(g),
                                   static_cast<uint32_t>(tm * 65536 + tn));
                     } else {
                         // Alg. 2: wait for every comm tile covering this CTA's A rows.
                         const int rlast = min(row0 + kBM, p.m) - 1;
                         const int f0 = row0 / p.rpct, f1 = rlast / p.rpct;
                         for (int f = f0; f <= f1; ++f)
-                            wait_flag(p.ag_flags[l] + f, p.epoch, p, p.ctrl[l], kErrAgFlagTimeout,
+                            wait_flag(p.ag_flags[l] + f, p.epoch, p, l, kErrAgFlagTimeout,
                                       static_cast<uint32_t>(f), static_cast<uint32_t>(tm * 65536 + tn));
                     }
                     // Flag acquire (generic proxy) before TMA reads (async proxy).
@@ -954,10 +1008,15 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             auto publish = [&](const Piece& P) {
                 if (P.ctr) {
                     if (p.ag_push) {  // the destination's counter, possibly on another GPU
-                        trace_event(p, P.meta >> 16, kEvSignalSet, p.global_rank[P.meta >> 16], P.meta & 0xFFFF, 0,
-                                    static_cast<uint32_t>(P.dest));
-                        if (p.slot_of[P.dest] >= 0) red_release_gpu_add(P.ctr, 1u);
-                        else red_release_sys_add(P.ctr, 1u);
+                        const bool hit = fault_hit(p, P.dest, P.meta & 0xFFFF);
+                        if (hit && p.fault_kind == kFaultDropSignal) {
+                            // dropped (fault injection)
+                        } else {
+                            trace_event(p, P.meta >> 16, kEvSignalSet, p.global_rank[P.meta >> 16], P.meta & 0xFFFF,
+                                        0, static_cast<uint32_t>(P.dest));
+                            if (p.slot_of[P.dest] >= 0) red_release_gpu_add(P.ctr, hit ? 2u : 1u);
+                            else red_release_sys_add(P.ctr, hit ? 2u : 1u);
+                        }
                     } else {
                         ag_signal(p, P.ctr, P.meta);
                     }
@@ -1002,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     // q = destination: my own rows go to its a_agg and count there.
                     if (p.slot_of[q] < 0 && q != checked_src) {
                         drain();  // (no wait may hold a signal)
-                        wait_flag(p.kdone[q], p.epoch - 1u, p, p.ctrl[l], kErrAgFlagTimeout,
+                        wait_flag(p.kdone[q], p.epoch - 1u, p, l, kErrAgFlagTimeout,
                                   static_cast<uint32_t>(p.ag_slot_index), 0xFFFE0000u | static_cast<uint32_t>(q));
                         checked_src = q;
                     }
@@ -1027,7 +1086,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         // waiting for our own-block pieces (no wait may hold a signal).
                         drain();
                         // The source's own slot (its shard copied into its a_agg) is complete.
-                        wait_flag(p.ag_ctr[q] + p.ag_slot_index, p.ag_mult * p.slot_pieces, p, p.ctrl[l],
+                        wait_flag(p.ag_ctr[q] + p.ag_slot_index, p.ag_mult * p.slot_pieces, p, l,
                                   kErrAgFlagTimeout, static_cast<uint32_t>(p.ag_slot_index),
                                   0xFFFF0000u | static_cast<uint32_t>(q));
                         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1163,11 +1222,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
                                     if (v == done) break;
                                     if (globaltimer() - t0 > p.timeout_ns) {
-                                        if (atomicCAS(p.ctrl[l] + 0, 0u, kErrAgFlagTimeout) == 0u) {
-                                            p.ctrl[l][1] = static_cast<uint32_t>(ti);
-                                            p.ctrl[l][2] = 0xFFFE0000u | static_cast<uint32_t>(split);
-                                            p.ctrl[l][3] = done;
-                                        }
+                                        record_error(p, l, kErrAgFlagTimeout, static_cast<uint32_t>(ti),
+                                                     0xFFFE0000u | static_cast<uint32_t>(split), done);
                                         break;
                                     }
                                     __nanosleep(64);
@@ -1303,7 +1359,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 const int o0 = row0 / p.rpr, o1 = (min(row0 + kBM, p.m) - 1) / p.rpr;
                 if (et == 0) trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o0));
                 for (int o = o0 + et; o <= o1; o += 128)
-                    rs_flag_set(p, o, p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
+                    rs_flag_set(p, l, o, tile_id, me);
             } else {
                 const int me = p.global_rank[l];
                 const uint32_t parity = p.epoch & 1u;
@@ -1335,7 +1391,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     const long long e0 = parity * p.stage_parity + stage_tile_off(lr0, tn, p.tiles_n) + q * 1024;
                     if (et == 0) {
                         if (pred >= 0)
-                            wait_flag(p.rs_flags[o] + tile_id * tp + pred, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+                            wait_flag(p.rs_flags[o] + tile_id * tp + pred, p.epoch, p, l, kErrRsFlagTimeout,
                                       static_cast<uint32_t>(tile_id), static_cast<uint32_t>(pred));
                         if (closes) trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(o));
                     }
@@ -1379,14 +1435,14 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     named_bar_sync(1, 128);
                     if (!closes && et == 0) {
                         trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o));
-                        rs_flag_set(p, o, p.rs_flags[o] + tile_id * tp + me, p.epoch);
+                        rs_flag_set(p, l, o, tile_id, me);
                     }
                 } else {
                 if (p.fused_reduce) {
                     // FusedReduce: each owner zeroes this parity's accumulator on its
                     // stream before the launch and stamps fr_ready; wait for that once.
                     if (et <= o1 - o0 && o0 + et != me)
-                        wait_flag(p.fr_ready[o0 + et], p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+                        wait_flag(p.fr_ready[o0 + et], p.epoch, p, l, kErrRsFlagTimeout,
                                   static_cast<uint32_t>(tile_id), static_cast<uint32_t>(o0 + et));
                     named_bar_sync(1, 128);
                 }
@@ -1439,7 +1495,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     const int o = o0 + et;
                     if (o != me) {
                         trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o));
-                        rs_flag_set(p, o, p.rs_flags[o] + tile_id * p.tp + me, p.epoch);
+                        rs_flag_set(p, l, o, tile_id, me);
                     }
                 }
                 // Phase 2: owned rows = sum of all partials in the canonical order.
@@ -1465,7 +1521,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     if (et == 0) {
                         for (int s = 0; s < p.tp; ++s)
                             if (s != me)
-                                wait_flag(p.rs_flags[me] + tile_id * p.tp + s, p.epoch, p, p.ctrl[l], kErrRsFlagTimeout,
+                                wait_flag(p.rs_flags[me] + tile_id * p.tp + s, p.epoch, p, l, kErrRsFlagTimeout,
                                           static_cast<uint32_t>(tile_id), static_cast<uint32_t>(s));
                         trace_event(p, l, kEvReduce, me, tm, tn, static_cast<uint32_t>(me));
                     }
@@ -1608,14 +1664,21 @@ cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t str
 
 int gemm_tile_rows(int cg) { return kBM * cg; }
 
+// Function attributes belong to each device's context: the dynamic shared
+// memory opt-in is set once per (kernel variant, device), tracked in a bitmask
+// that concurrent host threads update atomically (setting it twice is harmless).
 template <int MODE, int CG, int PB = 0>
 static cudaError_t launch_one(const GemmParams& p, int grid, cudaStream_t stream) {
-    static bool configured = false;
+    static std::atomic<uint64_t> configured{0};
     auto fn = flux_gemm_kernel<MODE, CG, PB>;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<CG, MODE>::kSmem);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+    if (bit == 0 || !(configured.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<CG, MODE>::kSmem);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);

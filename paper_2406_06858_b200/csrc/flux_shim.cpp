@@ -28,6 +28,7 @@ namespace {
         case FLUX_ERR_DIRECTORY: throw DirectoryError(msg);
         case FLUX_ERR_DEADLOCK: throw DeadlockError(msg);
         case FLUX_ERR_BOUNDS: throw BoundsError(msg);
+        case FLUX_ERR_RUNTIME: throw std::runtime_error(msg);  // e.g. "flag 3 on rank 1 set twice"
         default: throw std::runtime_error("flux: " + msg);
     }
 }

@@ -43,6 +43,32 @@ def init_process_group_communicator(max_problem: ProblemSpec, group=None) -> int
     return register(comm)
 
 
+def _check_mat(name: str, t: torch.Tensor, comm: Communicator, rows: int | None = None,
+               cols: int | None = None) -> None:
+    """The C ABI carries only (pointer, row pitch): everything else about a
+    caller tensor is checked here, before the kernels build TMA maps over it."""
+    if not isinstance(t, torch.Tensor) or t.dim() != 2:
+        raise ValueError(f"{name}: expected a 2-D tensor")
+    if t.dtype != torch.bfloat16:
+        raise ValueError(f"{name}: expected bfloat16, got {t.dtype}")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: expected a CUDA tensor")
+    dev = getattr(comm, "device", None)
+    if dev is not None and t.device.index != dev:
+        raise ValueError(f"{name}: on cuda:{t.device.index}, the communicator runs on cuda:{dev}")
+    if t.shape[0] > 1 and (t.stride(1) != 1 or t.stride(0) < t.shape[1]):
+        raise ValueError(f"{name}: expected a row-major view (stride(1) == 1, stride(0) >= cols), "
+                         f"got strides {tuple(t.stride())} for shape {tuple(t.shape)}")
+    if t.shape[0] <= 1 and t.stride(1) != 1:
+        raise ValueError(f"{name}: expected unit column stride")
+    if t.data_ptr() % 16 or (t.stride(0) * 2) % 16:
+        raise ValueError(f"{name}: base address and row pitch must be 16-byte aligned (TMA)")
+    if rows is not None and t.shape[0] != rows:
+        raise ValueError(f"{name}: expected {rows} rows, got {t.shape[0]}")
+    if cols is not None and t.shape[1] != cols:
+        raise ValueError(f"{name}: expected {cols} columns, got {t.shape[1]}")
+
+
 def _stream():
     """torch's current stream as a cudaStream_t. torch reports the legacy
     default stream as 0, which the C ABI reads as "library stream": pass
@@ -57,6 +83,8 @@ def ag_gemm(a_shard: torch.Tensor, weight: torch.Tensor, comm_id: int) -> torch.
     bf16 (nn.Linear layout); returns [m, n/tp] bf16."""
     comm = _REGISTRY[comm_id]
     tp, k = comm.tp, a_shard.shape[1]
+    _check_mat("a_shard", a_shard, comm)
+    _check_mat("weight", weight, comm, cols=k)
     p = ProblemSpec(a_shard.shape[0] * tp, weight.shape[0] * tp, k, tp, N.ALLGATHER_GEMM)
     out = torch.empty(p.m, weight.shape[0], dtype=torch.bfloat16, device=a_shard.device)
     comm.ag_gemm_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a_shard, weight, out)], streams=_stream())
@@ -75,6 +103,11 @@ def gemm_rs(a: torch.Tensor, weight: torch.Tensor, comm_id: int, b_kn: bool = Fa
     rank's [m/tp, n] bf16 rows (fixed-order fp32 sum)."""
     comm = _REGISTRY[comm_id]
     tp = comm.tp
+    _check_mat("a", a, comm)
+    if b_kn:
+        _check_mat("weight", weight, comm, rows=a.shape[1])
+    else:
+        _check_mat("weight", weight, comm, cols=a.shape[1])
     n = weight.shape[1] if b_kn else weight.shape[0]
     p = ProblemSpec(a.shape[0], n, a.shape[1] * tp, tp, N.GEMM_REDUCESCATTER)
     out = torch.empty(p.rows_per_rank(), p.n, dtype=torch.bfloat16, device=a.device)
@@ -103,6 +136,8 @@ def ag_gemm_act(a_shard: torch.Tensor, weight: torch.Tensor, comm_id: int,
     GEMM epilogue; also returns the pre-activation [m, n/tp] (SWIGLU: the output
     has half the columns — 128 gate + 128 up rows per 256-row weight group)."""
     comm = _REGISTRY[comm_id]
+    _check_mat("a_shard", a_shard, comm)
+    _check_mat("weight", weight, comm, cols=a_shard.shape[1])
     p = _ag_problem(comm, a_shard, weight.shape[0])
     swiglu = activation == N.ACT_SWIGLU
     out = torch.empty(p.m, weight.shape[0] // (2 if swiglu else 1), dtype=torch.bfloat16, device=a_shard.device)
@@ -128,9 +163,15 @@ def ag_gemm_dact(a_shard: torch.Tensor, weight: torch.Tensor, pre: torch.Tensor,
     dgate / dup in the gate/up grouping, twice the columns). b_kn: weight given
     as [k, n/tp] (e.g. the forward's W_down itself), used as AllGather(a) @ weight."""
     comm = _REGISTRY[comm_id]
+    _check_mat("a_shard", a_shard, comm)
+    if b_kn:
+        _check_mat("weight", weight, comm, rows=a_shard.shape[1])
+    else:
+        _check_mat("weight", weight, comm, cols=a_shard.shape[1])
     n_local = weight.shape[1] if b_kn else weight.shape[0]
     p = _ag_problem(comm, a_shard, n_local)
     width = n_local * (2 if activation == N.ACT_SWIGLU else 1)
+    _check_mat("pre", pre, comm, rows=p.m, cols=width)
     out = torch.empty(p.m, width, dtype=torch.bfloat16, device=a_shard.device)
     comm.ag_gemm_ex(p, TileShape(p.rows_per_rank(), p.local_cols()), [(a_shard, weight, out, pre)],
                     opts=N.default_opts(activation_grad=activation, b_layout=N.B_KN if b_kn else N.B_NK),
