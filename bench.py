@@ -47,7 +47,17 @@ WORKLOADS = {
     "decode-ag-up-m512": (0, 512, 28672, 8192, 8, "decode AllGather-GEMM Llama-2-70B MLP up-proj, M=512 tokens, TP=8"),
     "decode-rs-down-m256": (1, 256, 8192, 28672, 8, "decode GEMM-ReduceScatter Llama-2-70B MLP down-proj, M=256, TP=8"),
     "decode-rs-down-m512": (1, 512, 8192, 28672, 8, "decode GEMM-ReduceScatter Llama-2-70B MLP down-proj, M=512, TP=8"),
+    "decode-rs-attn-m128": (1, 128, 8192, 8192, 8, "decode GEMM-ReduceScatter Llama-2-70B attention-out, M=128, TP=8"),
+    "decode-rs-attn-m512": (1, 512, 8192, 8192, 8, "decode GEMM-ReduceScatter Llama-2-70B attention-out, M=512, TP=8"),
+    # One GPU's share of configs[4] at real TP=8 (per-GPU decode vs the ~9 us HBM roofline):
+    # the per-rank GEMM shapes as TP=1 problems (the rank's weight shard streamed once).
+    "rank-decode-ag-up-m16": (0, 16, 3584, 8192, 1, "one rank of decode AG-GEMM Llama-2-70B up-proj at TP=8: M=16, K=8192, N/TP=3584 (58.7 MB weight shard)"),
+    "rank-decode-ag-up-m128": (0, 128, 3584, 8192, 1, "one rank of decode AG-GEMM Llama-2-70B up-proj at TP=8: M=128, K=8192, N/TP=3584"),
+    "rank-decode-rs-down-m16": (1, 16, 8192, 3584, 1, "one rank of decode GEMM-RS Llama-2-70B down-proj at TP=8: M=16, K/TP=3584, N=8192 (58.7 MB weight shard)"),
+    "rank-decode-rs-down-m128": (1, 128, 8192, 3584, 1, "one rank of decode GEMM-RS Llama-2-70B down-proj at TP=8: M=128, K/TP=3584, N=8192"),
+    "rank-decode-rs-attn-m16": (1, 16, 8192, 1024, 1, "one rank of decode GEMM-RS Llama-2-70B attention-out at TP=8: M=16, K/TP=1024, N=8192 (16.8 MB weight shard)"),
 }
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (B200_PROFILING.md)
 FALLBACK_PEAKS = {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
 
 
@@ -59,6 +69,62 @@ def peaks():
         return d, "measured (MEASURED_PEAKS.json)"
     except Exception:
         return FALLBACK_PEAKS, "fallback (B200_PROFILING.md)"
+
+
+def roofline_work(pattern, m, n, k, tp, emulated, partial_bytes=4):
+    """Algorithmic work of ONE fused launch: (flops, HBM bytes,
+    NVLink bytes). Per rank:
+      AG  flops 2·M·(N/TP)·K; NVLink ingress (TP−1)/TP·M·K·2; HBM a_agg write +
+          read 2·M·K·2 + weight K·(N/TP)·2 + C M·(N/TP)·2 + the shard rows this
+          GPU serves its peers (TP−1)/TP·M·K·2.
+      RS  flops 2·M·N·(K/TP); NVLink egress (TP−1)/TP·M·N·4 (fp32 partials);
+          HBM A M·(K/TP)·2 + weight (K/TP)·N·2 + partials written by / read
+          for the owners 2·(TP−1)/TP·M·N·4 + C (M/TP)·N·2.
+    N=1 (every rank emulated on one GPU, one launch): TP × the per-rank work,
+    the transfers are HBM traffic (no NVLink term). N>1: one rank's work."""
+    rpr = m // tp
+    if pattern == 0:
+        nl = n // tp
+        flops = 2.0 * m * nl * k
+        nvl = (tp - 1) / tp * m * k * 2
+        hbm = 2.0 * m * k * 2 + k * nl * 2 + m * nl * 2 + nvl
+    else:
+        kl = k // tp
+        flops = 2.0 * m * n * kl
+        nvl = (tp - 1) / tp * m * n * partial_bytes
+        hbm = m * kl * 2.0 + kl * n * 2 + 2 * nvl + rpr * n * 2
+    ranks = tp if emulated else 1
+    return flops * ranks, hbm * ranks, (0.0 if emulated else nvl)
+
+
+def roofline_of(work, kernel_ms, pk, src):
+    """The bound is the slowest of tensor-core time, HBM time and NVLink time
+    at peak (north_star: "the slower of the compute at peak and the bytes over
+    NVLink", plus HBM so decode fractions stay <= 1); achieved and peak are in
+    the bound's unit, frac = roofline time / measured kernel time."""
+    flops, hbm, nvl = work
+    terms = {"tensor": flops / (pk["bf16_tflops"] * 1e12), "hbm": hbm / (pk["hbm_gbs"] * 1e9),
+             "nvlink": nvl / (NVLINK_GBS * 1e9)}
+    bound = max(terms, key=terms.get)
+    t = kernel_ms * 1e-3
+    if bound == "tensor":
+        achieved, peak, unit = flops / t / 1e12, pk["bf16_tflops"], "TFLOP/s"
+    elif bound == "hbm":
+        achieved, peak, unit = hbm / t / 1e9, pk["hbm_gbs"], "GB/s"
+    else:
+        achieved, peak, unit = nvl / t / 1e9, NVLINK_GBS, "GB/s"
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "terms_us": {k2: v * 1e6 for k2, v in terms.items()}, "roofline_us": terms[bound] * 1e6,
+            "kernel_ms": kernel_ms, "flops_per_launch": flops, "hbm_bytes_per_launch": hbm,
+            "nvlink_bytes_per_launch": nvl,
+            "peak_source": f"{src}: burst bf16 {pk['bf16_tflops']} TFLOP/s, HBM {pk['hbm_gbs']} GB/s; "
+                           f"NVLink {NVLINK_GBS} GB/s per direction (nominal)"}
+
+
+def bf16_tol(k):
+    """Parity tolerance for bf16 outputs (oracle/gpu_harness.tol):
+    8e-3 plus the fp32 accumulation term beyond k = 32768."""
+    return 8e-3 + max(0.0, 1e-4 * max(1.0, k / 1024.0) - 3.2e-3)
 
 
 # ---------------------------------------------------------------------------
@@ -262,7 +328,16 @@ def our_arm(args, wl):
     tile = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
     opts = fx.default_opts(ag_engine=args.ag_engine, cta_group=args.cta_group,
                            deterministic_reduce=0 if args.nondeterministic else 1)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    # L2 flush between timed steps (outside the events): write 256 MiB (> the
+    # 126 MB L2), then read another 256 MiB so the written lines are evicted
+    # (written back) before the next step starts — no dirty lines are left to
+    # drain inside the timed region.
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_rd = torch.ones(64 << 20, dtype=torch.int32, device=dev)
+
+    def l2_flush():
+        flush.zero_()
+        flush_rd.max()
 
     def op():
         if pattern == 0:
@@ -285,7 +360,7 @@ def our_arm(args, wl):
         total = 0.0
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         for _ in range(steps):
-            flush.zero_()
+            l2_flush()
             ev0.record()
             fn()
             ev1.record()
@@ -310,7 +385,7 @@ def our_arm(args, wl):
         times = {name: [] for name in fns}
         for _ in range(rounds):
             for name, fn in fns.items():
-                flush.zero_()
+                l2_flush()
                 barrier()
                 ev0.record()
                 fn()
@@ -326,6 +401,69 @@ def our_arm(args, wl):
             out[name] = t.item()
         return out
 
+    def parity_check():
+        """Row-sampled check of every rank's output of the last timed step
+        against an fp64 product of the same bf16 inputs (the oracle's math,
+        k-ascending dense dot products, rank-ordered sums; SURVEY §8c option
+        iii): a few rows per ownership block (first, last, comm-tile edges),
+        every column. At N>1 the sampled A rows / partial rows are exchanged
+        with torch.distributed, so a multi-GPU run checks itself."""
+        tp_ = prob.tp
+        rpr = prob.rows_per_rank()
+        offs = sorted({0, rpr - 1, rpr // 2, min(rpr - 1, 127), min(rpr - 1, 128)})
+        rows = [o * rpr + j for o in range(tp_) for j in offs]
+        S = len(rows)
+        idx = torch.tensor(rows, device=dev)
+        cpu_coll = dist is not None and share  # gloo plumbing: collectives on host tensors
+
+        def allsum(t):
+            if dist is None:
+                return t
+            if cpu_coll:
+                h = t.cpu()
+                dist.all_reduce(h)
+                return h.to(dev)
+            dist.all_reduce(t)
+            return t
+
+        worst = 0.0
+        if pattern == 0:
+            a_rows = torch.zeros(S, prob.local_k(), dtype=torch.float64, device=dev)
+            for i, gr in enumerate(rows):
+                o = gr // rpr
+                if o in my_ranks:
+                    a_rows[i] = comm.tensor(o, N.BUF_A_SHARD, prob)[gr - o * rpr].double()
+            a_rows = allsum(a_rows)
+            for r in my_ranks:
+                want = a_rows @ comm.tensor(r, N.BUF_B_SHARD, prob).double().t()
+                got = comm.tensor(r, N.BUF_C_OUT, prob).index_select(0, idx).double()
+                err = ((got - want).abs() / torch.clamp(torch.maximum(got.abs(), want.abs()), min=1.0)).max().item()
+                worst = max(worst, err)
+        else:
+            part = torch.zeros(S, prob.n, dtype=torch.float64, device=dev)
+            for r in my_ranks:  # rank order on one process (emulated); all_reduce across processes
+                a_s = comm.tensor(r, N.BUF_A_SHARD, prob).index_select(0, idx).double()
+                part += a_s @ comm.tensor(r, N.BUF_B_SHARD, prob).double().t()
+            part = allsum(part)
+            for r in my_ranks:
+                sel = [i for i, gr in enumerate(rows) if gr // rpr == r]
+                local = torch.tensor([rows[i] - r * rpr for i in sel], device=dev)
+                got = comm.tensor(r, N.BUF_C_OUT, prob).index_select(0, local).double()
+                want = part[sel]
+                err = ((got - want).abs() / torch.clamp(torch.maximum(got.abs(), want.abs()), min=1.0)).max().item()
+                worst = max(worst, err)
+        t = torch.tensor([worst], device=dev)
+        if dist is not None:
+            if cpu_coll:
+                t = t.cpu()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        worst = t.item()
+        tol = bf16_tol(prob.local_k())
+        return {"rows_checked_per_rank": S if pattern == 0 else len(offs), "max_rel_error": worst, "tol": tol,
+                "pass": bool(worst <= tol),
+                "reference": "fp64 product of the sampled rows on the same bf16 inputs (max_rel_error, "
+                             "matrix.cpp:11-25), max over ranks"}
+
     ag_transfer = ("copy-engine pull" if N.lib().flux_ag_engine(C.byref(prob.c()), fx.PULL, C.byref(opts)) == 1
                    else "in-kernel TMA pull (the GEMM's SMs)")
 
@@ -339,6 +477,7 @@ def our_arm(args, wl):
     comm.set_timing(False)
     flops = prob.flops()
     value = flops / (ms_fused * 1e-3) / 1e12
+    parity = parity_check()
 
     # ---- Eq. 1 / Eq. 2 ingredients ----
     # Measured round-robin (one step of each variant per round, L2 flushed
@@ -359,17 +498,17 @@ def our_arm(args, wl):
         else:
             if pattern == 0:
                 b = BL.DistAG(comm.tensor(rank, N.BUF_A_SHARD, prob).contiguous(),
-                              comm.tensor(rank, N.BUF_B_SHARD, prob).contiguous())
+                              comm.tensor(rank, N.BUF_B_SHARD, prob).contiguous(), host_collectives=share)
             else:
                 b = BL.DistRS(comm.tensor(rank, N.BUF_A_SHARD, prob).contiguous(),
-                              comm.tensor(rank, N.BUF_B_SHARD, prob).contiguous())
+                              comm.tensor(rank, N.BUF_B_SHARD, prob).contiguous(), host_collectives=share)
         if pattern == 0:
             b.unfused()  # fills the gathered buffers for gemm_only
         variants = {"fused": op, "local": lambda: comm.local_gemm(prob, opts, streams),
                     "nonoverlap": lambda: comm.nonoverlap(prob, opts, streams),
                     "cublas_gemm": b.gemm_only, "b1": b.unfused}
-        if emulated and pattern == 0:
-            variants["b2"] = b.decomposed
+        if (emulated and pattern == 0) or not emulated:
+            variants["b2"] = b.decomposed  # cuBLAS chunk GEMMs + chunked copies / NCCL (run_medium_grained)
         if emulated:  # the device decomposed baseline (flux_medium_grained, tp chunks)
             tile_b2 = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
             variants["b2_ours"] = lambda: comm.medium_grained(prob, tile_b2, tp, opts, streams)
@@ -377,19 +516,32 @@ def our_arm(args, wl):
         del b
         ms_f = med["fused"]
         t_gemm = min(med["local"], med["cublas_gemm"])
-        ect_fused = ms_f - t_gemm
-        ect_b1 = med["b1"] - t_gemm
+        # Eq. 2 (sim.cpp:577-586): ECT = T_op - T_gemm_nonsplit, E = 1 - ECT_fused / ECT_unfused. Each
+        # operator's exposed communication is taken against ITS OWN GEMM (the fused op against our
+        # plain GEMM, B1 against cuBLAS), so neither GEMM's speed counts as communication.
+        ect_fused = ms_f - med["local"]
+        ect_b1 = med["b1"] - med["cublas_gemm"]
+        # Second form: against our own serial baseline (run_nonoverlap: the same GEMM kernel after a
+        # serial copy-engine AllGather / before a serial reduce) — the same GEMM on both sides.
+        ect_serial = med["nonoverlap"] - med["local"]
         extra = {
             "t_fused_ms": ms_f, "t_gemm_nonsplit_ms": t_gemm, "t_gemm_ours_ms": med["local"],
             "t_gemm_cublas_ms": med["cublas_gemm"], "t_unfused_cublas_ms": med["b1"], "t_decomposed_ms": med.get("b2"),
             "t_decomposed_ours_ms": med.get("b2_ours"),
             "t_nonoverlap_ours_ms": med["nonoverlap"],
-            "ect_fused_ms": ect_fused, "ect_unfused_ms": ect_b1,
+            "ect_fused_ms": ect_fused, "ect_unfused_ms": ect_b1, "ect_nonoverlap_ours_ms": ect_serial,
             "overlap_efficiency": (1.0 - ect_fused / ect_b1) if ect_b1 > 0 else None,
+            "overlap_efficiency_vs_our_serial": (1.0 - ect_fused / ect_serial) if ect_serial > 0 else None,
             "speedup_vs_unfused": med["b1"] / ms_f,
-            "method": "round-robin medians (one step of each variant per round, L2 flushed before each)",
+            "speedup_vs_decomposed": (med["b2"] / ms_f) if med.get("b2") else None,
+            "speedup_vs_our_serial": med["nonoverlap"] / ms_f,
+            "method": "round-robin medians (one step of each variant per round, L2 flushed before each); "
+                      "ECT of each operator against its own GEMM (fused: our plain GEMM; B1: cuBLAS)",
             "unfused_baseline": ("device copies + cuBLAS (ranks emulated on one GPU)" if emulated
-                                 else "NCCL + cuBLAS"),
+                                 else ("gloo host collectives + cuBLAS (ranks sharing one GPU, test plumbing)" if share
+                                       else "NCCL + cuBLAS")),
+            "decomposed_baseline": ("cuBLAS chunk GEMMs + side-stream device copies" if emulated
+                                    else "cuBLAS chunk GEMMs + per-chunk NCCL broadcast / reduce (async)"),
         }
 
     # ---- e2e through the C ABI with host buffers ----
@@ -487,20 +639,19 @@ def our_arm(args, wl):
     # ---- roofline of the dominant kernel (the fused GEMM) ----
     pk, src = peaks()
     kms = statistics.mean(kernel_ms) if kernel_ms else ms_fused
-    flops_per_launch = flops / (world if not emulated else 1)
-    achieved = flops_per_launch / (kms * 1e-3) / 1e12
-    traffic = None
+    roofline = roofline_of(roofline_work(pattern, m, n, k, tp, emulated), kms, pk, src)
+    roofline["kernel"] = "flux_gemm_kernel<AG>" if pattern == 0 else "flux_gemm_kernel<RS>"
+    roofline["traffic"] = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof) and emulated:  # captured at N=1 (every rank in one launch)
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(wl)
+                tr = json.load(f)
+            roofline["traffic"] = tr.get(wl)
+            if roofline["traffic"] is not None:
+                roofline["traffic_source"] = tr.get("_source", "profiles/ncu_traffic.json (ncu --set full capture)")
         except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16_tflops"], "traffic": traffic, "peak_source": src + " burst bf16",
-                "kernel": "flux_gemm_kernel<AG>" if pattern == 0 else "flux_gemm_kernel<RS>",
-                "kernel_ms": kms, "flops_per_launch": flops_per_launch}
+            roofline["traffic"] = None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -517,8 +668,9 @@ def our_arm(args, wl):
             "config": {"workload": wl, "description": desc, "m": m, "n": n, "k": k, "tp": tp,
                        "ranks": "emulated on one GPU" if emulated else "one process per GPU (cudaIpc heaps)",
                        "parallelism": f"tp{tp}", "transfer": ag_transfer if pattern == 0 else "epilogue P2P",
-                       "l2": "flushed between timed steps (256 MiB write outside the events)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                       "l2": "flushed between timed steps outside the events (256 MiB write, then a 256 MiB read "
+                             "sweep so no dirty lines drain inside the timed region)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "overlap": extra,
         }
         print(json.dumps(line), flush=True)

@@ -157,6 +157,11 @@ int flux_grid_for(const flux_problem* problem, const flux_tile* tile, int* tile_
 int flux_tile_order(const flux_problem* problem, const flux_tile* tile, int kind, int rank,
                     int shift_offset, const int* arrival_blocks, int n_arrival, int* out_rows,
                     int* out_cols);
+/* map_tile(SwizzlePolicy{kind, rank, tp, shift_offset, arrival_blocks}, i, GridDims{tile_rows,
+ * tile_cols, row_blocks}) (swizzle.cpp:51-73): the single implementation of the tile bijection
+ * (flux_tile_order and the C++ shim use it). BoundsError for i outside the grid. */
+int flux_map_tile(int kind, int rank, int tp, int shift_offset, const int* arrival_blocks, int n_arrival,
+                  int tile_rows, int tile_cols, int row_blocks, int index, int* out_row, int* out_col);
 /* comm_order(Topology{NVLinkRing}, rank, tp, rows_per_rank, rpct): descriptors
  * (peer, row_begin, rows). *count receives the number written (<= max). */
 int flux_comm_order(int rank, int tp, int rows_per_rank, int rows_per_comm_tile, int* out_peer,
@@ -166,6 +171,10 @@ int flux_comm_order(int rank, int tp, int rows_per_rank, int rows_per_comm_tile,
 int flux_make_comm_spec(const flux_problem* problem, int rank, int rows_per_comm_tile,
                         int transfer, int* out_peer, int* out_row_begin, int* out_rows, int max,
                         int* count);
+
+/* CommTileSpec::validate (engine.cpp:40-75) of one rank's descriptor list. */
+int flux_validate_comm_spec(const flux_problem* problem, int rank, int rows_per_comm_tile, int transfer,
+                            const int* peer, const int* row_begin, const int* rows, int count);
 
 /* ---- communicator = symmetric heap + peer directory (workspace.hpp:22-43) --- */
 size_t flux_required_heap_bytes(const flux_problem* problem);
@@ -255,6 +264,28 @@ int flux_ag_gemm_ex(flux_comm* comm, const flux_problem* problem, const flux_til
 int flux_gemm_rs_ex(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
                     int write_mode, int swizzle_on, const flux_opts* opts, void* const* streams,
                     const flux_operands* operands);
+/* run_fused_allgather_gemm with the caller's comm specs (engine.hpp:107-111
+ * `comm_specs`): for every rank this process drives (in rank order; one in
+ * IPC mode) `count` descriptors (peer, row_begin, rows) at [slot * count + j],
+ * validated like CommTileSpec::validate (ConfigError / BoundsError). The
+ * copy-engine transfer loop walks them in the given order (engine.cpp:367-423)
+ * and the tiles follow the arrival order they imply (arrival_aligned_policy,
+ * swizzle.cpp:23-29 / the Push arrival sort, engine.cpp:480-501). */
+int flux_ag_gemm_ordered(flux_comm* comm, const flux_problem* problem, const flux_tile* tile,
+                         int rows_per_comm_tile, int transfer, int swizzle_on, const flux_opts* opts,
+                         void* const* streams, const flux_operands* operands, const int* order_peer,
+                         const int* order_row_begin, const int* order_rows, int count);
+/* TransferRecord of the last AllGather run with opts.trace on the copy-engine
+ * transfer engine (engine.hpp:79-85): per descriptor of `rank`'s comm spec, in
+ * issue order, the device times (ns, CUDA events on the copy stream relative to
+ * its first transfer) at which its copy completed and its flag was raised;
+ * copy_done_ns <= flag_set_ns (test_engine.cpp:102-115). */
+typedef struct {
+    int peer, row_begin, rows;
+    int64_t copy_done_ns, flag_set_ns;
+} flux_transfer_record;
+int flux_transfer_log(flux_comm* comm, int rank, flux_transfer_record* out, int max, int* count);
+
 /* ---- chained tensor-parallel MLP (paper Fig. 2, §3) ------
  * Forward: act = activation(AllGather(x) W_up^T) on every rank (AG-GEMM with
  * the activation in its epilogue), then out = ReduceScatter(act W_down^T)

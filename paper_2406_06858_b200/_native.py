@@ -106,6 +106,12 @@ class MlpGradOperands(C.Structure):
                 ("dx", Matrix)]
 
 
+class TransferRecord(C.Structure):
+    """flux_transfer_record (reference TransferRecord, engine.hpp:79-85)."""
+    _fields_ = [("peer", C.c_int), ("row_begin", C.c_int), ("rows", C.c_int), ("copy_done_ns", C.c_int64),
+                ("flag_set_ns", C.c_int64)]
+
+
 class BufferDesc(C.Structure):
     _fields_ = [("ptr", C.c_void_p), ("rows", C.c_int), ("cols", C.c_int), ("ld", C.c_int),
                 ("dtype", C.c_int)]
@@ -159,6 +165,13 @@ _SIGS = {
     "flux_mlp_backward_dx": (C.c_int, [C.c_void_p, _P(Mlp), _P(Opts), _P(C.c_void_p), _P(MlpGradOperands)]),
     "flux_mlp_required_heap_bytes": (C.c_size_t, [_P(Mlp)]),
     "flux_comm_inject_fault": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int]),
+    "flux_map_tile": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int,
+                                C.c_int, _P(C.c_int), _P(C.c_int)]),
+    "flux_validate_comm_spec": (C.c_int, [_P(Problem), C.c_int, C.c_int, C.c_int, _P(C.c_int), _P(C.c_int),
+                                          _P(C.c_int), C.c_int]),
+    "flux_ag_gemm_ordered": (C.c_int, [C.c_void_p, _P(Problem), _P(Tile), C.c_int, C.c_int, C.c_int, _P(Opts),
+                                       _P(C.c_void_p), _P(Operands), _P(C.c_int), _P(C.c_int), _P(C.c_int), C.c_int]),
+    "flux_transfer_log": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, _P(C.c_int)]),
     "flux_comm_set_check_double_set": (C.c_int, [C.c_void_p, C.c_int]),
 }
 

@@ -92,36 +92,72 @@ class EmulatedRS:
 
 
 class DistAG:
-    """One rank of a multi-process AllGather-GEMM: NCCL all-gather + cuBLAS."""
+    """One rank of a multi-process AllGather-GEMM: NCCL all-gather + cuBLAS (B1),
+    and the decomposed B2: per-chunk NCCL broadcasts from each chunk's owner,
+    issued asynchronously up front, each chunk's cuBLAS GEMM waiting only for
+    its own chunk (run_medium_grained, engine.cpp:653-728, partitions = tp).
+    host_collectives: stage through host tensors (gloo plumbing when the ranks
+    share one GPU in tests; no timing meaning)."""
 
-    def __init__(self, shard, weight, group=None):
+    def __init__(self, shard, weight, group=None, host_collectives=False):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
+        self.host = host_collectives
         self.tp = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
         self.shard, self.weight = shard, weight
+        self.rpr = shard.shape[0]
         self.gathered = torch.empty(shard.shape[0] * self.tp, shard.shape[1], dtype=shard.dtype, device=shard.device)
         self.out = torch.empty(self.gathered.shape[0], weight.shape[0], dtype=shard.dtype, device=shard.device)
 
     def gemm_only(self):
         torch.matmul(self.gathered, self.weight.t(), out=self.out)
 
+    def _all_gather(self):
+        if self.host:
+            parts = [torch.empty_like(self.shard, device="cpu") for _ in range(self.tp)]
+            self.dist.all_gather(parts, self.shard.cpu(), group=self.group)
+            self.gathered.copy_(torch.cat(parts).to(self.gathered.device))
+        else:
+            self.dist.all_gather_into_tensor(self.gathered, self.shard, group=self.group)
+
     def unfused(self):
-        self.dist.all_gather_into_tensor(self.gathered, self.shard, group=self.group)
+        self._all_gather()
         self.gemm_only()
+
+    def decomposed(self):
+        if self.host:
+            self.unfused()
+            return
+        self.gathered[self.rank * self.rpr:(self.rank + 1) * self.rpr].copy_(self.shard)
+        works = []
+        for c in range(self.tp):
+            chunk = self.gathered[c * self.rpr:(c + 1) * self.rpr]
+            works.append(self.dist.broadcast(chunk, src=c, group=self.group, async_op=True))
+        for c in range(self.tp):
+            works[c].wait()  # the compute stream waits for chunk c only
+            rows = slice(c * self.rpr, (c + 1) * self.rpr)
+            torch.matmul(self.gathered[rows], self.weight.t(), out=self.out[rows])
 
 
 class DistRS:
-    """One rank of a multi-process GEMM-ReduceScatter: cuBLAS + NCCL reduce-scatter."""
+    """One rank of a multi-process GEMM-ReduceScatter: cuBLAS + NCCL
+    reduce-scatter (B1), and the decomposed B2: per-chunk cuBLAS GEMMs whose
+    bf16 partial chunks are reduced to their owner asynchronously while the
+    next chunk computes (run_medium_grained, engine.cpp:653-728)."""
 
-    def __init__(self, a, weight, group=None):
+    def __init__(self, a, weight, group=None, host_collectives=False):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
+        self.host = host_collectives
         self.tp = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
         self.a, self.w = a, weight
+        self.rpr = a.shape[0] // self.tp
         self.partial = torch.empty(a.shape[0], weight.shape[0], dtype=a.dtype, device=a.device)
         self.out = torch.empty(a.shape[0] // self.tp, weight.shape[0], dtype=a.dtype, device=a.device)
 
@@ -130,4 +166,22 @@ class DistRS:
 
     def unfused(self):
         self.gemm_only()
-        self.dist.reduce_scatter_tensor(self.out, self.partial, group=self.group)
+        if self.host:
+            h = self.partial.float().cpu()
+            self.dist.all_reduce(h, group=self.group)
+            self.out.copy_(h[self.rank * self.rpr:(self.rank + 1) * self.rpr].to(self.out.device))
+        else:
+            self.dist.reduce_scatter_tensor(self.out, self.partial, group=self.group)
+
+    def decomposed(self):
+        if self.host:
+            self.unfused()
+            return
+        works = []
+        for c in range(self.tp):
+            rows = slice(c * self.rpr, (c + 1) * self.rpr)
+            torch.matmul(self.a[rows], self.w.t(), out=self.partial[rows])
+            works.append(self.dist.reduce(self.partial[rows], dst=c, group=self.group, async_op=True))
+        for w in works:
+            w.wait()
+        self.out.copy_(self.partial[self.rank * self.rpr:(self.rank + 1) * self.rpr])

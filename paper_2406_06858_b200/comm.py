@@ -217,6 +217,32 @@ class Communicator:
         N.check(N.lib().flux_ag_gemm_ex(self._h, C.byref(problem.c()), C.byref(tile.c()), rows_per_comm_tile, transfer,
                                         int(swizzle), C.byref(o), N.stream_array(streams), _operands(operands)))
 
+    def ag_gemm_ordered(self, problem: ProblemSpec, tile: TileShape, orders, rows_per_comm_tile: int,
+                        transfer: int = N.PULL, swizzle: bool = True, opts: Optional[N.Opts] = None, streams=None,
+                        operands=None) -> None:
+        """run_fused_allgather_gemm with the caller's comm specs: `orders` holds,
+        for every rank this process drives, its (peer, row_begin, rows) list."""
+        o = opts if opts is not None else N.default_opts()
+        count = len(orders[0]) if orders else 0
+        flat = [d for order in orders for d in order]
+        if any(len(order) != count for order in orders):
+            raise N.ConfigError("all ranks' comm orders must have the same length")
+        peer = (C.c_int * max(1, len(flat)))(*[d[0] for d in flat])
+        begin = (C.c_int * max(1, len(flat)))(*[d[1] for d in flat])
+        rows = (C.c_int * max(1, len(flat)))(*[d[2] for d in flat])
+        N.check(N.lib().flux_ag_gemm_ordered(self._h, C.byref(problem.c()), C.byref(tile.c()), rows_per_comm_tile,
+                                             transfer, int(swizzle), C.byref(o), N.stream_array(streams),
+                                             _operands(operands) if operands else None, peer, begin, rows, count))
+
+    def transfer_log(self, rank: int) -> list[dict]:
+        """TransferRecords of the last traced copy-engine AllGather (flux_transfer_log)."""
+        n = C.c_int()
+        N.check(N.lib().flux_transfer_log(self._h, rank, None, 0, C.byref(n)))
+        recs = (N.TransferRecord * max(1, n.value))()
+        N.check(N.lib().flux_transfer_log(self._h, rank, recs, n.value, C.byref(n)))
+        return [{"peer": r.peer, "row_begin": r.row_begin, "rows": r.rows, "copy_done_ns": r.copy_done_ns,
+                 "flag_set_ns": r.flag_set_ns} for r in recs[:n.value]]
+
     def gemm_rs_ex(self, problem: ProblemSpec, tile: TileShape, operands, write_mode: int = N.WRITE_ALLTOALL,
                    swizzle: bool = True, opts: Optional[N.Opts] = None, streams=None) -> None:
         o = opts if opts is not None else N.default_opts()
@@ -307,7 +333,8 @@ def required_heap_bytes(problem: ProblemSpec) -> int:
     return int(N.lib().flux_required_heap_bytes(C.byref(problem.c())))
 
 
-TRACE_KINDS = {1: "compute_start", 2: "signal_set", 3: "tile_write", 4: "reduce", 5: "wait", 6: "launch"}
+TRACE_KINDS = {1: "compute_start", 2: "signal_set", 3: "tile_write", 4: "reduce", 5: "wait", 6: "launch",
+               7: "copy_done"}
 
 
 def read_trace(comm: Communicator, rank: int, problem: ProblemSpec, max_records: int = 1 << 18) -> list[dict]:
@@ -340,3 +367,38 @@ def write_jsonl(path: str, events: list[dict]) -> None:
         for e in events:
             f.write(json.dumps({k: e[k] for k in ("event", "rank", "tile_row", "tile_col", "target", "logical_ts",
                                                   "wall_ns")}) + "\n")
+
+
+def chrome_trace(events: list[dict]) -> dict:
+    """The device event trace (read_trace) in the Chrome trace-event format of
+    the reference's write_chrome_trace (sim.cpp:597-610): {"traceEvents": [...]}
+    with "ph": "X" complete events (ts / dur in us, pid = rank, tid = lane).
+    Lanes: each CTA's lifetime (its launch records) is a span on tid = CTA
+    index; the tile-level events (compute_start, signal_set, tile_write,
+    reduce, copy_done) are zero-duration "X" events on tid = -1 (the rank's
+    signal lane) named "<kind> (row,col)" with the target in args."""
+    out = []
+    starts = {}
+    for e in events:
+        us = e["wall_ns"] / 1000.0
+        if e["event"] == "launch":
+            key = (e["rank"], e["tile_row"])
+            if e["tile_col"] == 0:
+                starts[key] = us
+            elif key in starts:
+                t0 = starts.pop(key)
+                out.append({"name": f"cta {e['tile_row']}", "ph": "X", "ts": t0, "dur": us - t0, "pid": e["rank"],
+                            "tid": e["tile_row"]})
+            continue
+        out.append({"name": f"{e['event']} ({e['tile_row']},{e['tile_col']})", "ph": "X", "ts": us, "dur": 0,
+                    "pid": e["rank"], "tid": -1, "args": {"target": e["target"], "logical_ts": e["logical_ts"]}})
+    return {"traceEvents": out}
+
+
+def write_chrome_trace(path: str, events: list[dict]) -> None:
+    """write_chrome_trace (sim.cpp:597-610) for the device event trace."""
+    import json
+
+    with open(path, "w") as f:
+        json.dump(chrome_trace(events), f)
+        f.write("\n")

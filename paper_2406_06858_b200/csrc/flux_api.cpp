@@ -256,8 +256,10 @@ int make_spec(const flux_problem* p, int rank, int rpct, int transfer, std::vect
     return validate_comm_spec(p, rank, rpct, transfer, out);
 }
 
-// Row-block visit order used by the AG kernel (engine.cpp:475-505).
-std::vector<int> ag_block_order(const flux_problem* p, int rank, int transfer, bool swizzle, int rpct) {
+// Row-block visit order used by the AG kernel (engine.cpp:475-505), from every
+// rank's comm spec for `transfer` (the reference's defaults or the caller's).
+std::vector<int> ag_block_order(const flux_problem* p, int rank, int transfer, bool swizzle,
+                                const std::vector<std::vector<Desc>>& specs) {
     const int tp = p->tp, rpr = rows_per_rank(p);
     if (!swizzle) {
         std::vector<int> b;
@@ -266,16 +268,16 @@ std::vector<int> ag_block_order(const flux_problem* p, int rank, int transfer, b
     }
     if (transfer == FLUX_PULL) {  // arrival_aligned_policy: local first, then peer_order(comm)
         std::vector<int> b{rank};
-        for (int q : peer_order(ring_order(rank, tp, rpr, rpct), rank, rpr)) b.push_back(q);
+        for (int q : peer_order(specs[rank], rank, rpr)) b.push_back(q);
+        for (int q = 0; q < tp; ++q)  // (a valid Pull spec names every peer; defensive)
+            if (std::find(b.begin(), b.end(), q) == b.end()) b.push_back(q);
         return b;
     }
     // Push: sources sorted by how early their list targets this rank.
     std::vector<std::pair<int, int>> arrivals;
     for (int s = 0; s < tp; ++s) {
         if (s == rank) continue;
-        std::vector<Desc> spec;
-        flux_problem q = *p;
-        make_spec(&q, s, rpct, FLUX_PUSH, spec);
+        const std::vector<Desc>& spec = specs[s];
         for (size_t i = 0; i < spec.size(); ++i)
             if (spec[i].peer == rank) {
                 arrivals.emplace_back(static_cast<int>(i), s);
@@ -288,6 +290,13 @@ std::vector<int> ag_block_order(const flux_problem* p, int rank, int transfer, b
     for (int s = 0; s < tp; ++s)
         if (std::find(b.begin(), b.end(), s) == b.end()) b.push_back(s);
     return b;
+}
+
+// The reference's comm specs of every rank (make_comm_specs, engine.cpp:77-99).
+int default_specs(const flux_problem* p, int rpct, int transfer, std::vector<std::vector<Desc>>& out) {
+    out.assign(p->tp, {});
+    for (int r = 0; r < p->tp; ++r) FLUX_TRY(make_spec(p, r, rpct, transfer, out[r]));
+    return FLUX_OK;
 }
 
 // Device tile sequence of one rank over the kBM x kBN grid. When ownership
@@ -458,7 +467,15 @@ struct flux_comm {
     };
     std::vector<OrderEntry> order_cache;
     uint64_t order_clock = 0;
-    uint32_t* err_host = nullptr;  // host-mapped error mirror [tp][4] (device waits write it on timeout)
+    uint32_t* err_host = nullptr;  // host-mapped error mirror [tp][8] (device waits write it on timeout)
+    // Copy-engine transfer log of the last traced AllGather (TransferRecord).
+    struct XferEntry {
+        int rank = 0, peer = 0, row_begin = 0, rows = 0;
+        cudaEvent_t base = nullptr, copy_ev = nullptr, flag_ev = nullptr;
+    };
+    std::vector<XferEntry> xfer_log;
+    std::vector<cudaEvent_t> xfer_events;  // pool
+    size_t xfer_used = 0;
     // Fault injection (flux_comm_inject_fault): armed for the next operator,
     // active while that operator enqueues its work.
     int fault_kind = 0, fault_rank = 0, fault_index = 0;
@@ -478,6 +495,7 @@ int check_comm(flux_comm* c) {
 // Message of a device error record {code, info0, info1, info2} of rank r
 // (the reference's DeadlockError / "set twice" texts, engine.cpp:149-162,401-403).
 std::string error_text(const uint32_t* err, int r) {
+    if (err[5] != 0) r = static_cast<int>(err[5]) - 1;  // the failing rank (records are shared by a launch)
     if (err[0] == kErrAgFlagTimeout)
         return "deadlock budget exhausted waiting for signal " + S(err[1]) + " for tile (" + S(err[2] >> 16) + "," +
                S(err[2] & 0xFFFF) + ") on rank " + S(r);
@@ -498,9 +516,9 @@ int begin_op(flux_comm* c) {
     if (c->err_host) {
         for (int r = 0; r < c->tp; ++r) {
             if (!c->ranks[r].local) continue;
-            const volatile uint32_t* h = c->err_host + 4 * r;
+            const volatile uint32_t* h = c->err_host + 8 * r;
             if (h[0] != 0) {
-                const uint32_t e[4] = {h[0], h[1], h[2], h[3]};
+                const uint32_t e[6] = {h[0], h[1], h[2], h[3], h[4], h[5]};
                 return fail(code_of(e[0]), "a previous operator failed on the device (" + error_text(e, r) +
                                                "); flux_sync reports and clears it");
             }
@@ -517,6 +535,10 @@ int begin_op(flux_comm* c) {
 // Operator exit: a host-detected failure (a copy-engine flag the transfer loop
 // set twice, engine.cpp:401-403) is raised once every piece of work is enqueued.
 int end_op(flux_comm* c) {
+    // An injected fault leaves the in-kernel AllGather's monotonic piece
+    // counters off their targets (a piece never counted, or counted twice):
+    // the next operator re-zeroes them (layout signature reset).
+    if (c->act_fault_kind != 0) c->ag_sig = 0;
     c->act_fault_kind = 0;
     if (!c->host_error.empty()) return fail(FLUX_ERR_RUNTIME, c->host_error);
     return FLUX_OK;
@@ -556,8 +578,8 @@ int alloc_heap(RankState& r, size_t bytes) {
 // device address).
 int alloc_err_host(flux_comm* c) {
     void* h = nullptr;
-    FLUX_CUDA(cudaHostAlloc(&h, sizeof(uint32_t) * 4 * kMaxRanks, cudaHostAllocMapped | cudaHostAllocPortable));
-    std::memset(h, 0, sizeof(uint32_t) * 4 * kMaxRanks);
+    FLUX_CUDA(cudaHostAlloc(&h, sizeof(uint32_t) * 8 * kMaxRanks, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(h, 0, sizeof(uint32_t) * 8 * kMaxRanks);
     c->err_host = static_cast<uint32_t*>(h);
     return FLUX_OK;
 }
@@ -707,6 +729,7 @@ struct OpCommon {
     int rs_units = 0;  // RS summed by the owners' reduction units (decode-sized blocks, sub-wave problems)
     int rs_chain = 0;         // RS with every rank in one launch: chained partial sums (kernel)
     const flux_operands* ops = nullptr;  // caller-provided operands (per rank; one entry in IPC mode)
+    bool trace_cursors_reset = false;    // the operator already zeroed the trace cursors (traced copy engines)
 };
 
 // Cross-process operator boundary (IPC mode): every operator stamps `done` and
@@ -882,7 +905,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 RankState& rs = c->ranks[g[li]];
                 prm.trace[li] = reinterpret_cast<unsigned long long*>(rs.heap + L.trace_off);
                 prm.trace_cursor[li] = at<uint32_t>(rs, kCtrlTraceCursor);
-                FLUX_CUDA(cudaMemsetAsync(prm.trace_cursor[li], 0, 4, lead));
+                if (!oc.trace_cursors_reset) FLUX_CUDA(cudaMemsetAsync(prm.trace_cursor[li], 0, 4, lead));
             }
         }
         if (extra) FLUX_TRY(extra(g, prm));
@@ -892,7 +915,10 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         // ceil(T / W) waves; the last T mod W tiles would leave most clusters
         // idle for a whole tile, so each runs as S <= 8 K-slices instead.
         prm.tail_splits = 0;
-        if ((mode == kModePlain || mode == kModeAG) && oc.o.activation != FLUX_ACT_SWIGLU) {
+        // GEMM-RS with owner reduction units (decode-sized blocks, sub-wave
+        // problems such as one GPU's decode share) splits the same way: the
+        // slices are summed before the partial is staged for its owners.
+        if ((mode == kModePlain || mode == kModeAG || mode == kModeRSUnits) && oc.o.activation != FLUX_ACT_SWIGLU) {
             const char* env = std::getenv("FLUX_TAIL_SPLIT");
             const int W = std::max(1, sm_count(dev) / cg), T = prm.num_tiles;
             const int R = T % W, kb = (lk + kBK - 1) / kBK;
@@ -998,33 +1024,51 @@ int flux_grid_for(const flux_problem* p, const flux_tile* t, int* tile_rows, int
     return FLUX_OK;
 }
 
-int flux_tile_order(const flux_problem* p, const flux_tile* t, int kind, int rank, int shift_offset,
-                    const int* arrival_blocks, int n_arrival, int* out_rows, int* out_cols) {
-    FLUX_TRY(validate_tiling(p, t));
-    const int tile_rows = p->m / t->tm, tile_cols = local_cols(p) / t->tn, tiles = tile_rows * tile_cols;
+int flux_map_tile(int kind, int rank, int tp, int shift_offset, const int* arrival_blocks, int n_arrival,
+                  int tile_rows, int tile_cols, int row_blocks, int index, int* out_row, int* out_col) {
+    const int tiles = tile_rows * tile_cols;
+    if (index < 0 || index >= tiles)
+        return fail(FLUX_ERR_BOUNDS, "tile index " + S(index) + " out of range [0," + S(tiles) + ")");
     if (kind == FLUX_SWIZZLE_NAIVE) {  // map_tile Naive: row-major (swizzle.cpp:54-56)
-        for (int i = 0; i < tiles; ++i) {
-            out_rows[i] = i / tile_cols;
-            out_cols[i] = i % tile_cols;
-        }
+        *out_row = index / tile_cols;
+        *out_col = index % tile_cols;
         return FLUX_OK;
     }
     if (kind != FLUX_SWIZZLE_RANK_SHIFTED && kind != FLUX_SWIZZLE_ARRIVAL_ALIGNED)
         return fail(FLUX_ERR_CONFIG, "unknown swizzle kind");
+    if (row_blocks != tp) return fail(FLUX_ERR_CONFIG, "grid row blocks != policy tp");
     std::vector<int> arrival(arrival_blocks ? arrival_blocks : nullptr,
                              arrival_blocks ? arrival_blocks + n_arrival : nullptr);
-    std::vector<int> blocks = block_order(kind, rank, p->tp, shift_offset, arrival);
-    if (static_cast<int>(blocks.size()) != p->tp)
+    const std::vector<int> blocks = block_order(kind, rank, tp, shift_offset, arrival);
+    if (static_cast<int>(blocks.size()) != row_blocks)
         return fail(FLUX_ERR_CONFIG, "arrival block list does not cover the grid (" + S(blocks.size()) +
-                                         " blocks for " + S(p->tp) + ")");
-    const int rpb = tile_rows / p->tp, per_block = rpb * tile_cols;
-    for (int i = 0; i < tiles; ++i) {
-        const int block = blocks[i / per_block];
-        const int within = i % per_block;
-        out_rows[i] = block * rpb + within % rpb;  // column-major within the block
-        out_cols[i] = within / rpb;
-    }
+                                         " blocks for " + S(row_blocks) + ")");
+    const int rpb = tile_rows / row_blocks, per_block = rpb * tile_cols;
+    const int block = blocks[index / per_block];
+    const int within = index % per_block;
+    *out_row = block * rpb + within % rpb;  // column-major within the block (swizzle.cpp:67-72)
+    *out_col = within / rpb;
     return FLUX_OK;
+}
+
+int flux_tile_order(const flux_problem* p, const flux_tile* t, int kind, int rank, int shift_offset,
+                    const int* arrival_blocks, int n_arrival, int* out_rows, int* out_cols) {
+    FLUX_TRY(validate_tiling(p, t));
+    const int tile_rows = p->m / t->tm, tile_cols = local_cols(p) / t->tn, tiles = tile_rows * tile_cols;
+    for (int i = 0; i < tiles; ++i)
+        FLUX_TRY(flux_map_tile(kind, rank, p->tp, shift_offset, arrival_blocks, n_arrival, tile_rows, tile_cols, p->tp,
+                               i, &out_rows[i], &out_cols[i]));
+    return FLUX_OK;
+}
+
+int flux_validate_comm_spec(const flux_problem* p, int rank, int rows_per_comm_tile, int transfer, const int* peer,
+                            const int* row_begin, const int* rows, int count) {
+    FLUX_TRY(validate_problem(p));
+    if (rank < 0 || rank >= p->tp) return fail(FLUX_ERR_CONFIG, "rank " + S(rank) + " >= tp");
+    if (transfer != FLUX_PULL && transfer != FLUX_PUSH) return fail(FLUX_ERR_CONFIG, "unknown transfer mode");
+    std::vector<Desc> order;
+    for (int i = 0; i < count; ++i) order.push_back({peer[i], row_begin[i], rows[i]});
+    return validate_comm_spec(p, rank, rows_per_comm_tile, transfer, order);
 }
 
 int flux_comm_order(int rank, int tp, int rpr, int rpct, int* out_peer, int* out_row_begin, int* out_rows, int max,
@@ -1216,6 +1260,7 @@ int flux_comm_destroy(flux_comm* c) {
         cudaEventDestroy(pr.second);
     }
     if (c->err_host) cudaFreeHost(c->err_host);
+    for (cudaEvent_t x : c->xfer_events) cudaEventDestroy(x);
     delete c;
     return FLUX_OK;
 }
@@ -1371,7 +1416,8 @@ static int check_activation(flux_comm* c, const flux_problem* p, const flux_opts
 // AllGather runs on the in-kernel transfer engine.
 // ---------------------------------------------------------------------------
 static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
-                        int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands);
+                        int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands,
+                        const std::vector<std::vector<Desc>>* custom = nullptr);
 static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
                         const flux_opts* opts, void* const* streams, const flux_operands* operands);
 static int local_gemm_impl(flux_comm* c, const flux_problem* p, const flux_opts* opts, void* const* streams);
@@ -1387,7 +1433,7 @@ static int graph_zero(flux_comm* c, const flux_problem* p, void* const* streams)
     add(kCtrlReady, kCtrlRedExit + 4 - kCtrlReady);  // ready / done / kdone / fr_ready / trace / work counters
     add(kAgFlagOffset, std::min<size_t>(kAgFlagCap, static_cast<size_t>(p->m)) * 4);
     add(kAgCtrGraphOffset, (static_cast<size_t>((p->m + kBM - 1) / kBM) + 1) * 4);
-    add(kTailCtrOffset, static_cast<size_t>(kTailCtrCap) * 4);
+    add(kTailCtrOffset, static_cast<size_t>(2 * kTailCtrCap) * 4);  // arrival + RS-units staged counters
     if (p->pattern == FLUX_GEMM_REDUCESCATTER) {
         const size_t tiles = static_cast<size_t>((p->m + kBM - 1) / kBM) * ((p->n + kBN - 1) / kBN);
         add(kRsFlagOffset, std::min(kRsFlagCap, tiles * p->tp) * 4);
@@ -1423,6 +1469,7 @@ static int run_op(flux_comm* c, const std::function<int()>& body) {
     FLUX_TRY(begin_op(c));
     const int rc = body();
     if (rc != FLUX_OK) {
+        if (c->act_fault_kind != 0) c->ag_sig = 0;
         c->act_fault_kind = 0;
         return rc;
     }
@@ -1497,7 +1544,8 @@ int flux_ag_gemm(flux_comm* c, const flux_problem* p, const flux_tile* tile, int
 }
 
 static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
-                        int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands) {
+                        int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands,
+                        const std::vector<std::vector<Desc>>* custom) {
     FLUX_TRY(check_comm(c));
     if (p && p->pattern != FLUX_ALLGATHER_GEMM)
         return fail(FLUX_ERR_CONFIG, "run_fused_allgather_gemm requires AllGatherGemm pattern");
@@ -1508,10 +1556,28 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     const int tp = p->tp, rpr = rows_per_rank(p);
     if (rpct <= 0) rpct = rpr;
     if (p->m / rpct > static_cast<int>(kAgFlagCap)) return fail(FLUX_ERR_CONFIG, "too many comm tiles");
-    std::vector<std::vector<Desc>> specs(tp);
-    for (int r = 0; r < tp; ++r) FLUX_TRY(make_spec(p, r, rpct, transfer, specs[r]));
+    // Comm specs: the reference's (make_comm_specs) or the caller's orders for
+    // the ranks this process drives (run_fused_allgather_gemm's comm_specs,
+    // engine.hpp:107-111; the transfer agent walks them, engine.cpp:367-423).
+    std::vector<std::vector<Desc>> specs, pull_specs;
+    FLUX_TRY(default_specs(p, rpct, transfer, specs));
     std::vector<int> mine;
     local_ranks_only(c, mine);
+    if (custom) {
+        for (int r : mine) {
+            const std::vector<Desc>& o = (*custom)[r];
+            FLUX_TRY(validate_comm_spec(p, r, rpct, transfer, o));
+            for (const Desc& d : o) {  // what the reference's copy_rows would reject at run time
+                const int owner = d.row_begin / rpr;
+                if (d.peer < 0 || d.peer >= tp || d.peer == r || (transfer == FLUX_PULL && d.peer != owner))
+                    return fail(FLUX_ERR_BOUNDS, "transfer descriptor peer " + S(d.peer) + " rows [" + S(d.row_begin) +
+                                                     ",+" + S(d.rows) + ") not served by that peer (rank " + S(r) + ")");
+            }
+            specs[r] = o;
+        }
+    }
+    if (transfer == FLUX_PULL) pull_specs = specs;
+    else FLUX_TRY(default_specs(p, rpct, FLUX_PULL, pull_specs));
     // Directory check: every peer this rank touches must be mapped (workspace.cpp:56-65).
     for (int r : mine)
         for (int q = 0; q < tp; ++q) FLUX_TRY(check_directory(c, r, q));
@@ -1591,7 +1657,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         for (int r : mine) {
             // Pieces always move in arrival order (own block first, then the ring);
             // the swizzle only decides the order the tiles consume them.
-            blocks[r] = ag_block_order(p, r, FLUX_PULL, true, rpct);
+            blocks[r] = ag_block_order(p, r, FLUX_PULL, true, pull_specs);
             seq[r] = device_sequence(p->m, local_cols(p), rpr, swizzle_on ? blocks[r] : std::vector<int>{}, kBM * cg,
                                      group_blocks(rpr, kBM * cg, /*ag=*/true));
         }
@@ -1599,7 +1665,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         const bool push = transfer == FLUX_PUSH;
         std::vector<std::vector<int>> blocks_all(tp);  // every rank's consumption order (Push tables)
         if (push)
-            for (int q = 0; q < tp; ++q) blocks_all[q] = ag_block_order(p, q, FLUX_PULL, true, rpct);
+            for (int q = 0; q < tp; ++q) blocks_all[q] = ag_block_order(p, q, FLUX_PULL, true, pull_specs);
         auto extra = [&](const std::vector<int>& g, GemmParams& prm) -> int {
             // Piece table in consumption order: every slot's own block first (peers
             // copy from it), then the others in the order the tiles need them.
@@ -1687,6 +1753,15 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         return FLUX_OK;
     }
 
+    // Traced: the copy engines stamp device-clock records into the trace rings
+    // too, so the cursors are zeroed before the copy stream starts.
+    if (oc.o.trace) {
+        for (int r : mine) {
+            FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
+            FLUX_CUDA(cudaMemsetAsync(c->ranks[r].heap + kCtrlTraceCursor, 0, 4, stream_for(c, r, streams)));
+        }
+        oc.trace_cursors_reset = true;
+    }
     // One copy-engine stream per device (several blocked stream-wait memops on
     // many streams can starve each other on shared hardware queues). It starts
     // after the caller's prior work (the A shards) and after the previous kernel
@@ -1708,7 +1783,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     // first so it computes ready (local) tiles while the host enqueues Alg. 3.
     std::vector<std::vector<uint32_t>> seq(tp);
     for (int r : mine)
-        seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, rpct),
+        seq[r] = device_sequence(p->m, local_cols(p), rpr, ag_block_order(p, r, transfer, swizzle_on != 0, specs),
                                  kBM * cg, group_blocks(rpr, kBM * cg, /*ag=*/true));
     auto launch_kernel = [&]() {
         return launch_groups(c, p, kModeAG, oc, streams, seq, rpct,
@@ -1747,10 +1822,66 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         }
         return FLUX_OK;
     };
+    std::vector<std::vector<uint8_t>> waited(tp, std::vector<uint8_t>(tp, 0));
+    // TransferRecord timing (opts.trace; engine.cpp:395-420): an event after
+    // each descriptor's copy and after its flag write on the copy stream,
+    // relative to one base event per copy stream (flux_transfer_log).
+    const bool log_xfer = oc.o.trace != 0;
+    if (log_xfer) {
+        c->xfer_log.clear();
+        c->xfer_used = 0;
+    }
+    auto next_event = [&](cudaEvent_t* ev) -> int {
+        if (c->xfer_used == c->xfer_events.size()) {
+            cudaEvent_t x;
+            FLUX_CUDA(cudaEventCreate(&x));
+            c->xfer_events.push_back(x);
+        }
+        *ev = c->xfer_events[c->xfer_used++];
+        return FLUX_OK;
+    };
+    cudaEvent_t xfer_base = nullptr;
+    // Device-clock stamp in the trace ring of `board` (the rank whose flag it is).
+    auto stamp = [&](cudaStream_t cs, int board, uint32_t kind, int flag, int peer) -> int {
+        if (!c->ranks[board].local) return FLUX_OK;
+        char* h = c->ranks[board].heap;
+        FLUX_CUDA(launch_trace_stamp(reinterpret_cast<unsigned long long*>(h + L.trace_off),
+                                     reinterpret_cast<uint32_t*>(h + kCtrlTraceCursor),
+                                     static_cast<uint32_t>(kTraceBytes / 16),
+                                     trace_word(kind, board, static_cast<uint32_t>(flag), flag, peer), cs));
+        return FLUX_OK;
+    };
+    auto log_copy = [&](cudaStream_t cs, int owner, const Desc& d) -> int {
+        if (!log_xfer) return FLUX_OK;
+        const int board = transfer == FLUX_PULL ? owner : d.peer;
+        FLUX_TRY(stamp(cs, board, kEvCopyDone, d.row_begin / rpct, d.peer));
+        flux_comm::XferEntry x;
+        x.rank = owner;
+        x.peer = d.peer;
+        x.row_begin = d.row_begin;
+        x.rows = d.rows;
+        x.base = xfer_base;
+        FLUX_TRY(next_event(&x.copy_ev));
+        FLUX_CUDA(cudaEventRecord(x.copy_ev, cs));
+        c->xfer_log.push_back(x);
+        return FLUX_OK;
+    };
+    auto log_flag = [&](cudaStream_t cs) -> int {
+        if (!log_xfer) return FLUX_OK;
+        const flux_comm::XferEntry& x = c->xfer_log.back();
+        FLUX_TRY(stamp(cs, transfer == FLUX_PULL ? x.rank : x.peer, kEvSignalSet, x.row_begin / rpct, x.peer));
+        FLUX_TRY(next_event(&c->xfer_log.back().flag_ev));
+        FLUX_CUDA(cudaEventRecord(c->xfer_log.back().flag_ev, cs));
+        return FLUX_OK;
+    };
     for (const auto& g : groups) {
         RankState& lead = c->ranks[g[0]];
         FLUX_CUDA(cudaSetDevice(lead.device));
         cudaStream_t cs = lead.copy_stream;
+        if (log_xfer) {
+            FLUX_TRY(next_event(&xfer_base));
+            FLUX_CUDA(cudaEventRecord(xfer_base, cs));
+        }
         auto in_group = [&](int q) { return std::find(g.begin(), g.end(), q) != g.end(); };
         // Remote peers finished pulling my previous shard before I overwrite it
         // (ranks sharing this stream are ordered by the stream itself).
@@ -1793,7 +1924,23 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
             for (int cr : g) {
                 FLUX_TRY(local_copy(cr));
                 RankState& rs = c->ranks[cr];
-                const std::vector<int> order = ag_block_order(p, cr, transfer, swizzle_on != 0, rpct);
+                if (transfer == FLUX_PULL) {
+                    // cr's comm spec in its own order (the reference transfer agent,
+                    // engine.cpp:378-405; the kernel's block order follows it).
+                    for (const Desc& d : specs[cr]) {
+                        const char* shard;
+                        size_t pitch;
+                        shard_of(d.peer, shard, pitch);
+                        FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
+                                           rowbytes, shard + static_cast<size_t>(d.row_begin - d.peer * rpr) * pitch,
+                                           pitch, d.rows));
+                        FLUX_TRY(log_copy(cs, cr, d));
+                        FLUX_TRY(set_flag(cs, cr, d.row_begin / rpct));
+                        FLUX_TRY(log_flag(cs));
+                    }
+                    continue;
+                }
+                const std::vector<int> order = ag_block_order(p, cr, transfer, swizzle_on != 0, specs);
                 for (int b : order) {
                     if (b == cr) continue;
                     const std::vector<Desc>& list = transfer == FLUX_PULL ? specs[cr] : specs[b];
@@ -1806,7 +1953,9 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
                         FLUX_TRY(copy_rows(cs, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
                                            rowbytes, shard + static_cast<size_t>(d.row_begin - b * rpr) * pitch, pitch,
                                            d.rows));
+                        FLUX_TRY(log_copy(cs, transfer == FLUX_PULL ? cr : b, d));
                         FLUX_TRY(set_flag(cs, cr, d.row_begin / rpct));
+                        FLUX_TRY(log_flag(cs));
                     }
                 }
             }
@@ -1833,7 +1982,8 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
                 const Desc& d = specs[r][i];
                 const int q = d.peer;
                 const RankState& qs = c->ranks[q];
-                const bool first = i == step * per_peer;
+                const bool first = !waited[r][q];  // first descriptor involving peer q in this operator
+                waited[r][q] = true;
                 if (transfer == FLUX_PULL) {
                     char* dst = rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes;
                     if (in_group(q)) {
@@ -1848,14 +1998,18 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
                                            qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes, rowbytes,
                                            d.rows));
                     }
+                    FLUX_TRY(log_copy(cs, r, d));
                     FLUX_TRY(set_flag(cs, r, d.row_begin / rpct));
+                    FLUX_TRY(log_flag(cs));
                 } else {
                     if (first && !in_group(q)) FLUX_TRY(wait_value_geq(cs, qs.heap + kCtrlKdone, e - 1));
                     // Push reads from my own a_agg slot (already holds my shard).
                     FLUX_TRY(copy_rows(cs, qs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
                                        rowbytes, rs.heap + L.a_agg.off + static_cast<size_t>(d.row_begin) * rowbytes,
                                        rowbytes, d.rows));
+                    FLUX_TRY(log_copy(cs, r, d));
                     FLUX_TRY(set_flag(cs, q, d.row_begin / rpct));
+                    FLUX_TRY(log_flag(cs));
                 }
             }
         }
@@ -2337,7 +2491,7 @@ int flux_sync(flux_comm* c) {
         FLUX_CUDA(cudaSetDevice(rs.device));
         FLUX_CUDA(cudaStreamSynchronize(rs.copy_stream));
         FLUX_CUDA(cudaDeviceSynchronize());
-        uint32_t err[4] = {0, 0, 0, 0};
+        uint32_t err[6] = {0, 0, 0, 0, 0, 0};
         FLUX_CUDA(cudaMemcpy(err, rs.heap + kCtrlErr, sizeof(err), cudaMemcpyDeviceToHost));
         if (err[0] != 0) {
             if (deadlock.empty()) {
@@ -2347,11 +2501,12 @@ int flux_sync(flux_comm* c) {
             // Clean state for the next operator: the error record and epoch,
             // the launch-scoped work counters a failed launch may have left
             // armed (dynamic tiles, reduction units), the host mirror.
+            c->ag_sig = 0;  // a failed in-kernel AllGather may have left its piece counters short
             const uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlErr, zero, 20, cudaMemcpyHostToDevice));
+            FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlErr, zero, 24, cudaMemcpyHostToDevice));
             FLUX_CUDA(cudaMemcpy(rs.heap + kCtrlDynCtr, zero, 16, cudaMemcpyHostToDevice));  // + reduction counters
         }
-        if (c->err_host) std::memset(c->err_host + 4 * r, 0, 16);
+        if (c->err_host) std::memset(c->err_host + 8 * r, 0, 32);
     }
     if (!deadlock.empty()) return fail(code, deadlock);
     return FLUX_OK;
@@ -2373,6 +2528,46 @@ int flux_trace_read(flux_comm* c, int rank, const flux_problem* p, void* out, si
     if (k) FLUX_CUDA(cudaMemcpy(out, rs.heap + layout_for(p).trace_off, k * 16, cudaMemcpyDeviceToHost));
     if (count) *count = k;
     return FLUX_OK;
+}
+
+int flux_transfer_log(flux_comm* c, int rank, flux_transfer_record* out, int max, int* count) {
+    if (!c) return fail(FLUX_ERR_CONFIG, "null communicator");
+    int n = 0;
+    for (const auto& x : c->xfer_log) {
+        if (x.rank != rank) continue;
+        if (n < max && out) {
+            FLUX_CUDA(cudaEventSynchronize(x.flag_ev));
+            float t_copy = 0.0f, t_flag = 0.0f;
+            FLUX_CUDA(cudaEventElapsedTime(&t_copy, x.base, x.copy_ev));
+            FLUX_CUDA(cudaEventElapsedTime(&t_flag, x.base, x.flag_ev));
+            out[n] = flux_transfer_record{x.peer, x.row_begin, x.rows, static_cast<int64_t>(t_copy * 1e6),
+                                          static_cast<int64_t>(t_flag * 1e6)};
+        }
+        ++n;
+    }
+    if (count) *count = n;
+    return FLUX_OK;
+}
+
+int flux_ag_gemm_ordered(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
+                         int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands,
+                         const int* order_peer, const int* order_row_begin, const int* order_rows, int count) {
+    return run_op(c, [&]() -> int {
+        if (!p || !order_peer || !order_row_begin || !order_rows || count < 0)
+            return fail(FLUX_ERR_CONFIG, "null comm order");
+        if (opts && opts->graph_safe) return fail(FLUX_ERR_CONFIG, "graph_safe operators use the reference comm order");
+        std::vector<std::vector<Desc>> custom(c->tp);
+        int slot = 0;
+        for (int r = 0; r < c->tp; ++r) {
+            if (!c->ranks[r].local) continue;
+            for (int j = 0; j < count; ++j) {
+                const size_t i = static_cast<size_t>(slot) * count + j;
+                custom[r].push_back({order_peer[i], order_row_begin[i], order_rows[i]});
+            }
+            ++slot;
+        }
+        return ag_gemm_impl(c, p, tile, rpct, transfer, swizzle_on, opts, streams, operands, &custom);
+    });
 }
 
 int flux_comm_inject_fault(flux_comm* c, int kind, int rank, int index) {

@@ -32,7 +32,7 @@ enum KernelMode : int { kModePlain = 0, kModeAG = 1, kModeRS = 2, kModeRSUnits =
 // two launch-scoped work counters (dynamic tiles, reduction units) are re-armed
 // by the last CTA / group of the launch that used them.
 constexpr size_t kCtrlErr = 0;          // u32[4]: code, info0, info1, info2
-constexpr size_t kCtrlErrEpoch = 16;    // u32: epoch of the operator whose wait recorded the error
+constexpr size_t kCtrlErrEpoch = 16;    // u32: epoch of the operator whose wait recorded the error; +4: failing rank + 1
 constexpr size_t kCtrlReady = 64;       // u32: epoch at which this rank's A shard is staged (AG pull source ready)
 constexpr size_t kCtrlDone = 68;        // u32: epoch whose peer pulls this rank has finished
 constexpr size_t kCtrlKdone = 72;       // u32: epoch whose kernel finished on this rank (push targets)
@@ -46,15 +46,21 @@ constexpr size_t kTraceBytes = size_t(4) << 20;  // trace ring at the end of the
 // Trace record kinds (the reference CausalityLog event names, engine.hpp:37-63).
 // kEvLaunch (not in the reference schema): a CTA's first (tile_col 0) and last (tile_col 1)
 // instruction, for launch-latency profiling.
+// kEvCopyDone (not in the reference schema): a copy-engine transfer's rows landed (before its flag).
 enum TraceKind : uint32_t { kEvComputeStart = 1, kEvSignalSet = 2, kEvTileWrite = 3, kEvReduce = 4, kEvWait = 5,
-                            kEvLaunch = 6 };
+                            kEvLaunch = 6, kEvCopyDone = 7 };
+__host__ __device__ inline uint64_t trace_word(uint32_t kind, int rank, uint32_t target, int tile_row, int tile_col) {
+    return (static_cast<uint64_t>(kind) << 60) | (static_cast<uint64_t>(rank & 0xF) << 56) |
+           (static_cast<uint64_t>(target & 0xFFFFFFu) << 32) | (static_cast<uint64_t>(tile_row & 0xFFFF) << 16) |
+           static_cast<uint64_t>(tile_col & 0xFFFF);
+}
 constexpr size_t kAgFlagOffset = 4096;  // u32[kAgFlagCap]: one flag per comm tile (SignalBoard)
 constexpr size_t kAgFlagCap = 16384;
 // In-kernel AllGather: u32[kAgGroupCap] monotonic piece counters per 128-row
 // group of a_agg (+ one own-block counter), +1 per landed piece, zeroed on layout change.
 // Tail split (Plain / AG): epoch-tagged arrival counters of the split tail tiles.
 constexpr size_t kTailCtrOffset = 72 * 1024;
-constexpr int kTailCtrCap = 256;
+constexpr int kTailCtrCap = 256;   // per counter set; two sets (slices parked / RS-units slices staged)
 constexpr int kTailMaxSplits = 8;
 constexpr int kTailWsCtas = 160;  // workspace slots (>= CTAs of one launch): 128 x 256 fp32 each
 constexpr size_t kAgCtrOffset = 128 * 1024;
@@ -197,5 +203,11 @@ struct ZeroParams {
     int nranges;
 };
 cudaError_t launch_zero_ranges(const ZeroParams& p, int nheaps, cudaStream_t stream);
+
+// Traced copy-engine transfers: one device-clock (%globaltimer) record in a
+// rank's trace ring, enqueued on the copy stream between its copies and flag
+// writes (a single-thread kernel that co-resides with the persistent GEMM).
+cudaError_t launch_trace_stamp(unsigned long long* ring, uint32_t* cursor, uint32_t cap, uint64_t word,
+                               cudaStream_t stream);
 
 }  // namespace fluxb200

@@ -319,25 +319,34 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 __device__ __forceinline__ uint32_t ld_acquire_flag(const GemmParams& p, const uint32_t* f) {
     return p.all_local && !(p.dbg & 512) ? ld_acquire_gpu(f) : ld_acquire_sys(f);
 }
-// First failure of local slot l in this operator: the control block's error
-// record (read by flux_sync) plus the host-mapped mirror the host checks at the
-// start of the next operator (so a failure cannot go unnoticed when the caller
-// never synchronises through flux_sync, e.g. the PyTorch ops).
+// First failure of an operator: the error record {code, info0, info1, info2,
+// epoch, failing rank + 1} goes into the launch's lead slot's control block
+// (slot 0: the first failure of the whole launch, which the sibling waits of
+// every slot watch, so one missing signal does not cascade into timeouts of
+// tiles stalled behind it) and into the failing slot's own; flux_sync reads
+// them. The host-mapped mirror ([global rank][8] u32) carries the same
+// records so the next operator call can report the failure without a sync.
 __device__ void record_error(const GemmParams& p, int l, uint32_t code, uint32_t info0, uint32_t info1,
                              uint32_t info2) {
-    uint32_t* ctrl = p.ctrl[l];
-    if (atomicCAS(ctrl + 0, 0u, code) != 0u) return;
-    ctrl[1] = info0;
-    ctrl[2] = info1;
-    ctrl[3] = info2;
-    ctrl[kCtrlErrEpoch / 4] = p.epoch;
-    if (p.err_host != nullptr) {
-        volatile uint32_t* h = p.err_host + 4 * p.global_rank[l];
-        h[1] = info0;
-        h[2] = info1;
-        h[3] = info2;
-        __threadfence_system();
-        h[0] = code;
+    const uint32_t who = static_cast<uint32_t>(p.global_rank[l]) + 1u;
+    for (int s = 0; s < (l == 0 ? 1 : 2); ++s) {
+        const int slot = s == 0 ? 0 : l;
+        uint32_t* ctrl = p.ctrl[slot];
+        if (atomicCAS(ctrl + 0, 0u, code) != 0u) continue;
+        ctrl[1] = info0;
+        ctrl[2] = info1;
+        ctrl[3] = info2;
+        ctrl[kCtrlErrEpoch / 4] = p.epoch;
+        ctrl[kCtrlErrEpoch / 4 + 1] = who;
+        if (p.err_host != nullptr) {
+            volatile uint32_t* h = p.err_host + 8 * p.global_rank[slot];
+            h[1] = info0;
+            h[2] = info1;
+            h[3] = info2;
+            h[5] = who;
+            __threadfence_system();
+            h[0] = code;
+        }
     }
     __threadfence_system();
 }
@@ -351,7 +360,7 @@ __device__ bool wait_flag(const uint32_t* flag, uint32_t target, const GemmParam
     if (static_cast<int32_t>(ld_acquire_flag(p, flag) - target) >= 0) return true;
     const uint64_t t0 = globaltimer();
     uint32_t ns = 32;
-    const volatile uint32_t* ctrl = p.ctrl[l];
+    const volatile uint32_t* ctrl = p.ctrl[0];  // the launch's first failure (record_error)
     for (;;) {
         __nanosleep(ns);
         if (ns < 256) ns <<= 1;
@@ -414,9 +423,7 @@ __device__ __forceinline__ void trace_event(const GemmParams& p, int l, uint32_t
     if (i >= p.trace_cap) return;
     unsigned long long* rec = p.trace[l] + 2ull * i;
     rec[0] = ts;
-    rec[1] = (static_cast<uint64_t>(kind) << 60) | (static_cast<uint64_t>(rank & 0xF) << 56) |
-             (static_cast<uint64_t>(target & 0xFFFFFFu) << 32) | (static_cast<uint64_t>(tile_row & 0xFFFF) << 16) |
-             static_cast<uint64_t>(tile_col & 0xFFFF);
+    rec[1] = trace_word(kind, rank, target, tile_row, tile_col);
 }
 
 // Publish one landed AG piece (trace timestamp taken before the release).
@@ -1145,6 +1152,60 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(as * kBN);
+            // Tail split (K-slices of one tile in the last wave): park this slice's
+            // accumulator, hand TMEM back to the MMA warp, wait until every slice
+            // of the tile has parked; returns this thread's row in slice 0's slot
+            // (slots are [column][row] fp32, slice s at + s * CG * 128 * 256).
+            auto park_tail_slice = [&]() -> const float* {
+                const int ti = (t - p.tail_base) / p.tail_splits;
+                const long long slot_stride = static_cast<long long>(kBM) * kBN;
+                // Slot layout [column][row] (row fastest): a warp's 32 rows of one
+                // column are 128 contiguous bytes, so these stores and the summing
+                // loads are coalesced without a shared-memory transpose.
+                float* mine = p.tail_ws + (static_cast<long long>(ti * p.tail_splits + split) * CG + cta_rank) *
+                                              slot_stride + q * 32 + lane;
+                for (int c = 0; c < kBN / 32; ++c) {
+                    if (col0 + c * 32 >= p.n) break;  // warp-uniform
+                    uint32_t r[32];
+                    tmem_ld32(tbase + c * 32, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) mine[(c * 32 + j) * kBM] = __uint_as_float(r[j]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(as * 8));
+                    else mbar_arrive(&tempty[as]);
+                }
+                released = true;
+                // All slices of this tile run in the same (last) wave: wait for
+                // every one of them, then each slice sums and stores its share
+                // of the 32-column chunks (c % slices == slice), so the
+                // reduction is spread over the slices' CTAs.
+                named_bar_sync(1, 128);
+                if (et == 0) {
+                    uint32_t* ctr = p.tail_ctr + ti * CG + cta_rank;
+                    const uint32_t done = ((p.tail_seq & 0xFFFFFFu) << 8) | static_cast<uint32_t>(p.tail_splits);
+                    if (tail_arrive(ctr, p.tail_seq) != static_cast<uint32_t>(p.tail_splits)) {
+                        const uint64_t t0 = globaltimer();
+                        for (;;) {
+                            uint32_t v;
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                            if (v == done) break;
+                            if (globaltimer() - t0 > p.timeout_ns) {
+                                record_error(p, l, kErrAgFlagTimeout, static_cast<uint32_t>(ti),
+                                             0xFFFE0000u | static_cast<uint32_t>(split), done);
+                                break;
+                            }
+                            __nanosleep(64);
+                        }
+                    }
+                }
+                named_bar_sync(1, 128);
+                return p.tail_ws + (static_cast<long long>(ti * p.tail_splits) * CG + cta_rank) * slot_stride + q * 32 +
+                       lane;
+            };
             if (row0 >= p.m) {
                 // Fully out-of-range half of a pair tile: nothing to store or signal.
             } else if (MODE != kModeRS && MODE != kModeRSUnits) {
@@ -1184,56 +1245,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     // arrive sums all of them in slice order and runs the epilogue.
                     bool do_store = true;
                     const float* tail_src = nullptr;
-                    if (split >= 0) {
-                        const int ti = (t - p.tail_base) / p.tail_splits;
-                        const long long slot_stride = static_cast<long long>(kBM) * kBN;
-                        // Slot layout [column][row] (row fastest): a warp's 32 rows of one
-                        // column are 128 contiguous bytes, so these stores and the last
-                        // arriver's loads are coalesced without a shared-memory transpose.
-                        float* mine = p.tail_ws + (static_cast<long long>(ti * p.tail_splits + split) * CG + cta_rank) *
-                                                      slot_stride + q * 32 + lane;
-                        for (int c = 0; c < kBN / 32; ++c) {
-                            if (col0 + c * 32 >= p.n) break;  // warp-uniform
-                            uint32_t r[32];
-                            tmem_ld32(tbase + c * 32, r);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) mine[(c * 32 + j) * kBM] = __uint_as_float(r[j]);
-                        }
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (CG == 2) mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(as * 8));
-                            else mbar_arrive(&tempty[as]);
-                        }
-                        released = true;
-                        // All slices of this tile run in the same (last) wave: wait for
-                        // every one of them, then each slice sums and stores its share
-                        // of the 32-column chunks (c % slices == slice), so the
-                        // reduction is spread over the slices' CTAs.
-                        named_bar_sync(1, 128);
-                        if (et == 0) {
-                            uint32_t* ctr = p.tail_ctr + ti * CG + cta_rank;
-                            const uint32_t done = ((p.tail_seq & 0xFFFFFFu) << 8) | static_cast<uint32_t>(p.tail_splits);
-                            if (tail_arrive(ctr, p.tail_seq) != static_cast<uint32_t>(p.tail_splits)) {
-                                const uint64_t t0 = globaltimer();
-                                for (;;) {
-                                    uint32_t v;
-                                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-                                    if (v == done) break;
-                                    if (globaltimer() - t0 > p.timeout_ns) {
-                                        record_error(p, l, kErrAgFlagTimeout, static_cast<uint32_t>(ti),
-                                                     0xFFFE0000u | static_cast<uint32_t>(split), done);
-                                        break;
-                                    }
-                                    __nanosleep(64);
-                                }
-                            }
-                        }
-                        named_bar_sync(1, 128);
-                        tail_src = p.tail_ws + (static_cast<long long>(ti * p.tail_splits) * CG + cta_rank) * slot_stride +
-                                   q * 32 + lane;
-                    }
+                    if (split >= 0) tail_src = park_tail_slice();
                     for (int c = 0; do_store && c < kBN / 32; ++c) {
                         const int col = col0 + c * 32;
                         if (col >= p.n) break;  // warp-uniform
@@ -1311,6 +1323,51 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 const int tile_id = tm * p.tiles_n + tn;
                 const int rpr = p.rpr;
                 const long long ld_stage = p.ld_stage;
+                if (split >= 0) {
+                    // Split-K (fewer tiles than SMs, e.g. one GPU's decode share): the
+                    // slices of the tile park their accumulators, each slice sums its
+                    // share of the 32-column chunks in slice order (deterministic) and
+                    // stores them into the owners' staging planes (row per thread, 128
+                    // contiguous bytes); the last slice to finish stamps the flags.
+                    const float* src = park_tail_slice();
+                    const long long slot_stride = static_cast<long long>(CG) * kBM * kBN;
+                    const int o = valid ? row / rpr : 0;
+                    for (int c = split; c < kBN / 32; c += p.tail_splits) {
+                        const int colc = col0 + c * 32;
+                        if (colc >= p.n) break;  // warp-uniform
+                        if (!valid || (p.dbg & 8)) continue;
+                        float v[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = __ldcg(src + (c * 32 + j) * kBM);
+                        for (int x = 1; x < p.tail_splits; ++x) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) v[j] += __ldcg(src + x * slot_stride + (c * 32 + j) * kBM);
+                        }
+                        const long long e = parity * p.stage_parity + me * p.stage_plane +
+                                            (row - static_cast<long long>(o) * rpr) * ld_stage + colc;
+                        if (colc + 32 <= p.n) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                st_part4<PB>(p.staging[o], e + j, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                        } else {
+                            for (int j = 0; j < 32 && colc + j < p.n; j += 4)  // ld_stage pads to 256 columns
+                                st_part4<PB>(p.staging[o], e + j, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                        }
+                    }
+                    // Every slice's stores precede its arrival; the last arrival
+                    // (acquire) stamps the owners' flags (release, cumulative).
+                    named_bar_sync(1, 128);
+                    if (et == 0) {
+                        __threadfence_system();
+                        const int ti = (t - p.tail_base) / p.tail_splits;
+                        uint32_t* ctr2 = p.tail_ctr + kTailCtrCap + ti * CG + cta_rank;
+                        if (tail_arrive(ctr2, p.tail_seq) == static_cast<uint32_t>(p.tail_splits)) {
+                            const int o0 = row0 / rpr, o1 = (min(row0 + kBM, p.m) - 1) / rpr;
+                            trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o0));
+                            for (int oo = o0; oo <= o1; ++oo) rs_flag_set(p, l, oo, tile_id, me);
+                        }
+                    }
+                } else {
                 for (int c = 0; c < kBN / 32; ++c) {
                     const int colc = col0 + c * 32;
                     if (colc >= p.n) break;  // warp-uniform
@@ -1360,6 +1417,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 if (et == 0) trace_event(p, l, kEvTileWrite, me, tm, tn, static_cast<uint32_t>(o0));
                 for (int o = o0 + et; o <= o1; o += 128)
                     rs_flag_set(p, l, o, tile_id, me);
+                }  // whole-tile staging
             } else {
                 const int me = p.global_rank[l];
                 const uint32_t parity = p.epoch & 1u;
@@ -1650,6 +1708,21 @@ __global__ void zero_ranges_kernel(ZeroParams p) {
         uint32_t* w = reinterpret_cast<uint32_t*>(h + p.off[r]);
         for (uint32_t i = threadIdx.x; i < p.bytes[r] / 4; i += blockDim.x) w[i] = 0u;
     }
+}
+
+__global__ void trace_stamp_kernel(unsigned long long* ring, uint32_t* cursor, uint32_t cap, uint64_t word) {
+    const uint64_t ts = globaltimer();
+    const uint32_t i = atomicAdd(cursor, 1u);
+    if (i < cap) {
+        ring[2ull * i] = ts;
+        ring[2ull * i + 1] = word;
+    }
+}
+
+cudaError_t launch_trace_stamp(unsigned long long* ring, uint32_t* cursor, uint32_t cap, uint64_t word,
+                               cudaStream_t stream) {
+    trace_stamp_kernel<<<1, 1, 0, stream>>>(ring, cursor, cap, word);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_zero_ranges(const ZeroParams& p, int nheaps, cudaStream_t stream) {

@@ -307,23 +307,12 @@ SwizzlePolicy arrival_aligned_policy(int rank, int tp, const std::vector<Transfe
     return p;
 }
 TileCoord map_tile(const SwizzlePolicy& policy, int i, const GridDims& g) {
-    if (i < 0 || i >= g.tiles())
-        throw BoundsError("tile index " + std::to_string(i) + " out of range [0," + std::to_string(g.tiles()) + ")");
-    if (policy.kind == SwizzleKind::Naive) return {i / g.tile_cols, i % g.tile_cols};
-    if (g.row_blocks != policy.tp) throw ConfigError("grid row blocks != policy tp");
-    std::vector<int> blocks = policy.arrival_blocks;
-    if (policy.kind == SwizzleKind::RankShifted || blocks.empty()) {
-        blocks.clear();
-        const int start = policy.kind == SwizzleKind::RankShifted ? (policy.rank + policy.shift_offset) % policy.tp
-                                                                  : policy.rank;
-        for (int d = 0; d < policy.tp; ++d) blocks.push_back((start + d) % policy.tp);
-    }
-    if (static_cast<int>(blocks.size()) != g.row_blocks)
-        throw ConfigError("arrival block list does not cover the grid (" + std::to_string(blocks.size()) +
-                          " blocks for " + std::to_string(g.row_blocks) + ")");
-    const int rpb = g.tile_rows_per_block(), per_block = rpb * g.tile_cols;
-    const int within = i % per_block;
-    return {blocks[i / per_block] * rpb + within % rpb, within / rpb};
+    static const int kKind[] = {FLUX_SWIZZLE_NAIVE, FLUX_SWIZZLE_RANK_SHIFTED, FLUX_SWIZZLE_ARRIVAL_ALIGNED};
+    TileCoord t;
+    ok(flux_map_tile(kKind[static_cast<int>(policy.kind)], policy.rank, policy.tp, policy.shift_offset,
+                     policy.arrival_blocks.data(), static_cast<int>(policy.arrival_blocks.size()), g.tile_rows,
+                     g.tile_cols, g.row_blocks, i, &t.row, &t.col));
+    return t;
 }
 std::vector<TileCoord> tile_order(const SwizzlePolicy& policy, const GridDims& g) {
     std::vector<TileCoord> out;
@@ -409,32 +398,15 @@ WriteMode write_mode_from_string(const std::string& s) {
 }
 
 void CommTileSpec::validate(const ProblemSpec& p, int rank, TransferMode mode) const {
-    const int rpr = p.rows_per_rank();
-    if (rows_per_comm_tile <= 0 || rpr % rows_per_comm_tile != 0)
-        throw ConfigError("rows_per_comm_tile=" + std::to_string(rows_per_comm_tile) + " must divide m/tp=" +
-                          std::to_string(rpr));
-    const int per = rpr / rows_per_comm_tile;
-    std::vector<int> seen(p.m / rows_per_comm_tile, 0);
+    const flux_problem cp = cprob(p);
+    std::vector<int> peer, begin, rows;
     for (const TransferDesc& d : order) {
-        if (d.rows != rows_per_comm_tile || d.row_begin % rows_per_comm_tile != 0 || d.row_begin < 0 ||
-            d.row_begin + d.rows > p.m)
-            throw BoundsError("transfer descriptor rows [" + std::to_string(d.row_begin) + ",+" +
-                              std::to_string(d.rows) + ") invalid");
-        ++seen[d.row_begin / rows_per_comm_tile];
+        peer.push_back(d.peer);
+        begin.push_back(d.row_begin);
+        rows.push_back(d.rows);
     }
-    for (int t = 0; t < static_cast<int>(seen.size()); ++t) {
-        const bool local = t / per == rank;
-        if (mode == TransferMode::Pull) {
-            if (!local && seen[t] != 1)
-                throw ConfigError("comm order must cover non-local comm tile " + std::to_string(t) +
-                                  " exactly once (saw " + std::to_string(seen[t]) + ")");
-            if (local && seen[t] != 0) throw ConfigError("comm order must not include local comm tiles");
-        } else {
-            if (local && seen[t] != p.tp - 1)
-                throw ConfigError("push order must carry local comm tile " + std::to_string(t) + " to every peer");
-            if (!local && seen[t] != 0) throw ConfigError("push order may only move local comm tiles");
-        }
-    }
+    ok(flux_validate_comm_spec(&cp, rank, rows_per_comm_tile, mode == TransferMode::Pull ? FLUX_PULL : FLUX_PUSH,
+                               peer.data(), begin.data(), rows.data(), static_cast<int>(order.size())));
 }
 
 std::vector<CommTileSpec> make_comm_specs(const ProblemSpec& p, const Topology&, int rpct, TransferMode mode) {
@@ -494,14 +466,56 @@ EngineResult run_fused_allgather_gemm(const ProblemSpec& p, ShardedWorkspace& ws
     const flux_problem cp = cprob(p);
     const flux_tile ct{tile.tm, tile.tn};
     flux_opts o = copts(opts);
-    o.trace = 1;  // EngineResult::log
-    ok(flux_ag_gemm(c, &cp, &ct, rpct, transfer == TransferMode::Pull ? FLUX_PULL : FLUX_PUSH, swizzle_on ? 1 : 0, &o,
-                    nullptr));
+    o.trace = 1;      // EngineResult::log and the TransferRecords
+    o.ag_engine = 1;  // the copy-engine transfer loop walks the caller's comm orders (engine.cpp:367-423)
+    const size_t count = comm[0].order.size();
+    std::vector<int> peer, begin, rows;
+    for (int r = 0; r < p.tp; ++r) {
+        if (comm[r].order.size() != count) throw ConfigError("all ranks' comm orders must have the same length");
+        for (const TransferDesc& d : comm[r].order) {
+            peer.push_back(d.peer);
+            begin.push_back(d.row_begin);
+            rows.push_back(d.rows);
+        }
+    }
+    ok(flux_ag_gemm_ordered(c, &cp, &ct, rpct, transfer == TransferMode::Pull ? FLUX_PULL : FLUX_PUSH,
+                            swizzle_on ? 1 : 0, &o, nullptr, nullptr, peer.data(), begin.data(), rows.data(),
+                            static_cast<int>(count)));
     ok(flux_sync(c));
     if (traces) {
+        // Device times of every descriptor's copy completion and flag write
+        // (CUDA events on the copy stream); logical timestamps order all of
+        // them, copies before flags on equal times (the reference's run clock).
         traces->assign(p.tp, {});
-        for (int r = 0; r < p.tp; ++r)
-            for (const TransferDesc& d : comm[r].order) (*traces)[r].push_back(TransferRecord{d, 0, 0, 0, 0});
+        struct Tick {
+            int64_t ns;
+            int phase, rank;
+            size_t idx;
+        };
+        std::vector<Tick> ticks;
+        for (int r = 0; r < p.tp; ++r) {
+            std::vector<flux_transfer_record> recs(count);
+            int n = 0;
+            ok(flux_transfer_log(c, r, recs.data(), static_cast<int>(count), &n));
+            for (int i = 0; i < n && i < static_cast<int>(count); ++i) {
+                TransferRecord tr;
+                tr.desc = TransferDesc{recs[i].peer, recs[i].row_begin, recs[i].rows, LinkClass::IntraNuma, -1, -1};
+                for (const TransferDesc& d : comm[r].order)
+                    if (d.row_begin == recs[i].row_begin && d.peer == recs[i].peer) tr.desc = d;
+                tr.copy_done_ns = recs[i].copy_done_ns;
+                tr.flag_set_ns = recs[i].flag_set_ns;
+                (*traces)[r].push_back(tr);
+                ticks.push_back({tr.copy_done_ns, 0, r, (*traces)[r].size() - 1});
+                ticks.push_back({tr.flag_set_ns, 1, r, (*traces)[r].size() - 1});
+            }
+        }
+        std::stable_sort(ticks.begin(), ticks.end(), [](const Tick& a, const Tick& b) {
+            return a.ns != b.ns ? a.ns < b.ns : a.phase < b.phase;
+        });
+        for (size_t i = 0; i < ticks.size(); ++i) {
+            TransferRecord& tr = (*traces)[ticks[i].rank][ticks[i].idx];
+            (ticks[i].phase == 0 ? tr.copy_logical_ts : tr.flag_logical_ts) = i + 1;
+        }
     }
     EngineResult res = collect(c, p, ws);
     res.log = device_log(c, p);

@@ -2,6 +2,7 @@
 // acceptance.cpp) compiled unchanged against the B200 drop-in header and run
 // on the GPU in tolerance mode. Prints one PASS/FAIL line per check; exit 1 on
 // any failure. `--host-only` runs only the checks that need no GPU.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -196,6 +197,33 @@ static void device_checks() {
         w = std::max(w, worst(got, oracle(q, s)));
     }
     check(w <= 1e-4, "24 random cases, all tp, worst rel err " + std::to_string(w));
+    // test_engine.cpp:102-115 on the device: the copy-engine transfer loop walks the
+    // caller's comm order (here each rank's ring list reversed) and records, per
+    // descriptor, device times with copy_done <= flag_set and copy tick < flag tick.
+    {
+        ProblemSpec q{64, 32, 48, 4, Pattern::AllGatherGemm};
+        ShardedWorkspace s = ShardedWorkspace::make_random(q, 7);
+        auto specs = make_comm_specs(q, Topology{}, 8, TransferMode::Pull);
+        for (auto& sp : specs) std::reverse(sp.order.begin(), sp.order.end());
+        std::vector<std::vector<TransferRecord>> traces;
+        auto res = run_fused_allgather_gemm(q, s, {8, 8}, specs, TransferMode::Pull, true, EngineOptions{}, &traces);
+        bool timed = traces.size() == 4, ordered = true;
+        for (int r = 0; r < 4 && timed; ++r) {
+            timed = timed && traces[r].size() == specs[r].order.size();
+            for (size_t i = 0; i < traces[r].size() && timed; ++i) {
+                const TransferRecord& t = traces[r][i];
+                timed = timed && t.copy_done_ns <= t.flag_set_ns && t.copy_logical_ts < t.flag_logical_ts;
+                ordered = ordered && t.desc.row_begin == specs[r].order[i].row_begin && t.desc.peer == specs[r].order[i].peer;
+            }
+        }
+        check(timed, "TransferRecords: copy_done_ns <= flag_set_ns, copy tick before flag tick, one per descriptor");
+        check(ordered, "the transfer loop walks the caller's (non-ring) comm order");
+        check(worst(res.outputs, oracle(q, s)) <= 1e-4, "all-gather on a caller comm order within 1e-4");
+        auto bad = make_comm_specs(q, Topology{}, 8, TransferMode::Pull);
+        bad[1].order[0] = bad[1].order[1];
+        check(throws<ConfigError>([&] { run_fused_allgather_gemm(q, s, {8, 8}, bad, TransferMode::Pull, true); }),
+              "comm order covering a tile twice raises ConfigError");
+    }
     // test_engine.cpp:182-188 DirectoryError
     ShardedWorkspace d = ShardedWorkspace::make_random(p, 1);
     d.drop_directory_entry(1, 2);

@@ -20,7 +20,7 @@ def test_committed_bench_line_has_every_contract_key():
     assert d["config"]["workload"] == "llama70b-up-ag" and d["unit"] == "TFLOPS" and d["higher_is_better"] is True
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
-    assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] <= 1.0
+    assert r["bound"] in ("hbm", "tensor", "nvlink") and 0 < r["frac"] <= 1.0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-6
     c = d["cpu_baseline"]
     assert {"value", "unit", "cores", "kind", "sample"} <= set(c) and c["kind"] in ("reference", "port")

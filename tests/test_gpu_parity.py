@@ -68,6 +68,10 @@ CASES = [
     (RS, 192, 300, 96, 2), (RS, 64, 64, 64, 1),
     # columns not a multiple of 4 / of the tile; decode-sized blocks straddling tiles
     (RS, 24, 301, 40, 4), (RS, 200, 257, 64, 8), (RS, 360, 515, 96, 8), (AG, 96, 300, 136, 4),
+    # fewer tiles than SMs with several K-blocks: split-K reduction units (slices summed in order,
+    # then staged for the owners), incl. TP=1 (one GPU's decode share) and ragged columns
+    (RS, 1024, 1024, 1024, 2), (RS, 32, 1024, 2048, 2), (RS, 16, 2048, 4096, 8), (RS, 16, 2048, 3584, 1),
+    (RS, 48, 1000, 1536, 4),
 ]
 
 

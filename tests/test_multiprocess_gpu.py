@@ -33,13 +33,15 @@ def test_two_processes_ipc_match_oracle():
 @pytest.mark.gpu
 @pytest.mark.parametrize("workload", ["llama70b-up-ag", "llama70b-down-rs"])
 def test_bench_two_ranks_ipc_path(workload):
-    """bench.py's N>1 path (one process per rank, IPC communicator, max-over-ranks
-    timing, rank 0 prints one JSON line), with both ranks sharing this box's GPU
-    (FLUX_BENCH_SHARE_GPU=1: gloo plumbing instead of NCCL)."""
+    """bench.py's full N>1 path (one process per rank, IPC communicator,
+    max-over-ranks timing, the row-sampled parity check across processes, the
+    Eq. 2 block with the B1 / B2 baselines, e2e; rank 0 prints one JSON line),
+    with both ranks sharing this box's GPU (FLUX_BENCH_SHARE_GPU=1: gloo
+    plumbing, host-staged collectives for the baselines)."""
     env = dict(os.environ, FLUX_BENCH_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29541", os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--quick", "--no-cpu-baseline", "--workload", workload]
+           "--steps", "3", "--warmup", "3", "--workload", workload]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     print(out.stdout[-3000:], out.stderr[-3000:])
     assert out.returncode == 0
@@ -47,3 +49,8 @@ def test_bench_two_ranks_ipc_path(workload):
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["tp"] == 2 and d["value"] > 0
+    assert d["parity"]["pass"], d["parity"]
+    ov = d["overlap"]
+    assert ov["t_unfused_cublas_ms"] > 0 and ov["t_decomposed_ms"] > 0 and ov["t_nonoverlap_ours_ms"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["roofline"]["nvlink_bytes_per_launch"] > 0  # one rank's share at N>1
