@@ -158,8 +158,10 @@ class Communicator:
             devs = (C.c_int * tp)(*(devices if devices is not None else [0] * tp))
             N.check(N.lib().flux_comm_create(tp, devs, C.byref(N.CommOpts(heap_bytes)), C.byref(self._h)))
         self.rank = N.lib().flux_comm_rank(self._h)
-        # The device this process drives (single device or IPC mode), else None.
-        devs_l = list(devices) if devices is not None else [0] * tp
+        # Device of every rank this process drives, and the device this process
+        # drives when it is a single one (IPC mode, or every rank on one GPU).
+        devs_l = list(devices) if devices is not None else [device if device is not None else 0] * tp
+        self.devices = devs_l
         self.device = device if device is not None else (devs_l[0] if len(set(devs_l)) == 1 else None)
 
     @classmethod
@@ -189,9 +191,10 @@ class Communicator:
         import torch
 
         d = self.buffer(rank, kind, problem)
+        dev = torch.device("cuda", self.devices[rank] if rank < len(self.devices) else 0)
         if d.dtype == N.F32:
-            return torch.as_tensor(_CAI(d.ptr, d.rows, d.cols, d.ld, "<f4", 4), device="cuda")
-        t = torch.as_tensor(_CAI(d.ptr, d.rows, d.cols, d.ld, "<i2", 2), device="cuda")
+            return torch.as_tensor(_CAI(d.ptr, d.rows, d.cols, d.ld, "<f4", 4), device=dev)
+        t = torch.as_tensor(_CAI(d.ptr, d.rows, d.cols, d.ld, "<i2", 2), device=dev)
         return t.view(torch.bfloat16)
 
     def copy_in(self, rank: int, kind: int, problem: ProblemSpec, host_ptr: int, host_ld: int, stream=None):
@@ -333,8 +336,7 @@ def required_heap_bytes(problem: ProblemSpec) -> int:
     return int(N.lib().flux_required_heap_bytes(C.byref(problem.c())))
 
 
-TRACE_KINDS = {1: "compute_start", 2: "signal_set", 3: "tile_write", 4: "reduce", 5: "wait", 6: "launch",
-               7: "copy_done"}
+TRACE_KINDS = {1: "compute_start", 2: "signal_set", 3: "tile_write", 4: "reduce", 5: "wait", 6: "launch"}
 
 
 def read_trace(comm: Communicator, rank: int, problem: ProblemSpec, max_records: int = 1 << 18) -> list[dict]:

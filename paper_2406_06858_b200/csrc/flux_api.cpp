@@ -729,7 +729,6 @@ struct OpCommon {
     int rs_units = 0;  // RS summed by the owners' reduction units (decode-sized blocks, sub-wave problems)
     int rs_chain = 0;         // RS with every rank in one launch: chained partial sums (kernel)
     const flux_operands* ops = nullptr;  // caller-provided operands (per rank; one entry in IPC mode)
-    bool trace_cursors_reset = false;    // the operator already zeroed the trace cursors (traced copy engines)
 };
 
 // Cross-process operator boundary (IPC mode): every operator stamps `done` and
@@ -905,7 +904,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 RankState& rs = c->ranks[g[li]];
                 prm.trace[li] = reinterpret_cast<unsigned long long*>(rs.heap + L.trace_off);
                 prm.trace_cursor[li] = at<uint32_t>(rs, kCtrlTraceCursor);
-                if (!oc.trace_cursors_reset) FLUX_CUDA(cudaMemsetAsync(prm.trace_cursor[li], 0, 4, lead));
+                FLUX_CUDA(cudaMemsetAsync(prm.trace_cursor[li], 0, 4, lead));
             }
         }
         if (extra) FLUX_TRY(extra(g, prm));
@@ -1753,15 +1752,6 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         return FLUX_OK;
     }
 
-    // Traced: the copy engines stamp device-clock records into the trace rings
-    // too, so the cursors are zeroed before the copy stream starts.
-    if (oc.o.trace) {
-        for (int r : mine) {
-            FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
-            FLUX_CUDA(cudaMemsetAsync(c->ranks[r].heap + kCtrlTraceCursor, 0, 4, stream_for(c, r, streams)));
-        }
-        oc.trace_cursors_reset = true;
-    }
     // One copy-engine stream per device (several blocked stream-wait memops on
     // many streams can starve each other on shared hardware queues). It starts
     // after the caller's prior work (the A shards) and after the previous kernel
@@ -1841,20 +1831,8 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         return FLUX_OK;
     };
     cudaEvent_t xfer_base = nullptr;
-    // Device-clock stamp in the trace ring of `board` (the rank whose flag it is).
-    auto stamp = [&](cudaStream_t cs, int board, uint32_t kind, int flag, int peer) -> int {
-        if (!c->ranks[board].local) return FLUX_OK;
-        char* h = c->ranks[board].heap;
-        FLUX_CUDA(launch_trace_stamp(reinterpret_cast<unsigned long long*>(h + L.trace_off),
-                                     reinterpret_cast<uint32_t*>(h + kCtrlTraceCursor),
-                                     static_cast<uint32_t>(kTraceBytes / 16),
-                                     trace_word(kind, board, static_cast<uint32_t>(flag), flag, peer), cs));
-        return FLUX_OK;
-    };
     auto log_copy = [&](cudaStream_t cs, int owner, const Desc& d) -> int {
         if (!log_xfer) return FLUX_OK;
-        const int board = transfer == FLUX_PULL ? owner : d.peer;
-        FLUX_TRY(stamp(cs, board, kEvCopyDone, d.row_begin / rpct, d.peer));
         flux_comm::XferEntry x;
         x.rank = owner;
         x.peer = d.peer;
@@ -1868,8 +1846,6 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     };
     auto log_flag = [&](cudaStream_t cs) -> int {
         if (!log_xfer) return FLUX_OK;
-        const flux_comm::XferEntry& x = c->xfer_log.back();
-        FLUX_TRY(stamp(cs, transfer == FLUX_PULL ? x.rank : x.peer, kEvSignalSet, x.row_begin / rpct, x.peer));
         FLUX_TRY(next_event(&c->xfer_log.back().flag_ev));
         FLUX_CUDA(cudaEventRecord(c->xfer_log.back().flag_ev, cs));
         return FLUX_OK;

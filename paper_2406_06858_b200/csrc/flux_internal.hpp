@@ -46,9 +46,8 @@ constexpr size_t kTraceBytes = size_t(4) << 20;  // trace ring at the end of the
 // Trace record kinds (the reference CausalityLog event names, engine.hpp:37-63).
 // kEvLaunch (not in the reference schema): a CTA's first (tile_col 0) and last (tile_col 1)
 // instruction, for launch-latency profiling.
-// kEvCopyDone (not in the reference schema): a copy-engine transfer's rows landed (before its flag).
 enum TraceKind : uint32_t { kEvComputeStart = 1, kEvSignalSet = 2, kEvTileWrite = 3, kEvReduce = 4, kEvWait = 5,
-                            kEvLaunch = 6, kEvCopyDone = 7 };
+                            kEvLaunch = 6 };
 __host__ __device__ inline uint64_t trace_word(uint32_t kind, int rank, uint32_t target, int tile_row, int tile_col) {
     return (static_cast<uint64_t>(kind) << 60) | (static_cast<uint64_t>(rank & 0xF) << 56) |
            (static_cast<uint64_t>(target & 0xFFFFFFu) << 32) | (static_cast<uint64_t>(tile_row & 0xFFFF) << 16) |
@@ -203,11 +202,5 @@ struct ZeroParams {
     int nranges;
 };
 cudaError_t launch_zero_ranges(const ZeroParams& p, int nheaps, cudaStream_t stream);
-
-// Traced copy-engine transfers: one device-clock (%globaltimer) record in a
-// rank's trace ring, enqueued on the copy stream between its copies and flag
-// writes (a single-thread kernel that co-resides with the persistent GEMM).
-cudaError_t launch_trace_stamp(unsigned long long* ring, uint32_t* cursor, uint32_t cap, uint64_t word,
-                               cudaStream_t stream);
 
 }  // namespace fluxb200

@@ -1169,8 +1169,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     uint32_t r[32];
                     tmem_ld32(tbase + c * 32, r);
                     tmem_ld_wait();
+                    if (valid) {  // rows past m (decode-sized M) are never read back
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) mine[(c * 32 + j) * kBM] = __uint_as_float(r[j]);
+                        for (int j = 0; j < 32; ++j) mine[(c * 32 + j) * kBM] = __uint_as_float(r[j]);
+                    }
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -1708,21 +1710,6 @@ __global__ void zero_ranges_kernel(ZeroParams p) {
         uint32_t* w = reinterpret_cast<uint32_t*>(h + p.off[r]);
         for (uint32_t i = threadIdx.x; i < p.bytes[r] / 4; i += blockDim.x) w[i] = 0u;
     }
-}
-
-__global__ void trace_stamp_kernel(unsigned long long* ring, uint32_t* cursor, uint32_t cap, uint64_t word) {
-    const uint64_t ts = globaltimer();
-    const uint32_t i = atomicAdd(cursor, 1u);
-    if (i < cap) {
-        ring[2ull * i] = ts;
-        ring[2ull * i + 1] = word;
-    }
-}
-
-cudaError_t launch_trace_stamp(unsigned long long* ring, uint32_t* cursor, uint32_t cap, uint64_t word,
-                               cudaStream_t stream) {
-    trace_stamp_kernel<<<1, 1, 0, stream>>>(ring, cursor, cap, word);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_zero_ranges(const ZeroParams& p, int nheaps, cudaStream_t stream) {

@@ -466,8 +466,12 @@ EngineResult run_fused_allgather_gemm(const ProblemSpec& p, ShardedWorkspace& ws
     const flux_problem cp = cprob(p);
     const flux_tile ct{tile.tm, tile.tn};
     flux_opts o = copts(opts);
-    o.trace = 1;      // EngineResult::log and the TransferRecords
-    o.ag_engine = 1;  // the copy-engine transfer loop walks the caller's comm orders (engine.cpp:367-423)
+    o.trace = 1;  // EngineResult::log (and the TransferRecords)
+    // TransferRecords come from the copy-engine transfer loop, which walks the
+    // caller's comm orders descriptor by descriptor (engine.cpp:367-423); without
+    // them the library's automatic engine runs (the tiles follow the arrival
+    // order the comm orders imply either way).
+    if (traces) o.ag_engine = 1;
     const size_t count = comm[0].order.size();
     std::vector<int> peer, begin, rows;
     for (int r = 0; r < p.tp; ++r) {

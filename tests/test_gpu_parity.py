@@ -262,7 +262,34 @@ FULL_SIZE = {  # BASELINE.json configs: Llama-2-70B MLP (TP=8, RS also TP=2/4), 
     "llama-rs-tp4": (RS, 4096, 8192, 28672, 4), "llama-rs-tp2": (RS, 4096, 8192, 28672, 2),
     "gpt3-ag": (AG, 8192, 49152, 12288, 8), "gpt3-rs": (RS, 8192, 12288, 49152, 8),
     "decode-ag-m16": (AG, 16, 28672, 8192, 8), "decode-rs-m512": (RS, 512, 8192, 28672, 8),
+    # the rest of configs[4] (decode sweep): AG up M=128/256/512, RS down M=16/128/256, attention-out
+    # (K=N=8192) M=16/128/512, and the C1 oracle-plumbing config at full size
+    "decode-ag-m128": (AG, 128, 28672, 8192, 8), "decode-ag-m256": (AG, 256, 28672, 8192, 8),
+    "decode-ag-m512": (AG, 512, 28672, 8192, 8),
+    "decode-rs-m16": (RS, 16, 8192, 28672, 8), "decode-rs-m128": (RS, 128, 8192, 28672, 8),
+    "decode-rs-m256": (RS, 256, 8192, 28672, 8),
+    "decode-attn-m16": (RS, 16, 8192, 8192, 8), "decode-attn-m128": (RS, 128, 8192, 8192, 8),
+    "decode-attn-m512": (RS, 512, 8192, 8192, 8),
+    # one GPU's share of the decode configs (TP=1 problems with the per-rank shapes)
+    "rank-decode-ag-m16": (AG, 16, 3584, 8192, 1), "rank-decode-rs-m16": (RS, 16, 8192, 3584, 1),
+    "rank-decode-rs-m128": (RS, 128, 8192, 3584, 1),
 }
+
+
+def test_c1_oracle_plumbing_config_matches_oracle_and_reference_engine():
+    """BASELINE configs[0] exactly: GEMM-ReduceScatter M=N=K=1024 at TP=2 (the
+    reference's CPU oracle-plumbing config), every output element against the
+    fp64 oracle; the oracle itself equals the reference's fused engine bitwise
+    at this size (tests/test_oracle.py)."""
+    p = fx.ProblemSpec(1024, 1024, 1024, 2, RS)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=42)
+        want = _oracle(p, a, b)
+        for f32 in (True, False):
+            for write_mode in (fx.WRITE_ALLTOALL, fx.FUSED_REDUCE):
+                got = _run(comm, p, f32, write_mode=write_mode)
+                for r in range(p.tp):
+                    assert O.max_rel_error(got[r], want[r]) <= H.tol(f32, p.k), (f32, write_mode, r)
 
 
 @pytest.mark.slow
