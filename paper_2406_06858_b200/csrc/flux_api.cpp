@@ -2529,7 +2529,7 @@ int flux_ag_gemm_ordered(flux_comm* c, const flux_problem* p, const flux_tile* t
                          int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands,
                          const int* order_peer, const int* order_row_begin, const int* order_rows, int count) {
     return run_op(c, [&]() -> int {
-        if (!p || !order_peer || !order_row_begin || !order_rows || count < 0)
+        if (!p || count < 0 || (count > 0 && (!order_peer || !order_row_begin || !order_rows)))
             return fail(FLUX_ERR_CONFIG, "null comm order");
         if (opts && opts->graph_safe) return fail(FLUX_ERR_CONFIG, "graph_safe operators use the reference comm order");
         std::vector<std::vector<Desc>> custom(c->tp);
