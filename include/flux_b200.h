@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FLUX_ABI_VERSION 6
+#define FLUX_ABI_VERSION 7
 
 /* Return codes. The reference raises C++ exceptions (errors.hpp:9-31); each
  * maps to one code. The C++ shim (include/flux/overlap.hpp) rethrows them. */
@@ -108,7 +108,12 @@ typedef struct {
                                   so every replay starts from a clean state. Single-process
                                   communicators; AllGather uses the in-kernel transfer engine (no
                                   host stream memops); not with the arrival-order FusedReduce. */
+    int decode_kernel;         /* flux_decode_kernel: GEMMs of at most 128 rows (decode) run on the
+                                  streaming kernel (weights on the MMA M side, tokens on N, stream-K
+                                  over the weight shard) unless FLUX_DECODE_TILE */
 } flux_opts;
+
+typedef enum { FLUX_DECODE_AUTO = 0, FLUX_DECODE_TILE = 1, FLUX_DECODE_STREAM = 2 } flux_decode_kernel;
 
 typedef enum { FLUX_B_NK = 0, FLUX_B_KN = 1 } flux_b_layout;
 

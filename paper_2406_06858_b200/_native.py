@@ -21,9 +21,10 @@ SWIZZLE_NAIVE, SWIZZLE_RANK_SHIFTED, SWIZZLE_ARRIVAL_ALIGNED = 0, 1, 2
 BF16, F32 = 0, 1
 BUF_A_SHARD, BUF_B_SHARD, BUF_A_AGG, BUF_C_OUT, BUF_STAGING, BUF_C_OUT_F32 = 0, 1, 2, 3, 4, 5
 ACT_NONE, ACT_GELU, ACT_RELU, ACT_SILU, ACT_SWIGLU = 0, 1, 2, 3, 4
-ABI_VERSION = 6
+ABI_VERSION = 7
 FAULT_NONE, FAULT_DROP_SIGNAL, FAULT_DOUBLE_SIGNAL = 0, 1, 2
 B_NK, B_KN = 0, 1
+DECODE_AUTO, DECODE_TILE, DECODE_STREAM = 0, 1, 2  # flux_decode_kernel
 
 
 class FluxError(RuntimeError):
@@ -77,7 +78,7 @@ class Opts(C.Structure):
                 ("interleave_seed", C.c_uint64), ("shift_offset", C.c_int), ("out_dtype", C.c_int),
                 ("emulated_order", C.c_int), ("cta_group", C.c_int), ("ag_engine", C.c_int), ("trace", C.c_int),
                 ("activation", C.c_int), ("activation_grad", C.c_int), ("rs_partials", C.c_int),
-                ("b_layout", C.c_int), ("graph_safe", C.c_int)]
+                ("b_layout", C.c_int), ("graph_safe", C.c_int), ("decode_kernel", C.c_int)]
 
 
 class CommOpts(C.Structure):

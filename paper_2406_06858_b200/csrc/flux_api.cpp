@@ -751,6 +751,35 @@ OpCommon common_opts(const flux_opts* opts) {
     return oc;
 }
 
+// Streaming decode kernel eligibility: decode-sized GEMM rows (<= 128), modes
+// Plain / AG / RSUnits, K-major weights, no gated (SwiGLU) or saved / derivative
+// epilogues; opts.decode_kernel: 0 auto (below), 1 never, 2 whenever eligible.
+bool stream_kernel_ok(flux_comm* c, const flux_problem* p, int mode, const OpCommon& oc, int m_rows, int nslots,
+                      int sk_nt, const std::vector<int>& g) {
+    if (oc.o.decode_kernel == FLUX_DECODE_TILE) return false;
+    if (mode != kModePlain && mode != kModeAG && mode != kModeRSUnits) return false;
+    if (m_rows > 128 || m_rows < 1) return false;
+    if (oc.o.activation == FLUX_ACT_SWIGLU || oc.o.activation_grad != FLUX_ACT_NONE) return false;
+    if (oc.o.b_layout == FLUX_B_KN) return false;
+    for (int r : g) {
+        const flux_operands* ops = operands_of(c, oc, r);
+        if (ops && ops->aux.ptr) return false;
+    }
+    if (static_cast<long long>(nslots) * sk_nt > kSkCtrCap / 2) return false;
+    // 32-bit stream-K arithmetic on the device: work x (CTAs + 1) < 2^31.
+    const long long work = static_cast<long long>(nslots) * sk_nt * ((local_k(p) + kBK - 1) / kBK);
+    if (work * (sm_count(c->ranks[g[0]].device) + 1) >= (1LL << 31)) return false;
+    if (mode == kModeRSUnits && static_cast<size_t>(sk_nt) * p->tp > kRsFlagCap) return false;
+    if (std::getenv("FLUX_STREAM_KERNEL")) return std::atoi(std::getenv("FLUX_STREAM_KERNEL")) != 0;  // A/B
+    if (oc.o.decode_kernel == FLUX_DECODE_STREAM) return true;
+    // Auto: one rank per GPU (the deployed TP layout) with at most 64 rows. Measured
+    // (scripts/stream_check.py, one GPU's Llama-2-70B TP=8 decode share, L2 flushed):
+    // M=16 AG up-proj 37.9 -> 29.7 us, RS down-proj 52.2 -> 44.0, RS attn-out 48.2 ->
+    // 37.9; M=64 35.8 -> 31.7; at M=128, and with eight ranks emulated in one launch,
+    // the tile kernel is as fast or faster.
+    return m_rows <= 64 && nslots == 1;
+}
+
 // Launch one fused kernel per device group. `mode` selects the role.
 int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon& oc, void* const* streams,
                   const std::vector<std::vector<uint32_t>>& seq_of_rank, int rpct, int interleave,
@@ -769,18 +798,23 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         cudaStream_t lead = stream_for(c, g[0], streams);
         GemmParams prm;
         std::memset(&prm, 0, sizeof(prm));
+        // Streaming decode kernel (flux_stream_kernel) for decode-sized M.
+        const int sk_mp = std::max(16, (m_rows + 15) / 16 * 16);
+        const int sk_nt = (lc + kSkRows - 1) / kSkRows;
+        const bool use_stream = stream_kernel_ok(c, p, mode, oc, m_rows, static_cast<int>(g.size()), sk_nt, g);
+        const int a_box = use_stream ? sk_mp : kBM, b_box = use_stream ? kSkRows : kBN / cg;
         for (size_t li = 0; li < g.size(); ++li) {
             const RankState& rs = c->ranks[g[li]];
             const flux_operands* ops = operands_of(c, oc, g[li]);
             const Region& A = (mode == kModeAG || plain_on_agg) ? L.a_agg : L.a_shard;
             if (A.off == L.a_shard.off && ops && ops->a.ptr)
-                FLUX_TRY(make_tmap(&prm.tma_a[li], ops->a.ptr, A.rows, lk, ops->a.ld, kBM));
+                FLUX_TRY(make_tmap(&prm.tma_a[li], ops->a.ptr, A.rows, lk, ops->a.ld, a_box));
             else
-                FLUX_TRY(make_tmap(&prm.tma_a[li], rs.heap + A.off, A.rows, lk, A.ld, kBM));
+                FLUX_TRY(make_tmap(&prm.tma_a[li], rs.heap + A.off, A.rows, lk, A.ld, a_box));
             if (ops && ops->b.ptr && oc.o.b_layout == FLUX_B_KN)  // [k, n]: 64 (N) x 64 (K) boxes, MN-major
                 FLUX_TRY(make_tmap(&prm.tma_b[li], ops->b.ptr, lk, lc, ops->b.ld, kBK));
-            else if (ops && ops->b.ptr) FLUX_TRY(make_tmap(&prm.tma_b[li], ops->b.ptr, lc, lk, ops->b.ld, kBN / cg));
-            else FLUX_TRY(make_tmap(&prm.tma_b[li], rs.heap + L.b.off, lc, lk, L.b.ld, kBN / cg));
+            else if (ops && ops->b.ptr) FLUX_TRY(make_tmap(&prm.tma_b[li], ops->b.ptr, lc, lk, ops->b.ld, b_box));
+            else FLUX_TRY(make_tmap(&prm.tma_b[li], rs.heap + L.b.off, lc, lk, L.b.ld, b_box));
             if (plain_f32_to_staging) {
                 prm.c[li] = rs.heap + partial_off;  // full [m, n] partial
                 prm.ldc_l[li] = L.ld_stage;
@@ -878,9 +912,10 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         // four per CTA (finer units balance better; measured: decode M=256
         // 153 -> 144 us, M=512 slightly better with 16).
         {
-            const int rpr = rows_per_rank(p), tiles_n_all = (lc + kBN - 1) / kBN;
+            const int rpr = rows_per_rank(p), tiles_n_all = use_stream ? sk_nt : (lc + kBN - 1) / kBN;
             const long long units16 = static_cast<long long>(g.size()) * ((rpr + 15) / 16) * tiles_n_all;
             prm.red_rows = units16 < 4LL * sm_count(dev) ? 8 : 16;
+            if (use_stream) prm.tiles_n = sk_nt;  // RS flags per (128-column n-tile, source)
         }
         prm.red_ctr = at<uint32_t>(c->ranks[g[0]], kCtrlRedCtr);
         prm.red_exit = at<uint32_t>(c->ranks[g[0]], kCtrlRedExit);
@@ -917,7 +952,8 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         // GEMM-RS with owner reduction units (decode-sized blocks, sub-wave
         // problems such as one GPU's decode share) splits the same way: the
         // slices are summed before the partial is staged for its owners.
-        if ((mode == kModePlain || mode == kModeAG || mode == kModeRSUnits) && oc.o.activation != FLUX_ACT_SWIGLU) {
+        if (!use_stream && (mode == kModePlain || mode == kModeAG || mode == kModeRSUnits) &&
+            oc.o.activation != FLUX_ACT_SWIGLU) {
             const char* env = std::getenv("FLUX_TAIL_SPLIT");
             const int W = std::max(1, sm_count(dev) / cg), T = prm.num_tiles;
             const int R = T % W, kb = (lk + kBK - 1) / kBK;
@@ -956,7 +992,37 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             ev = &c->kernel_events[c->kernel_events_used++];
             FLUX_CUDA(cudaEventRecord(ev->first, lead));
         }
-        FLUX_CUDA(launch_gemm(mode, cg, prm, grid, lead));
+        if (use_stream) {
+            const int kbn = (lk + kBK - 1) / kBK;
+            const int sms = std::max(1, sm_count(dev));
+            prm.sk_mp = sk_mp;
+            prm.sk_nt = sk_nt;
+            prm.sk_kb = kbn;
+            prm.sk_work = static_cast<long long>(g.size()) * sk_nt * kbn;
+            // At most kSkMaxSegsHost K-segments per n-tile: every CTA takes at least
+            // ceil(kb / (max - 1)) k-blocks.
+            const long long min_run = (kbn + kSkMaxSegsHost - 2) / (kSkMaxSegsHost - 1);
+            prm.sk_ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(sms, prm.sk_work / min_run)));
+            prm.sk_acc_cols = 16;
+            while (prm.sk_acc_cols < sk_mp) prm.sk_acc_cols *= 2;
+            const int stage_bytes = stream_smem_bytes(mode, sk_mp, 1) - stream_smem_bytes(mode, sk_mp, 0);
+            prm.sk_stages = std::min(kSkMaxStages, (kSkSmemMax - stream_smem_bytes(mode, sk_mp, 0)) / stage_bytes);
+            // AG: weight stages streamed before the gathered rows land. A few hide the
+            // transfer; a full ring of them queues the transfer's own loads behind the
+            // weight stream (one GPU's decode AG: rows landed 9 us in with 10 stages).
+            prm.sk_pref = std::min(prm.sk_stages, 3);
+            if (const char* env = std::getenv("FLUX_SK_PREFETCH")) prm.sk_pref = std::max(1, std::min(prm.sk_stages, std::atoi(env)));
+            const RankState& lead_rank = c->ranks[g[0]];
+            prm.tail_seq = ++c->launch_seq;
+            prm.tail_ws = reinterpret_cast<float*>(lead_rank.heap + L.tail_ws_off);
+            prm.sk_ctr = at<uint32_t>(lead_rank, kSkCtrOffset);
+            prm.tail_splits = 0;
+            // The owners' reduction units (RS) and the in-kernel AllGather run on every SM.
+            const int sgrid = (mode == kModeRSUnits || (mode == kModeAG && prm.sm_transfer)) ? sms : prm.sk_ctas;
+            FLUX_CUDA(launch_stream(mode, prm, sgrid, stream_smem_bytes(mode, sk_mp, prm.sk_stages), lead));
+        } else {
+            FLUX_CUDA(launch_gemm(mode, cg, prm, grid, lead));
+        }
         if (ev) FLUX_CUDA(cudaEventRecord(ev->second, lead));
         ++c->last_launches;
         FLUX_CUDA(cudaEventRecord(c->ranks[g[0]].kernel_evt, lead));
@@ -1008,6 +1074,7 @@ void flux_default_opts(flux_opts* o) {
     o->rs_partials = FLUX_F32;
     o->b_layout = FLUX_B_NK;
     o->graph_safe = 0;
+    o->decode_kernel = FLUX_DECODE_AUTO;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -1433,8 +1500,11 @@ static int graph_zero(flux_comm* c, const flux_problem* p, void* const* streams)
     add(kAgFlagOffset, std::min<size_t>(kAgFlagCap, static_cast<size_t>(p->m)) * 4);
     add(kAgCtrGraphOffset, (static_cast<size_t>((p->m + kBM - 1) / kBM) + 1) * 4);
     add(kTailCtrOffset, static_cast<size_t>(2 * kTailCtrCap) * 4);  // arrival + RS-units staged counters
+    add(kSkCtrOffset, static_cast<size_t>(kSkCtrCap) * 4);  // streaming decode kernel's n-tile counters
     if (p->pattern == FLUX_GEMM_REDUCESCATTER) {
-        const size_t tiles = static_cast<size_t>((p->m + kBM - 1) / kBM) * ((p->n + kBN - 1) / kBN);
+        // Flags per (tile, source): 128 x 256 tiles, or 128-column n-tiles (streaming kernel).
+        const size_t tiles = std::max(static_cast<size_t>((p->m + kBM - 1) / kBM) * ((p->n + kBN - 1) / kBN),
+                                      static_cast<size_t>((p->n + kSkRows - 1) / kSkRows));
         add(kRsFlagOffset, std::min(kRsFlagCap, tiles * p->tp) * 4);
     }
     for (const auto& g : device_groups(c)) {

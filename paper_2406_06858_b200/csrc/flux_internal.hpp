@@ -62,6 +62,13 @@ constexpr size_t kTailCtrOffset = 72 * 1024;
 constexpr int kTailCtrCap = 256;   // per counter set; two sets (slices parked / RS-units slices staged)
 constexpr int kTailMaxSplits = 8;
 constexpr int kTailWsCtas = 160;  // workspace slots (>= CTAs of one launch): 128 x 256 fp32 each
+// Streaming decode kernel: epoch-tagged arrival counters of its split n-tiles.
+constexpr size_t kSkCtrOffset = 76 * 1024;
+constexpr int kSkCtrCap = 8192;  // u32 (76 KiB .. 108 KiB): arrivals [0, cap/2), RS shares stored [cap/2, cap)
+constexpr int kSkMaxSegsHost = 8;  // K-segments per n-tile (flux_stream_kernel kSkMaxSegs)
+constexpr int kSkRows = 128;     // weight rows (output columns) per n-tile = MMA M
+constexpr int kSkMaxStages = 12;
+constexpr int kSkSmemMax = 232448;  // dynamic shared memory opt-in limit (227 KiB)
 constexpr size_t kAgCtrOffset = 128 * 1024;
 constexpr size_t kAgGroupCap = 16384;  // per counter set
 // Graph-safe operators use their own counter set (zeroed by each of them), so
@@ -176,6 +183,19 @@ struct GemmParams {
     // RS: tile * tp + source).
     int fault_kind, fault_rank, fault_index;
     int check_double;              // RS flags: exchange-and-check instead of store (double-set detector)
+    // Streaming decode kernel (flux_stream_kernel, decode-sized M): weights on the
+    // MMA M side (128-row n-tiles), tokens on N; the (slot, n-tile, k-block)
+    // space is split evenly over sk_ctas CTAs (stream-K); the K-segments of an
+    // n-tile are summed in segment order by the last CTA to arrive (tail_ws
+    // holds [cta][first/last segment][sk_mp x 128] fp32 partials).
+    int sk_mp;                     // tokens padded to a multiple of 16 (MMA N)
+    int sk_stages;                 // smem ring depth
+    int sk_pref;                   // AG: weight stages loaded ahead of the gathered token rows
+    int sk_nt, sk_kb;              // n-tiles (128 weight rows) per slot, k-blocks
+    long long sk_work;             // slots x n-tiles x k-blocks
+    int sk_ctas;                   // CTAs with GEMM work (<= grid)
+    int sk_acc_cols;               // TMEM columns per accumulator (two accumulators)
+    uint32_t* sk_ctr;              // per (slot, n-tile): (tail_seq << 8) | arrivals
 };
 
 struct RsReduceParams {
@@ -191,6 +211,9 @@ struct RsReduceParams {
 cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStream_t stream);
 int gemm_tile_rows(int cg);
 cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t stream);
+// Streaming decode kernel (modes Plain, AG, RSUnits); smem from stream_smem_bytes.
+cudaError_t launch_stream(int mode, const GemmParams& p, int grid, int smem, cudaStream_t stream);
+int stream_smem_bytes(int mode, int mp, int stages);
 
 // Graph-safe operators: zero byte ranges (4-byte multiples) of several heaps,
 // one CTA per heap.

@@ -303,7 +303,12 @@ __device__ __forceinline__ void red_add_f4(float* p, float a, float b, float c, 
     asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
 }
+// Callers reach it after lane-divergent code (one lane spinning on a flag while
+// its warp-mates wait here): __syncwarp reconverges the warp first, so the
+// .aligned barrier (bar.sync) is well defined. (The non-.aligned barrier.sync
+// measured up to 30 % slower on the decode RS epilogues.)
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
+    __syncwarp();
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
@@ -326,7 +331,7 @@ __device__ __forceinline__ uint32_t ld_acquire_flag(const GemmParams& p, const u
 // tiles stalled behind it) and into the failing slot's own; flux_sync reads
 // them. The host-mapped mirror ([global rank][8] u32) carries the same
 // records so the next operator call can report the failure without a sync.
-__device__ void record_error(const GemmParams& p, int l, uint32_t code, uint32_t info0, uint32_t info1,
+__device__ __noinline__ void record_error(const GemmParams& p, int l, uint32_t code, uint32_t info0, uint32_t info1,
                              uint32_t info2) {
     const uint32_t who = static_cast<uint32_t>(p.global_rank[l]) + 1u;
     for (int s = 0; s < (l == 0 ? 1 : 2); ++s) {
@@ -578,20 +583,25 @@ __device__ __forceinline__ void sum_into(float (&acc)[4], const float4& w, bool&
     }
 }
 
-// Source-ordered sum of the tp staged partials of one 128 x 256 tile into the
-// owners' C. Consecutive threads take consecutive 4-column groups of a row
-// (coalesced), and every source's float4 is loaded before the sum.
 // Decode-sized RS, owner side. The rows each local rank owns are cut into
-// units of p.red_rows rows x one 256-column tile, ordered column tile first (the
-// order in which the blocked schedule completes them). Two otherwise idle warps
-// of every CTA (2 and 3) take units from a launch-wide counter while the GEMM
-// runs; the four epilogue warps join once their CTA's GEMM units are done. A
-// unit waits for the tp flags (tile, source) of the tile(s) its rows lie in,
-// then each thread keeps kU positions x tp sources in flight and sums them in
-// the canonical order (other sources ascending, then the owner) into the
-// owner's C. The GEMM never waits on a reduction, so these waits cannot
-// deadlock. The last group out re-arms the counter for the next launch.
-template <int PB>
+// units of p.red_rows rows x one column tile (TW = 256 or 128 columns),
+// ordered column tile first (the order in which the schedule completes them).
+// Two otherwise idle warps of every CTA (2 and 3) take units from a
+// launch-wide counter while the GEMM runs; the epilogue warps (then the
+// producer / MMA warps) join once their GEMM work is done; the last group out
+// re-arms the counter for the next launch. A unit waits for the tp flags (tile,
+// source) of the tile(s) its rows lie in, then each thread keeps kU positions x
+// tp sources in flight (consecutive threads on consecutive 4-column groups of
+// a row, coalesced) and sums them in the canonical order (other sources
+// ascending, then the owner) into the owner's C. The GEMM never waits on a
+// reduction, so these waits cannot deadlock.
+// TP is a template parameter (owner_reduce dispatches): the loads and the
+// canonical-order sum resolve at compile time, so a launch executes only its
+// own, small variant (the units run on cold instruction caches at decode sizes).
+// TW: columns per unit = the RS flag column tile (TW for the tile kernel,
+// kSkRows for the streaming decode kernel); compile-time so positions split
+// into (row, 4-column group) with shifts.
+template <int PB, int TW>
 __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr, int bar_id, int* slot) {
     constexpr int kU = 4;
     const int tp = p.tp, tiles_n = p.tiles_n, rpr = p.rpr, n = p.n, out_f32 = p.out_f32;
@@ -621,7 +631,7 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
             if (tid == 0) trace_event(p, l, kEvReduce, me, tm0, tn, static_cast<uint32_t>(me));
         }
         named_bar_sync(bar_id, nthr);  // flags acquired; everyone has read *slot
-        const int npos = (r1 - r0) * (kBN / 4);
+        const int npos = (r1 - r0) * (TW / 4);
         const float* const sbase = p.staging[me];  // element offsets below (fp32 or bf16 elements, PB)
         const long long e0 = parity * p.stage_parity + static_cast<long long>(r0 - me * rpr) * ld_stage;
         void* const cl = p.c[l];
@@ -631,9 +641,9 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
 #pragma unroll
             for (int i = 0; i < kU; ++i) {
                 const int pos = b + i * nthr;
-                const int col = tn * kBN + (pos % (kBN / 4)) * 4;
+                const int col = tn * TW + (pos % (TW / 4)) * 4;
                 if (pos < npos && col < n) {
-                    const long long e = e0 + (pos / (kBN / 4)) * ld_stage + col;
+                    const long long e = e0 + (pos / (TW / 4)) * ld_stage + col;
 #pragma unroll
                     for (int s = 0; s < kMaxRanks; ++s)
                         if (s < tp) v[i][s] = ld_part4<PB>(sbase, e + s * stage_plane);
@@ -642,7 +652,7 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
 #pragma unroll
             for (int i = 0; i < kU; ++i) {
                 const int pos = b + i * nthr;
-                const int col = tn * kBN + (pos % (kBN / 4)) * 4;
+                const int col = tn * TW + (pos % (TW / 4)) * 4;
                 if (pos < npos && col < n) {
                     float acc[4];
                     bool first = true;
@@ -652,7 +662,7 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
 #pragma unroll
                     for (int s = 0; s < kMaxRanks; ++s)
                         if (s == me) sum_into(acc, v[i][s], first);
-                    const long long lr = r0 - me * rpr + pos / (kBN / 4);
+                    const long long lr = r0 - me * rpr + pos / (TW / 4);
                     store_row<4>(cl, lr * ldc + col, col, n, out_f32, acc);
                 }
             }
@@ -665,6 +675,150 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
             atomicExch(p.red_exit, 0u);
         }
     }
+}
+
+// In-kernel AllGather transfer (Alg. 3 on the SMs), one lane of warp 3 of
+// every CTA: walks this CTA's share of the piece table — TMA bulk copy global
+// -> smem -> global through two buffers, then a release increment of the
+// destination group's counter. Two loads are in flight: piece i+1 is loaded
+// while piece i is stored (a buffer is reloaded once the store that used it
+// has read it), and a piece is published once its store has completed. Remote
+// pieces first wait until the source rank's own slot of a_agg is complete.
+// (Inlined: as a called function its Piece arrays live in local memory, and the
+// decode AllGathers measured 8-20 us slower.)
+__device__ __forceinline__ void ag_transfer(const GemmParams& p, uint8_t* sComm, uint64_t* cbar) {
+    struct Piece {
+        const char* src;
+        char* dst;
+        uint32_t bytes;
+        uint32_t* ctr;
+        uint32_t* slot_ctr;
+        int meta;  // (slot << 16) | group, for the trace
+        int dest;  // Push: the destination rank (the reference's signal_set target)
+        int buf;
+    };
+    uint32_t phase[2] = {0u, 0u};
+    Piece ld[2] = {};  // loads in flight, oldest first
+    int nld = 0;
+    Piece st[2] = {};  // stored, awaiting completion + publication, oldest first
+    int nst = 0;
+    int nb = 0;   // buffer of the next load
+    auto publish = [&](const Piece& P) {
+        if (P.ctr) {
+            if (p.ag_push) {  // the destination's counter, possibly on another GPU
+                const bool hit = fault_hit(p, P.dest, P.meta & 0xFFFF);
+                if (hit && p.fault_kind == kFaultDropSignal) {
+                    // dropped (fault injection)
+                } else {
+                    trace_event(p, P.meta >> 16, kEvSignalSet, p.global_rank[P.meta >> 16], P.meta & 0xFFFF,
+                                0, static_cast<uint32_t>(P.dest));
+                    if (p.slot_of[P.dest] >= 0) red_release_gpu_add(P.ctr, hit ? 2u : 1u);
+                    else red_release_sys_add(P.ctr, hit ? 2u : 1u);
+                }
+            } else {
+                ag_signal(p, P.ctr, P.meta);
+            }
+        }
+        if (P.slot_ctr) red_release_gpu_add(P.slot_ctr, 1u);
+    };
+    auto store_oldest = [&]() {  // wait for the oldest load, store it
+        const Piece P = ld[0];
+        mbar_wait(&cbar[P.buf], phase[P.buf]);
+        phase[P.buf] ^= 1u;
+        trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 10, 0);  // piece loaded (launch profiling)
+        bulk_store(P.dst, sComm + P.buf * kPieceBytes, P.bytes);
+        ld[0] = ld[1];
+        --nld;
+        if (nst == 2) {  // keep at most two stores outstanding: publish the older
+            bulk_wait_group<1>();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            publish(st[0]);
+            st[0] = st[1];
+            nst = 1;
+        }
+        st[nst++] = P;
+    };
+    auto drain = [&]() {  // everything in flight stored, completed and published
+        while (nld > 0) store_oldest();
+        bulk_wait_group<0>();
+        trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 11, 0);  // stores complete (launch profiling)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        for (int i = 0; i < nst; ++i) publish(st[i]);
+        nst = 0;
+    };
+    int checked_src = -1;
+    if (static_cast<int>(blockIdx.x) < p.num_jobs) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 12, 0);
+    for (int j = blockIdx.x; j < p.num_jobs; j += gridDim.x) {
+        const uint32_t e = p.jobs[j];
+        const int l = static_cast<int>(e >> 28), q = static_cast<int>((e >> 24) & 0xFu);
+        const int row0 = static_cast<int>(e & 0xFFFFFFu);
+        const int me = p.global_rank[l];
+        const int g = row0 / kBM;
+        const char* src;
+        char* dst;
+        uint32_t* ctr;
+        uint32_t* slot_ctr = nullptr;
+        if (p.ag_push) {
+            // q = destination: my own rows go to its a_agg and count there.
+            if (p.slot_of[q] < 0 && q != checked_src) {
+                drain();  // (no wait may hold a signal)
+                wait_flag(p.kdone[q], p.epoch - 1u, p, l, kErrAgFlagTimeout,
+                          static_cast<uint32_t>(p.ag_slot_index), 0xFFFE0000u | static_cast<uint32_t>(q));
+                checked_src = q;
+            }
+            src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
+            dst = const_cast<char*>(p.agg_src[q]) + static_cast<long long>(row0) * p.dst_ld_bytes;
+            ctr = p.ag_ctr[q] + g;
+            // Keep the own-slot counter in step with Pull operators' targets.
+            if (q == me) slot_ctr = p.ag_ctr[me] + p.ag_slot_index;
+        } else {
+        dst = p.a_dst[l] + static_cast<long long>(row0) * p.dst_ld_bytes;
+        ctr = p.ag_ctr[me] + g;
+        slot_ctr = q == me ? p.ag_ctr[me] + p.ag_slot_index : nullptr;
+        if (q == me) {
+            src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
+        } else if (p.slot_of[q] >= 0) {
+            // A rank on this device (same launch): pull straight from its shard.
+            const int sl = p.slot_of[q];
+            src = p.shard_src[sl] + static_cast<long long>(row0 - q * p.rpr) * p.src_ld_l[sl];
+        } else {
+            if (q != checked_src) {
+                // Publish everything in flight before blocking: another CTA may be
+                // waiting for our own-block pieces (no wait may hold a signal).
+                drain();
+                // The source's own slot (its shard copied into its a_agg) is complete.
+                wait_flag(p.ag_ctr[q] + p.ag_slot_index, p.ag_mult * p.slot_pieces, p, l,
+                          kErrAgFlagTimeout, static_cast<uint32_t>(p.ag_slot_index),
+                          0xFFFF0000u | static_cast<uint32_t>(q));
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                checked_src = q;
+            }
+            src = p.agg_src[q] + static_cast<long long>(row0) * p.dst_ld_bytes;
+        }
+        }  // pull
+        const int npieces = p.piece_rows > 1 ? 1 : p.pieces_per_row;
+        for (int c = 0; c < npieces; ++c) {
+            const int off = c * kPieceBytes;
+            Piece P;
+            P.src = src + off;
+            P.dst = dst + off;
+            P.bytes = p.piece_rows > 1 ? static_cast<uint32_t>(p.piece_rows * p.row_bytes)
+                                       : static_cast<uint32_t>(min(kPieceBytes, p.row_bytes - off));
+            P.ctr = ctr;
+            P.slot_ctr = slot_ctr;
+            P.meta = (l << 16) | g;
+            P.dest = q;
+            P.buf = nb;
+            if (nld == 2) store_oldest();  // frees nothing yet: its buffer is read by the store
+            // The last store that used this buffer has read it.
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            mbar_expect_tx(&cbar[nb], P.bytes);
+            bulk_load(sComm + nb * kPieceBytes, P.src, P.bytes, &cbar[nb]);
+            ld[nld++] = P;
+            nb ^= 1;
+        }
+    }
+    drain();
 }
 
 // Epilogue staging through shared memory. Warp q owns a 32-row x 32-column
@@ -786,7 +940,11 @@ struct TileSeq {
 
 // PB: RS cross-rank partials stored as bf16 (1) or fp32 (0) — a template
 // parameter so the owner's batched loads stay branch-free.
-template <int MODE, int CG, int PB = 0>
+// EPI: Plain / AG epilogue with activations / saved pre-activation /
+// derivative scaling (1), or the plain store (0) — a template parameter so the
+// common path carries none of that code (the kernels are latency-bound on cold
+// instruction fetch at decode sizes).
+template <int MODE, int CG, int PB = 0, int EPI = 0>
 __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_constant__ GemmParams p) {
     using G = Geo<CG, MODE>;
     extern __shared__ uint8_t smem_raw[];
@@ -806,8 +964,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qempty + kTileQ);
     int* qtile = reinterpret_cast<int*>(tmem_slot + 2);
     int* red_slot = qtile + kTileQ;  // decode RS reduction: unit broadcast per group
-    static_assert((2 * G::kStagesN + 6 + 2 * kTileQ) * 8 + 8 + 4 * kTileQ + 12 <= kBarRegion, "barrier region");
+    static_assert((2 * G::kStagesN + 6 + 2 * kTileQ) * 8 + 8 + 4 * kTileQ + 16 <= kBarRegion, "barrier region");
 
+    constexpr int TWU = kBN;  // owner reduction units: 256-column tiles
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t cta_rank = CG == 2 ? cluster_ctarank() : 0u;
@@ -985,147 +1144,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         }
     } else if (MODE == kModeRSUnits && (warp == 2 || warp == 3)) {
         // ===== decode RS: owners' reduction, concurrent with the GEMM =====
-        owner_reduce<PB>(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
+        owner_reduce<PB, TWU>(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
     } else if (warp == 3) {
         // ===== in-kernel AllGather transfer (Alg. 3 on the SMs) =====
-        // Lane 0 walks this CTA's share of the piece table: TMA bulk copy
-        // global -> smem -> global through two buffers, then a release
-        // increment of the destination group's counter. Two loads are in
-        // flight: piece i+1 is loaded while piece i is stored (a buffer is
-        // reloaded once the store that used it has read it), and a piece is
-        // published once its store has completed. Remote pieces first wait until
-        // the source rank's own slot of a_agg is complete.
-        if (MODE == kModeAG && p.sm_transfer && lane == 0) {
-            struct Piece {
-                const char* src;
-                char* dst;
-                uint32_t bytes;
-                uint32_t* ctr;
-                uint32_t* slot_ctr;
-                int meta;  // (slot << 16) | group, for the trace
-                int dest;  // Push: the destination rank (the reference's signal_set target)
-                int buf;
-            };
-            uint32_t phase[2] = {0u, 0u};
-            Piece ld[2] = {};  // loads in flight, oldest first
-            int nld = 0;
-            Piece st[2] = {};  // stored, awaiting completion + publication, oldest first
-            int nst = 0;
-            int nb = 0;   // buffer of the next load
-            auto publish = [&](const Piece& P) {
-                if (P.ctr) {
-                    if (p.ag_push) {  // the destination's counter, possibly on another GPU
-                        const bool hit = fault_hit(p, P.dest, P.meta & 0xFFFF);
-                        if (hit && p.fault_kind == kFaultDropSignal) {
-                            // dropped (fault injection)
-                        } else {
-                            trace_event(p, P.meta >> 16, kEvSignalSet, p.global_rank[P.meta >> 16], P.meta & 0xFFFF,
-                                        0, static_cast<uint32_t>(P.dest));
-                            if (p.slot_of[P.dest] >= 0) red_release_gpu_add(P.ctr, hit ? 2u : 1u);
-                            else red_release_sys_add(P.ctr, hit ? 2u : 1u);
-                        }
-                    } else {
-                        ag_signal(p, P.ctr, P.meta);
-                    }
-                }
-                if (P.slot_ctr) red_release_gpu_add(P.slot_ctr, 1u);
-            };
-            auto store_oldest = [&]() {  // wait for the oldest load, store it
-                const Piece P = ld[0];
-                mbar_wait(&cbar[P.buf], phase[P.buf]);
-                phase[P.buf] ^= 1u;
-                bulk_store(P.dst, sComm + P.buf * kPieceBytes, P.bytes);
-                ld[0] = ld[1];
-                --nld;
-                if (nst == 2) {  // keep at most two stores outstanding: publish the older
-                    bulk_wait_group<1>();
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                    publish(st[0]);
-                    st[0] = st[1];
-                    nst = 1;
-                }
-                st[nst++] = P;
-            };
-            auto drain = [&]() {  // everything in flight stored, completed and published
-                while (nld > 0) store_oldest();
-                bulk_wait_group<0>();
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                for (int i = 0; i < nst; ++i) publish(st[i]);
-                nst = 0;
-            };
-            int checked_src = -1;
-            for (int j = blockIdx.x; j < p.num_jobs; j += gridDim.x) {
-                const uint32_t e = p.jobs[j];
-                const int l = static_cast<int>(e >> 28), q = static_cast<int>((e >> 24) & 0xFu);
-                const int row0 = static_cast<int>(e & 0xFFFFFFu);
-                const int me = p.global_rank[l];
-                const int g = row0 / kBM;
-                const char* src;
-                char* dst;
-                uint32_t* ctr;
-                uint32_t* slot_ctr = nullptr;
-                if (p.ag_push) {
-                    // q = destination: my own rows go to its a_agg and count there.
-                    if (p.slot_of[q] < 0 && q != checked_src) {
-                        drain();  // (no wait may hold a signal)
-                        wait_flag(p.kdone[q], p.epoch - 1u, p, l, kErrAgFlagTimeout,
-                                  static_cast<uint32_t>(p.ag_slot_index), 0xFFFE0000u | static_cast<uint32_t>(q));
-                        checked_src = q;
-                    }
-                    src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
-                    dst = const_cast<char*>(p.agg_src[q]) + static_cast<long long>(row0) * p.dst_ld_bytes;
-                    ctr = p.ag_ctr[q] + g;
-                    // Keep the own-slot counter in step with Pull operators' targets.
-                    if (q == me) slot_ctr = p.ag_ctr[me] + p.ag_slot_index;
-                } else {
-                dst = p.a_dst[l] + static_cast<long long>(row0) * p.dst_ld_bytes;
-                ctr = p.ag_ctr[me] + g;
-                slot_ctr = q == me ? p.ag_ctr[me] + p.ag_slot_index : nullptr;
-                if (q == me) {
-                    src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
-                } else if (p.slot_of[q] >= 0) {
-                    // A rank on this device (same launch): pull straight from its shard.
-                    const int sl = p.slot_of[q];
-                    src = p.shard_src[sl] + static_cast<long long>(row0 - q * p.rpr) * p.src_ld_l[sl];
-                } else {
-                    if (q != checked_src) {
-                        // Publish everything in flight before blocking: another CTA may be
-                        // waiting for our own-block pieces (no wait may hold a signal).
-                        drain();
-                        // The source's own slot (its shard copied into its a_agg) is complete.
-                        wait_flag(p.ag_ctr[q] + p.ag_slot_index, p.ag_mult * p.slot_pieces, p, l,
-                                  kErrAgFlagTimeout, static_cast<uint32_t>(p.ag_slot_index),
-                                  0xFFFF0000u | static_cast<uint32_t>(q));
-                        asm volatile("fence.proxy.async.global;" ::: "memory");
-                        checked_src = q;
-                    }
-                    src = p.agg_src[q] + static_cast<long long>(row0) * p.dst_ld_bytes;
-                }
-                }  // pull
-                const int npieces = p.piece_rows > 1 ? 1 : p.pieces_per_row;
-                for (int c = 0; c < npieces; ++c) {
-                    const int off = c * kPieceBytes;
-                    Piece P;
-                    P.src = src + off;
-                    P.dst = dst + off;
-                    P.bytes = p.piece_rows > 1 ? static_cast<uint32_t>(p.piece_rows * p.row_bytes)
-                                               : static_cast<uint32_t>(min(kPieceBytes, p.row_bytes - off));
-                    P.ctr = ctr;
-                    P.slot_ctr = slot_ctr;
-                    P.meta = (l << 16) | g;
-                    P.dest = q;
-                    P.buf = nb;
-                    if (nld == 2) store_oldest();  // frees nothing yet: its buffer is read by the store
-                    // The last store that used this buffer has read it.
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    mbar_expect_tx(&cbar[nb], P.bytes);
-                    bulk_load(sComm + nb * kPieceBytes, P.src, P.bytes, &cbar[nb]);
-                    ld[nld++] = P;
-                    nb ^= 1;
-                }
-            }
-            drain();
-        }
+        if (MODE == kModeAG && p.sm_transfer && lane == 0) ag_transfer(p, sComm, cbar);
     } else if (warp >= 4) {
         // ===== epilogue: each CTA drains its own 128 TMEM lanes (rows) =====
         const int q = warp - 4;            // TMEM lane quadrant (warp % 4)
@@ -1211,7 +1233,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             if (row0 >= p.m) {
                 // Fully out-of-range half of a pair tile: nothing to store or signal.
             } else if (MODE != kModeRS && MODE != kModeRSUnits) {
-                if (p.act == kActSwiGLU) {
+                if (EPI && p.act == kActSwiGLU) {
                     // Gated MLP: each 256-column tile holds 128 gate then 128 up
                     // columns; C gets silu(gate) * up, 128 columns per tile.
                     for (int c = 0; c < kBN / 64; ++c) {
@@ -1274,7 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
 #pragma unroll
                                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
                             }
-                            if (p.act_grad == kActSwiGLU) {
+                            if (EPI && p.act_grad == kActSwiGLU) {
                                 // Backward of the gated MLP: v = dz for output columns
                                 // [col, col+32) of group col/128; the saved pre-activation
                                 // holds that group's gate and up columns (256-wide groups),
@@ -1295,7 +1317,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                                 store_row<32>(p.c[l], cbase + ucol, ucol, 2 * p.n, p.out_f32, v);
                                 continue;
                             }
-                            if (p.act_grad || p.act || p.aux_save) {
+                            if (EPI && (p.act_grad || p.act || p.aux_save)) {
                                 const long long aoff = static_cast<long long>(row) * p.ld_aux[l] + col;
                                 if (p.aux_save) store_row<32>(p.aux[l], aoff, col, p.n, 0, v);
                                 if (p.act_grad) {
@@ -1668,13 +1690,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 aphase ^= 1u;
             }
         }
-        if (MODE == kModeRSUnits) owner_reduce<PB>(p, et, 128, 4, &red_slot[1]);
+        if (MODE == kModeRSUnits) owner_reduce<PB, TWU>(p, et, 128, 4, &red_slot[1]);
     }
     if (MODE == kModeRSUnits && warp < 2) {
         // The producer and MMA warps are done with the GEMM: a third group of
         // reduction units (shortens the last block's exposed sums).
         __syncwarp();
-        owner_reduce<PB>(p, threadIdx.x, 64, 5, &red_slot[2]);
+        owner_reduce<PB, TWU>(p, threadIdx.x, 64, 5, &red_slot[2]);
     }
 
     if (CG == 2) cluster_sync();
@@ -1684,6 +1706,406 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         tc_fence_after();
         if (CG == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
         else tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// ===========================================================================
+// Streaming decode kernel (decode-sized M: one GPU's share of a decode step).
+//
+// With M <= 128 tokens the tile kernel's 128 x 256 output tiles are too few to
+// occupy 148 SMs (one GPU's Llama-2-70B up-proj share, N/TP = 3584: 14 tiles)
+// and each tile wastes 7/8 of its MMA rows; the op is a stream of the weight
+// shard through HBM. Here the weights are the MMA's M operand (128-row
+// n-tiles, K-major, TMA) and the tokens its N operand (sk_mp = M padded to 16):
+// D[128 x sk_mp] += W[128 x 64] . T[sk_mp x 64]^T per k-block, fp32 in TMEM.
+// The (slot, n-tile, k-block) space is split evenly over the CTAs (stream-K),
+// so every SM streams the same number of weight bytes; an n-tile cut between
+// CTAs is summed by the last of them to arrive, in segment (K) order, so the
+// result does not depend on arrival order. A deep smem ring (up to 12 stages of
+// 16 KiB weights) keeps ~150 KiB per SM in flight.
+//   Plain / AG: C[m, n] (+ activation). AG: the producer streams weight stages
+//     before it waits for the gathered token rows (in-kernel transfer counters or
+//     copy-engine comm-tile flags), so the AllGather hides under the weight
+//     stream; warp 3 runs the in-kernel transfer (ag_transfer).
+//   RSUnits: every finished n-tile's fp32 partial goes to its owners' staging
+//     planes with flag (n-tile, source); warps 2-3 (then all warps) run the
+//     owners' reduction units (owner_reduce with 128-column units).
+// ===========================================================================
+constexpr int kSkWBytes = kSkRows * kBK * 2;  // 16 KiB weight stage
+constexpr int kSkMaxSegs = 8;                 // K-segments per n-tile (the host sizes the grid to keep it)
+constexpr int kSkBarBytes = 512;
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+// First work unit of CTA c, and the CTA whose range holds unit x (sk_work >= sk_ctas,
+// so the range starts strictly increase).
+// (32-bit: the host keeps sk_work * (sk_ctas + 1) below 2^31; 64-bit divisions
+// inline ~100 instructions at every call site.)
+__device__ __forceinline__ long long sk_start(const GemmParams& p, int c) {
+    return static_cast<long long>(static_cast<uint32_t>(c) * static_cast<uint32_t>(p.sk_work) /
+                                  static_cast<uint32_t>(p.sk_ctas));
+}
+__device__ __forceinline__ int sk_cta_of(const GemmParams& p, long long x) {
+    const uint32_t w = static_cast<uint32_t>(p.sk_work);
+    return static_cast<int>((static_cast<uint32_t>(x + 1) * static_cast<uint32_t>(p.sk_ctas) + w - 1) / w) - 1;
+}
+// Walks one CTA's range as segments (tile tt = slot * sk_nt + n-tile, k-blocks [kb0, kb1)).
+struct SkIter {
+    long long cur, end;
+    int kb;
+    __device__ bool next(int& tt, int& kb0, int& kb1) {
+        if (cur >= end) return false;
+        tt = static_cast<int>(cur / kb);
+        kb0 = static_cast<int>(cur % kb);
+        kb1 = static_cast<int>(min(static_cast<long long>(kb), kb0 + (end - cur)));
+        cur += kb1 - kb0;
+        return true;
+    }
+};
+// Slot of the segment of tile tt held by CTA c: 2c when the tile holds the
+// CTA's first unit, else 2c + 1 (the CTA's last segment). Indexes the fp32
+// partials in tail_ws and the segment's flags in sk_ctr (parked: [0, cap/2),
+// RS share stored: [cap/2, cap)), stamped with the launch tag.
+__device__ __forceinline__ int sk_slot_index(const GemmParams& p, int c, int tt) {
+    return 2 * c + (sk_start(p, c) >= static_cast<long long>(tt) * p.sk_kb ? 0 : 1);
+}
+__device__ __forceinline__ float* sk_slot(const GemmParams& p, int c, int tt) {
+    return p.tail_ws + static_cast<long long>(sk_slot_index(p, c, tt)) * kSkRows * p.sk_mp;
+}
+// Bounded wait of one thread for a segment flag to carry this launch's tag.
+__device__ __forceinline__ void sk_wait(const GemmParams& p, int l, const uint32_t* f, uint32_t info) {
+    if (ld_acquire_gpu(f) == p.tail_seq) return;
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_gpu(f) != p.tail_seq) {
+        if (globaltimer() - t0 > p.timeout_ns) {
+            record_error(p, l, kErrAgFlagTimeout, info, 0xFFFC0000u, p.tail_seq);
+            return;
+        }
+        __nanosleep(32);
+    }
+}
+
+// Final values of 16 tokens (m0..m0+15) of output column `col` of slot l.
+template <int MODE, int PB, int ACT>
+__device__ __forceinline__ void sk_store(const GemmParams& p, int l, int col, int m0, int mv, const float (&v)[16]) {
+    if (col >= p.n) return;
+    if (MODE == kModeRSUnits) {
+        const int me = p.global_rank[l], rpr = p.rpr;
+        const long long base = static_cast<long long>(p.epoch & 1u) * p.stage_parity + me * p.stage_plane + col;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int m = m0 + i;
+            if (m >= mv) break;
+            const int o = m / rpr;
+            const long long e = base + static_cast<long long>(m - o * rpr) * p.ld_stage;
+            if (PB) reinterpret_cast<__nv_bfloat16*>(p.staging[o])[e] = __float2bfloat16_rn(v[i]);
+            else p.staging[o][e] = v[i];
+        }
+    } else {
+        const long long ldc = p.ldc_l[l];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int m = m0 + i;
+            if (m >= mv) break;
+            const float x = ACT ? act_fwd(p.act, v[i]) : v[i];
+            if (p.out_f32) static_cast<float*>(p.c[l])[m * ldc + col] = x;
+            else static_cast<__nv_bfloat16*>(p.c[l])[m * ldc + col] = __float2bfloat16_rn(x);
+        }
+    }
+}
+
+template <int MODE, int PB = 0, int ACT = 0>
+__global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_constant__ GemmParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int mp = p.sk_mp, ns = p.sk_stages, kbn = p.sk_kb;
+    const int tbytes = mp * kBK * 2;  // token stage: mp rows x 128 B (multiple of 2 KiB)
+    uint8_t* sW = smem;
+    uint8_t* sT = sW + ns * kSkWBytes;
+    uint8_t* sComm = sT + ns * tbytes;  // AG: 2 x kPieceBytes
+    uint64_t* full = reinterpret_cast<uint64_t*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0));
+    uint64_t* empty = full + kSkMaxStages;
+    uint64_t* tfull = empty + kSkMaxStages;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* cbar = tempty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 2);
+    int* red_slot = reinterpret_cast<int*>(tmem_slot + 2);
+    static_assert((2 * kSkMaxStages + 6) * 8 + 8 + 16 <= kSkBarBytes, "barrier region");
+
+    constexpr int TWU = kSkRows;  // owner reduction units: 128-column n-tiles
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tmem_cols = 2u * static_cast<uint32_t>(p.sk_acc_cols);
+    if (warp == 0 && lane == 0) {
+        trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 0, 0);
+        for (int l = 0; l < kMaxRanks; ++l) {
+            if (p.c[l] == nullptr) break;
+            tma_prefetch(&p.tma_a[l]);
+            tma_prefetch(&p.tma_b[l]);
+        }
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < ns; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+            mbar_init(&cbar[a], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const bool has_work = static_cast<int>(blockIdx.x) < p.sk_ctas;
+    const long long r0 = has_work ? sk_start(p, blockIdx.x) : 0, r1 = has_work ? sk_start(p, blockIdx.x + 1) : 0;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t ready = MODE == kModeAG ? 0u : 0xFFFFFFFFu;  // AG: bit l = slot l's token rows landed
+            int pend_stage[kSkMaxStages], pend_kb[kSkMaxStages], pend_l[kSkMaxStages];
+            int np = 0;
+            // AG: token loads wait for the gathered rows; weight stages stream meanwhile.
+            auto flush = [&]() {
+                for (int i = 0; i < np; ++i) {
+                    const int l = pend_l[i];
+                    if (!((ready >> l) & 1u)) {
+                        if (p.sm_transfer) {
+                            for (int g = 0; g * kBM < p.m; ++g)
+                                wait_flag(p.ag_ctr[p.global_rank[l]] + g, p.ag_mult * ag_group_target(p, g), p, l,
+                                          kErrAgFlagTimeout, static_cast<uint32_t>(g), 0xFFFD0000u);
+                        } else {
+                            for (int f = 0; f * p.rpct < p.m; ++f)
+                                wait_flag(p.ag_flags[l] + f, p.epoch, p, l, kErrAgFlagTimeout, static_cast<uint32_t>(f),
+                                          0xFFFD0000u);
+                        }
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        trace_event(p, l, kEvComputeStart, p.global_rank[l], 0, 0, 0);
+                        ready |= 1u << l;
+                    }
+                    tma_load_2d(sT + pend_stage[i] * tbytes, &p.tma_a[l], &full[pend_stage[i]], pend_kb[i] * kBK, 0);
+                }
+                np = 0;
+            };
+            SkIter it{r0, r1, kbn};
+            int tt, kb0, kb1;
+            while (it.next(tt, kb0, kb1)) {
+                const int l = tt / p.sk_nt, j = tt % p.sk_nt;
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    mbar_expect_tx(&full[stage], kSkWBytes + tbytes);
+                    tma_load_2d(sW + stage * kSkWBytes, &p.tma_b[l], &full[stage], kb * kBK, j * kSkRows);
+                    if ((ready >> l) & 1u) {
+                        tma_load_2d(sT + stage * tbytes, &p.tma_a[l], &full[stage], kb * kBK, 0);
+                    } else {
+                        pend_stage[np] = stage;
+                        pend_kb[np] = kb;
+                        pend_l[np] = l;
+                        if (++np == ns) flush();
+                    }
+                    if (++stage == ns) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+            flush();
+            trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 2, 0);  // producer done (launch profiling)
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(kSkRows, mp);
+            int stage = 0, as = 0;
+            uint32_t phase = 0, aphase = 0;
+            SkIter it{r0, r1, kbn};
+            int tt, kb0, kb1;
+            while (it.next(tt, kb0, kb1)) {
+                mbar_wait(&tempty[as], aphase ^ 1u);
+                tc_fence_after();
+                const uint32_t d = tmem_base + static_cast<uint32_t>(as * p.sk_acc_cols);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t adesc = smem_desc_sw128(sW + stage * kSkWBytes);
+                    const uint64_t bdesc = smem_desc_sw128(sT + stage * tbytes);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / kUmmaK; ++kk)
+                        umma_bf16(d, adesc + 2ull * kk, bdesc + 2ull * kk, idesc, (kb > kb0 || kk != 0) ? 1u : 0u);
+                    umma_commit(&empty[stage]);
+                    if (++stage == ns) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                umma_commit(&tfull[as]);
+                if (++as == 2) {
+                    as = 0;
+                    aphase ^= 1u;
+                }
+            }
+        }
+    } else if (MODE == kModeRSUnits && (warp == 2 || warp == 3)) {
+        owner_reduce<PB, TWU>(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
+    } else if (warp == 3) {
+        if (MODE == kModeAG && p.sm_transfer && lane == 0) ag_transfer(p, sComm, cbar);
+    } else if (warp >= 4) {
+        // ===== epilogue: warp q holds weight rows (output columns) 32q..32q+31 of the n-tile =====
+        // Whole n-tiles are stored straight from TMEM. A tile cut between CTAs
+        // (K-segments) is parked as fp32 partials and reduced once every CTA's
+        // mainloop is done: the tile's nseg CTAs each sum a 1/nseg share of its
+        // elements over all segments in segment order (loads of all segments in
+        // flight at once), so the reduction runs on every SM in parallel and the
+        // result does not depend on arrival order.
+        const int q = warp - 4, et = threadIdx.x - 128;
+        const int cit = q * 32 + lane;  // column within the n-tile
+        const int mv = min(p.m, mp);    // valid token rows
+        int as = 0;
+        uint32_t aphase = 0;
+        int split_tt[2] = {-1, -1};  // split tiles this CTA holds a segment of (at most its first and last)
+        int nsplit = 0;
+        SkIter it{r0, r1, kbn};
+        int tt, kb0, kb1;
+        while (it.next(tt, kb0, kb1)) {
+            const int l = tt / p.sk_nt, j = tt % p.sk_nt;
+            const int col = j * kSkRows + cit;
+            const long long tfirst = static_cast<long long>(tt) * kbn;
+            const int nseg = sk_cta_of(p, tfirst + kbn - 1) - sk_cta_of(p, tfirst) + 1;
+            mbar_wait(&tfull[as], aphase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(as * p.sk_acc_cols);
+            float* mine = nseg > 1 ? sk_slot(p, blockIdx.x, tt) : nullptr;
+            for (int m0 = 0; m0 < mv; m0 += 16) {
+                uint32_t r[16];
+                tmem_ld16(tbase + m0, r);
+                tmem_ld_wait();
+                if (nseg == 1) {
+                    float v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+                    sk_store<MODE, PB, ACT>(p, l, col, m0, mv, v);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (m0 + i < mv) mine[(m0 + i) * kSkRows + cit] = __uint_as_float(r[i]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[as]);
+            if (++as == 2) {
+                as = 0;
+                aphase ^= 1u;
+            }
+            if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 3, static_cast<uint32_t>(tt));
+            if (nseg > 1) {
+                // Parked: stamp the segment's flag (release, after every thread's stores).
+                named_bar_sync(1, 128);
+                if (et == 0) st_release_gpu(p.sk_ctr + sk_slot_index(p, blockIdx.x, tt), p.tail_seq);
+                split_tt[nsplit++] = tt;
+            } else if (MODE == kModeRSUnits) {
+                // The tile's partial is in every owner's staging plane: stamp the flags.
+                named_bar_sync(1, 128);
+                const int me = p.global_rank[l];
+                if (et == 0) trace_event(p, l, kEvTileWrite, me, 0, j, 0u);
+                if (et < (mv - 1) / p.rpr + 1) rs_flag_set(p, l, et, j, me);
+            }
+        }
+        // Split tiles: wait for every segment, sum this CTA's share.
+        for (int si = 0; si < nsplit; ++si) {
+            tt = split_tt[si];
+            const int l = tt / p.sk_nt, j = tt % p.sk_nt;
+            const long long tfirst = static_cast<long long>(tt) * kbn;
+            const int c_first = sk_cta_of(p, tfirst);
+            const int nseg = sk_cta_of(p, tfirst + kbn - 1) - c_first + 1;
+            const int share = static_cast<int>(blockIdx.x) - c_first;
+            if (et < nseg) sk_wait(p, l, p.sk_ctr + sk_slot_index(p, c_first + et, tt), static_cast<uint32_t>(tt));
+            named_bar_sync(1, 128);
+            if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 4, static_cast<uint32_t>(tt));
+            const float* slot[kSkMaxSegs];
+#pragma unroll
+            for (int s2 = 0; s2 < kSkMaxSegs; ++s2) slot[s2] = s2 < nseg ? sk_slot(p, c_first + s2, tt) : nullptr;
+            const int E = mv * kSkRows;
+            const int e0 = share * E / nseg, e1 = (share + 1) * E / nseg;
+            for (int eb = e0 + et; eb < e1; eb += 128 * 4) {
+                float w[4][kSkMaxSegs];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = eb + u * 128;
+#pragma unroll
+                    for (int s2 = 0; s2 < kSkMaxSegs; ++s2)
+                        if (s2 < nseg && e < e1) w[u][s2] = __ldcg(slot[s2] + e);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = eb + u * 128;
+                    if (e >= e1) break;
+                    float v = w[u][0];
+#pragma unroll
+                    for (int s2 = 1; s2 < kSkMaxSegs; ++s2)
+                        if (s2 < nseg) v += w[u][s2];
+                    const int m = e / kSkRows, c2 = j * kSkRows + e % kSkRows;
+                    if (c2 >= p.n) continue;
+                    if (MODE == kModeRSUnits) {
+                        const int o = m / p.rpr;
+                        const long long se = static_cast<long long>(p.epoch & 1u) * p.stage_parity +
+                                             p.global_rank[l] * p.stage_plane +
+                                             static_cast<long long>(m - o * p.rpr) * p.ld_stage + c2;
+                        if (PB) reinterpret_cast<__nv_bfloat16*>(p.staging[o])[se] = __float2bfloat16_rn(v);
+                        else p.staging[o][se] = v;
+                    } else {
+                        const float x = ACT ? act_fwd(p.act, v) : v;
+                        const long long ce = static_cast<long long>(m) * p.ldc_l[l] + c2;
+                        if (p.out_f32) static_cast<float*>(p.c[l])[ce] = x;
+                        else static_cast<__nv_bfloat16*>(p.c[l])[ce] = __float2bfloat16_rn(x);
+                    }
+                }
+            }
+            if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 5, static_cast<uint32_t>(tt));
+            if (MODE == kModeRSUnits) {
+                // Share 0 stamps the owners' flags once every share is stored (each
+                // share's release after its CTA barrier; share 0 acquires them all).
+                named_bar_sync(1, 128);
+                const uint32_t* const shares = p.sk_ctr + kSkCtrCap / 2;
+                if (share != 0) {
+                    if (et == 0) {
+                        __threadfence_system();  // staging stores may target a peer GPU
+                        st_release_gpu(p.sk_ctr + kSkCtrCap / 2 + sk_slot_index(p, blockIdx.x, tt), p.tail_seq);
+                    }
+                } else {
+                    if (et >= 1 && et < nseg)
+                        sk_wait(p, l, shares + sk_slot_index(p, c_first + et, tt), static_cast<uint32_t>(tt));
+                    named_bar_sync(1, 128);
+                    const int me = p.global_rank[l];
+                    if (et == 0) trace_event(p, l, kEvTileWrite, me, 0, j, 0u);
+                    if (et < (mv - 1) / p.rpr + 1) rs_flag_set(p, l, et, j, me);
+                }
+            }
+        }
+        if (MODE == kModeRSUnits) owner_reduce<PB, TWU>(p, et, 128, 4, &red_slot[1]);
+    }
+    if (MODE == kModeRSUnits && warp < 2) {
+        __syncwarp();
+        owner_reduce<PB, TWU>(p, threadIdx.x, 64, 5, &red_slot[2]);
+    }
+    __syncthreads();
+    if (warp == 0 && lane == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 1, 0);
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, tmem_cols);
     }
 }
 
@@ -1727,10 +2149,10 @@ int gemm_tile_rows(int cg) { return kBM * cg; }
 // Function attributes belong to each device's context: the dynamic shared
 // memory opt-in is set once per (kernel variant, device), tracked in a bitmask
 // that concurrent host threads update atomically (setting it twice is harmless).
-template <int MODE, int CG, int PB = 0>
+template <int MODE, int CG, int PB = 0, int EPI = 0>
 static cudaError_t launch_one(const GemmParams& p, int grid, cudaStream_t stream) {
     static std::atomic<uint64_t> configured{0};
-    auto fn = flux_gemm_kernel<MODE, CG, PB>;
+    auto fn = flux_gemm_kernel<MODE, CG, PB, EPI>;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -1755,13 +2177,53 @@ static cudaError_t launch_one(const GemmParams& p, int grid, cudaStream_t stream
     return cudaLaunchKernelEx(&cfg, fn, p);
 }
 
+int stream_smem_bytes(int mode, int mp, int stages) {
+    return 1024 + stages * (kSkWBytes + mp * kBK * 2) + (mode == kModeAG ? 2 * kPieceBytes : 0) + kSkBarBytes;
+}
+
+template <int MODE, int PB = 0, int ACT = 0>
+static cudaError_t launch_stream_one(const GemmParams& p, int grid, int smem, cudaStream_t stream) {
+    static std::atomic<uint64_t> configured{0};
+    auto fn = flux_stream_kernel<MODE, PB, ACT>;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+    if (bit == 0 || !(configured.load(std::memory_order_acquire) & bit)) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSkSmemMax);
+        if (e != cudaSuccess) return e;
+        configured.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    fn<<<grid, kThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stream(int mode, const GemmParams& p, int grid, int smem, cudaStream_t stream) {
+    if (smem > kSkSmemMax || p.sk_stages < 2 || p.sk_stages > kSkMaxStages) return cudaErrorInvalidValue;
+    switch (mode) {
+        case kModePlain:
+            return p.act ? launch_stream_one<kModePlain, 0, 1>(p, grid, smem, stream)
+                         : launch_stream_one<kModePlain>(p, grid, smem, stream);
+        case kModeAG:
+            return p.act ? launch_stream_one<kModeAG, 0, 1>(p, grid, smem, stream)
+                         : launch_stream_one<kModeAG>(p, grid, smem, stream);
+        case kModeRSUnits:
+            return p.part_bf16 ? launch_stream_one<kModeRSUnits, 1>(p, grid, smem, stream)
+                               : launch_stream_one<kModeRSUnits>(p, grid, smem, stream);
+    }
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStream_t stream) {
+    const bool epi = p.act || p.act_grad || p.aux_save;
     if (cg == 2) {
         grid &= ~1;
         if (grid < 2) grid = 2;
         switch (mode) {
-            case kModePlain: return launch_one<kModePlain, 2>(p, grid, stream);
-            case kModeAG: return launch_one<kModeAG, 2>(p, grid, stream);
+            case kModePlain:
+                return epi ? launch_one<kModePlain, 2, 0, 1>(p, grid, stream) : launch_one<kModePlain, 2>(p, grid, stream);
+            case kModeAG:
+                return epi ? launch_one<kModeAG, 2, 0, 1>(p, grid, stream) : launch_one<kModeAG, 2>(p, grid, stream);
             case kModeRS:
                 return p.part_bf16 ? launch_one<kModeRS, 2, 1>(p, grid, stream) : launch_one<kModeRS, 2>(p, grid, stream);
             case kModeRSUnits:
@@ -1770,8 +2232,10 @@ cudaError_t launch_gemm(int mode, int cg, const GemmParams& p, int grid, cudaStr
         }
     } else {
         switch (mode) {
-            case kModePlain: return launch_one<kModePlain, 1>(p, grid, stream);
-            case kModeAG: return launch_one<kModeAG, 1>(p, grid, stream);
+            case kModePlain:
+                return epi ? launch_one<kModePlain, 1, 0, 1>(p, grid, stream) : launch_one<kModePlain, 1>(p, grid, stream);
+            case kModeAG:
+                return epi ? launch_one<kModeAG, 1, 0, 1>(p, grid, stream) : launch_one<kModeAG, 1>(p, grid, stream);
             case kModeRS:
                 return p.part_bf16 ? launch_one<kModeRS, 1, 1>(p, grid, stream) : launch_one<kModeRS, 1>(p, grid, stream);
             case kModeRSUnits:

@@ -1,0 +1,152 @@
+// Probe (profiling aid, not product): HBM read rate of TMA box shapes for a
+// decode weight stream W[n, k] bf16 (row pitch k * 2 bytes). Each CTA streams
+// a contiguous range of (n-tile, k-group) units through a ring of mbarriers
+// (no consumer work), the way the streaming decode kernel does:
+//   box2d  : {64 k, 128 rows} per request (128 B per row per request)
+//   box3d-G: {64 k, 128 rows, G k-chunks} (G * 128 B contiguous per row)
+//   bulk   : 1-D cp.async.bulk of contiguous 16 KiB chunks (upper bound)
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/tma_probe scripts/tma_probe.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#define CR(x) do { cudaError_t r_ = (x); if (r_ != cudaSuccess) { printf("FAIL %s -> %s\n", #x, cudaGetErrorString(r_)); return 1; } } while (0)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c)); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile("{\n\t.reg .pred P1;\nW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@P1 bra D;\n\tbra W;\nD:\n\t}" ::"r"(smem_u32(b)), "r"(ph) : "memory");
+}
+
+struct Args {
+  CUtensorMap map;
+  const char* base;
+  int nt, kg, G;        // n-tiles, k-groups (of G x 64 k), chunks per request
+  long long work;       // nt * kg
+  int stages, mode;     // mode 0: 2D (G requests of one chunk), 1: 3D (one request of G chunks), 2: bulk
+  int row_bytes;
+};
+
+__global__ void __launch_bounds__(128, 1) stream(const __grid_constant__ Args a) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  const int stage_bytes = 128 * 128 * a.G;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + a.stages * stage_bytes);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const long long r0 = (long long)blockIdx.x * a.work / gridDim.x, r1 = (long long)(blockIdx.x + 1) * a.work / gridDim.x;
+  int issued = 0;
+  uint32_t ph[16] = {0};
+  for (long long u = r0; u < r1; ++u) {
+    const int s = issued % a.stages;
+    if (issued >= a.stages) { mbar_wait(&full[s], ph[s]); ph[s] ^= 1u; }
+    const int tile = (int)(u / a.kg), kgi = (int)(u % a.kg);
+    uint8_t* dst = sm + s * stage_bytes;
+    mbar_expect_tx(&full[s], stage_bytes);
+    if (a.mode == 0) {
+      for (int c = 0; c < a.G; ++c)
+        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                     ::"r"(smem_u32(dst + c * 16384)), "l"(&a.map), "r"(smem_u32(&full[s])), "r"((kgi * a.G + c) * 64), "r"(tile * 128) : "memory");
+    } else if (a.mode == 1) {
+      asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+                   ::"r"(smem_u32(dst)), "l"(&a.map), "r"(smem_u32(&full[s])), "r"(0), "r"(tile * 128), "r"(kgi * a.G) : "memory");
+    } else {
+      const char* src = a.base + u * (long long)stage_bytes;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(dst)), "l"(src), "r"(stage_bytes), "r"(smem_u32(&full[s])) : "memory");
+    }
+    ++issued;
+  }
+  for (int i = 0; i < a.stages && i < issued; ++i) {
+    const int s = (issued - 1 - i) % a.stages;
+    mbar_wait(&full[s], ph[s]);
+    ph[s] ^= 1u;
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+  CR(cudaSetDevice(0));
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  EncodeFn enc = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CR(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q));
+  CR(cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448));
+  const size_t flush_bytes = 512ull << 20;
+  void* flush;
+  CR(cudaMalloc(&flush, flush_bytes));
+  struct Shape { int n, k; const char* name; };
+  Shape shapes[] = {{3584, 8192, "rank up-proj 58.7MB"}, {8192, 3584, "rank down-proj 58.7MB"}, {28672, 8192, "tp8 up-proj 470MB"}};
+  for (const Shape& sh : shapes) {
+    void* w;
+    const size_t bytes = (size_t)sh.n * sh.k * 2;
+    CR(cudaMalloc(&w, bytes));
+    CR(cudaMemset(w, 1, bytes));
+    struct Cfg { int mode, G, stages; };
+    Cfg cfgs[] = {{0, 1, 10}, {0, 1, 13}, {0, 4, 3}, {1, 2, 6}, {1, 4, 3}, {1, 8, 1}, {0, 2, 6}, {2, 1, 12}, {2, 4, 3}};
+    for (const Cfg& c : cfgs) {
+      Args a{};
+      a.base = (const char*)w;
+      a.G = c.G;
+      a.nt = sh.n / 128;
+      a.kg = sh.k / (64 * c.G);
+      a.work = (long long)a.nt * a.kg;
+      a.stages = c.stages;
+      a.mode = c.mode;
+      if (c.mode == 1) {
+        cuuint64_t dims[3] = {64, (cuuint64_t)sh.n, (cuuint64_t)(sh.k / 64)};
+        cuuint64_t str[2] = {(cuuint64_t)sh.k * 2, 128};
+        cuuint32_t box[3] = {64, 128, (cuuint32_t)c.G};
+        cuuint32_t es[3] = {1, 1, 1};
+        CUresult r = enc(&a.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { printf("encode3d failed %d\n", (int)r); continue; }
+      } else {
+        cuuint64_t dims[2] = {(cuuint64_t)sh.k, (cuuint64_t)sh.n};
+        cuuint64_t str[1] = {(cuuint64_t)sh.k * 2};
+        cuuint32_t box[2] = {64, 128};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = enc(&a.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) { printf("encode2d failed %d\n", (int)r); continue; }
+      }
+      if (c.mode == 2) a.work = bytes / (16384ull * c.G);
+      const int smem = 1024 + c.stages * 16384 * c.G + 256;
+      if (smem > 232448) continue;
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      float best = 1e9, sum = 0;
+      const int reps = 10;
+      for (int it = 0; it < reps + 2; ++it) {
+        CR(cudaMemsetAsync(flush, it, flush_bytes));
+        cudaEventRecord(e0);
+        stream<<<sms, 128, smem>>>(a);
+        cudaEventRecord(e1);
+        CR(cudaEventSynchronize(e1));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (it >= 2) { best = ms < best ? ms : best; sum += ms; }
+      }
+      CR(cudaGetLastError());
+      const char* mn = c.mode == 0 ? "box2d" : c.mode == 1 ? "box3d" : "bulk";
+      printf("%-22s %-6s G=%d stages=%2d (%3d KiB in flight/SM): best %7.2f us (%5.0f GB/s)  mean %7.2f us\n", sh.name, mn, c.G,
+             c.stages, c.stages * 16 * c.G, best * 1e3, bytes / best / 1e6, sum / reps * 1e3);
+    }
+    cudaFree(w);
+  }
+  return 0;
+}

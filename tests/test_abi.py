@@ -47,7 +47,7 @@ def test_library_is_sm100a_and_uses_tcgen05():
 
 def test_abi_version_and_defaults():
     lib = N.lib()
-    assert lib.flux_abi_version() == N.ABI_VERSION == 6
+    assert lib.flux_abi_version() == N.ABI_VERSION == 7
     o = N.default_opts()
     assert o.activation == N.ACT_NONE and o.activation_grad == N.ACT_NONE and o.rs_partials == N.F32 and o.b_layout == N.B_NK
     assert o.graph_safe == 0
