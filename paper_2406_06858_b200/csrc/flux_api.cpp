@@ -806,7 +806,10 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         for (size_t li = 0; li < g.size(); ++li) {
             const RankState& rs = c->ranks[g[li]];
             const flux_operands* ops = operands_of(c, oc, g[li]);
-            const Region& A = (mode == kModeAG || plain_on_agg) ? L.a_agg : L.a_shard;
+            // AG at tp = 1: the gathered A is the rank's own shard; the GEMM reads it
+            // there and waits for nothing (the shard still lands in a_agg).
+            const bool direct = mode == kModeAG && p->tp == 1;
+            const Region& A = ((mode == kModeAG && !direct) || plain_on_agg) ? L.a_agg : L.a_shard;
             if (A.off == L.a_shard.off && ops && ops->a.ptr)
                 FLUX_TRY(make_tmap(&prm.tma_a[li], ops->a.ptr, A.rows, lk, ops->a.ld, a_box));
             else
@@ -886,6 +889,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         FLUX_TRY(upload_order(c, dev, order, &order_dev, lead));
         prm.order = order_dev;
         prm.num_tiles = static_cast<int>(order.size());
+        prm.ag_direct = mode == kModeAG && p->tp == 1 ? 1 : 0;
         prm.m = m_rows;
         prm.n = lc;
         prm.k = lk;
@@ -1017,8 +1021,8 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             prm.tail_ws = reinterpret_cast<float*>(lead_rank.heap + L.tail_ws_off);
             prm.sk_ctr = at<uint32_t>(lead_rank, kSkCtrOffset);
             prm.tail_splits = 0;
-            // The owners' reduction units (RS) and the in-kernel AllGather run on every SM.
-            const int sgrid = (mode == kModeRSUnits || (mode == kModeAG && prm.sm_transfer)) ? sms : prm.sk_ctas;
+            // The in-kernel AllGather runs on every SM.
+            const int sgrid = (mode == kModeAG && prm.sm_transfer) ? sms : prm.sk_ctas;
             FLUX_CUDA(launch_stream(mode, prm, sgrid, stream_smem_bytes(mode, sk_mp, prm.sk_stages), lead));
         } else {
             FLUX_CUDA(launch_gemm(mode, cg, prm, grid, lead));

@@ -120,6 +120,7 @@ struct GemmParams {
     int fused_reduce;              // RS: 1 = red.add into the owner accumulator (arrival order)
     // AG in-kernel transfer (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies)
     int sm_transfer;
+    int ag_direct;                 // AG with tp = 1: A is read from the rank's own shard (the gathered A), no waits
     const uint32_t* jobs;          // (slot << 28) | (src rank << 24) | first row of the piece chunk
     int num_jobs;
     int piece_rows;                // rows per piece chunk (contiguous rows), >= 1

@@ -595,15 +595,11 @@ __device__ __forceinline__ void sum_into(float (&acc)[4], const float4& w, bool&
 // a row, coalesced) and sums them in the canonical order (other sources
 // ascending, then the owner) into the owner's C. The GEMM never waits on a
 // reduction, so these waits cannot deadlock.
-// TP is a template parameter (owner_reduce dispatches): the loads and the
-// canonical-order sum resolve at compile time, so a launch executes only its
-// own, small variant (the units run on cold instruction caches at decode sizes).
 // TW: columns per unit = the RS flag column tile (TW for the tile kernel,
 // kSkRows for the streaming decode kernel); compile-time so positions split
-// into (row, 4-column group) with shifts.
-template <int PB, int TW>
-__device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr, int bar_id, int* slot) {
-    constexpr int kU = 4;
+// into (row, 4-column group) with shifts. kU: positions per thread in flight.
+template <int PB, int TW, int kU = 4>
+__device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr, int bar_id, int* slot, bool warm) {
     const int tp = p.tp, tiles_n = p.tiles_n, rpr = p.rpr, n = p.n, out_f32 = p.out_f32;
     const long long ld_stage = p.ld_stage, stage_plane = p.stage_plane;
     const uint32_t epoch = p.epoch, parity = p.epoch & 1u;
@@ -624,18 +620,26 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
         const int me = p.global_rank[l];
         const int r0 = me * rpr + (rem % nch) * red_rows, r1 = min(r0 + red_rows, (me + 1) * rpr);
         const int tm0 = r0 / kBM, tm1 = (r1 - 1) / kBM;
-        if (tid < (tm1 - tm0 + 1) * tp && !no_wait) {
-            const int tile_id = (tm0 + tid / tp) * tiles_n + tn;
-            wait_flag(p.rs_flags[me] + tile_id * tp + tid % tp, epoch, p, l, kErrRsFlagTimeout,
-                      static_cast<uint32_t>(tile_id), static_cast<uint32_t>(tid % tp));
-            if (tid == 0) trace_event(p, l, kEvReduce, me, tm0, tn, static_cast<uint32_t>(me));
-        }
-        named_bar_sync(bar_id, nthr);  // flags acquired; everyone has read *slot
         const int npos = (r1 - r0) * (TW / 4);
         const float* const sbase = p.staging[me];  // element offsets below (fp32 or bf16 elements, PB)
         const long long e0 = parity * p.stage_parity + static_cast<long long>(r0 - me * rpr) * ld_stage;
         void* const cl = p.c[l];
         const long long ldc = p.ldc_l[l];
+        // warm: a group that starts with the kernel runs its first unit's body
+        // once dry (loads issued, stores off) before it waits, so the body's
+        // instructions and the unit's staging lines are cached by the time the
+        // partials land (the body otherwise runs on a cold instruction cache,
+        // fetched from DRAM after an L2 flush: ~10 us at decode sizes).
+        for (int pass = warm ? 0 : 1; pass < 2; ++pass) {
+        if (pass == 1) {
+            if (tid < (tm1 - tm0 + 1) * tp && !no_wait) {
+                const int tile_id = (tm0 + tid / tp) * tiles_n + tn;
+                wait_flag(p.rs_flags[me] + tile_id * tp + tid % tp, epoch, p, l, kErrRsFlagTimeout,
+                          static_cast<uint32_t>(tile_id), static_cast<uint32_t>(tid % tp));
+                if (tid == 0) trace_event(p, l, kEvReduce, me, tm0, tn, static_cast<uint32_t>(me));
+            }
+            named_bar_sync(bar_id, nthr);  // flags acquired; everyone has read *slot
+        }
         for (int b = tid; b < npos; b += nthr * kU) {
             float4 v[kU][kMaxRanks];
 #pragma unroll
@@ -663,12 +667,16 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
                     for (int s = 0; s < kMaxRanks; ++s)
                         if (s == me) sum_into(acc, v[i][s], first);
                     const long long lr = r0 - me * rpr + pos / (TW / 4);
-                    store_row<4>(cl, lr * ldc + col, col, n, out_f32, acc);
+                    if (pass == 1) store_row<4>(cl, lr * ldc + col, col, n, out_f32, acc);
                 }
             }
         }
+        }
+        warm = false;
+        if (tid == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 13, static_cast<uint32_t>(u));  // unit summed (profiling)
     }
     if (tid == 0) {
+        trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 17 + bar_id, 0);  // group out of units (profiling)
         __threadfence();
         if (atomicAdd(p.red_exit, 1u) == 3u * gridDim.x - 1u) {  // three groups per CTA
             atomicExch(p.red_ctr, 0u);
@@ -1032,7 +1040,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     const uint32_t r = static_cast<uint32_t>((jit * 0x2545F4914F6CDD1Dull) >> 40);
                     if ((r & 15u) == 0u) __nanosleep(r & 0xFFFFu);
                 }
-                if (MODE == kModeAG && row0 < p.m) {
+                if (MODE == kModeAG && row0 < p.m && !p.ag_direct) {
                     if (p.sm_transfer) {
                         // In-kernel transfer: every piece of this 128-row group landed.
                         const int g = row0 / kBM;
@@ -1144,7 +1152,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         }
     } else if (MODE == kModeRSUnits && (warp == 2 || warp == 3)) {
         // ===== decode RS: owners' reduction, concurrent with the GEMM =====
-        owner_reduce<PB, TWU>(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
+        owner_reduce<PB, TWU>(p, threadIdx.x - 64, 64, 3, &red_slot[0], false);
     } else if (warp == 3) {
         // ===== in-kernel AllGather transfer (Alg. 3 on the SMs) =====
         if (MODE == kModeAG && p.sm_transfer && lane == 0) ag_transfer(p, sComm, cbar);
@@ -1690,13 +1698,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 aphase ^= 1u;
             }
         }
-        if (MODE == kModeRSUnits) owner_reduce<PB, TWU>(p, et, 128, 4, &red_slot[1]);
+        if (MODE == kModeRSUnits) owner_reduce<PB, TWU>(p, et, 128, 4, &red_slot[1], false);
     }
     if (MODE == kModeRSUnits && warp < 2) {
         // The producer and MMA warps are done with the GEMM: a third group of
         // reduction units (shortens the last block's exposed sums).
         __syncwarp();
-        owner_reduce<PB, TWU>(p, threadIdx.x, 64, 5, &red_slot[2]);
+        owner_reduce<PB, TWU>(p, threadIdx.x, 64, 5, &red_slot[2], false);
     }
 
     if (CG == 2) cluster_sync();
@@ -1727,9 +1735,11 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
 //     before it waits for the gathered token rows (in-kernel transfer counters or
 //     copy-engine comm-tile flags), so the AllGather hides under the weight
 //     stream; warp 3 runs the in-kernel transfer (ag_transfer).
-//   RSUnits: every finished n-tile's fp32 partial goes to its owners' staging
-//     planes with flag (n-tile, source); warps 2-3 (then all warps) run the
-//     owners' reduction units (owner_reduce with 128-column units).
+//   RSUnits: every finished n-tile's partial goes to its owners' staging planes
+//     with flag (n-tile, source); the CTA that finishes the n-tile then sums its
+//     own rank's rows of it over every source (after their flags) into C, so
+//     the reduction runs in the epilogue that just produced the tile (no
+//     separate reduction pass, no cold code after the weight stream).
 // ===========================================================================
 constexpr int kSkWBytes = kSkRows * kBK * 2;  // 16 KiB weight stage
 constexpr int kSkMaxSegs = 8;                 // K-segments per n-tile (the host sizes the grid to keep it)
@@ -1771,27 +1781,14 @@ struct SkIter {
 };
 // Slot of the segment of tile tt held by CTA c: 2c when the tile holds the
 // CTA's first unit, else 2c + 1 (the CTA's last segment). Indexes the fp32
-// partials in tail_ws and the segment's flags in sk_ctr (parked: [0, cap/2),
-// RS share stored: [cap/2, cap)), stamped with the launch tag.
+// partials parked in tail_ws; sk_ctr[tt] counts the tile's parked segments
+// (tagged with the launch sequence number, tail_arrive).
 __device__ __forceinline__ int sk_slot_index(const GemmParams& p, int c, int tt) {
     return 2 * c + (sk_start(p, c) >= static_cast<long long>(tt) * p.sk_kb ? 0 : 1);
 }
 __device__ __forceinline__ float* sk_slot(const GemmParams& p, int c, int tt) {
     return p.tail_ws + static_cast<long long>(sk_slot_index(p, c, tt)) * kSkRows * p.sk_mp;
 }
-// Bounded wait of one thread for a segment flag to carry this launch's tag.
-__device__ __forceinline__ void sk_wait(const GemmParams& p, int l, const uint32_t* f, uint32_t info) {
-    if (ld_acquire_gpu(f) == p.tail_seq) return;
-    const uint64_t t0 = globaltimer();
-    while (ld_acquire_gpu(f) != p.tail_seq) {
-        if (globaltimer() - t0 > p.timeout_ns) {
-            record_error(p, l, kErrAgFlagTimeout, info, 0xFFFC0000u, p.tail_seq);
-            return;
-        }
-        __nanosleep(32);
-    }
-}
-
 // Final values of 16 tokens (m0..m0+15) of output column `col` of slot l.
 template <int MODE, int PB, int ACT>
 __device__ __forceinline__ void sk_store(const GemmParams& p, int l, int col, int m0, int mv, const float (&v)[16]) {
@@ -1837,9 +1834,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
     uint64_t* cbar = tempty + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 2);
     int* red_slot = reinterpret_cast<int*>(tmem_slot + 2);
-    static_assert((2 * kSkMaxStages + 6) * 8 + 8 + 16 <= kSkBarBytes, "barrier region");
+    static_assert((2 * kSkMaxStages + 6) * 8 + 8 + 16 <= kSkBarBytes, "barrier region");  // red_slot[0..3]
 
-    constexpr int TWU = kSkRows;  // owner reduction units: 128-column n-tiles
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tmem_cols = 2u * static_cast<uint32_t>(p.sk_acc_cols);
     if (warp == 0 && lane == 0) {
@@ -1875,7 +1871,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            uint32_t ready = MODE == kModeAG ? 0u : 0xFFFFFFFFu;  // AG: bit l = slot l's token rows landed
+            uint32_t ready = MODE == kModeAG && !p.ag_direct ? 0u : 0xFFFFFFFFu;  // AG: bit l = slot l's token rows landed
             int pend_stage[kSkMaxStages], pend_kb[kSkMaxStages], pend_l[kSkMaxStages];
             int np = 0;
             // AG: token loads wait for the gathered rows; weight stages stream meanwhile.
@@ -1958,32 +1954,28 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                 }
             }
         }
-    } else if (MODE == kModeRSUnits && (warp == 2 || warp == 3)) {
-        owner_reduce<PB, TWU>(p, threadIdx.x - 64, 64, 3, &red_slot[0]);
     } else if (warp == 3) {
         if (MODE == kModeAG && p.sm_transfer && lane == 0) ag_transfer(p, sComm, cbar);
     } else if (warp >= 4) {
         // ===== epilogue: warp q holds weight rows (output columns) 32q..32q+31 of the n-tile =====
         // Whole n-tiles are stored straight from TMEM. A tile cut between CTAs
-        // (K-segments) is parked as fp32 partials and reduced once every CTA's
-        // mainloop is done: the tile's nseg CTAs each sum a 1/nseg share of its
-        // elements over all segments in segment order (loads of all segments in
-        // flight at once), so the reduction runs on every SM in parallel and the
-        // result does not depend on arrival order.
+        // (K-segments) is parked as fp32 partials; the CTA whose segment arrives
+        // last (a launch-tagged arrival counter per tile) sums every segment in
+        // segment (K) order and stores the tile, so no CTA waits for another and
+        // the result does not depend on arrival order.
         const int q = warp - 4, et = threadIdx.x - 128;
         const int cit = q * 32 + lane;  // column within the n-tile
         const int mv = min(p.m, mp);    // valid token rows
         int as = 0;
         uint32_t aphase = 0;
-        int split_tt[2] = {-1, -1};  // split tiles this CTA holds a segment of (at most its first and last)
-        int nsplit = 0;
         SkIter it{r0, r1, kbn};
         int tt, kb0, kb1;
         while (it.next(tt, kb0, kb1)) {
             const int l = tt / p.sk_nt, j = tt % p.sk_nt;
             const int col = j * kSkRows + cit;
             const long long tfirst = static_cast<long long>(tt) * kbn;
-            const int nseg = sk_cta_of(p, tfirst + kbn - 1) - sk_cta_of(p, tfirst) + 1;
+            const int c_first = sk_cta_of(p, tfirst);
+            const int nseg = sk_cta_of(p, tfirst + kbn - 1) - c_first + 1;
             mbar_wait(&tfull[as], aphase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(as * p.sk_acc_cols);
@@ -2011,96 +2003,107 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                 aphase ^= 1u;
             }
             if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 3, static_cast<uint32_t>(tt));
-            if (nseg > 1) {
-                // Parked: stamp the segment's flag (release, after every thread's stores).
+            bool done = nseg == 1;
+            if (!done) {
+                // Arrival (acq_rel, after the CTA barrier: every thread's parked
+                // stores are released; the last arrival acquires the others').
                 named_bar_sync(1, 128);
-                if (et == 0) st_release_gpu(p.sk_ctr + sk_slot_index(p, blockIdx.x, tt), p.tail_seq);
-                split_tt[nsplit++] = tt;
-            } else if (MODE == kModeRSUnits) {
-                // The tile's partial is in every owner's staging plane: stamp the flags.
+                if (et == 0) red_slot[3] = static_cast<int>(tail_arrive(p.sk_ctr + tt, p.tail_seq));
                 named_bar_sync(1, 128);
-                const int me = p.global_rank[l];
+                done = red_slot[3] == nseg;
+                if (done) {
+                    if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 4, static_cast<uint32_t>(tt));
+                    const float* slot[kSkMaxSegs];
+#pragma unroll
+                    for (int s2 = 0; s2 < kSkMaxSegs; ++s2) slot[s2] = s2 < nseg ? sk_slot(p, c_first + s2, tt) : nullptr;
+                    // float4 groups of the [mv x 128] tile, two per thread in flight
+                    // with every segment's load (one L2 round trip per two groups).
+                    const int E4 = mv * (kSkRows / 4);
+                    for (int fb = et; fb < E4; fb += 128 * 2) {
+                        float4 w[2][kSkMaxSegs];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int f = fb + u * 128;
+#pragma unroll
+                            for (int s2 = 0; s2 < kSkMaxSegs; ++s2)
+                                if (s2 < nseg && f < E4) w[u][s2] = ld_cg_f4(slot[s2] + 4 * f);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int f = fb + u * 128;
+                            if (f >= E4) break;
+                            float v[4] = {w[u][0].x, w[u][0].y, w[u][0].z, w[u][0].w};
+#pragma unroll
+                            for (int s2 = 1; s2 < kSkMaxSegs; ++s2)
+                                if (s2 < nseg) {
+                                    v[0] += w[u][s2].x;
+                                    v[1] += w[u][s2].y;
+                                    v[2] += w[u][s2].z;
+                                    v[3] += w[u][s2].w;
+                                }
+                            const int m = f / (kSkRows / 4), c2 = j * kSkRows + (f % (kSkRows / 4)) * 4;
+                            if (c2 >= p.n) continue;
+                            if (MODE == kModeRSUnits) {
+                                const int o = m / p.rpr;
+                                const long long se = static_cast<long long>(p.epoch & 1u) * p.stage_parity +
+                                                     p.global_rank[l] * p.stage_plane +
+                                                     static_cast<long long>(m - o * p.rpr) * p.ld_stage + c2;
+                                st_part4<PB>(p.staging[o], se, make_float4(v[0], v[1], v[2], v[3]));
+                            } else {
+                                if (ACT) {
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) v[i] = act_fwd(p.act, v[i]);
+                                }
+                                store_row<4>(p.c[l], static_cast<long long>(m) * p.ldc_l[l] + c2, c2, p.n, p.out_f32, v);
+                            }
+                        }
+                    }
+                    if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 5, static_cast<uint32_t>(tt));
+                }
+            }
+            if (done && MODE == kModeRSUnits) {
+                // The tile's partial is in every owner's staging plane (this rank's
+                // own rows included): stamp the peers' flags, then finish this rank's
+                // own rows here — wait for the other sources' partials of the tile
+                // and sum the planes in the canonical order (other sources
+                // ascending, then this rank) into C. Every CTA publishes a tile
+                // before it waits on that tile, and CTAs walk their tiles in order,
+                // so the waits cannot form a cycle.
+                named_bar_sync(1, 128);
+                const int me = p.global_rank[l], tp = p.tp, rpr = p.rpr;
                 if (et == 0) trace_event(p, l, kEvTileWrite, me, 0, j, 0u);
-                if (et < (mv - 1) / p.rpr + 1) rs_flag_set(p, l, et, j, me);
-            }
-        }
-        // Split tiles: wait for every segment, sum this CTA's share.
-        for (int si = 0; si < nsplit; ++si) {
-            tt = split_tt[si];
-            const int l = tt / p.sk_nt, j = tt % p.sk_nt;
-            const long long tfirst = static_cast<long long>(tt) * kbn;
-            const int c_first = sk_cta_of(p, tfirst);
-            const int nseg = sk_cta_of(p, tfirst + kbn - 1) - c_first + 1;
-            const int share = static_cast<int>(blockIdx.x) - c_first;
-            if (et < nseg) sk_wait(p, l, p.sk_ctr + sk_slot_index(p, c_first + et, tt), static_cast<uint32_t>(tt));
-            named_bar_sync(1, 128);
-            if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 4, static_cast<uint32_t>(tt));
-            const float* slot[kSkMaxSegs];
-#pragma unroll
-            for (int s2 = 0; s2 < kSkMaxSegs; ++s2) slot[s2] = s2 < nseg ? sk_slot(p, c_first + s2, tt) : nullptr;
-            const int E = mv * kSkRows;
-            const int e0 = share * E / nseg, e1 = (share + 1) * E / nseg;
-            for (int eb = e0 + et; eb < e1; eb += 128 * 4) {
-                float w[4][kSkMaxSegs];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = eb + u * 128;
-#pragma unroll
-                    for (int s2 = 0; s2 < kSkMaxSegs; ++s2)
-                        if (s2 < nseg && e < e1) w[u][s2] = __ldcg(slot[s2] + e);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int e = eb + u * 128;
-                    if (e >= e1) break;
-                    float v = w[u][0];
-#pragma unroll
-                    for (int s2 = 1; s2 < kSkMaxSegs; ++s2)
-                        if (s2 < nseg) v += w[u][s2];
-                    const int m = e / kSkRows, c2 = j * kSkRows + e % kSkRows;
-                    if (c2 >= p.n) continue;
-                    if (MODE == kModeRSUnits) {
-                        const int o = m / p.rpr;
-                        const long long se = static_cast<long long>(p.epoch & 1u) * p.stage_parity +
-                                             p.global_rank[l] * p.stage_plane +
-                                             static_cast<long long>(m - o * p.rpr) * p.ld_stage + c2;
-                        if (PB) reinterpret_cast<__nv_bfloat16*>(p.staging[o])[se] = __float2bfloat16_rn(v);
-                        else p.staging[o][se] = v;
-                    } else {
-                        const float x = ACT ? act_fwd(p.act, v) : v;
-                        const long long ce = static_cast<long long>(m) * p.ldc_l[l] + c2;
-                        if (p.out_f32) static_cast<float*>(p.c[l])[ce] = x;
-                        else static_cast<__nv_bfloat16*>(p.c[l])[ce] = __float2bfloat16_rn(x);
-                    }
-                }
-            }
-            if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 5, static_cast<uint32_t>(tt));
-            if (MODE == kModeRSUnits) {
-                // Share 0 stamps the owners' flags once every share is stored (each
-                // share's release after its CTA barrier; share 0 acquires them all).
+                if (et < tp && et != me) rs_flag_set(p, l, et, j, me);
+                if (et < tp && et != me)
+                    wait_flag(p.rs_flags[me] + j * tp + et, p.epoch, p, l, kErrRsFlagTimeout,
+                              static_cast<uint32_t>(j), static_cast<uint32_t>(et));
                 named_bar_sync(1, 128);
-                const uint32_t* const shares = p.sk_ctr + kSkCtrCap / 2;
-                if (share != 0) {
-                    if (et == 0) {
-                        __threadfence_system();  // staging stores may target a peer GPU
-                        st_release_gpu(p.sk_ctr + kSkCtrCap / 2 + sk_slot_index(p, blockIdx.x, tt), p.tail_seq);
-                    }
-                } else {
-                    if (et >= 1 && et < nseg)
-                        sk_wait(p, l, shares + sk_slot_index(p, c_first + et, tt), static_cast<uint32_t>(tt));
-                    named_bar_sync(1, 128);
-                    const int me = p.global_rank[l];
-                    if (et == 0) trace_event(p, l, kEvTileWrite, me, 0, j, 0u);
-                    if (et < (mv - 1) / p.rpr + 1) rs_flag_set(p, l, et, j, me);
+                if (et == 0) trace_event(p, l, kEvReduce, me, 0, j, static_cast<uint32_t>(me));
+                const float* const sbase = p.staging[me];
+                const long long e0 = static_cast<long long>(p.epoch & 1u) * p.stage_parity;
+                const int F = min(rpr, mv - me * rpr) * (kSkRows / 4);  // float4 groups of my rows
+                for (int f = et; f < F; f += 128) {
+                    const int lr = f / (kSkRows / 4), c2 = j * kSkRows + (f % (kSkRows / 4)) * 4;
+                    if (c2 >= p.n) continue;
+                    const long long e = e0 + static_cast<long long>(lr) * p.ld_stage + c2;
+                    float4 w[kMaxRanks];
+#pragma unroll
+                    for (int s2 = 0; s2 < kMaxRanks; ++s2)
+                        if (s2 < tp) w[s2] = ld_part4<PB>(sbase, e + s2 * p.stage_plane);
+                    float acc[4];
+                    bool first = true;
+#pragma unroll
+                    for (int s2 = 0; s2 < kMaxRanks; ++s2)
+                        if (s2 < tp && s2 != me) sum_into(acc, w[s2], first);
+#pragma unroll
+                    for (int s2 = 0; s2 < kMaxRanks; ++s2)
+                        if (s2 == me) sum_into(acc, w[s2], first);
+                    store_row<4>(p.c[l], static_cast<long long>(lr) * p.ldc_l[l] + c2, c2, p.n, p.out_f32, acc);
                 }
             }
         }
-        if (MODE == kModeRSUnits) owner_reduce<PB, TWU>(p, et, 128, 4, &red_slot[1]);
+        if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 7, 0);  // epilogue done (profiling)
     }
-    if (MODE == kModeRSUnits && warp < 2) {
-        __syncwarp();
-        owner_reduce<PB, TWU>(p, threadIdx.x, 64, 5, &red_slot[2]);
-    }
+    if (threadIdx.x % 32 == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 24 + warp, 0);  // warp at the exit barrier (profiling)
     __syncthreads();
     if (warp == 0 && lane == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 1, 0);
     if (warp == 2) {

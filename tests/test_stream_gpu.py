@@ -179,16 +179,16 @@ def test_stream_kernel_graph_replay(case):
 
 
 def test_stream_kernel_dropped_rs_flag_raises_deadlock_error():
-    """A dropped (n-tile, source) flag leaves an owner unit waiting: the
-    bounded device wait raises DeadlockError naming the flag, and the
-    communicator runs the next operator correctly."""
+    """A dropped (n-tile, source) flag leaves the owner's epilogue waiting for
+    that source's partial: the bounded device wait raises DeadlockError naming
+    the flag, and the communicator runs the next operator correctly."""
     p = fx.ProblemSpec(16, 1024, 512, 2, RS)
     with H.make_comm(p) as comm:
         a, b = H.upload(comm, p, seed=3)
-        comm.inject_fault(fx.FAULT_DROP_SIGNAL, 1, 3)  # owner 1, flag (n-tile 1) x tp 2 + source 1
+        comm.inject_fault(fx.FAULT_DROP_SIGNAL, 1, 2)  # owner 1, flag (n-tile 1) x tp 2 + source 0
         with pytest.raises(fx.DeadlockError) as ei:
             _run(comm, p, True, decode_kernel=STREAM, wall_budget_s=0.5)
-        assert "waiting for partial of tile 1 from source 1" in str(ei.value), str(ei.value)
+        assert "waiting for partial of tile 1 from source 0" in str(ei.value), str(ei.value)
         got = _run(comm, p, True, decode_kernel=STREAM)
         want = O.dense_oracle(RS, p.m, p.n, p.k, p.tp, a, b)
         for r in range(p.tp):
