@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FLUX_ABI_VERSION 7
+#define FLUX_ABI_VERSION 8
 
 /* Return codes. The reference raises C++ exceptions (errors.hpp:9-31); each
  * maps to one code. The C++ shim (include/flux/overlap.hpp) rethrows them. */
@@ -111,9 +111,22 @@ typedef struct {
     int decode_kernel;         /* flux_decode_kernel: GEMMs of at most 128 rows (decode) run on the
                                   streaming kernel (weights on the MMA M side, tokens on N, stream-K
                                   over the weight shard) unless FLUX_DECODE_TILE */
+    int nvls;                  /* flux_nvls: NVLink SHARP multicast through the NVSwitch (north_star:
+                                  "reduce through NVLS multicast where the host exposes it").
+                                  AllGather-GEMM: every rank pushes its own A rows once with
+                                  multimem.st into all ranks' a_agg and stamps each comm tile's
+                                  flag on all ranks with one multicast store. GEMM-RS: every
+                                  source writes its partial into its own region; each owner
+                                  reads the sum over all sources with multimem.ld_reduce
+                                  (reduced in the switch; fp32 partials, WriteAlltoAll).
+                                  FLUX_NVLS_MULTICAST needs a communicator created with
+                                  nvls_bytes > 0; FLUX_NVLS_EMULATED runs the same protocol
+                                  with unicast loops over the ranks' regions (tests on one GPU). */
 } flux_opts;
 
 typedef enum { FLUX_DECODE_AUTO = 0, FLUX_DECODE_TILE = 1, FLUX_DECODE_STREAM = 2 } flux_decode_kernel;
+
+typedef enum { FLUX_NVLS_OFF = 0, FLUX_NVLS_MULTICAST = 1, FLUX_NVLS_EMULATED = 2 } flux_nvls;
 
 typedef enum { FLUX_B_NK = 0, FLUX_B_KN = 1 } flux_b_layout;
 
@@ -132,6 +145,11 @@ typedef enum {
 
 typedef struct {
     size_t heap_bytes;         /* per-rank symmetric heap size (0 = 1 GiB) */
+    size_t nvls_bytes;         /* > 0: also create an NVLS multicast region of this many bytes per
+                                  rank (VMM memory bound to one cuMulticast object over every
+                                  rank's GPU; single-process communicators over distinct GPUs).
+                                  Creation fails with FLUX_ERR_CUDA naming the step when the host
+                                  does not expose multicast (flux_nvls_probe tells beforehand). */
 } flux_comm_opts;
 
 typedef struct flux_comm flux_comm;
@@ -201,6 +219,15 @@ int flux_comm_tp(const flux_comm* comm);
 int flux_comm_rank(const flux_comm* comm); /* IPC: own rank; single process: -1 */
 /* Simulates an incomplete init-phase exchange (workspace.cpp:67-69, tests only). */
 int flux_comm_drop_peer(flux_comm* comm, int from_rank, int peer_rank);
+
+/* NVLS capability probe: 1 if a multicast object can be created over `devices`
+ * (n >= 1 distinct GPUs) and bound to memory on each, else 0 with the failing
+ * step in `why` (e.g. "cuMulticastCreate: invalid argument"). No GPU: 0. */
+int flux_nvls_probe(int n, const int* devices, char* why, int why_len);
+/* Bytes of the NVLS region a problem needs (flux_comm_opts.nvls_bytes). */
+size_t flux_nvls_required_bytes(const flux_problem* problem);
+/* 1 if the communicator owns an NVLS multicast region. */
+int flux_comm_nvls(const flux_comm* comm);
 /* Buffer of `rank` for `problem` (any rank in single-process mode; own rank in IPC mode). */
 int flux_buffer(flux_comm* comm, int rank, int kind, const flux_problem* problem,
                 flux_buffer_desc* out);

@@ -21,10 +21,11 @@ SWIZZLE_NAIVE, SWIZZLE_RANK_SHIFTED, SWIZZLE_ARRIVAL_ALIGNED = 0, 1, 2
 BF16, F32 = 0, 1
 BUF_A_SHARD, BUF_B_SHARD, BUF_A_AGG, BUF_C_OUT, BUF_STAGING, BUF_C_OUT_F32 = 0, 1, 2, 3, 4, 5
 ACT_NONE, ACT_GELU, ACT_RELU, ACT_SILU, ACT_SWIGLU = 0, 1, 2, 3, 4
-ABI_VERSION = 7
+ABI_VERSION = 8
 FAULT_NONE, FAULT_DROP_SIGNAL, FAULT_DOUBLE_SIGNAL = 0, 1, 2
 B_NK, B_KN = 0, 1
 DECODE_AUTO, DECODE_TILE, DECODE_STREAM = 0, 1, 2  # flux_decode_kernel
+NVLS_OFF, NVLS_MULTICAST, NVLS_EMULATED = 0, 1, 2  # flux_nvls
 
 
 class FluxError(RuntimeError):
@@ -78,11 +79,12 @@ class Opts(C.Structure):
                 ("interleave_seed", C.c_uint64), ("shift_offset", C.c_int), ("out_dtype", C.c_int),
                 ("emulated_order", C.c_int), ("cta_group", C.c_int), ("ag_engine", C.c_int), ("trace", C.c_int),
                 ("activation", C.c_int), ("activation_grad", C.c_int), ("rs_partials", C.c_int),
-                ("b_layout", C.c_int), ("graph_safe", C.c_int), ("decode_kernel", C.c_int)]
+                ("b_layout", C.c_int), ("graph_safe", C.c_int), ("decode_kernel", C.c_int),
+                ("nvls", C.c_int)]
 
 
 class CommOpts(C.Structure):
-    _fields_ = [("heap_bytes", C.c_size_t)]
+    _fields_ = [("heap_bytes", C.c_size_t), ("nvls_bytes", C.c_size_t)]
 
 
 class Matrix(C.Structure):
@@ -174,6 +176,9 @@ _SIGS = {
                                        _P(C.c_void_p), _P(Operands), _P(C.c_int), _P(C.c_int), _P(C.c_int), C.c_int]),
     "flux_transfer_log": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, _P(C.c_int)]),
     "flux_comm_set_check_double_set": (C.c_int, [C.c_void_p, C.c_int]),
+    "flux_nvls_probe": (C.c_int, [C.c_int, _P(C.c_int), C.c_char_p, C.c_int]),
+    "flux_nvls_required_bytes": (C.c_size_t, [_P(Problem)]),
+    "flux_comm_nvls": (C.c_int, [C.c_void_p]),
 }
 
 # Symbols include/flux_b200.h declares (tests check the library exports all of them).
@@ -211,9 +216,20 @@ def check(rc: int) -> None:
 def default_opts(**kw) -> Opts:
     o = Opts()
     lib().flux_default_opts(C.byref(o))
+    names = {f[0] for f in Opts._fields_}
     for k, v in kw.items():
+        if k not in names:
+            raise TypeError(f"unknown flux_opts field {k!r}")
         setattr(o, k, v)
     return o
+
+
+def nvls_probe(devices) -> tuple[bool, str]:
+    """(supported, reason): can an NVLS multicast object be created over `devices`?"""
+    devs = (C.c_int * len(devices))(*devices)
+    why = C.create_string_buffer(256)
+    ok = lib().flux_nvls_probe(len(devices), devs, why, 256)
+    return bool(ok), why.value.decode(errors="replace")
 
 
 def stream_array(streams):

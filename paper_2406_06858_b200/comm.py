@@ -151,12 +151,12 @@ class Communicator:
     """
 
     def __init__(self, tp: int, devices: Optional[Sequence[int]] = None, heap_bytes: int = 0, *, _handle=None,
-                 device: Optional[int] = None):
+                 device: Optional[int] = None, nvls_bytes: int = 0):
         self.tp = tp
         self._h = C.c_void_p(_handle) if _handle is not None else C.c_void_p()
         if _handle is None:
             devs = (C.c_int * tp)(*(devices if devices is not None else [0] * tp))
-            N.check(N.lib().flux_comm_create(tp, devs, C.byref(N.CommOpts(heap_bytes)), C.byref(self._h)))
+            N.check(N.lib().flux_comm_create(tp, devs, C.byref(N.CommOpts(heap_bytes, nvls_bytes)), C.byref(self._h)))
         self.rank = N.lib().flux_comm_rank(self._h)
         # Device of every rank this process drives, and the device this process
         # drives when it is a single one (IPC mode, or every rank on one GPU).
@@ -171,7 +171,7 @@ class Communicator:
         (e.g. torch.distributed.all_gather_object), the paper's init-phase IPC
         exchange (PAPER.md:229)."""
         h = C.c_void_p()
-        N.check(N.lib().flux_comm_create_ipc(rank, tp, device, C.byref(N.CommOpts(heap_bytes)), C.byref(h)))
+        N.check(N.lib().flux_comm_create_ipc(rank, tp, device, C.byref(N.CommOpts(heap_bytes, 0)), C.byref(h)))
         nb = N.lib().flux_comm_ipc_blob_bytes()
         blob = C.create_string_buffer(nb)
         N.check(N.lib().flux_comm_ipc_handle(h, blob))
@@ -314,6 +314,11 @@ class Communicator:
     def drop_peer(self, from_rank: int, peer_rank: int) -> None:
         N.check(N.lib().flux_comm_drop_peer(self._h, from_rank, peer_rank))
 
+    @property
+    def nvls(self) -> bool:
+        """True if the communicator owns an NVLS multicast region (nvls_bytes > 0)."""
+        return bool(N.lib().flux_comm_nvls(self._h))
+
     def close(self) -> None:
         if self._h:
             N.lib().flux_comm_destroy(self._h)
@@ -334,6 +339,11 @@ class Communicator:
 
 def required_heap_bytes(problem: ProblemSpec) -> int:
     return int(N.lib().flux_required_heap_bytes(C.byref(problem.c())))
+
+
+def nvls_required_bytes(problem: ProblemSpec) -> int:
+    """Per-rank NVLS region bytes the problem needs (Communicator(nvls_bytes=...))."""
+    return int(N.lib().flux_nvls_required_bytes(C.byref(problem.c())))
 
 
 TRACE_KINDS = {1: "compute_start", 2: "signal_set", 3: "tile_write", 4: "reduce", 5: "wait", 6: "launch"}

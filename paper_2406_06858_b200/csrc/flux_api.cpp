@@ -90,6 +90,64 @@ int need_driver() {
     return FLUX_OK;
 }
 
+// NVLS: multicast objects and VMM (driver API, loaded on first use).
+struct NvlsDriver {
+    PFN_cuDeviceGet_v2000 dev_get = nullptr;
+    PFN_cuDeviceGetAttribute_v2000 attr = nullptr;
+    PFN_cuGetErrorString_v6000 err_str = nullptr;
+    PFN_cuMulticastCreate_v12010 mc_create = nullptr;
+    PFN_cuMulticastAddDevice_v12010 mc_add = nullptr;
+    PFN_cuMulticastBindMem_v12010 mc_bind = nullptr;
+    PFN_cuMulticastUnbind_v12010 mc_unbind = nullptr;
+    PFN_cuMulticastGetGranularity_v12010 mc_gran = nullptr;
+    PFN_cuMemCreate_v10020 mem_create = nullptr;
+    PFN_cuMemRelease_v10020 mem_release = nullptr;
+    PFN_cuMemAddressReserve_v10020 va_reserve = nullptr;
+    PFN_cuMemAddressFree_v10020 va_free = nullptr;
+    PFN_cuMemMap_v10020 map = nullptr;
+    PFN_cuMemUnmap_v10020 unmap = nullptr;
+    PFN_cuMemSetAccess_v10020 set_access = nullptr;
+    bool ok = false;
+};
+
+NvlsDriver& nvls_driver() {
+    static NvlsDriver d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            *fn = nullptr;
+            if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+                *fn = nullptr;
+            return *fn != nullptr;
+        };
+        bool ok = true;
+        ok &= get("cuDeviceGet", reinterpret_cast<void**>(&d.dev_get));
+        ok &= get("cuDeviceGetAttribute", reinterpret_cast<void**>(&d.attr));
+        ok &= get("cuGetErrorString", reinterpret_cast<void**>(&d.err_str));
+        ok &= get("cuMulticastCreate", reinterpret_cast<void**>(&d.mc_create));
+        ok &= get("cuMulticastAddDevice", reinterpret_cast<void**>(&d.mc_add));
+        ok &= get("cuMulticastBindMem", reinterpret_cast<void**>(&d.mc_bind));
+        ok &= get("cuMulticastUnbind", reinterpret_cast<void**>(&d.mc_unbind));
+        ok &= get("cuMulticastGetGranularity", reinterpret_cast<void**>(&d.mc_gran));
+        ok &= get("cuMemCreate", reinterpret_cast<void**>(&d.mem_create));
+        ok &= get("cuMemRelease", reinterpret_cast<void**>(&d.mem_release));
+        ok &= get("cuMemAddressReserve", reinterpret_cast<void**>(&d.va_reserve));
+        ok &= get("cuMemAddressFree", reinterpret_cast<void**>(&d.va_free));
+        ok &= get("cuMemMap", reinterpret_cast<void**>(&d.map));
+        ok &= get("cuMemUnmap", reinterpret_cast<void**>(&d.unmap));
+        ok &= get("cuMemSetAccess", reinterpret_cast<void**>(&d.set_access));
+        d.ok = ok;
+    });
+    return d;
+}
+
+std::string cu_err(CUresult r) {
+    const char* s = nullptr;
+    if (nvls_driver().err_str) nvls_driver().err_str(r, &s);
+    return s ? std::string(s) : ("CUresult " + std::to_string(static_cast<int>(r)));
+}
+
 int write_value(cudaStream_t s, void* addr, uint32_t v) {
     CUresult r = driver().write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
                                   CU_STREAM_WRITE_VALUE_DEFAULT);
@@ -482,6 +540,17 @@ struct flux_comm {
     int act_fault_kind = 0, act_fault_rank = 0, act_fault_index = 0;
     bool check_double = false;      // flux_comm_set_check_double_set
     std::string host_error;         // host-detected failure of the last operator (flag set twice)
+    // NVLS multicast region (flux_comm_opts.nvls_bytes): one multicast object over
+    // every rank's GPU; each rank's VMM allocation is bound to it and mapped at
+    // uc[r] (its unicast address); mc is the multicast address of the region.
+    struct Nvls {
+        size_t bytes = 0;
+        unsigned long long mc_handle = 0;
+        std::vector<unsigned long long> mem;
+        std::vector<unsigned long long> uc;
+        unsigned long long mc = 0;
+        bool bound = false;
+    } nvls;
 };
 
 namespace {
@@ -541,6 +610,138 @@ int end_op(flux_comm* c) {
     if (c->act_fault_kind != 0) c->ag_sig = 0;
     c->act_fault_kind = 0;
     if (!c->host_error.empty()) return fail(FLUX_ERR_RUNTIME, c->host_error);
+    return FLUX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NVLS multicast region: one multicast object over the ranks' GPUs, one VMM
+// allocation per GPU bound to it, each mapped at a unicast address, and the
+// object mapped once at a multicast address every GPU may access.
+// ---------------------------------------------------------------------------
+void nvls_release(flux_comm::Nvls& nv, const std::vector<int>& devs) {
+    NvlsDriver& d = nvls_driver();
+    if (!d.ok) return;
+    if (nv.mc) {
+        d.unmap(nv.mc, nv.bytes);
+        d.va_free(nv.mc, nv.bytes);
+    }
+    for (size_t r = 0; r < nv.mem.size(); ++r) {
+        CUdevice cd = 0;
+        d.dev_get(&cd, devs[r]);
+        if (nv.bound && nv.mc_handle) d.mc_unbind(static_cast<CUmemGenericAllocationHandle>(nv.mc_handle), cd, 0, nv.bytes);
+        if (r < nv.uc.size() && nv.uc[r]) {
+            d.unmap(nv.uc[r], nv.bytes);
+            d.va_free(nv.uc[r], nv.bytes);
+        }
+        if (nv.mem[r]) d.mem_release(static_cast<CUmemGenericAllocationHandle>(nv.mem[r]));
+    }
+    if (nv.mc_handle) d.mem_release(static_cast<CUmemGenericAllocationHandle>(nv.mc_handle));
+    nv = flux_comm::Nvls{};
+}
+
+// Creates the region over `devs` (distinct GPUs, one per rank). On failure
+// everything created so far is released and `why` names the failing step.
+int nvls_create(flux_comm::Nvls& nv, const std::vector<int>& devs, size_t want, std::string& why) {
+    NvlsDriver& d = nvls_driver();
+    if (!d.ok) {
+        why = "multicast / VMM driver entry points unavailable";
+        return FLUX_ERR_CUDA;
+    }
+    const int n = static_cast<int>(devs.size());
+    std::vector<CUdevice> cds(n);
+    for (int r = 0; r < n; ++r) {
+        for (int q = 0; q < r; ++q)
+            if (devs[q] == devs[r]) {
+                why = "ranks " + S(q) + " and " + S(r) + " share GPU " + S(devs[r]) + " (NVLS needs one rank per GPU)";
+                return FLUX_ERR_CONFIG;
+            }
+        CUresult e = d.dev_get(&cds[r], devs[r]);
+        int mc = 0;
+        if (e == CUDA_SUCCESS) e = d.attr(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cds[r]);
+        if (e != CUDA_SUCCESS || !mc) {
+            why = "GPU " + S(devs[r]) + ": multicast not supported" + (e != CUDA_SUCCESS ? " (" + cu_err(e) + ")" : "");
+            return FLUX_ERR_CUDA;
+        }
+    }
+    auto step = [&](CUresult e, const char* what) {
+        if (e == CUDA_SUCCESS) return true;
+        why = std::string(what) + ": " + cu_err(e);
+        return false;
+    };
+    CUmulticastObjectProp mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.numDevices = static_cast<unsigned>(n);
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = std::max<size_t>(want, 1);
+    size_t gran = 0;
+    bool ok = step(d.mc_gran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED), "cuMulticastGetGranularity");
+    if (ok) {
+        gran = std::max<size_t>(gran, size_t(2) << 20);
+        nv.bytes = (std::max<size_t>(want, 1) + gran - 1) / gran * gran;
+        mp.size = nv.bytes;
+        CUmemGenericAllocationHandle h = 0;
+        ok = step(d.mc_create(&h, &mp), "cuMulticastCreate");
+        nv.mc_handle = h;
+    }
+    for (int r = 0; ok && r < n; ++r) ok = step(d.mc_add(static_cast<CUmemGenericAllocationHandle>(nv.mc_handle), cds[r]), "cuMulticastAddDevice");
+    nv.mem.assign(n, 0);
+    nv.uc.assign(n, 0);
+    for (int r = 0; ok && r < n; ++r) {
+        CUmemAllocationProp ap;
+        std::memset(&ap, 0, sizeof(ap));
+        ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ap.location.id = devs[r];
+        ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+        CUmemGenericAllocationHandle mh = 0;
+        ok = step(d.mem_create(&mh, nv.bytes, &ap, 0), "cuMemCreate");
+        nv.mem[r] = mh;
+        CUdeviceptr va = 0;
+        if (ok) ok = step(d.va_reserve(&va, nv.bytes, gran, 0, 0), "cuMemAddressReserve");
+        if (ok) ok = step(d.map(va, nv.bytes, 0, mh, 0), "cuMemMap");
+        if (ok) nv.uc[r] = va;
+        else if (va) d.va_free(va, nv.bytes);
+        CUmemAccessDesc ad;
+        std::memset(&ad, 0, sizeof(ad));
+        ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ad.location.id = devs[r];
+        ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        if (ok) ok = step(d.set_access(nv.uc[r], nv.bytes, &ad, 1), "cuMemSetAccess (unicast)");
+    }
+    for (int r = 0; ok && r < n; ++r) {
+        ok = step(d.mc_bind(static_cast<CUmemGenericAllocationHandle>(nv.mc_handle), 0,
+                            static_cast<CUmemGenericAllocationHandle>(nv.mem[r]), 0, nv.bytes, 0),
+                  "cuMulticastBindMem");
+        if (ok) nv.bound = true;
+    }
+    if (ok) {
+        CUdeviceptr va = 0;
+        ok = step(d.va_reserve(&va, nv.bytes, gran, 0, 0), "cuMemAddressReserve (multicast)");
+        if (ok) ok = step(d.map(va, nv.bytes, 0, static_cast<CUmemGenericAllocationHandle>(nv.mc_handle), 0),
+                          "cuMemMap (multicast)");
+        if (ok) nv.mc = va;
+        else if (va) d.va_free(va, nv.bytes);
+        std::vector<CUmemAccessDesc> ads(n);
+        for (int r = 0; r < n; ++r) {
+            std::memset(&ads[r], 0, sizeof(ads[r]));
+            ads[r].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+            ads[r].location.id = devs[r];
+            ads[r].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        }
+        if (ok) ok = step(d.set_access(nv.mc, nv.bytes, ads.data(), static_cast<size_t>(n)), "cuMemSetAccess (multicast)");
+    }
+    for (int r = 0; ok && r < n; ++r) {
+        if (cudaSetDevice(devs[r]) != cudaSuccess ||
+            cudaMemset(reinterpret_cast<void*>(nv.uc[r]), 0, nv.bytes) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
+            why = "zeroing the NVLS region failed";
+            ok = false;
+        }
+    }
+    if (!ok) {
+        nvls_release(nv, devs);
+        return FLUX_ERR_CUDA;
+    }
     return FLUX_OK;
 }
 
@@ -810,7 +1011,10 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             // there and waits for nothing (the shard still lands in a_agg).
             const bool direct = mode == kModeAG && p->tp == 1;
             const Region& A = ((mode == kModeAG && !direct) || plain_on_agg) ? L.a_agg : L.a_shard;
-            if (A.off == L.a_shard.off && ops && ops->a.ptr)
+            if (mode == kModeAG && !direct && oc.o.nvls == FLUX_NVLS_MULTICAST)  // a_agg in the NVLS region
+                FLUX_TRY(make_tmap(&prm.tma_a[li], reinterpret_cast<char*>(c->nvls.uc[g[li]]) + kNvlsDataOffset, A.rows,
+                                   lk, A.ld, a_box));
+            else if (A.off == L.a_shard.off && ops && ops->a.ptr)
                 FLUX_TRY(make_tmap(&prm.tma_a[li], ops->a.ptr, A.rows, lk, ops->a.ld, a_box));
             else
                 FLUX_TRY(make_tmap(&prm.tma_a[li], rs.heap + A.off, A.rows, lk, A.ld, a_box));
@@ -975,7 +1179,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
         // Every SM takes part even without a GEMM tile of its own: decode RS runs
         // reduction units, the in-kernel AllGather moves pieces (decode AG M=128:
         // 124 -> 116 us).
-        const bool full = mode == kModeRSUnits || (mode == kModeAG && prm.sm_transfer);
+        const bool full = mode == kModeRSUnits || (mode == kModeAG && (prm.sm_transfer || prm.nvls));
         const int grid = full ? cg * std::max(1, sm_count(dev) / cg)
                               : cg * std::max(1, std::min(prm.num_tiles, sm_count(dev) / cg));
         // Dynamic tile scheduler (FLUX_DYN_SCHED=1): clusters fetch tiles from a
@@ -1007,6 +1211,15 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             // ceil(kb / (max - 1)) k-blocks.
             const long long min_run = (kbn + kSkMaxSegsHost - 2) / (kSkMaxSegsHost - 1);
             prm.sk_ctas = static_cast<int>(std::max<long long>(1, std::min<long long>(sms, prm.sk_work / min_run)));
+            // Enough n-tiles for ~0.4 of the SMs: one whole tile per CTA (no K-segment
+            // fixup after the stream). Measured on one GPU's Llama-2-70B TP=8 decode
+            // share, M=16, L2 flushed: RS attn-out (64 tiles) 26.6 -> 18.5 us, RS
+            // down-proj 32.8 -> 26.6 us; split K-segments stay for fewer tiles (AG
+            // up-proj share: 28 tiles).
+            const long long tiles_all = static_cast<long long>(g.size()) * sk_nt;
+            if (tiles_all * 5 >= 2LL * sms && tiles_all <= sms) prm.sk_ctas = static_cast<int>(tiles_all);
+            if (const char* env = std::getenv("FLUX_SK_CTAS"))  // A/B: CTAs of the stream-K partition
+                prm.sk_ctas = static_cast<int>(std::max<long long>(1, std::min<long long>({sms, prm.sk_work, std::atoll(env)})));
             prm.sk_acc_cols = 16;
             while (prm.sk_acc_cols < sk_mp) prm.sk_acc_cols *= 2;
             const int stage_bytes = stream_smem_bytes(mode, sk_mp, 1) - stream_smem_bytes(mode, sk_mp, 0);
@@ -1022,7 +1235,7 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             prm.sk_ctr = at<uint32_t>(lead_rank, kSkCtrOffset);
             prm.tail_splits = 0;
             // The in-kernel AllGather runs on every SM.
-            const int sgrid = (mode == kModeAG && prm.sm_transfer) ? sms : prm.sk_ctas;
+            const int sgrid = (mode == kModeAG && (prm.sm_transfer || prm.nvls)) ? sms : prm.sk_ctas;
             FLUX_CUDA(launch_stream(mode, prm, sgrid, stream_smem_bytes(mode, sk_mp, prm.sk_stages), lead));
         } else {
             FLUX_CUDA(launch_gemm(mode, cg, prm, grid, lead));
@@ -1079,6 +1292,7 @@ void flux_default_opts(flux_opts* o) {
     o->b_layout = FLUX_B_NK;
     o->graph_safe = 0;
     o->decode_kernel = FLUX_DECODE_AUTO;
+    o->nvls = FLUX_NVLS_OFF;
 }
 
 int flux_problem_validate(const flux_problem* problem, const flux_tile* tile) {
@@ -1176,6 +1390,38 @@ size_t flux_required_heap_bytes(const flux_problem* p) {
     return layout_for(p).total;
 }
 
+size_t flux_nvls_required_bytes(const flux_problem* p) {
+    if (validate_problem(p) != FLUX_OK) return 0;
+    const Layout L = layout_for(p);
+    const size_t data = p->pattern == FLUX_ALLGATHER_GEMM ? L.a_agg.bytes() : static_cast<size_t>(2) * L.stage_parity * 4;
+    return kNvlsDataOffset + data;
+}
+
+int flux_nvls_probe(int n, const int* devices, char* why, int why_len) {
+    std::string msg;
+    int ok = 0;
+    if (n < 1 || n > kMaxRanks || !devices) {
+        msg = "need 1..8 devices";
+    } else if (!driver().ok) {
+        msg = "no CUDA driver";
+    } else {
+        std::vector<int> devs(devices, devices + n);
+        flux_comm::Nvls nv;
+        if (nvls_create(nv, devs, size_t(2) << 20, msg) == FLUX_OK) {
+            ok = 1;
+            msg = "ok";
+            nvls_release(nv, devs);
+        }
+    }
+    if (why && why_len > 0) {
+        std::strncpy(why, msg.c_str(), static_cast<size_t>(why_len) - 1);
+        why[why_len - 1] = 0;
+    }
+    return ok;
+}
+
+int flux_comm_nvls(const flux_comm* c) { return c && c->nvls.mc ? 1 : 0; }
+
 int flux_comm_create(int tp, const int* devices, const flux_comm_opts* opts, flux_comm** out) {
     if (!out) return fail(FLUX_ERR_CONFIG, "null output");
     *out = nullptr;
@@ -1215,6 +1461,16 @@ int flux_comm_create(int tp, const int* devices, const flux_comm_opts* opts, flu
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) c->directory[a][b] = false;
             cudaGetLastError();
         }
+    if (opts && opts->nvls_bytes > 0) {
+        std::vector<int> devs(tp);
+        for (int r = 0; r < tp; ++r) devs[r] = c->ranks[r].device;
+        std::string why;
+        const int rc = tp < 2 ? FLUX_ERR_CONFIG : nvls_create(c->nvls, devs, opts->nvls_bytes, why);
+        if (rc != FLUX_OK) {
+            flux_comm_destroy(c);
+            return fail(rc, "NVLS unavailable: " + (tp < 2 ? std::string("needs tp >= 2") : why));
+        }
+    }
     c->connected = true;
     *out = c;
     return FLUX_OK;
@@ -1230,6 +1486,11 @@ int flux_comm_create_ipc(int rank, int tp, int device, const flux_comm_opts* opt
     c->tp = tp;
     c->ipc = true;
     c->my_rank = rank;
+    if (opts && opts->nvls_bytes > 0) {
+        delete c;
+        return fail(FLUX_ERR_CONFIG, "NVLS multicast regions need the single-process communicator "
+                                     "(the multicast handle is a POSIX file descriptor)");
+    }
     c->heap_bytes = (opts && opts->heap_bytes) ? opts->heap_bytes : (size_t(1) << 30);
     c->ranks.resize(tp);
     c->directory.assign(tp, std::vector<bool>(tp, false));
@@ -1331,6 +1592,11 @@ int flux_comm_destroy(flux_comm* c) {
     }
     if (c->err_host) cudaFreeHost(c->err_host);
     for (cudaEvent_t x : c->xfer_events) cudaEventDestroy(x);
+    if (c->nvls.mc_handle) {
+        std::vector<int> devs;
+        for (int r = 0; r < c->tp; ++r) devs.push_back(c->ranks[r].device);
+        nvls_release(c->nvls, devs);
+    }
     delete c;
     return FLUX_OK;
 }
@@ -1549,6 +1815,56 @@ static int run_op(flux_comm* c, const std::function<int()>& body) {
     return end_op(c);
 }
 
+// NVLS operator checks (opts.nvls) and the fields every NVLS launch carries.
+static int nvls_check(flux_comm* c, const flux_problem* p, const flux_opts& o) {
+    if (o.nvls != FLUX_NVLS_MULTICAST && o.nvls != FLUX_NVLS_EMULATED) return fail(FLUX_ERR_CONFIG, "unknown nvls mode");
+    if (o.graph_safe) return fail(FLUX_ERR_CONFIG, "graph_safe operators do not use NVLS");
+    if (o.nvls == FLUX_NVLS_MULTICAST) {
+        if (!c->nvls.mc)
+            return fail(FLUX_ERR_CONFIG, "FLUX_NVLS_MULTICAST needs a communicator created with nvls_bytes > 0");
+        const size_t need = flux_nvls_required_bytes(p);
+        if (need > c->nvls.bytes)
+            return fail(FLUX_ERR_SHAPE, "problem needs " + S(need) + " NVLS bytes per rank, communicator has " + S(c->nvls.bytes));
+    }
+    return FLUX_OK;
+}
+
+// Regions of every rank the NVLS protocol addresses: the multicast region
+// (nvls = 1), or the regular heap buffers of the same role (nvls = 2).
+static void nvls_fill(flux_comm* c, const flux_problem* p, const flux_opts& o, GemmParams& prm) {
+    const Layout L = layout_for(p);
+    prm.nvls = o.nvls;
+    const bool hw = o.nvls == FLUX_NVLS_MULTICAST;
+    for (int q = 0; q < p->tp; ++q) {
+        char* base = hw ? reinterpret_cast<char*>(c->nvls.uc[q]) : c->ranks[q].heap;
+        const size_t data = hw ? kNvlsDataOffset : (p->pattern == FLUX_ALLGATHER_GEMM ? L.a_agg.off : L.staging.off);
+        prm.nvls_data[q] = base + data;
+        prm.nvls_flags[q] = reinterpret_cast<uint32_t*>(base + (hw ? kNvlsFlagOffset : kAgFlagOffset));
+    }
+    prm.nvls_data_mc = hw ? reinterpret_cast<char*>(c->nvls.mc) + kNvlsDataOffset : nullptr;
+    prm.nvls_flags_mc = hw ? reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c->nvls.mc) + kNvlsFlagOffset) : nullptr;
+    prm.nvls_ld_bytes = static_cast<long long>(L.a_agg.ld) * 2;
+}
+
+// WAR across devices before an NVLS operator: multicast stores and reductions
+// touch every rank's region, so each rank's launch follows every peer's
+// previous kernel (in-process peers on other GPUs: events; other processes:
+// their `done` stamp of the previous epoch).
+static int nvls_war(flux_comm* c, const std::vector<int>& mine, void* const* streams, uint32_t e) {
+    for (int r : mine) {
+        RankState& rs = c->ranks[r];
+        FLUX_CUDA(cudaSetDevice(rs.device));
+        cudaStream_t s = stream_for(c, r, streams);
+        for (int q = 0; q < c->tp; ++q) {
+            if (q == r) continue;
+            if (!c->ranks[q].local) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
+            else if (c->ranks[q].device != rs.device && c->ranks[q].kernel_evt_valid)
+                FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[q].kernel_evt, 0));
+        }
+    }
+    return FLUX_OK;
+}
+
 static int ag_gemm_ex_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
                            int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands);
 static int gemm_rs_ex_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int write_mode, int swizzle_on,
@@ -1662,6 +1978,46 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     const uint32_t e = ++c->epoch;
     const size_t rowbytes = static_cast<size_t>(L.a_agg.ld) * 2;
     const int lk = local_k(p);
+
+    // ---- NVLS: warp 3 of the GEMM pushes each rank's own comm tiles into every
+    // rank's a_agg with multicast stores and stamps their flags on every rank;
+    // the tiles wait on the flags (Alg. 2) ----
+    if (oc.o.nvls != FLUX_NVLS_OFF) {
+        FLUX_TRY(nvls_check(c, p, oc.o));
+        if (lk % 8 != 0) return fail(FLUX_ERR_CONFIG, "NVLS AllGather needs k % 8 == 0 (16-byte multicast stores)");
+        if (custom) return fail(FLUX_ERR_CONFIG, "NVLS pushes each rank's own rows to every rank at once; caller comm orders apply to the copy-engine and in-kernel transfers");
+        const int cg = choose_cg(p, oc.o);
+        std::vector<std::vector<uint32_t>> seq(tp);
+        for (int r : mine) {
+            const std::vector<int> blocks = ag_block_order(p, r, FLUX_PULL, true, pull_specs);
+            seq[r] = device_sequence(p->m, local_cols(p), rpr, swizzle_on ? blocks : std::vector<int>{}, kBM * cg,
+                                     group_blocks(rpr, kBM * cg, /*ag=*/true));
+        }
+        FLUX_TRY(nvls_war(c, mine, streams, e));
+        auto extra = [&](const std::vector<int>& g, GemmParams& prm) -> int {
+            nvls_fill(c, p, oc.o, prm);
+            prm.sm_transfer = 0;
+            prm.row_bytes = lk * 2;
+            for (size_t li = 0; li < g.size(); ++li) {
+                const flux_operands* ops = operands_of(c, oc, g[li]);
+                prm.ag_flags[li] = prm.nvls_flags[g[li]];
+                prm.shard_src[li] = ops && ops->a.ptr ? static_cast<const char*>(ops->a.ptr)
+                                                      : c->ranks[g[li]].heap + L.a_shard.off;
+                prm.src_ld_l[li] = static_cast<long long>(ops && ops->a.ptr ? ops->a.ld : L.a_shard.ld) * 2;
+            }
+            return FLUX_OK;
+        };
+        FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, kInterleaveRank, cg, false, -1, 0, extra));
+        if (c->ipc) {
+            for (int r : mine) {
+                FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
+                cudaStream_t s = stream_for(c, r, streams);
+                FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlDone, e));
+                FLUX_TRY(write_value(s, c->ranks[r].heap + kCtrlKdone, e));
+            }
+        }
+        return FLUX_OK;
+    }
 
     // ---- transfer engine: copy engines (Alg. 3 on a stream) or the GEMM's own
     // SMs (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies) ----
@@ -2113,6 +2469,17 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     c->kernel_events_used = 0;
     ++c->epoch;
     const int cg = choose_cg(p, oc.o);
+    // NVLS: sources keep their partials in their own region, owners read the
+    // sum over every source with multimem.ld_reduce (the owners' reduction
+    // units, or the streaming kernel's epilogue).
+    const bool nvls = oc.o.nvls != FLUX_NVLS_OFF;
+    if (nvls) {
+        FLUX_TRY(nvls_check(c, p, oc.o));
+        if (write_mode != FLUX_WRITE_ALLTOALL)
+            return fail(FLUX_ERR_CONFIG, "NVLS GEMM-RS reduces in the switch: use WriteAlltoAll (FusedReduce red.adds into the owner)");
+        if (oc.o.rs_partials != FLUX_F32) return fail(FLUX_ERR_CONFIG, "NVLS GEMM-RS carries fp32 partials");
+        FLUX_TRY(nvls_war(c, mine, streams, c->epoch));
+    }
     // FusedReduce (engine.cpp:304-319, arrival-order accumulation): sources red.add
     // into the owner's fp32 accumulator. Deterministic FusedReduce (rank-ordered
     // gate, :293-303) is served by the source-ordered owner sum, which gives the
@@ -2149,7 +2516,7 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     // Ownership blocks narrower than a device tile (decode-sized M): sources
     // stage whole tiles, owners sum their rows at the end of the kernel.
     const int tiles_n = (p->n + kBN - 1) / kBN;
-    oc.rs_units = (rpr % kBM != 0 && !oc.fused_reduce) ? 1 : 0;
+    oc.rs_units = ((rpr % kBM != 0 || nvls) && !oc.fused_reduce) ? 1 : 0;
     oc.ops = operands;
     if (oc.o.rs_partials != FLUX_F32 && oc.o.rs_partials != FLUX_BF16)
         return fail(FLUX_ERR_CONFIG, "rs_partials must be F32 or BF16");
@@ -2190,8 +2557,14 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     }
     const int interleave =
         oc.rs_units ? kInterleaveBlock : (aligned ? kInterleaveRankTail : kInterleaveStep);
+    std::function<int(const std::vector<int>&, GemmParams&)> extra = nullptr;
+    if (nvls)
+        extra = [&](const std::vector<int>&, GemmParams& prm) -> int {
+            nvls_fill(c, p, oc.o, prm);
+            return FLUX_OK;
+        };
     FLUX_TRY(launch_groups(c, p, oc.rs_units ? kModeRSUnits : kModeRS, oc, streams, seq, 0, interleave, cg,
-                           false, -1, oc.rs_units ? 0 : tail));
+                           false, -1, oc.rs_units ? 0 : tail, extra));
     return mark_op_done(c, streams, c->epoch);
 }
 

@@ -78,6 +78,11 @@ constexpr int kPieceBytes = 16384;      // one TMA bulk copy (global -> smem -> 
 constexpr size_t kRsFlagOffset = 256 * 1024;  // u32[tile][src]: partial of tile from src landed
 constexpr size_t kRsFlagCap = (512 * 1024) / 4;
 constexpr size_t kDataOffset = 1 << 20;
+// NVLS region (flux_comm_opts.nvls_bytes; one VMM allocation per rank bound to
+// one multicast object): AllGather comm-tile flags, then the data area (AG:
+// a_agg [m, k] bf16; RS: the source's partial planes, [parity][owner][rpr][n] fp32).
+constexpr size_t kNvlsFlagOffset = 0;
+constexpr size_t kNvlsDataOffset = 64 * 1024;  // kAgFlagCap u32 flags before it
 
 // Error codes written by device waits into the control block.
 constexpr uint32_t kErrAgFlagTimeout = 1;
@@ -120,6 +125,14 @@ struct GemmParams {
     int fused_reduce;              // RS: 1 = red.add into the owner accumulator (arrival order)
     // AG in-kernel transfer (warp 3 of every CTA pulls a_agg pieces with TMA bulk copies)
     int sm_transfer;
+    // NVLS (opts.nvls): 1 multicast through the NVSwitch (multimem.*), 2 the same
+    // protocol with unicast loops over every rank's region (tests on one GPU).
+    int nvls;
+    char* nvls_data[kMaxRanks];        // per GLOBAL rank: data area (unicast)
+    uint32_t* nvls_flags[kMaxRanks];   // per GLOBAL rank: AG comm-tile flags (unicast)
+    char* nvls_data_mc;                // nvls = 1: multicast address of the data area
+    uint32_t* nvls_flags_mc;           // nvls = 1: multicast address of the flags
+    long long nvls_ld_bytes;           // AG: row pitch of a_agg in the data area
     int ag_direct;                 // AG with tp = 1: A is read from the rank's own shard (the gathered A), no waits
     const uint32_t* jobs;          // (slot << 28) | (src rank << 24) | first row of the piece chunk
     int num_jobs;

@@ -276,6 +276,75 @@ __device__ __forceinline__ void st_part4(float* base, long long e, const float4&
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(base) + e) = w;
 }
 
+// ---- NVLS: multimem through the NVSwitch (opts.nvls) --------------------------------
+// nvls = 1: one access to the multicast address reaches every rank's copy (the
+// switch replicates stores and reduces loads); nvls = 2: the same protocol as
+// unicast loops over the ranks' regions (tests on one GPU). Regular accesses to
+// the same memory use the unicast addresses: fence.proxy.alias orders the two.
+__device__ __forceinline__ void nvls_st16(const GemmParams& p, long long off, const uint4& v) {
+    if (p.nvls == 1) {
+        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p.nvls_data_mc + off),
+                     "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
+    } else {
+#pragma unroll
+        for (int r = 0; r < kMaxRanks; ++r)
+            if (r < p.tp) *reinterpret_cast<uint4*>(p.nvls_data[r] + off) = v;
+    }
+}
+// AllGather comm-tile flag f stamped with the operator's epoch on every rank
+// (release, system scope: after the tile's rows, which every lane of the warp
+// stored before the caller's __syncwarp).
+__device__ __forceinline__ void nvls_flag_set(const GemmParams& p, int f) {
+    asm volatile("fence.proxy.alias;" ::: "memory");
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    if (p.nvls == 1) {
+        asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(p.nvls_flags_mc + f), "r"(p.epoch) : "memory");
+    } else {
+#pragma unroll
+        for (int r = 0; r < kMaxRanks; ++r)
+            if (r < p.tp) st_release_sys(p.nvls_flags[r] + f, p.epoch);
+    }
+}
+// Sum over every rank of the 4 fp32 at element offset e of the data areas (the
+// owner's rows of all sources' partials): reduced in the switch (nvls = 1), or
+// in rank order (nvls = 2).
+__device__ __forceinline__ float4 nvls_ld_reduce4(const GemmParams& p, long long e) {
+    float4 v;
+    if (p.nvls == 1) {
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "l"(reinterpret_cast<const float*>(p.nvls_data_mc) + e)
+                     : "memory");
+        return v;
+    }
+    float4 w[kMaxRanks];
+#pragma unroll
+    for (int r = 0; r < kMaxRanks; ++r)
+        if (r < p.tp) w[r] = ld_cg_f4(reinterpret_cast<const float*>(p.nvls_data[r]) + e);
+    v = w[0];
+#pragma unroll
+    for (int r = 1; r < kMaxRanks; ++r)
+        if (r < p.tp) {
+            v.x += w[r].x;
+            v.y += w[r].y;
+            v.z += w[r].z;
+            v.w += w[r].w;
+        }
+    return v;
+}
+// GEMM-RS partial of source `me` for owner o's rows: with NVLS the source keeps
+// it in its own region (plane o; the owner reduces over the sources through the
+// multicast address), else it goes to the owner's staging region (plane me).
+__device__ __forceinline__ float* rs_plane_base(const GemmParams& p, int o, int me, long long& plane_off) {
+    if (p.nvls) {
+        plane_off = static_cast<long long>(o) * p.stage_plane;
+        return reinterpret_cast<float*>(p.nvls_data[me]);
+    }
+    plane_off = static_cast<long long>(me) * p.stage_plane;
+    return p.staging[o];
+}
+
 // ---- bulk copies (in-kernel AllGather transfer) -----------------------------------
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -388,6 +457,7 @@ __device__ __forceinline__ bool fault_hit(const GemmParams& p, int rank, int ind
 // previous stamp of the same epoch is an error (SignalBoard::set returning
 // false, signal_board.hpp:25-28 / engine.cpp:401-403).
 __device__ void rs_flag_set(const GemmParams& p, int l, int o, int tile_id, int src) {
+    if (p.nvls) asm volatile("fence.proxy.alias;" ::: "memory");  // the partial (unicast) before the flag
     const int idx = tile_id * p.tp + src;
     uint32_t* f = p.rs_flags[o] + idx;
     const bool hit = fault_hit(p, o, idx);
@@ -639,6 +709,7 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
                 if (tid == 0) trace_event(p, l, kEvReduce, me, tm0, tn, static_cast<uint32_t>(me));
             }
             named_bar_sync(bar_id, nthr);  // flags acquired; everyone has read *slot
+            if (p.nvls) asm volatile("fence.proxy.alias;" ::: "memory");
         }
         for (int b = tid; b < npos; b += nthr * kU) {
             float4 v[kU][kMaxRanks];
@@ -648,9 +719,13 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
                 const int col = tn * TW + (pos % (TW / 4)) * 4;
                 if (pos < npos && col < n) {
                     const long long e = e0 + (pos / (TW / 4)) * ld_stage + col;
+                    if (p.nvls) {
+                        v[i][0] = nvls_ld_reduce4(p, e + me * stage_plane);  // every source, summed in the switch
+                    } else {
 #pragma unroll
-                    for (int s = 0; s < kMaxRanks; ++s)
-                        if (s < tp) v[i][s] = ld_part4<PB>(sbase, e + s * stage_plane);
+                        for (int s = 0; s < kMaxRanks; ++s)
+                            if (s < tp) v[i][s] = ld_part4<PB>(sbase, e + s * stage_plane);
+                    }
                 }
             }
 #pragma unroll
@@ -660,12 +735,16 @@ __device__ __noinline__ void owner_reduce(const GemmParams& p, int tid, int nthr
                 if (pos < npos && col < n) {
                     float acc[4];
                     bool first = true;
+                    if (p.nvls) {
+                        sum_into(acc, v[i][0], first);
+                    } else {
 #pragma unroll
-                    for (int s = 0; s < kMaxRanks; ++s)
-                        if (s < tp && s != me) sum_into(acc, v[i][s], first);
+                        for (int s = 0; s < kMaxRanks; ++s)
+                            if (s < tp && s != me) sum_into(acc, v[i][s], first);
 #pragma unroll
-                    for (int s = 0; s < kMaxRanks; ++s)
-                        if (s == me) sum_into(acc, v[i][s], first);
+                        for (int s = 0; s < kMaxRanks; ++s)
+                            if (s == me) sum_into(acc, v[i][s], first);
+                    }
                     const long long lr = r0 - me * rpr + pos / (TW / 4);
                     if (pass == 1) store_row<4>(cl, lr * ldc + col, col, n, out_f32, acc);
                 }
@@ -827,6 +906,53 @@ __device__ __forceinline__ void ag_transfer(const GemmParams& p, uint8_t* sComm,
         }
     }
     drain();
+}
+
+// NVLS AllGather push (warp 3, every lane): each local slot's own comm tiles
+// (rpct rows of its block, the reference's Push descriptors of that rank,
+// engine.cpp:406-419, with every peer as destination at once) go to every
+// rank's a_agg with one multicast store per 16 bytes, then the tile's flag is
+// stamped on every rank. The consumers wait on those flags exactly as for the
+// copy-engine transfer (Alg. 2). Peers finished reading their a_agg for the
+// previous operator before this launch (host stream waits).
+__device__ void ag_push_nvls(const GemmParams& p, int lane) {
+    int nl = 0;
+    while (nl < kMaxRanks && p.c[nl] != nullptr) ++nl;
+    const int tpr = p.rpr / p.rpct;  // comm tiles per rank block
+    const int n16 = p.row_bytes / 16;
+    const int total = p.rpct * n16;
+    constexpr int kU = 4;
+    for (int j = blockIdx.x; j < nl * tpr; j += gridDim.x) {
+        const int l = j / tpr, me = p.global_rank[l];
+        const int f = me * tpr + j % tpr;
+        const int row0 = f * p.rpct;
+        const char* src = p.shard_src[l] + static_cast<long long>(row0 - me * p.rpr) * p.src_ld_l[l];
+        const long long dst = static_cast<long long>(row0) * p.nvls_ld_bytes;
+        for (int c0 = lane; c0 < total; c0 += 32 * kU) {
+            uint4 v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int idx = c0 + u * 32;
+                if (idx < total)
+                    v[u] = __ldg(reinterpret_cast<const uint4*>(src + static_cast<long long>(idx / n16) * p.src_ld_l[l]) +
+                                 idx % n16);
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int idx = c0 + u * 32;
+                if (idx < total) nvls_st16(p, dst + static_cast<long long>(idx / n16) * p.nvls_ld_bytes + 16ll * (idx % n16), v[u]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const bool hit = fault_hit(p, me, f);
+            if (!(hit && p.fault_kind == kFaultDropSignal)) {
+                trace_event(p, l, kEvSignalSet, me, f, 0, static_cast<uint32_t>(f));
+                nvls_flag_set(p, f);
+            }
+        }
+        __syncwarp();
+    }
 }
 
 // Epilogue staging through shared memory. Warp q owns a 32-row x 32-column
@@ -1155,7 +1281,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         owner_reduce<PB, TWU>(p, threadIdx.x - 64, 64, 3, &red_slot[0], false);
     } else if (warp == 3) {
         // ===== in-kernel AllGather transfer (Alg. 3 on the SMs) =====
-        if (MODE == kModeAG && p.sm_transfer && lane == 0) ag_transfer(p, sComm, cbar);
+        if (MODE == kModeAG && p.nvls) ag_push_nvls(p, lane);
+        else if (MODE == kModeAG && p.sm_transfer && lane == 0) ag_transfer(p, sComm, cbar);
     } else if (warp >= 4) {
         // ===== epilogue: each CTA drains its own 128 TMEM lanes (rows) =====
         const int q = warp - 4;            // TMEM lane quadrant (warp % 4)
@@ -1375,15 +1502,17 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
 #pragma unroll
                             for (int j = 0; j < 32; ++j) v[j] += __ldcg(src + x * slot_stride + (c * 32 + j) * kBM);
                         }
-                        const long long e = parity * p.stage_parity + me * p.stage_plane +
+                        long long pl;
+                        float* const dst = rs_plane_base(p, o, me, pl);
+                        const long long e = parity * p.stage_parity + pl +
                                             (row - static_cast<long long>(o) * rpr) * ld_stage + colc;
                         if (colc + 32 <= p.n) {
 #pragma unroll
                             for (int j = 0; j < 32; j += 4)
-                                st_part4<PB>(p.staging[o], e + j, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                                st_part4<PB>(dst, e + j, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
                         } else {
                             for (int j = 0; j < 32 && colc + j < p.n; j += 4)  // ld_stage pads to 256 columns
-                                st_part4<PB>(p.staging[o], e + j, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+                                st_part4<PB>(dst, e + j, make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
                         }
                     }
                     // Every slice's stores precede its arrival; the last arrival
@@ -1412,11 +1541,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     if (row0 + q * 32 + 32 > p.m || (p.dbg & 64)) {  // dbg 64: ablation, always direct
                         if (valid) {
                             const int o = row / rpr;
-                            const long long e = parity * p.stage_parity + me * p.stage_plane +
+                            long long pl;
+                            float* const dst = rs_plane_base(p, o, me, pl);
+                            const long long e = parity * p.stage_parity + pl +
                                                 (row - static_cast<long long>(o) * rpr) * ld_stage + colc;
 #pragma unroll
                             for (int j = 0; j < 32; j += 4)
-                                st_part4<PB>(p.staging[o], e + j,
+                                st_part4<PB>(dst, e + j,
                                              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
                                                          __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
                         }
@@ -1430,9 +1561,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         const int grow = row0 + q * 32 + i;
                         if (grow >= p.m || col >= p.n) continue;
                         const int o = grow / rpr;
-                        st_part4<PB>(p.staging[o],
-                                     parity * p.stage_parity + me * p.stage_plane +
-                                         (grow - static_cast<long long>(o) * rpr) * ld_stage + col,
+                        long long pl;
+                        float* const dst = rs_plane_base(p, o, me, pl);
+                        st_part4<PB>(dst, parity * p.stage_parity + pl + (grow - static_cast<long long>(o) * rpr) * ld_stage + col,
                                      epi_read(wbuf, i, g));
                     }
                 }
@@ -1795,15 +1926,17 @@ __device__ __forceinline__ void sk_store(const GemmParams& p, int l, int col, in
     if (col >= p.n) return;
     if (MODE == kModeRSUnits) {
         const int me = p.global_rank[l], rpr = p.rpr;
-        const long long base = static_cast<long long>(p.epoch & 1u) * p.stage_parity + me * p.stage_plane + col;
+        const long long base = static_cast<long long>(p.epoch & 1u) * p.stage_parity + col;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             const int m = m0 + i;
             if (m >= mv) break;
             const int o = m / rpr;
-            const long long e = base + static_cast<long long>(m - o * rpr) * p.ld_stage;
-            if (PB) reinterpret_cast<__nv_bfloat16*>(p.staging[o])[e] = __float2bfloat16_rn(v[i]);
-            else p.staging[o][e] = v[i];
+            long long pl;
+            float* const dst = rs_plane_base(p, o, me, pl);
+            const long long e = base + pl + static_cast<long long>(m - o * rpr) * p.ld_stage;
+            if (PB) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(v[i]);
+            else dst[e] = v[i];
         }
     } else {
         const long long ldc = p.ldc_l[l];
@@ -1955,7 +2088,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
             }
         }
     } else if (warp == 3) {
-        if (MODE == kModeAG && p.sm_transfer && lane == 0) ag_transfer(p, sComm, cbar);
+        if (MODE == kModeAG && p.nvls) ag_push_nvls(p, lane);
+        else if (MODE == kModeAG && p.sm_transfer && lane == 0) ag_transfer(p, sComm, cbar);
     } else if (warp >= 4) {
         // ===== epilogue: warp q holds weight rows (output columns) 32q..32q+31 of the n-tile =====
         // Whole n-tiles are stored straight from TMEM. A tile cut between CTAs
@@ -2045,10 +2179,11 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                             if (c2 >= p.n) continue;
                             if (MODE == kModeRSUnits) {
                                 const int o = m / p.rpr;
-                                const long long se = static_cast<long long>(p.epoch & 1u) * p.stage_parity +
-                                                     p.global_rank[l] * p.stage_plane +
+                                long long pl;
+                                float* const dst = rs_plane_base(p, o, p.global_rank[l], pl);
+                                const long long se = static_cast<long long>(p.epoch & 1u) * p.stage_parity + pl +
                                                      static_cast<long long>(m - o * p.rpr) * p.ld_stage + c2;
-                                st_part4<PB>(p.staging[o], se, make_float4(v[0], v[1], v[2], v[3]));
+                                st_part4<PB>(dst, se, make_float4(v[0], v[1], v[2], v[3]));
                             } else {
                                 if (ACT) {
 #pragma unroll
@@ -2069,6 +2204,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                 // ascending, then this rank) into C. Every CTA publishes a tile
                 // before it waits on that tile, and CTAs walk their tiles in order,
                 // so the waits cannot form a cycle.
+                if (p.nvls) asm volatile("fence.proxy.alias;" ::: "memory");  // own rows: unicast stores, multicast reads
                 named_bar_sync(1, 128);
                 const int me = p.global_rank[l], tp = p.tp, rpr = p.rpr;
                 if (et == 0) trace_event(p, l, kEvTileWrite, me, 0, j, 0u);
@@ -2081,15 +2217,25 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                 const float* const sbase = p.staging[me];
                 const long long e0 = static_cast<long long>(p.epoch & 1u) * p.stage_parity;
                 const int F = min(rpr, mv - me * rpr) * (kSkRows / 4);  // float4 groups of my rows
+                // (One group per thread at a time: this code runs once per launch on a
+                // cold instruction cache, where a batched, longer body measured slower.)
                 for (int f = et; f < F; f += 128) {
                     const int lr = f / (kSkRows / 4), c2 = j * kSkRows + (f % (kSkRows / 4)) * 4;
                     if (c2 >= p.n) continue;
                     const long long e = e0 + static_cast<long long>(lr) * p.ld_stage + c2;
+                    float acc[4];
+                    if (p.nvls) {
+                        asm volatile("fence.proxy.alias;" ::: "memory");
+                        const float4 r4 = nvls_ld_reduce4(p, e + me * p.stage_plane);
+                        acc[0] = r4.x;
+                        acc[1] = r4.y;
+                        acc[2] = r4.z;
+                        acc[3] = r4.w;
+                    } else {
                     float4 w[kMaxRanks];
 #pragma unroll
                     for (int s2 = 0; s2 < kMaxRanks; ++s2)
                         if (s2 < tp) w[s2] = ld_part4<PB>(sbase, e + s2 * p.stage_plane);
-                    float acc[4];
                     bool first = true;
 #pragma unroll
                     for (int s2 = 0; s2 < kMaxRanks; ++s2)
@@ -2097,6 +2243,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
 #pragma unroll
                     for (int s2 = 0; s2 < kMaxRanks; ++s2)
                         if (s2 == me) sum_into(acc, w[s2], first);
+                    }
                     store_row<4>(p.c[l], static_cast<long long>(lr) * p.ldc_l[l] + c2, c2, p.n, p.out_f32, acc);
                 }
             }

@@ -41,13 +41,14 @@ def test_library_is_sm100a_and_uses_tcgen05():
     assert "UTCHMMA" in out  # tcgen05.mma
     assert "UTMALDG" in out  # TMA loads
     assert "LDTM" in out     # tcgen05.ld (TMEM -> registers)
+    assert "LDGMC" in out    # multimem.ld_reduce (NVLS owner-side reduction in the switch)
     elf = subprocess.run(["cuobjdump", "-lelf", N.LIB_PATH], capture_output=True, text=True, check=True).stdout
     assert "sm_100a" in elf
 
 
 def test_abi_version_and_defaults():
     lib = N.lib()
-    assert lib.flux_abi_version() == N.ABI_VERSION == 7
+    assert lib.flux_abi_version() == N.ABI_VERSION == 8
     o = N.default_opts()
     assert o.activation == N.ACT_NONE and o.activation_grad == N.ACT_NONE and o.rs_partials == N.F32 and o.b_layout == N.B_NK
     assert o.graph_safe == 0
