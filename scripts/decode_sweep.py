@@ -23,9 +23,16 @@ args = ap.parse_args()
 torch.cuda.set_stream(torch.cuda.Stream())
 st = torch.cuda.current_stream().cuda_stream
 HBM = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
-shapes = {"ag-up": (0, 28672, 8192), "rs-down": (1, 8192, 28672), "rs-attn-out": (1, 8192, 8192)}
+# TP=8 emulated on one GPU (every rank's work in one launch), and one GPU's
+# share at TP=8 (tp=1 problems with the per-rank shapes: what one GPU streams).
+shapes = {"ag-up": (0, 28672, 8192, 8), "rs-down": (1, 8192, 28672, 8), "rs-attn-out": (1, 8192, 8192, 8),
+          "rank-ag-up": (0, 3584, 8192, 1), "rank-rs-down": (1, 8192, 3584, 1), "rank-rs-attn-out": (1, 8192, 1024, 1)}
+ap2 = [x for x in os.environ.get("SWEEP_SHAPES", "").split(",") if x]
+if ap2:
+    shapes = {k: v for k, v in shapes.items() if k in ap2}
 rows = []
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush_rd = torch.ones(64 << 20, dtype=torch.int32, device="cuda")  # read sweep: no dirty lines left in L2
 
 
 def timed(fn):
@@ -36,14 +43,14 @@ def timed(fn):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(args.iters):
         flush.zero_()
+        flush_rd.max()
         e0.record(); fn(); e1.record(); e1.synchronize()
         tot += e0.elapsed_time(e1)
     return tot / args.iters
 
 
-for name, (pat, n, k) in shapes.items():
+for name, (pat, n, k, tp) in shapes.items():
     for m in [int(x) for x in args.ms.split(",")]:
-        tp = 8
         p = fx.ProblemSpec(m, n, k, tp, pat)
         comm = fx.Communicator(tp, [0] * tp, heap_bytes=fx.required_heap_bytes(p) + (16 << 20))
         for r in range(tp):
