@@ -289,31 +289,42 @@ def gpu_measure(comm: Communicator, problem: ProblemSpec, repetitions: int, stre
 
 
 def gpu_verify(comm: Communicator, problem: ProblemSpec, rows: int = 64, tol: float = 8e-3, streams=None):
-    """Correctness gate: each rank's bf16 output on `rows` sampled rows against
-    fp32 cuBLAS products of the same bf16 operands (max |d| / max(1, |ref|))."""
+    """Correctness gate (the reference's verify_config, tune.cpp:129-149): each
+    rank's bf16 output on `rows` sampled rows against the fp64 product of the
+    same bf16 operands (the oracle's definition: k-ascending fp64 GEMM, RS
+    partials summed in rank order), with the reference metric max|a-b| /
+    max(1, |a|, |b|) (matrix.cpp:11-25) and the stated bf16 tolerance."""
     import torch
 
     tp = problem.tp
-    a = [comm.tensor(r, N.BUF_A_SHARD, problem).float() for r in range(tp)]
-    b = [comm.tensor(r, N.BUF_B_SHARD, problem).float() for r in range(tp)]
+    a = [comm.tensor(r, N.BUF_A_SHARD, problem).double() for r in range(tp)]
+    b = [comm.tensor(r, N.BUF_B_SHARD, problem).double() for r in range(tp)]
+    dev = a[0].device
     m_out = problem.m if problem.pattern == N.ALLGATHER_GEMM else problem.rows_per_rank()
-    idx = torch.linspace(0, m_out - 1, steps=min(rows, m_out), device="cuda").round().long().unique()
+    idx = torch.linspace(0, m_out - 1, steps=min(rows, m_out), device=dev).round().long().unique()
     if problem.pattern == N.ALLGATHER_GEMM:
-        gathered = torch.cat(a)[idx]
-        refs = [gathered @ b[r].t() for r in range(tp)]
+        gathered = torch.cat([x.to(dev) for x in a])[idx]
+        refs = [gathered.to(b[r].device) @ b[r].t() for r in range(tp)]
     else:
         rpr = problem.rows_per_rank()
         refs = []
         for r in range(tp):
             rows_g = idx + r * rpr
-            refs.append(sum(a[s][rows_g] @ b[s].t() for s in range(tp)))
+            acc = None
+            for s in range(tp):  # rank order, like the oracle's reduce (oracle.cpp:49-53)
+                part = (a[s][rows_g.to(a[s].device)] @ b[s].t()).to(dev)
+                acc = part if acc is None else acc + part
+            refs.append(acc)
 
     def verify(cfg: TuneConfig) -> None:
         run_config(comm, problem, cfg, streams)
         comm.sync()
         for r in range(tp):
-            got = comm.tensor(r, N.BUF_C_OUT, problem).float()[idx]
-            err = ((got - refs[r]).abs().max() / refs[r].abs().max().clamp(min=1.0)).item()
+            got = comm.tensor(r, N.BUF_C_OUT, problem).double()
+            ref = refs[r].to(got.device)
+            got = got[idx.to(got.device)]
+            den = torch.maximum(torch.maximum(got.abs(), ref.abs()), torch.ones_like(ref))
+            err = ((got - ref).abs() / den).max().item()
             if not err <= tol:
                 raise AssertionError(f"rank {r}: max rel err {err:.3e} > {tol}")
 
