@@ -1223,7 +1223,37 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             prm.sk_acc_cols = 16;
             while (prm.sk_acc_cols < sk_mp) prm.sk_acc_cols *= 2;
             const int stage_bytes = stream_smem_bytes(mode, sk_mp, 1) - stream_smem_bytes(mode, sk_mp, 0);
-            prm.sk_stages = std::min(kSkMaxStages, (kSkSmemMax - stream_smem_bytes(mode, sk_mp, 0)) / stage_bytes);
+            prm.sk_cluster = 1;
+            // Cluster split-K: with at most half as many n-tiles as SMs, clusters of
+            // c CTAs (c = 8, 4, 2; every CTA >= 2 k-blocks) split each tile's K and
+            // meet in the leader's shared memory (no global fixup round trip). Every
+            // cluster must be resident at once (cross-cluster waits: AllGather pieces,
+            // RS flags), checked with the occupancy API. FLUX_SK_CLUSTER=c forces c
+            // (1 = off) for A/B runs.
+            {
+                const char* envc = std::getenv("FLUX_SK_CLUSTER");
+                const int forced = envc ? std::atoi(envc) : 0;
+                const bool full_grid = mode == kModeAG && (prm.sm_transfer || prm.nvls);
+                for (int cl : {8, 4, 2}) {
+                    if (forced > 0 && cl != forced) continue;
+                    if (tiles_all * cl > sms || kbn < 2 * cl) continue;
+                    const int st = std::min(kSkMaxStages, (kSkSmemMax - stream_smem_bytes(mode, sk_mp, 0, cl)) / stage_bytes);
+                    if (st < 4) continue;
+                    GemmParams q = prm;
+                    q.sk_cluster = cl;
+                    q.sk_stages = st;
+                    const int maxc = stream_max_clusters(mode, q, cl, stream_smem_bytes(mode, sk_mp, st, cl));
+                    const int launched = full_grid ? std::min(sms / cl, maxc) : static_cast<int>(tiles_all);
+                    if (maxc < launched || launched < tiles_all) continue;
+                    if (forced == 0 && tiles_all * 2 > sms) continue;  // auto: only when tiles <= SMs / 2
+                    prm.sk_cluster = cl;
+                    prm.sk_ctas = static_cast<int>(tiles_all) * cl;
+                    prm.sk_stages = st;
+                    break;
+                }
+            }
+            if (prm.sk_cluster == 1)
+                prm.sk_stages = std::min(kSkMaxStages, (kSkSmemMax - stream_smem_bytes(mode, sk_mp, 0)) / stage_bytes);
             // AG: weight stages streamed before the gathered rows land. A few hide the
             // transfer; a full ring of them queues the transfer's own loads behind the
             // weight stream (one GPU's decode AG: rows landed 9 us in with 10 stages).
@@ -1234,9 +1264,13 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             prm.tail_ws = reinterpret_cast<float*>(lead_rank.heap + L.tail_ws_off);
             prm.sk_ctr = at<uint32_t>(lead_rank, kSkCtrOffset);
             prm.tail_splits = 0;
-            // The in-kernel AllGather runs on every SM.
-            const int sgrid = (mode == kModeAG && (prm.sm_transfer || prm.nvls)) ? sms : prm.sk_ctas;
-            FLUX_CUDA(launch_stream(mode, prm, sgrid, stream_smem_bytes(mode, sk_mp, prm.sk_stages), lead));
+            // The in-kernel AllGather runs on every SM (whole clusters, all resident).
+            int sgrid = (mode == kModeAG && (prm.sm_transfer || prm.nvls)) ? sms : prm.sk_ctas;
+            if (prm.sk_cluster > 1 && sgrid != prm.sk_ctas) {
+                const int smem_c = stream_smem_bytes(mode, sk_mp, prm.sk_stages, prm.sk_cluster);
+                sgrid = std::min(sms / prm.sk_cluster, stream_max_clusters(mode, prm, prm.sk_cluster, smem_c)) * prm.sk_cluster;
+            }
+            FLUX_CUDA(launch_stream(mode, prm, sgrid, stream_smem_bytes(mode, sk_mp, prm.sk_stages, prm.sk_cluster), lead));
         } else {
             FLUX_CUDA(launch_gemm(mode, cg, prm, grid, lead));
         }

@@ -209,6 +209,8 @@ struct GemmParams {
     long long sk_work;             // slots x n-tiles x k-blocks
     int sk_ctas;                   // CTAs with GEMM work (<= grid)
     int sk_acc_cols;               // TMEM columns per accumulator (two accumulators)
+    int sk_cluster;                // > 1: clusters of this many CTAs split each n-tile's K; the
+                                   // partial accumulators meet in the leader's shared memory (DSMEM)
     uint32_t* sk_ctr;              // per (slot, n-tile): (tail_seq << 8) | arrivals
 };
 
@@ -227,7 +229,8 @@ int gemm_tile_rows(int cg);
 cudaError_t launch_rs_reduce(const RsReduceParams& p, int grid, cudaStream_t stream);
 // Streaming decode kernel (modes Plain, AG, RSUnits); smem from stream_smem_bytes.
 cudaError_t launch_stream(int mode, const GemmParams& p, int grid, int smem, cudaStream_t stream);
-int stream_smem_bytes(int mode, int mp, int stages);
+int stream_smem_bytes(int mode, int mp, int stages, int cluster = 1);
+int stream_max_clusters(int mode, const GemmParams& p, int cluster, int smem);
 
 // Graph-safe operators: zero byte ranges (4-byte multiples) of several heaps,
 // one CTA per heap.

@@ -1901,7 +1901,16 @@ __device__ __forceinline__ int sk_cta_of(const GemmParams& p, long long x) {
 struct SkIter {
     long long cur, end;
     int kb;
+    int cl = 1, c = 0, t = 0, nq = 0, ntiles = 0;  // cluster split-K: tiles t, t + nq, ...; K-segment c of cl
     __device__ bool next(int& tt, int& kb0, int& kb1) {
+        if (cl > 1) {
+            if (t >= ntiles) return false;
+            tt = t;
+            kb0 = c * kb / cl;
+            kb1 = (c + 1) * kb / cl;
+            t += nq;
+            return true;
+        }
         if (cur >= end) return false;
         tt = static_cast<int>(cur / kb);
         kb0 = static_cast<int>(cur % kb);
@@ -1910,6 +1919,22 @@ struct SkIter {
         return true;
     }
 };
+__device__ __forceinline__ SkIter sk_iter(const GemmParams& p, long long r0, long long r1) {
+    SkIter it{r0, r1, p.sk_kb};
+    if (p.sk_cluster > 1) {
+        it.cl = p.sk_cluster;
+        it.c = static_cast<int>(blockIdx.x) % it.cl;
+        it.t = static_cast<int>(blockIdx.x) / it.cl;
+        it.nq = p.sk_ctas / it.cl;
+        it.ntiles = static_cast<int>(p.sk_work / p.sk_kb);
+    }
+    return it;
+}
+__device__ __forceinline__ void st_shared_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
 // Slot of the segment of tile tt held by CTA c: 2c when the tile holds the
 // CTA's first unit, else 2c + 1 (the CTA's last segment). Indexes the fp32
 // partials parked in tail_ws; sk_ctr[tt] counts the tile's parked segments
@@ -1951,6 +1976,59 @@ __device__ __forceinline__ void sk_store(const GemmParams& p, int l, int col, in
     }
 }
 
+// GEMM-RS in the streaming kernel, once n-tile j of slot l is complete in this
+// CTA and its partial rows are in every owner's plane (this rank's own rows
+// included): stamp the peers' flags, then finish this rank's own rows here —
+// wait for the other sources' partials of the tile and sum the planes in the
+// canonical order (other sources ascending, then this rank) into C. Every CTA
+// publishes a tile before it waits on that tile, and CTAs walk their tiles in
+// order, so the waits cannot form a cycle. Epilogue warps (128 threads).
+template <int PB>
+__device__ __forceinline__ void sk_rs_finish(const GemmParams& p, int l, int j, int mv, int et) {
+    if (p.nvls) asm volatile("fence.proxy.alias;" ::: "memory");  // own rows: unicast stores, multicast reads
+    named_bar_sync(1, 128);
+    const int me = p.global_rank[l], tp = p.tp, rpr = p.rpr;
+    if (et == 0) trace_event(p, l, kEvTileWrite, me, 0, j, 0u);
+    if (et < tp && et != me) rs_flag_set(p, l, et, j, me);
+    if (et < tp && et != me)
+        wait_flag(p.rs_flags[me] + j * tp + et, p.epoch, p, l, kErrRsFlagTimeout,
+                  static_cast<uint32_t>(j), static_cast<uint32_t>(et));
+    named_bar_sync(1, 128);
+    if (et == 0) trace_event(p, l, kEvReduce, me, 0, j, static_cast<uint32_t>(me));
+    const float* const sbase = p.staging[me];
+    const long long e0 = static_cast<long long>(p.epoch & 1u) * p.stage_parity;
+    const int F = min(rpr, mv - me * rpr) * (kSkRows / 4);  // float4 groups of my rows
+    // (One group per thread at a time: this code runs once per launch on a
+    // cold instruction cache, where a batched, longer body measured slower.)
+    for (int f = et; f < F; f += 128) {
+        const int lr = f / (kSkRows / 4), c2 = j * kSkRows + (f % (kSkRows / 4)) * 4;
+        if (c2 >= p.n) continue;
+        const long long e = e0 + static_cast<long long>(lr) * p.ld_stage + c2;
+        float acc[4];
+        if (p.nvls) {
+            asm volatile("fence.proxy.alias;" ::: "memory");
+            const float4 r4 = nvls_ld_reduce4(p, e + me * p.stage_plane);
+            acc[0] = r4.x;
+            acc[1] = r4.y;
+            acc[2] = r4.z;
+            acc[3] = r4.w;
+        } else {
+            float4 w[kMaxRanks];
+#pragma unroll
+            for (int s2 = 0; s2 < kMaxRanks; ++s2)
+                if (s2 < tp) w[s2] = ld_part4<PB>(sbase, e + s2 * p.stage_plane);
+            bool first = true;
+#pragma unroll
+            for (int s2 = 0; s2 < kMaxRanks; ++s2)
+                if (s2 < tp && s2 != me) sum_into(acc, w[s2], first);
+#pragma unroll
+            for (int s2 = 0; s2 < kMaxRanks; ++s2)
+                if (s2 == me) sum_into(acc, w[s2], first);
+        }
+        store_row<4>(p.c[l], static_cast<long long>(lr) * p.ldc_l[l] + c2, c2, p.n, p.out_f32, acc);
+    }
+}
+
 template <int MODE, int PB = 0, int ACT = 0>
 __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_constant__ GemmParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -1960,14 +2038,20 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
     uint8_t* sW = smem;
     uint8_t* sT = sW + ns * kSkWBytes;
     uint8_t* sComm = sT + ns * tbytes;  // AG: 2 x kPieceBytes
-    uint64_t* full = reinterpret_cast<uint64_t*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0));
+    // Cluster split-K: the leader's reduction buffer, one [128 columns][mp + 4]
+    // fp32 slot per non-leader segment (padded rows: conflict-free v4 stores).
+    const int cl = p.sk_cluster, ldr = mp + 4;
+    float* sRed = reinterpret_cast<float*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0));
+    const int red_bytes = cl > 1 ? (cl - 1) * kSkRows * ldr * 4 : 0;
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sRed) + red_bytes);
     uint64_t* empty = full + kSkMaxStages;
     uint64_t* tfull = empty + kSkMaxStages;
     uint64_t* tempty = tfull + 2;
     uint64_t* cbar = tempty + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cbar + 2);
     int* red_slot = reinterpret_cast<int*>(tmem_slot + 2);
-    static_assert((2 * kSkMaxStages + 6) * 8 + 8 + 16 <= kSkBarBytes, "barrier region");  // red_slot[0..3]
+    uint64_t* red_bar = reinterpret_cast<uint64_t*>(red_slot + 4);  // [0] leader: segments in, [1] buffer free
+    static_assert((2 * kSkMaxStages + 6) * 8 + 8 + 16 + 16 <= kSkBarBytes, "barrier region");  // red_slot[0..3], red_bar[0..1]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tmem_cols = 2u * static_cast<uint32_t>(p.sk_acc_cols);
@@ -1989,11 +2073,16 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
             mbar_init(&tempty[a], 4);
             mbar_init(&cbar[a], 1);
         }
+        if (cl > 1) {
+            mbar_init(&red_bar[0], (cl - 1) * 128);
+            mbar_init(&red_bar[1], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) tmem_alloc(tmem_slot, tmem_cols);
     tc_fence_before();
     __syncthreads();
+    if (cl > 1) cluster_sync();  // every CTA's barriers initialised before remote arrivals
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const bool has_work = static_cast<int>(blockIdx.x) < p.sk_ctas;
@@ -2029,7 +2118,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                 }
                 np = 0;
             };
-            SkIter it{r0, r1, kbn};
+            SkIter it = sk_iter(p, r0, r1);
             int tt, kb0, kb1;
             while (it.next(tt, kb0, kb1)) {
                 const int l = tt / p.sk_nt, j = tt % p.sk_nt;
@@ -2060,7 +2149,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
             const uint32_t idesc = make_idesc(kSkRows, mp);
             int stage = 0, as = 0;
             uint32_t phase = 0, aphase = 0;
-            SkIter it{r0, r1, kbn};
+            SkIter it = sk_iter(p, r0, r1);
             int tt, kb0, kb1;
             while (it.next(tt, kb0, kb1)) {
                 mbar_wait(&tempty[as], aphase ^ 1u);
@@ -2102,8 +2191,78 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
         const int mv = min(p.m, mp);    // valid token rows
         int as = 0;
         uint32_t aphase = 0;
-        SkIter it{r0, r1, kbn};
         int tt, kb0, kb1;
+        if (cl > 1) {
+            // Cluster split-K: CTA c of the cluster holds K-segment c of the tile;
+            // the non-leaders put their fp32 accumulators into the leader's shared
+            // memory (st.shared::cluster), the leader adds them to its own in
+            // segment order and stores the tile. No global round trip, nothing
+            // waits outside the cluster.
+            const uint32_t crank = cluster_ctarank();
+            uint32_t fphase = 0, ephase = 0;
+            SkIter cit_it = sk_iter(p, r0, r1);
+            while (cit_it.next(tt, kb0, kb1)) {
+                const int l = tt / p.sk_nt, j = tt % p.sk_nt;
+                const int col = j * kSkRows + cit;
+                mbar_wait(&tfull[as], aphase);
+                tc_fence_after();
+                const uint32_t tbase =
+                    tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(as * p.sk_acc_cols);
+                if (crank != 0) {
+                    mbar_wait(&red_bar[1], ephase ^ 1u);  // the leader has read this slot's previous tile
+                    ephase ^= 1u;
+                    const uint32_t dst = mapa(smem_u32(sRed + ((crank - 1) * kSkRows + cit) * ldr), 0);
+                    for (int m0 = 0; m0 < mv; m0 += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(tbase + m0, r);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            st_shared_cluster_v4(dst + static_cast<uint32_t>(m0 + i) * 4u, r[i], r[i + 1], r[i + 2], r[i + 3]);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[as]);
+                    mbar_arrive_cluster(mapa(smem_u32(&red_bar[0]), 0));  // release: this thread's stores
+                } else {
+                    mbar_wait_acq_cluster(&red_bar[0], fphase);
+                    fphase ^= 1u;
+                    for (int m0 = 0; m0 < mv; m0 += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(tbase + m0, r);
+                        tmem_ld_wait();
+                        float v[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+                        for (int s2 = 1; s2 < cl; ++s2) {
+                            const float4* src = reinterpret_cast<const float4*>(sRed + ((s2 - 1) * kSkRows + cit) * ldr + m0);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float4 w = src[i];
+                                v[4 * i] += w.x;
+                                v[4 * i + 1] += w.y;
+                                v[4 * i + 2] += w.z;
+                                v[4 * i + 3] += w.w;
+                            }
+                        }
+                        sk_store<MODE, PB, ACT>(p, l, col, m0, mv, v);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[as]);
+                    named_bar_sync(1, 128);  // every leader thread has read the slots
+                    if (et >= 1 && et < cl) mbar_arrive_cluster(mapa(smem_u32(&red_bar[1]), static_cast<uint32_t>(et)));
+                    if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 5, static_cast<uint32_t>(tt));
+                    if (MODE == kModeRSUnits) sk_rs_finish<PB>(p, l, j, mv, et);
+                }
+                if (++as == 2) {
+                    as = 0;
+                    aphase ^= 1u;
+                }
+            }
+        }
+        SkIter it{r0, r1, kbn};
+        if (cl > 1) it.end = it.cur;  // (the cluster path above did the work)
         while (it.next(tt, kb0, kb1)) {
             const int l = tt / p.sk_nt, j = tt % p.sk_nt;
             const int col = j * kSkRows + cit;
@@ -2196,62 +2355,13 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                     if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 5, static_cast<uint32_t>(tt));
                 }
             }
-            if (done && MODE == kModeRSUnits) {
-                // The tile's partial is in every owner's staging plane (this rank's
-                // own rows included): stamp the peers' flags, then finish this rank's
-                // own rows here — wait for the other sources' partials of the tile
-                // and sum the planes in the canonical order (other sources
-                // ascending, then this rank) into C. Every CTA publishes a tile
-                // before it waits on that tile, and CTAs walk their tiles in order,
-                // so the waits cannot form a cycle.
-                if (p.nvls) asm volatile("fence.proxy.alias;" ::: "memory");  // own rows: unicast stores, multicast reads
-                named_bar_sync(1, 128);
-                const int me = p.global_rank[l], tp = p.tp, rpr = p.rpr;
-                if (et == 0) trace_event(p, l, kEvTileWrite, me, 0, j, 0u);
-                if (et < tp && et != me) rs_flag_set(p, l, et, j, me);
-                if (et < tp && et != me)
-                    wait_flag(p.rs_flags[me] + j * tp + et, p.epoch, p, l, kErrRsFlagTimeout,
-                              static_cast<uint32_t>(j), static_cast<uint32_t>(et));
-                named_bar_sync(1, 128);
-                if (et == 0) trace_event(p, l, kEvReduce, me, 0, j, static_cast<uint32_t>(me));
-                const float* const sbase = p.staging[me];
-                const long long e0 = static_cast<long long>(p.epoch & 1u) * p.stage_parity;
-                const int F = min(rpr, mv - me * rpr) * (kSkRows / 4);  // float4 groups of my rows
-                // (One group per thread at a time: this code runs once per launch on a
-                // cold instruction cache, where a batched, longer body measured slower.)
-                for (int f = et; f < F; f += 128) {
-                    const int lr = f / (kSkRows / 4), c2 = j * kSkRows + (f % (kSkRows / 4)) * 4;
-                    if (c2 >= p.n) continue;
-                    const long long e = e0 + static_cast<long long>(lr) * p.ld_stage + c2;
-                    float acc[4];
-                    if (p.nvls) {
-                        asm volatile("fence.proxy.alias;" ::: "memory");
-                        const float4 r4 = nvls_ld_reduce4(p, e + me * p.stage_plane);
-                        acc[0] = r4.x;
-                        acc[1] = r4.y;
-                        acc[2] = r4.z;
-                        acc[3] = r4.w;
-                    } else {
-                    float4 w[kMaxRanks];
-#pragma unroll
-                    for (int s2 = 0; s2 < kMaxRanks; ++s2)
-                        if (s2 < tp) w[s2] = ld_part4<PB>(sbase, e + s2 * p.stage_plane);
-                    bool first = true;
-#pragma unroll
-                    for (int s2 = 0; s2 < kMaxRanks; ++s2)
-                        if (s2 < tp && s2 != me) sum_into(acc, w[s2], first);
-#pragma unroll
-                    for (int s2 = 0; s2 < kMaxRanks; ++s2)
-                        if (s2 == me) sum_into(acc, w[s2], first);
-                    }
-                    store_row<4>(p.c[l], static_cast<long long>(lr) * p.ldc_l[l] + c2, c2, p.n, p.out_f32, acc);
-                }
-            }
+            if (done && MODE == kModeRSUnits) sk_rs_finish<PB>(p, l, j, mv, et);
         }
         if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 7, 0);  // epilogue done (profiling)
     }
     if (threadIdx.x % 32 == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 24 + warp, 0);  // warp at the exit barrier (profiling)
     __syncthreads();
+    if (cl > 1) cluster_sync();  // no CTA exits while a peer may still arrive on its barriers
     if (warp == 0 && lane == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 1, 0);
     if (warp == 2) {
         tc_fence_after();
@@ -2327,12 +2437,14 @@ static cudaError_t launch_one(const GemmParams& p, int grid, cudaStream_t stream
     return cudaLaunchKernelEx(&cfg, fn, p);
 }
 
-int stream_smem_bytes(int mode, int mp, int stages) {
-    return 1024 + stages * (kSkWBytes + mp * kBK * 2) + (mode == kModeAG ? 2 * kPieceBytes : 0) + kSkBarBytes;
+int stream_smem_bytes(int mode, int mp, int stages, int cluster) {
+    return 1024 + stages * (kSkWBytes + mp * kBK * 2) + (mode == kModeAG ? 2 * kPieceBytes : 0) + kSkBarBytes +
+           (cluster > 1 ? (cluster - 1) * kSkRows * (mp + 4) * 4 : 0);
 }
 
 template <int MODE, int PB = 0, int ACT = 0>
-static cudaError_t launch_stream_one(const GemmParams& p, int grid, int smem, cudaStream_t stream) {
+static cudaError_t stream_config(const GemmParams& p, int grid, int smem, cudaStream_t stream,
+                                 cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attr) {
     static std::atomic<uint64_t> configured{0};
     auto fn = flux_stream_kernel<MODE, PB, ACT>;
     int dev = 0;
@@ -2341,11 +2453,57 @@ static cudaError_t launch_stream_one(const GemmParams& p, int grid, int smem, cu
     const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
     if (bit == 0 || !(configured.load(std::memory_order_acquire) & bit)) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSkSmemMax);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         configured.fetch_or(bit, std::memory_order_acq_rel);
     }
-    fn<<<grid, kThreads, smem, stream>>>(p);
-    return cudaGetLastError();
+    cfg = cudaLaunchConfig_t{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.sk_cluster > 1 ? p.sk_cluster : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaSuccess;
+}
+
+template <int MODE, int PB = 0, int ACT = 0>
+static cudaError_t launch_stream_one(const GemmParams& p, int grid, int smem, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[1];
+    cudaError_t e = stream_config<MODE, PB, ACT>(p, grid, smem, stream, cfg, attr);
+    if (e != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, flux_stream_kernel<MODE, PB, ACT>, p);
+}
+
+template <int MODE, int PB = 0, int ACT = 0>
+static int max_clusters_one(const GemmParams& p, int smem) {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[1];
+    if (stream_config<MODE, PB, ACT>(p, p.sk_cluster, smem, nullptr, cfg, attr) != cudaSuccess) return 0;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, flux_stream_kernel<MODE, PB, ACT>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// Clusters of p.sk_cluster CTAs (smem bytes each) that can be resident at once.
+int stream_max_clusters(int mode, const GemmParams& p, int cluster, int smem) {
+    GemmParams q = p;
+    q.sk_cluster = cluster;
+    switch (mode) {
+        case kModePlain: return p.act ? max_clusters_one<kModePlain, 0, 1>(q, smem) : max_clusters_one<kModePlain>(q, smem);
+        case kModeAG: return p.act ? max_clusters_one<kModeAG, 0, 1>(q, smem) : max_clusters_one<kModeAG>(q, smem);
+        case kModeRSUnits:
+            return p.part_bf16 ? max_clusters_one<kModeRSUnits, 1>(q, smem) : max_clusters_one<kModeRSUnits>(q, smem);
+    }
+    return 0;
 }
 
 cudaError_t launch_stream(int mode, const GemmParams& p, int grid, int smem, cudaStream_t stream) {

@@ -1,4 +1,6 @@
-O=gpurun_out/r2; mkdir -p $O
-FLUX_SERIALIZE_TRANSFERS=1 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_headline_serialized.csv python bench.py --steps 3 --warmup 3 --quick --no-cpu-baseline > $O/launch_ser.out 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_headline_smengine.csv python bench.py --steps 3 --warmup 3 --quick --no-cpu-baseline --ag-engine 2 > $O/launch_sm.out 2>&1
-tail -c 300 $O/launch_ser.out; tail -c 300 $O/launch_sm.out
+timeout 600 python -m pytest tests/test_stream_gpu.py tests/test_nvls_gpu.py -x -q 2>&1 | tail -3
+for cl in 1 0 2 4; do
+for args in "0 16 3584 8192 1" "1 16 8192 3584 1" "1 16 8192 1024 1" "1 64 8192 3584 1"; do
+  echo "== cl=$cl $args"
+  FLUX_SK_CLUSTER=$cl timeout 120 python scripts/stream_trace.py $args 2>&1 | grep -E "kernel|cta end|Error|error" | tail -3
+done; done
