@@ -971,6 +971,15 @@ bool stream_kernel_ok(flux_comm* c, const flux_problem* p, int mode, const OpCom
     const long long work = static_cast<long long>(nslots) * sk_nt * ((local_k(p) + kBK - 1) / kBK);
     if (work * (sm_count(c->ranks[g[0]].device) + 1) >= (1LL << 31)) return false;
     if (mode == kModeRSUnits && static_cast<size_t>(sk_nt) * p->tp > kRsFlagCap) return false;
+    // GEMM-RS finishes a tile's owner rows in the epilogue that completed it, after
+    // the other sources' flags. With one rank per launch every CTA walks tiles in
+    // increasing n-tile order on every rank, so the waits form no cycle. With
+    // several ranks in one launch and CTAs holding more than one tile, a CTA's
+    // range wraps from one slot's last tiles to the next slot's first (a wait on
+    // tile 63 of every slot ahead of tile 0 of the next): that mix stays on the
+    // tile kernel (its owner units never block the GEMM).
+    if (mode == kModeRSUnits && nslots > 1 && static_cast<long long>(nslots) * sk_nt > sm_count(c->ranks[g[0]].device))
+        return false;
     if (std::getenv("FLUX_STREAM_KERNEL")) return std::atoi(std::getenv("FLUX_STREAM_KERNEL")) != 0;  // A/B
     if (oc.o.decode_kernel == FLUX_DECODE_STREAM) return true;
     // Auto: one rank per GPU (the deployed TP layout) with at most 64 rows. Measured

@@ -193,3 +193,18 @@ def test_stream_kernel_dropped_rs_flag_raises_deadlock_error():
         want = O.dense_oracle(RS, p.m, p.n, p.k, p.tp, a, b)
         for r in range(p.tp):
             assert O.max_rel_error(got[r], want[r]) <= H.tol(True, p.k), r
+
+
+def test_stream_kernel_rs_many_ranks_per_launch_stays_deadlock_free():
+    """Several emulated ranks in one launch with more n-tiles than SMs: a
+    streaming GEMM-RS would wait on tiles ahead of its own range (the slot
+    wrap), so the request runs on the tile kernel and stays right."""
+    p = fx.ProblemSpec(16, 8192, 3584, 8, RS)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=21)
+        got = _run(comm, p, True, decode_kernel=STREAM, wall_budget_s=5.0)
+        rows = [[0, 1]] * 8
+        for r in range(8):
+            want = O.rs_rows(p.m, p.n, p.k, 8, a, b, r, rows[r])
+            assert O.max_rel_error(got[r][rows[r]], want) <= H.tol(True, p.k), r
+
