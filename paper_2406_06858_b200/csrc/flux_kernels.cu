@@ -1142,6 +1142,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (warp == 0 && lane == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 30, 0);  // prologue done (profiling)
 
     const int k_blocks = (p.k + kBK - 1) / kBK;
 
@@ -1233,6 +1234,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             uint32_t phase = 0;
             int as = 0;
             uint32_t aphase = 0;
+            bool first_mma = true;
             TileSeq seq{&p, cluster_id, num_clusters, static_cast<int>(cta_rank)};
             seq.fetcher = false;
             for (int t = seq.next<CG>(qfull, qempty, qtile); t >= 0; t = seq.next<CG>(qfull, qempty, qtile)) {
@@ -1246,6 +1248,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    if (kb == kb0 && first_mma) {  // first stage landed (launch profiling)
+                        trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 32, 0);
+                        first_mma = false;
+                    }
                     const uint64_t adesc = smem_desc_sw128(sA + stage * G::kABytes);
                     const uint64_t bdesc = p.b_mn ? smem_desc_mn_sw128(sB + stage * G::kBBytes)
                                                   : smem_desc_sw128(sB + stage * G::kBBytes);
@@ -1291,6 +1297,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         const uint32_t tempty_leader = CG == 2 ? mapa(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
         int as = 0;
         uint32_t aphase = 0;
+        bool first_epi = true;
         TileSeq seq{&p, cluster_id, num_clusters, static_cast<int>(cta_rank)};
         seq.fetcher = false;
         for (int t = seq.next<CG>(qfull, qempty, qtile); t >= 0; t = seq.next<CG>(qfull, qempty, qtile)) {
@@ -1307,6 +1314,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
             bool released = false;
             mbar_wait(&tfull[as], aphase);
             tc_fence_after();
+            if (et == 0 && first_epi) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 33, 0);  // first accumulator ready
             const uint32_t tbase = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(as * kBN);
             // Tail split (K-slices of one tile in the last wave): park this slice's
@@ -1824,6 +1832,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                     else mbar_arrive(&tempty[as]);
                 }
             }
+            if (et == 0 && first_epi) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 34, 0);  // first tile stored
+            first_epi = false;
             if (++as == 2) {
                 as = 0;
                 aphase ^= 1u;

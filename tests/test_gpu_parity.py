@@ -618,3 +618,21 @@ def test_medium_grained_baseline(case):
         if tp > 1:
             with pytest.raises(fx.ConfigError, match="must be tp or 2\\*tp"):
                 comm.medium_grained(p, tile, 3 * tp)
+
+
+@pytest.mark.parametrize("case", [(AG, 500, 600, 2048, 1), (AG, 640, 512, 2048, 4), (RS, 128, 512, 8192, 4),
+                                  (RS, 64, 512, 16384, 8)], ids=lambda c: "x".join(map(str, c)))
+def test_tail_split_last_wave_matches_oracle(case):
+    """The last partial wave's tiles run as K-slices (each CTA of the wave sums
+    its share of the slices in slice order) when K is long enough to pay for it
+    (>= 24 k-blocks per rank): AG and the decode-sized RS units on the tile
+    kernel, against the oracle."""
+    pat, m, n, k, tp = case
+    p = fx.ProblemSpec(m, n, k, tp, pat)
+    with H.make_comm(p) as comm:
+        a, b = H.upload(comm, p, seed=m + k)
+        split = _run(comm, p, True, decode_kernel=fx.DECODE_TILE)
+        want = _oracle(p, a, b)
+        for r in range(tp):
+            assert O.max_rel_error(split[r], want[r]) <= H.tol(True, k), r
+

@@ -110,7 +110,7 @@ def test_graph_replay_local_gemm_and_mlp():
                 ref = full[r * (m // tp):(r + 1) * (m // tp)]
                 assert (out[r].float() - ref).abs().max() <= 3e-2 * max(1.0, ref.abs().max().item()), (it, r)
 
-    p = fx.ProblemSpec(1000, 600, 200, 1, AG)  # tail split on (ragged last wave)
+    p = fx.ProblemSpec(1000, 600, 2048, 1, AG)  # tail split on (ragged last wave, K long enough to split)
     with H.make_comm(p) as comm:
         st = [side.cuda_stream]
         gl = fx.default_opts(out_dtype=fx.F32, graph_safe=1)
