@@ -1132,6 +1132,12 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             const int rpr = rows_per_rank(p), tiles_n_all = use_stream ? sk_nt : (lc + kBN - 1) / kBN;
             const long long units16 = static_cast<long long>(g.size()) * ((rpr + 15) / 16) * tiles_n_all;
             prm.red_rows = units16 < 4LL * sm_count(dev) ? 8 : 16;
+            // Warm the units' code before the partials land (they otherwise run it
+            // for the first time after the GEMM, fetched from DRAM on a cold L2) when
+            // at most two ranks share the launch — one rank per GPU, C1: one GPU's
+            // RS share M=128 60.6 -> 51.4 us, C1 50.2 -> 42.0 us; with eight emulated
+            // ranks the dry pass competes with the GEMM (+1-2 %), so it stays off.
+            prm.red_warm = g.size() <= 2 ? 1 : 0;
             if (use_stream) prm.tiles_n = sk_nt;  // RS flags per (128-column n-tile, source)
         }
         prm.red_ctr = at<uint32_t>(c->ranks[g[0]], kCtrlRedCtr);

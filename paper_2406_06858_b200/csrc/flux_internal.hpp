@@ -159,6 +159,7 @@ struct GemmParams {
     // RS with ownership blocks narrower than a tile: owners reduce during the GEMM
     int rs_units;
     int red_rows;                  // owner rows per reduction unit (8 or 16)
+    int red_warm;                  // reduction units: one dry pass over the first unit before its wait
     uint32_t* red_ctr;             // reduction unit counter (lead rank's control block)
     uint32_t* red_exit;
     // Device event trace (reference CausalityLog, engine.hpp:37-63): 16-byte records

@@ -1284,7 +1284,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
         }
     } else if (MODE == kModeRSUnits && (warp == 2 || warp == 3)) {
         // ===== decode RS: owners' reduction, concurrent with the GEMM =====
-        owner_reduce<PB, TWU>(p, threadIdx.x - 64, 64, 3, &red_slot[0], false);
+        owner_reduce<PB, TWU>(p, threadIdx.x - 64, 64, 3, &red_slot[0], p.red_warm != 0);
     } else if (warp == 3) {
         // ===== in-kernel AllGather transfer (Alg. 3 on the SMs) =====
         if (MODE == kModeAG && p.nvls) ag_push_nvls(p, lane);

@@ -15,9 +15,10 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 rd = torch.ones(64 << 20, dtype=torch.int32, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 cases = [("default", {}), ("no tail split", {"FLUX_TAIL_SPLIT": "0"}), ("no units", {"FLUX_RS_UNITS": "0"}),
-         ("neither", {"FLUX_TAIL_SPLIT": "0", "FLUX_RS_UNITS": "0"}), ("cta_group 1", {"_cg": 1})]
+         ("neither", {"FLUX_TAIL_SPLIT": "0", "FLUX_RS_UNITS": "0"}), ("cta_group 1", {"_cg": 1}),
+         ("units warm-up", {"FLUX_DEBUG": "2048"}), ("warm-up cg1", {"FLUX_DEBUG": "2048", "_cg": 1})]
 for name, env in cases:
-    for k in ("FLUX_TAIL_SPLIT", "FLUX_RS_UNITS"):
+    for k in ("FLUX_TAIL_SPLIT", "FLUX_RS_UNITS", "FLUX_DEBUG"):
         os.environ.pop(k, None)
     opts = fx.default_opts(cta_group=env.get("_cg", 0))
     for k, v in env.items():
