@@ -54,3 +54,25 @@ def test_abi_version_and_defaults():
     assert o.graph_safe == 0
     assert o.deterministic_reduce == 1 and o.shift_offset == 1 and o.wall_budget_s == 10.0
     assert o.poll_budget == 10_000_000  # EngineOptions defaults (engine.hpp:65-72)
+
+
+def test_nvls_host_contract():
+    """NVLS options without a GPU: off by default, region size per problem,
+    the probe answers with a reason, unknown option names are rejected."""
+    import ctypes as C
+
+    import pytest
+
+    import paper_2406_06858_b200 as fx
+
+    assert N.default_opts().nvls == N.NVLS_OFF
+    assert C.sizeof(N.CommOpts) == 2 * C.sizeof(C.c_size_t)
+    ag = fx.ProblemSpec(4096, 28672, 8192, 8, fx.ALLGATHER_GEMM)
+    rs = fx.ProblemSpec(4096, 8192, 28672, 8, fx.GEMM_REDUCESCATTER)
+    assert fx.nvls_required_bytes(ag) == 64 * 1024 + 4096 * 8192 * 2  # flags, then a_agg [m, k] bf16
+    assert fx.nvls_required_bytes(rs) == 64 * 1024 + 2 * 4096 * 8192 * 4  # flags, then 2 parities of [m, n] fp32
+    assert fx.nvls_required_bytes(fx.ProblemSpec(10, 16, 16, 4, fx.ALLGATHER_GEMM)) == 0  # invalid (m % tp)
+    ok, why = fx.nvls_probe([0])
+    assert isinstance(ok, bool) and why
+    with pytest.raises(TypeError):
+        fx.default_opts(nvls_mode=1)
