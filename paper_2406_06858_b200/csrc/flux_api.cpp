@@ -1255,18 +1255,27 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                 for (int cl : {8, 4, 2}) {
                     if (forced > 0 && cl != forced) continue;
                     if (tiles_all * cl > sms || kbn < 2 * cl) continue;
-                    const int st = std::min(kSkMaxStages, (kSkSmemMax - stream_smem_bytes(mode, sk_mp, 0, cl)) / stage_bytes);
+                    int st = std::min(kSkMaxStages, (kSkSmemMax - stream_smem_bytes(mode, sk_mp, 0, cl)) / stage_bytes);
+                    // Ring mode (one tile per cluster): the leader's drained stage ring holds
+                    // the slots, so the dedicated buffer's stages come back (M = 64 AG:
+                    // cluster of 4 with 3 -> 8 stages).
+                    const int st_ring = std::min(kSkMaxStages, (kSkSmemMax - stream_smem_bytes(mode, sk_mp, 0)) / stage_bytes);
+                    const bool ring = st < 8 && static_cast<long long>(st_ring) * stage_bytes >=
+                                                    static_cast<long long>(cl - 1) * kSkRows * (sk_mp + 4) * 4;
+                    if (ring) st = st_ring;
                     if (st < 4) continue;
                     GemmParams q = prm;
                     q.sk_cluster = cl;
                     q.sk_stages = st;
-                    const int maxc = stream_max_clusters(mode, q, cl, stream_smem_bytes(mode, sk_mp, st, cl));
+                    q.sk_red_ring = ring ? 1 : 0;
+                    const int maxc = stream_max_clusters(mode, q, cl, stream_smem_bytes(mode, sk_mp, st, ring ? 1 : cl));
                     const int launched = full_grid ? std::min(sms / cl, maxc) : static_cast<int>(tiles_all);
                     if (maxc < launched || launched < tiles_all) continue;
                     if (forced == 0 && tiles_all * 2 > sms) continue;  // auto: only when tiles <= SMs / 2
                     prm.sk_cluster = cl;
                     prm.sk_ctas = static_cast<int>(tiles_all) * cl;
                     prm.sk_stages = st;
+                    prm.sk_red_ring = ring ? 1 : 0;
                     break;
                 }
             }
@@ -1284,11 +1293,10 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
             prm.tail_splits = 0;
             // The in-kernel AllGather runs on every SM (whole clusters, all resident).
             int sgrid = (mode == kModeAG && (prm.sm_transfer || prm.nvls)) ? sms : prm.sk_ctas;
-            if (prm.sk_cluster > 1 && sgrid != prm.sk_ctas) {
-                const int smem_c = stream_smem_bytes(mode, sk_mp, prm.sk_stages, prm.sk_cluster);
-                sgrid = std::min(sms / prm.sk_cluster, stream_max_clusters(mode, prm, prm.sk_cluster, smem_c)) * prm.sk_cluster;
-            }
-            FLUX_CUDA(launch_stream(mode, prm, sgrid, stream_smem_bytes(mode, sk_mp, prm.sk_stages, prm.sk_cluster), lead));
+            const int smem_launch = stream_smem_bytes(mode, sk_mp, prm.sk_stages, prm.sk_red_ring ? 1 : prm.sk_cluster);
+            if (prm.sk_cluster > 1 && sgrid != prm.sk_ctas)
+                sgrid = std::min(sms / prm.sk_cluster, stream_max_clusters(mode, prm, prm.sk_cluster, smem_launch)) * prm.sk_cluster;
+            FLUX_CUDA(launch_stream(mode, prm, sgrid, smem_launch, lead));
         } else {
             FLUX_CUDA(launch_gemm(mode, cg, prm, grid, lead));
         }

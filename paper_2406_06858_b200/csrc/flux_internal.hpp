@@ -212,6 +212,8 @@ struct GemmParams {
     int sk_acc_cols;               // TMEM columns per accumulator (two accumulators)
     int sk_cluster;                // > 1: clusters of this many CTAs split each n-tile's K; the
                                    // partial accumulators meet in the leader's shared memory (DSMEM)
+    int sk_red_ring;               // 1: one tile per cluster; the leader's drained stage ring is the
+                                   // reduction buffer (no dedicated one, so more stages fit)
     uint32_t* sk_ctr;              // per (slot, n-tile): (tail_seq << 8) | arrivals
 };
 

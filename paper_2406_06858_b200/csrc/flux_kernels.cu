@@ -2051,9 +2051,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
     // Cluster split-K: the leader's reduction buffer, one [128 columns][mp + 4]
     // fp32 slot per non-leader segment (padded rows: conflict-free v4 stores).
     const int cl = p.sk_cluster, ldr = mp + 4;
-    float* sRed = reinterpret_cast<float*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0));
-    const int red_bytes = cl > 1 ? (cl - 1) * kSkRows * ldr * 4 : 0;
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sRed) + red_bytes);
+    const bool ring = cl > 1 && p.sk_red_ring;  // one tile per cluster: the drained ring holds the slots
+    float* sRed = ring ? reinterpret_cast<float*>(sW) : reinterpret_cast<float*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0));
+    const int red_bytes = cl > 1 && !ring ? (cl - 1) * kSkRows * ldr * 4 : 0;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0) + red_bytes);
     uint64_t* empty = full + kSkMaxStages;
     uint64_t* tfull = empty + kSkMaxStages;
     uint64_t* tempty = tfull + 2;
@@ -2219,7 +2220,10 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                 const uint32_t tbase =
                     tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(as * p.sk_acc_cols);
                 if (crank != 0) {
-                    mbar_wait(&red_bar[1], ephase ^ 1u);  // the leader has read this slot's previous tile
+                    // Buffer mode: the leader has read this slot's previous tile (the first
+                    // wait passes). Ring mode: the leader's own MMAs are done, so its stage
+                    // ring is free to receive.
+                    mbar_wait(&red_bar[1], ring ? ephase : (ephase ^ 1u));
                     ephase ^= 1u;
                     const uint32_t dst = mapa(smem_u32(sRed + ((crank - 1) * kSkRows + cit) * ldr), 0);
                     for (int m0 = 0; m0 < mv; m0 += 16) {
@@ -2235,6 +2239,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                     if (lane == 0) mbar_arrive(&tempty[as]);
                     mbar_arrive_cluster(mapa(smem_u32(&red_bar[0]), 0));  // release: this thread's stores
                 } else {
+                    if (ring && et >= 1 && et < cl)  // my MMAs retired: the ring may take the slots
+                        mbar_arrive_cluster(mapa(smem_u32(&red_bar[1]), static_cast<uint32_t>(et)));
                     mbar_wait_acq_cluster(&red_bar[0], fphase);
                     fphase ^= 1u;
                     for (int m0 = 0; m0 < mv; m0 += 16) {
@@ -2261,7 +2267,8 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[as]);
                     named_bar_sync(1, 128);  // every leader thread has read the slots
-                    if (et >= 1 && et < cl) mbar_arrive_cluster(mapa(smem_u32(&red_bar[1]), static_cast<uint32_t>(et)));
+                    if (!ring && et >= 1 && et < cl)
+                        mbar_arrive_cluster(mapa(smem_u32(&red_bar[1]), static_cast<uint32_t>(et)));
                     if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 5, static_cast<uint32_t>(tt));
                     if (MODE == kModeRSUnits) sk_rs_finish<PB>(p, l, j, mv, et);
                 }
