@@ -228,6 +228,17 @@ int flux_nvls_probe(int n, const int* devices, char* why, int why_len);
 size_t flux_nvls_required_bytes(const flux_problem* problem);
 /* 1 if the communicator owns an NVLS multicast region. */
 int flux_comm_nvls(const flux_comm* comm);
+/* NVLS for one process per GPU, after flux_comm_ipc_connect. The multicast
+ * handle is a POSIX file descriptor the caller hands from rank 0 to the others
+ * (a Unix socket with SCM_RIGHTS; comm.py does it): rank 0 _export()s it, the
+ * others _import() it (the fd is consumed), every rank _add_device()s its GPU,
+ * and once all have (caller's barrier) every rank _bind()s its memory; a second
+ * barrier before the first NVLS operator (peers' regions zeroed). Errors name
+ * the failing step ("NVLS unavailable: cuMulticastCreate: ..."). */
+int flux_comm_nvls_ipc_export(flux_comm* comm, size_t nvls_bytes, int* fd_out);
+int flux_comm_nvls_ipc_import(flux_comm* comm, size_t nvls_bytes, int fd);
+int flux_comm_nvls_ipc_add_device(flux_comm* comm);
+int flux_comm_nvls_ipc_bind(flux_comm* comm);
 /* Buffer of `rank` for `problem` (any rank in single-process mode; own rank in IPC mode). */
 int flux_buffer(flux_comm* comm, int rank, int kind, const flux_problem* problem,
                 flux_buffer_desc* out);

@@ -179,6 +179,10 @@ _SIGS = {
     "flux_nvls_probe": (C.c_int, [C.c_int, _P(C.c_int), C.c_char_p, C.c_int]),
     "flux_nvls_required_bytes": (C.c_size_t, [_P(Problem)]),
     "flux_comm_nvls": (C.c_int, [C.c_void_p]),
+    "flux_comm_nvls_ipc_export": (C.c_int, [C.c_void_p, C.c_size_t, _P(C.c_int)]),
+    "flux_comm_nvls_ipc_import": (C.c_int, [C.c_void_p, C.c_size_t, C.c_int]),
+    "flux_comm_nvls_ipc_add_device": (C.c_int, [C.c_void_p]),
+    "flux_comm_nvls_ipc_bind": (C.c_int, [C.c_void_p]),
 }
 
 # Symbols include/flux_b200.h declares (tests check the library exports all of them).

@@ -9,6 +9,7 @@ ShardedWorkspace + peer directory, workspace.hpp:22-43) and runs
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
 
@@ -166,10 +167,13 @@ class Communicator:
 
     @classmethod
     def ipc(cls, rank: int, tp: int, device: int, heap_bytes: int,
-            all_gather_bytes: Callable[[bytes], list[bytes]]) -> "Communicator":
+            all_gather_bytes: Callable[[bytes], list[bytes]], nvls_bytes: int = 0) -> "Communicator":
         """Multi-process constructor: `all_gather_bytes` exchanges handle blobs
         (e.g. torch.distributed.all_gather_object), the paper's init-phase IPC
-        exchange (PAPER.md:229)."""
+        exchange. `nvls_bytes` > 0 also sets up the NVLS
+        multicast region (rank 0's multicast handle reaches the peers as a file
+        descriptor over a Unix socket); every rank raises the same error if the
+        host does not expose it."""
         h = C.c_void_p()
         N.check(N.lib().flux_comm_create_ipc(rank, tp, device, C.byref(N.CommOpts(heap_bytes, 0)), C.byref(h)))
         nb = N.lib().flux_comm_ipc_blob_bytes()
@@ -178,7 +182,38 @@ class Communicator:
         blobs = all_gather_bytes(blob.raw)
         joined = C.create_string_buffer(b"".join(blobs), nb * tp)
         N.check(N.lib().flux_comm_ipc_connect(h, joined))
-        return cls(tp, _handle=h.value, device=device)
+        comm = cls(tp, _handle=h.value, device=device)
+        if nvls_bytes:
+            try:
+                comm._nvls_ipc_setup(rank, tp, nvls_bytes, all_gather_bytes)
+            except Exception:
+                comm.close()
+                raise
+        return comm
+
+    def _nvls_ipc_setup(self, rank: int, tp: int, nvls_bytes: int, all_gather_bytes) -> None:
+        lib = N.lib()
+        status, server, name = b"ok", None, b""
+        if rank == 0:
+            fd = C.c_int(-1)
+            if lib.flux_comm_nvls_ipc_export(self._h, nvls_bytes, C.byref(fd)) != N.OK:
+                status = lib.flux_last_error()
+            else:
+                name = ("flux-nvls-%d-%s" % (os.getpid(), os.urandom(6).hex())).encode()
+                server = fd_server(name.decode(), fd.value)  # listening before the peers learn the name
+        got = all_gather_bytes(status + b"\0" + name)
+        st0, name0 = got[0].split(b"\0", 1)
+        if st0 != b"ok":
+            raise N.CudaError(st0.decode(errors="replace"))
+        if rank == 0:
+            server.serve(tp - 1)
+        else:
+            fd = fd_receive(name0.decode())
+            N.check(lib.flux_comm_nvls_ipc_import(self._h, nvls_bytes, fd))
+        N.check(lib.flux_comm_nvls_ipc_add_device(self._h))
+        all_gather_bytes(b"added")  # every GPU is in the object before anyone binds
+        N.check(lib.flux_comm_nvls_ipc_bind(self._h))
+        all_gather_bytes(b"bound")  # every region mapped and zeroed before the first operator
 
     # ---- buffers -------------------------------------------------------------
     def buffer(self, rank: int, kind: int, problem: ProblemSpec) -> N.BufferDesc:
@@ -414,3 +449,60 @@ def write_chrome_trace(path: str, events: list[dict]) -> None:
     with open(path, "w") as f:
         json.dump(chrome_trace(events), f)
         f.write("\n")
+
+
+# ---------------------------------------------------------------------------
+# file-descriptor hand-off between the processes of one node (NVLS multicast
+# handles are POSIX file descriptors): an abstract-namespace Unix socket and
+# SCM_RIGHTS (socket.send_fds / recv_fds).
+# ---------------------------------------------------------------------------
+class fd_server:
+    """Listens on abstract socket `name`; serve(n) hands `fd` to n clients,
+    then closes the socket and the fd."""
+
+    def __init__(self, name: str, fd: int):
+        import socket
+
+        self.fd = fd
+        self.sock = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        self.sock.bind("\0" + name)
+        self.sock.listen(64)
+
+    def serve(self, n: int, timeout_s: float = 60.0) -> None:
+        import socket
+
+        self.sock.settimeout(timeout_s)
+        try:
+            for _ in range(n):
+                conn, _ = self.sock.accept()
+                with conn:
+                    socket.send_fds(conn, [b"fd"], [self.fd])
+                    conn.recv(1)  # the client holds its copy before we close ours
+        finally:
+            self.sock.close()
+            os.close(self.fd)
+
+
+def fd_receive(name: str, timeout_s: float = 60.0) -> int:
+    """The file descriptor served on abstract socket `name` (a new fd in this process)."""
+    import socket
+    import time
+
+    deadline = time.monotonic() + timeout_s
+    while True:
+        s = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        try:
+            s.connect("\0" + name)
+            break
+        except OSError:
+            s.close()
+            if time.monotonic() > deadline:
+                raise
+            time.sleep(0.01)
+    with s:
+        _, fds, _, _ = socket.recv_fds(s, 16, 1)
+        s.sendall(b"k")
+    if not fds:
+        raise OSError("no file descriptor received on " + name)
+    return fds[0]
+

@@ -107,6 +107,8 @@ struct NvlsDriver {
     PFN_cuMemMap_v10020 map = nullptr;
     PFN_cuMemUnmap_v10020 unmap = nullptr;
     PFN_cuMemSetAccess_v10020 set_access = nullptr;
+    PFN_cuMemExportToShareableHandle_v10020 export_handle = nullptr;
+    PFN_cuMemImportFromShareableHandle_v10020 import_handle = nullptr;
     bool ok = false;
 };
 
@@ -137,6 +139,8 @@ NvlsDriver& nvls_driver() {
         ok &= get("cuMemMap", reinterpret_cast<void**>(&d.map));
         ok &= get("cuMemUnmap", reinterpret_cast<void**>(&d.unmap));
         ok &= get("cuMemSetAccess", reinterpret_cast<void**>(&d.set_access));
+        ok &= get("cuMemExportToShareableHandle", reinterpret_cast<void**>(&d.export_handle));
+        ok &= get("cuMemImportFromShareableHandle", reinterpret_cast<void**>(&d.import_handle));
         d.ok = ok;
     });
     return d;
@@ -626,6 +630,7 @@ void nvls_release(flux_comm::Nvls& nv, const std::vector<int>& devs) {
         d.va_free(nv.mc, nv.bytes);
     }
     for (size_t r = 0; r < nv.mem.size(); ++r) {
+        if (!nv.mem[r]) continue;  // (one process per GPU: only this rank's memory is ours)
         CUdevice cd = 0;
         d.dev_get(&cd, devs[r]);
         if (nv.bound && nv.mc_handle) d.mc_unbind(static_cast<CUmemGenericAllocationHandle>(nv.mc_handle), cd, 0, nv.bytes);
@@ -1482,6 +1487,135 @@ int flux_nvls_probe(int n, const int* devices, char* why, int why_len) {
 
 int flux_comm_nvls(const flux_comm* c) { return c && c->nvls.mc ? 1 : 0; }
 
+// NVLS for one process per GPU: the multicast object is created by rank 0 and
+// its POSIX file-descriptor handle passed to the peers by the caller (a Unix
+// socket with SCM_RIGHTS, comm.py); each rank then adds its GPU, and once every
+// rank has (the caller's barrier), binds its own VMM memory and maps the region.
+static int nvls_ipc_geometry(flux_comm* c, size_t want, size_t* bytes, size_t* gran) {
+    NvlsDriver& d = nvls_driver();
+    if (!d.ok) return fail(FLUX_ERR_CUDA, "NVLS unavailable: multicast / VMM driver entry points unavailable");
+    if (!c || !c->ipc || !c->connected) return fail(FLUX_ERR_CONFIG, "NVLS IPC setup needs a connected IPC communicator");
+    if (c->tp < 2) return fail(FLUX_ERR_CONFIG, "NVLS unavailable: needs tp >= 2");
+    if (c->nvls.mc_handle) return fail(FLUX_ERR_CONFIG, "the communicator already has an NVLS region");
+    CUmulticastObjectProp mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.numDevices = static_cast<unsigned>(c->tp);
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = std::max<size_t>(want, 1);
+    CUresult e = d.mc_gran(gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+    if (e != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "NVLS unavailable: cuMulticastGetGranularity: " + cu_err(e));
+    *gran = std::max<size_t>(*gran, size_t(2) << 20);
+    *bytes = (std::max<size_t>(want, 1) + *gran - 1) / *gran * *gran;
+    return FLUX_OK;
+}
+
+int flux_comm_nvls_ipc_export(flux_comm* c, size_t want, int* fd_out) {
+    size_t bytes = 0, gran = 0;
+    FLUX_TRY(nvls_ipc_geometry(c, want, &bytes, &gran));
+    if (c->my_rank != 0 || !fd_out) return fail(FLUX_ERR_CONFIG, "rank 0 creates and exports the multicast object");
+    NvlsDriver& d = nvls_driver();
+    CUmulticastObjectProp mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.numDevices = static_cast<unsigned>(c->tp);
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = bytes;
+    CUmemGenericAllocationHandle h = 0;
+    CUresult e = d.mc_create(&h, &mp);
+    if (e != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "NVLS unavailable: cuMulticastCreate: " + cu_err(e));
+    int fd = -1;
+    e = d.export_handle(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
+    if (e != CUDA_SUCCESS) {
+        d.mem_release(h);
+        return fail(FLUX_ERR_CUDA, "NVLS unavailable: cuMemExportToShareableHandle: " + cu_err(e));
+    }
+    c->nvls = flux_comm::Nvls{};
+    c->nvls.bytes = bytes;
+    c->nvls.mc_handle = h;
+    *fd_out = fd;
+    return FLUX_OK;
+}
+
+int flux_comm_nvls_ipc_import(flux_comm* c, size_t want, int fd) {
+    size_t bytes = 0, gran = 0;
+    FLUX_TRY(nvls_ipc_geometry(c, want, &bytes, &gran));
+    if (c->my_rank == 0) return fail(FLUX_ERR_CONFIG, "rank 0 exports the multicast object; the others import it");
+    NvlsDriver& d = nvls_driver();
+    CUmemGenericAllocationHandle h = 0;
+    CUresult e = d.import_handle(&h, reinterpret_cast<void*>(static_cast<uintptr_t>(fd)), CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    close(fd);
+    if (e != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "NVLS unavailable: cuMemImportFromShareableHandle: " + cu_err(e));
+    c->nvls = flux_comm::Nvls{};
+    c->nvls.bytes = bytes;
+    c->nvls.mc_handle = h;
+    return FLUX_OK;
+}
+
+int flux_comm_nvls_ipc_add_device(flux_comm* c) {
+    if (!c || !c->ipc || !c->nvls.mc_handle) return fail(FLUX_ERR_CONFIG, "no multicast object to add this GPU to");
+    NvlsDriver& d = nvls_driver();
+    CUdevice cd = 0;
+    CUresult e = d.dev_get(&cd, c->ranks[c->my_rank].device);
+    if (e == CUDA_SUCCESS) e = d.mc_add(static_cast<CUmemGenericAllocationHandle>(c->nvls.mc_handle), cd);
+    if (e != CUDA_SUCCESS) return fail(FLUX_ERR_CUDA, "NVLS unavailable: cuMulticastAddDevice: " + cu_err(e));
+    return FLUX_OK;
+}
+
+int flux_comm_nvls_ipc_bind(flux_comm* c) {
+    if (!c || !c->ipc || !c->nvls.mc_handle) return fail(FLUX_ERR_CONFIG, "no multicast object to bind");
+    NvlsDriver& d = nvls_driver();
+    flux_comm::Nvls& nv = c->nvls;
+    const int me = c->my_rank, dev = c->ranks[me].device;
+    const size_t gran = size_t(2) << 20;
+    nv.mem.assign(c->tp, 0);
+    nv.uc.assign(c->tp, 0);
+    std::vector<int> devs(c->tp, dev);
+    auto bail = [&](CUresult e, const char* what) {
+        const std::string msg = std::string("NVLS unavailable: ") + what + ": " + cu_err(e);
+        nvls_release(nv, devs);
+        return fail(FLUX_ERR_CUDA, msg);
+    };
+    CUmemAllocationProp ap;
+    std::memset(&ap, 0, sizeof(ap));
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = dev;
+    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    CUmemGenericAllocationHandle mh = 0;
+    CUresult e = d.mem_create(&mh, nv.bytes, &ap, 0);
+    if (e != CUDA_SUCCESS) return bail(e, "cuMemCreate");
+    nv.mem[me] = mh;
+    CUdeviceptr va = 0;
+    if ((e = d.va_reserve(&va, nv.bytes, gran, 0, 0)) != CUDA_SUCCESS) return bail(e, "cuMemAddressReserve");
+    if ((e = d.map(va, nv.bytes, 0, mh, 0)) != CUDA_SUCCESS) {
+        d.va_free(va, nv.bytes);
+        return bail(e, "cuMemMap");
+    }
+    nv.uc[me] = va;
+    CUmemAccessDesc ad;
+    std::memset(&ad, 0, sizeof(ad));
+    ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ad.location.id = dev;
+    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if ((e = d.set_access(va, nv.bytes, &ad, 1)) != CUDA_SUCCESS) return bail(e, "cuMemSetAccess (unicast)");
+    if ((e = d.mc_bind(static_cast<CUmemGenericAllocationHandle>(nv.mc_handle), 0, mh, 0, nv.bytes, 0)) != CUDA_SUCCESS)
+        return bail(e, "cuMulticastBindMem");
+    nv.bound = true;
+    CUdeviceptr mva = 0;
+    if ((e = d.va_reserve(&mva, nv.bytes, gran, 0, 0)) != CUDA_SUCCESS) return bail(e, "cuMemAddressReserve (multicast)");
+    if ((e = d.map(mva, nv.bytes, 0, static_cast<CUmemGenericAllocationHandle>(nv.mc_handle), 0)) != CUDA_SUCCESS) {
+        d.va_free(mva, nv.bytes);
+        return bail(e, "cuMemMap (multicast)");
+    }
+    nv.mc = mva;
+    if ((e = d.set_access(mva, nv.bytes, &ad, 1)) != CUDA_SUCCESS) return bail(e, "cuMemSetAccess (multicast)");
+    if (cudaSetDevice(dev) != cudaSuccess || cudaMemset(reinterpret_cast<void*>(va), 0, nv.bytes) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+        nvls_release(nv, devs);
+        return fail(FLUX_ERR_CUDA, "NVLS unavailable: zeroing the region failed");
+    }
+    return FLUX_OK;
+}
+
 int flux_comm_create(int tp, const int* devices, const flux_comm_opts* opts, flux_comm** out) {
     if (!out) return fail(FLUX_ERR_CONFIG, "null output");
     *out = nullptr;
@@ -1548,8 +1682,8 @@ int flux_comm_create_ipc(int rank, int tp, int device, const flux_comm_opts* opt
     c->my_rank = rank;
     if (opts && opts->nvls_bytes > 0) {
         delete c;
-        return fail(FLUX_ERR_CONFIG, "NVLS multicast regions need the single-process communicator "
-                                     "(the multicast handle is a POSIX file descriptor)");
+        return fail(FLUX_ERR_CONFIG, "one process per GPU: set up NVLS with flux_comm_nvls_ipc_export / _import / "
+                                     "_add_device / _bind after flux_comm_ipc_connect (nvls_bytes must be 0 here)");
     }
     c->heap_bytes = (opts && opts->heap_bytes) ? opts->heap_bytes : (size_t(1) << 30);
     c->ranks.resize(tp);
@@ -1896,7 +2030,13 @@ static void nvls_fill(flux_comm* c, const flux_problem* p, const flux_opts& o, G
     prm.nvls = o.nvls;
     const bool hw = o.nvls == FLUX_NVLS_MULTICAST;
     for (int q = 0; q < p->tp; ++q) {
-        char* base = hw ? reinterpret_cast<char*>(c->nvls.uc[q]) : c->ranks[q].heap;
+        char* base = hw ? reinterpret_cast<char*>(q < static_cast<int>(c->nvls.uc.size()) ? c->nvls.uc[q] : 0)
+                        : c->ranks[q].heap;
+        if (!base) {  // a peer's region in another process: reached only through the multicast address
+            prm.nvls_data[q] = nullptr;
+            prm.nvls_flags[q] = nullptr;
+            continue;
+        }
         const size_t data = hw ? kNvlsDataOffset : (p->pattern == FLUX_ALLGATHER_GEMM ? L.a_agg.off : L.staging.off);
         prm.nvls_data[q] = base + data;
         prm.nvls_flags[q] = reinterpret_cast<uint32_t*>(base + (hw ? kNvlsFlagOffset : kAgFlagOffset));

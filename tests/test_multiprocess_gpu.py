@@ -54,3 +54,25 @@ def test_bench_two_ranks_ipc_path(workload):
     assert ov["t_unfused_cublas_ms"] > 0 and ov["t_decomposed_ms"] > 0 and ov["t_nonoverlap_ours_ms"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["roofline"]["nvlink_bytes_per_launch"] > 0  # one rank's share at N>1
+
+
+@pytest.mark.gpu
+def test_two_processes_nvls():
+    """NVLS through the one-process-per-GPU communicator: the multicast handle
+    travels from rank 0 to the peer as a file descriptor. Where the host exposes
+    multicast both ranks match the oracle through multimem; otherwise both raise
+    the same error (nothing hangs). The emulated protocol over the peers'
+    IPC-mapped regions matches the oracle either way."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29547", os.path.join(ROOT, "scripts", "mp_nvls_worker.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(out.stdout[-4000:], out.stderr[-4000:])
+    assert out.returncode == 0
+    res = [json.loads(l.split(" ", 2)[2]) for l in out.stdout.splitlines() if l.startswith("RESULT")]
+    assert len(res) == 2
+    assert res[0]["multicast"] == res[1]["multicast"] or all(r["multicast"].startswith("error") for r in res)
+    for r in res:
+        assert len(r["results"]) == (6 if r["multicast"] == "ok" else 3)
+        for case, (err, tol) in r["results"].items():
+            assert err <= tol, (case, err, tol)
+
