@@ -1540,6 +1540,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                 for (int c = 0; c < kBN / 32; ++c) {
                     const int colc = col0 + c * 32;
                     if (colc >= p.n) break;  // warp-uniform
+                    if (et == 0 && first_epi && (c == 1 || c == 4)) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 34 + c, 0);  // chunk c of the first tile (profiling)
                     uint32_t r[32];
                     tmem_ld32(tbase + c * 32, r);
                     tmem_ld_wait();

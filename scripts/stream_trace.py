@@ -50,7 +50,8 @@ names = {0: "cta start", 2: "producer done", 3: "segment drained", 4: "split wai
          1: "cta end", 10: "AG piece loaded", 11: "AG stores done", 12: "AG transfer start", 13: "RS unit summed", 14: "RS unit bar (t0)", 15: "RS unit bar (t32)", 20: "RS group w2-3 done",
          21: "RS group epi done", 22: "RS group w0-1 done", 6: "epi segs drained", 7: "epi splits done", 8: "w0-1 join RS",
          **{24 + w: f"warp {w} at exit" for w in range(8)},
-         30: "prologue done", 32: "first stage landed", 33: "first acc ready", 34: "first tile stored"}
+         30: "prologue done", 32: "first stage landed", 33: "first acc ready", 34: "first tile stored",
+         35: "1st tile chunk 1", 38: "1st tile chunk 4"}
 for key in sorted(by, key=lambda k: sorted(by[k])[len(by[k]) // 2]):
     v = sorted(by[key])
     name = names.get(key[1], key[0]) if key[0] == "launch" else key[0]
