@@ -981,7 +981,12 @@ __device__ __forceinline__ long long stage_tile_off(long long lr0, int tn, int t
     return ((lr0 / kBM) * tiles_n + tn) * static_cast<long long>(kBM * kBN);
 }
 __device__ __forceinline__ float4 epi_read(const uint8_t* wbuf, int i, int g) {
-    return *reinterpret_cast<const float4*>(wbuf + i * 128 + ((g ^ (i & 7)) << 4));
+    // ld.shared (a plain dereference compiled to a generic LD here)
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(smem_u32(wbuf + i * 128 + ((g ^ (i & 7)) << 4))));
+    return v;
 }
 
 }  // namespace
@@ -1537,6 +1542,24 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         }
                     }
                 } else {
+                // Staging address of each of the 8 rows this lane writes through the
+                // smem window (row it * 4 + lane / 8 of the warp's 32), computed once
+                // per tile: the chunk loop only adds the column (the per-store owner
+                // division and 64-bit plane arithmetic dominated it: C1 1.45 us per
+                // 32-column chunk).
+                char* rowp[8];
+#pragma unroll
+                for (int it = 0; it < 8; ++it) {
+                    const int grow = row0 + q * 32 + it * 4 + (lane >> 3);
+                    rowp[it] = nullptr;
+                    if (grow < p.m) {
+                        const int o = grow / rpr;
+                        long long pl;
+                        float* const dst = rs_plane_base(p, o, me, pl);
+                        const long long e = parity * p.stage_parity + pl + (grow - static_cast<long long>(o) * rpr) * ld_stage;
+                        rowp[it] = reinterpret_cast<char*>(dst) + e * (PB ? 2 : 4);
+                    }
+                }
                 for (int c = 0; c < kBN / 32; ++c) {
                     const int colc = col0 + c * 32;
                     if (colc >= p.n) break;  // warp-uniform
@@ -1563,17 +1586,11 @@ __global__ void __launch_bounds__(kThreads, 1) flux_gemm_kernel(const __grid_con
                         continue;
                     }
                     epi_stage(wbuf, lane, r);
+                    const int col = colc + (lane & 7) * 4;
 #pragma unroll
                     for (int it = 0; it < 8; ++it) {
-                        const int i = it * 4 + (lane >> 3), g = lane & 7;
-                        const int col = colc + g * 4;
-                        const int grow = row0 + q * 32 + i;
-                        if (grow >= p.m || col >= p.n) continue;
-                        const int o = grow / rpr;
-                        long long pl;
-                        float* const dst = rs_plane_base(p, o, me, pl);
-                        st_part4<PB>(dst, parity * p.stage_parity + pl + (grow - static_cast<long long>(o) * rpr) * ld_stage + col,
-                                     epi_read(wbuf, i, g));
+                        if (rowp[it] == nullptr || col >= p.n) continue;
+                        st_part4<PB>(reinterpret_cast<float*>(rowp[it]), col, epi_read(wbuf, it * 4 + (lane >> 3), lane & 7));
                     }
                 }
                 // The accumulator is in staging now: hand TMEM back to the MMA warp.
