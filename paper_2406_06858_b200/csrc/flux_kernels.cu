@@ -1980,16 +1980,25 @@ __device__ __forceinline__ void sk_store(const GemmParams& p, int l, int col, in
     if (MODE == kModeRSUnits) {
         const int me = p.global_rank[l], rpr = p.rpr;
         const long long base = static_cast<long long>(p.epoch & 1u) * p.stage_parity + col;
+        // Owner and row within its block advance with the row (one division per
+        // 16 rows, not one per store).
+        int o = m0 / rpr, lr = m0 - o * rpr;
+        long long pl;
+        float* dst = rs_plane_base(p, o, me, pl);
+        long long e = base + pl + static_cast<long long>(lr) * p.ld_stage;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const int m = m0 + i;
-            if (m >= mv) break;
-            const int o = m / rpr;
-            long long pl;
-            float* const dst = rs_plane_base(p, o, me, pl);
-            const long long e = base + pl + static_cast<long long>(m - o * rpr) * p.ld_stage;
+            if (m0 + i >= mv) break;
+            if (lr == rpr) {
+                ++o;
+                lr = 0;
+                dst = rs_plane_base(p, o, me, pl);
+                e = base + pl;
+            }
             if (PB) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(v[i]);
             else dst[e] = v[i];
+            ++lr;
+            e += p.ld_stage;
         }
     } else {
         const long long ldc = p.ldc_l[l];
