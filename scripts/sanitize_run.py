@@ -1,6 +1,7 @@
 """Small fused runs for compute-sanitizer (memcheck / racecheck / synccheck):
 AG on both transfer engines, RS chained / owner-sum / decode owner units,
-FusedReduce, the dynamic tile scheduler,
+FusedReduce, the dynamic tile scheduler, the streaming decode kernel (cluster
+split-K in buffer and ring mode, stream-K), the emulated NVLS protocol,
 and the MLP chain, each checked against a cuBLAS product. Usage:
     compute-sanitizer --tool memcheck python scripts/sanitize_run.py"""
 import os
@@ -51,15 +52,29 @@ cases = [("AG copy engines", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM
          ("AG in-kernel Push", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(ag_engine=2, push=1)),
          ("RS smaller than a wave (owner units)", fx.ProblemSpec(1024, 1024, 512, 2, fx.GEMM_REDUCESCATTER), {}),
          ("RS decode, bf16 partials", fx.ProblemSpec(64, 512, 512, 4, fx.GEMM_REDUCESCATTER), dict(rs_partials=fx.BF16)),
-         ("AG graph-safe", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(graph_safe=1))]
+         ("AG graph-safe", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(graph_safe=1)),
+         # streaming decode kernel: cluster split-K (buffer / ring mode), stream-K, whole tiles
+         ("stream AG, clusters of 8", fx.ProblemSpec(16, 1024, 2048, 1, fx.ALLGATHER_GEMM), dict(decode_kernel=2)),
+         ("stream RS M=64, cluster ring mode", fx.ProblemSpec(64, 1024, 2048, 1, fx.GEMM_REDUCESCATTER),
+          dict(decode_kernel=2)),
+         ("stream RS tp=4, clusters", fx.ProblemSpec(16, 1024, 1024, 4, fx.GEMM_REDUCESCATTER), dict(decode_kernel=2)),
+         ("stream AG stream-K segments", fx.ProblemSpec(16, 1024, 8192, 1, fx.ALLGATHER_GEMM),
+          dict(decode_kernel=2, env="FLUX_SK_CLUSTER")),
+         # NVLS protocol (emulated multicast)
+         ("NVLS AG (emulated)", fx.ProblemSpec(512, 1024, 256, 4, fx.ALLGATHER_GEMM), dict(nvls=2)),
+         ("NVLS RS units (emulated)", fx.ProblemSpec(512, 1024, 512, 4, fx.GEMM_REDUCESCATTER), dict(nvls=2)),
+         ("NVLS RS stream (emulated)", fx.ProblemSpec(16, 1024, 1024, 4, fx.GEMM_REDUCESCATTER), dict(nvls=2, decode_kernel=2))]
+only = os.environ.get("SANITIZE_ONLY")  # e.g. "0,1": run these case indices
+if only:
+    cases = [cases[int(i)] for i in only.split(",")]
 for tag, p, kw in cases:
     kw = dict(kw)
     env = kw.pop("env", None)
     push = kw.pop("push", 0)
+    for var in ("FLUX_DYN_SCHED", "FLUX_SK_CLUSTER"):
+        os.environ.pop(var, None)
     if env:
         os.environ[env] = "1"
-    else:
-        os.environ.pop("FLUX_DYN_SCHED", None)
     with fx.Communicator(p.tp, [0] * p.tp, heap_bytes=fx.required_heap_bytes(p)) as comm:
         fill(comm, p, 1)
         opts = fx.default_opts(wall_budget_s=120.0, **kw)
@@ -71,6 +86,9 @@ for tag, p, kw in cases:
             comm.gemm_rs(p, tile, wm, "Naive" not in tag, opts)
         comm.sync()
         check(comm, p, tag, kw.get("rs_partials") == fx.BF16)
+if only:
+    print("SANITIZE-RUN-DONE", flush=True)
+    sys.exit(0)
 spec = fx.MlpSpec(m=512, hidden=256, ffn=1024, tp=2, activation=fx.ACT_GELU)
 x = [torch.randn(256, 256, device="cuda").to(torch.bfloat16) for _ in range(2)]
 wu = [torch.randn(512, 256, device="cuda").mul(0.05).to(torch.bfloat16) for _ in range(2)]
