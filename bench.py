@@ -303,15 +303,30 @@ def our_arm(args, wl):
     tp = tp_wl if emulated else world
     prob = fx.ProblemSpec(m, n, k, tp, pattern)
     heap = fx.required_heap_bytes(prob) + (64 << 20)
+    # --nvls: NVLS multicast (the AllGather push / GEMM-RS owner sums through the
+    # NVSwitch); ranks emulated on one GPU run the same protocol with unicast
+    # loops (FLUX_NVLS_EMULATED). Off by default; "unavailable" (with the reason)
+    # when the host exposes no multicast, and the run continues without it.
+    nvls_mode, nvls_note = fx.NVLS_OFF, None
     if emulated:
         comm = fx.Communicator(tp, [local_rank] * tp, heap_bytes=heap)
         my_ranks = list(range(tp))
+        if args.nvls:
+            nvls_mode, nvls_note = fx.NVLS_EMULATED, "emulated (unicast loops over the ranks' regions on one GPU)"
     else:
         def gather(blob):
             out = [None] * world
             dist.all_gather_object(out, blob)
             return out
-        comm = fx.Communicator.ipc(rank, tp, local_rank, heap, gather)
+        comm = None
+        if args.nvls:
+            try:
+                comm = fx.Communicator.ipc(rank, tp, local_rank, heap, gather, nvls_bytes=fx.nvls_required_bytes(prob))
+                nvls_mode, nvls_note = fx.NVLS_MULTICAST, "multicast (multimem through the NVSwitch)"
+            except fx.FluxError as e:
+                nvls_note = "unavailable: " + str(e)
+        if comm is None:
+            comm = fx.Communicator.ipc(rank, tp, local_rank, heap, gather)
         my_ranks = [rank]
 
     # synthetic inputs (uniform [-1, 1), bf16) straight into the symmetric heaps
@@ -327,7 +342,7 @@ def our_arm(args, wl):
     streams = [stream] * (tp if emulated else 1)
     tile = fx.TileShape(prob.rows_per_rank(), prob.local_cols())
     opts = fx.default_opts(ag_engine=args.ag_engine, cta_group=args.cta_group,
-                           deterministic_reduce=0 if args.nondeterministic else 1)
+                           deterministic_reduce=0 if args.nondeterministic else 1, nvls=nvls_mode)
     # L2 flush between timed steps (outside the events): write 256 MiB (> the
     # 126 MB L2), then read another 256 MiB so the written lines are evicted
     # (written back) before the next step starts — no dirty lines are left to
@@ -667,12 +682,16 @@ def our_arm(args, wl):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform[-1,1) bf16)",
             "config": {"workload": wl, "description": desc, "m": m, "n": n, "k": k, "tp": tp,
                        "ranks": "emulated on one GPU" if emulated else "one process per GPU (cudaIpc heaps)",
-                       "parallelism": f"tp{tp}", "transfer": ag_transfer if pattern == 0 else "epilogue P2P",
+                       "parallelism": f"tp{tp}",
+                       "transfer": ("NVLS " + nvls_note if nvls_mode != fx.NVLS_OFF else
+                                    (ag_transfer if pattern == 0 else "epilogue P2P")),
                        "l2": "flushed between timed steps outside the events (256 MiB write, then a 256 MiB read "
                              "sweep so no dirty lines drain inside the timed region)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "overlap": extra,
         }
+        if args.nvls:
+            line["nvls"] = nvls_note
         print(json.dumps(line), flush=True)
     comm.close()
     if dist is not None:
@@ -692,6 +711,7 @@ def main():
     ap.add_argument("--ag-engine", type=int, default=0, help="0 auto, 1 copy engines, 2 in-kernel (SM) transfers")
     ap.add_argument("--cta-group", type=int, default=0, help="0 auto, 1 single-CTA tiles, 2 CTA pairs")
     ap.add_argument("--write-mode", type=int, default=0, help="RS: 0 WriteAlltoAll, 1 FusedReduce")
+    ap.add_argument("--nvls", type=int, default=0, help="1: NVLS multicast (emulated when ranks share one GPU)")
     ap.add_argument("--nondeterministic", action="store_true", help="RS FusedReduce in arrival order (red.add)")
     args = ap.parse_args()
     if args.impl == "reference":
