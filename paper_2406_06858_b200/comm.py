@@ -192,28 +192,47 @@ class Communicator:
         return comm
 
     def _nvls_ipc_setup(self, rank: int, tp: int, nvls_bytes: int, all_gather_bytes) -> None:
+        """Every step ends with an exchange of per-rank status, so a failure on
+        any rank raises the same error on all of them (nobody waits forever)."""
         lib = N.lib()
+
+        def agree(status: bytes, payload: bytes = b"") -> list[bytes]:
+            got = all_gather_bytes(status + b"\0" + payload)
+            for r, g in enumerate(got):
+                st = g.split(b"\0", 1)[0]
+                if st != b"ok":
+                    raise N.CudaError(f"rank {r}: " + st.decode(errors="replace"))
+            return [g.split(b"\0", 1)[1] for g in got]
+
         status, server, name = b"ok", None, b""
         if rank == 0:
             fd = C.c_int(-1)
-            if lib.flux_comm_nvls_ipc_export(self._h, nvls_bytes, C.byref(fd)) != N.OK:
-                status = lib.flux_last_error()
+            try:
+                if lib.flux_comm_nvls_ipc_export(self._h, nvls_bytes, C.byref(fd)) != N.OK:
+                    status = lib.flux_last_error()
+                else:
+                    name = ("flux-nvls-%d-%s" % (os.getpid(), os.urandom(6).hex())).encode()
+                    server = fd_server(name.decode(), fd.value)  # listening before the peers learn the name
+            except OSError as e:
+                status = ("fd hand-off socket: %s" % e).encode()
+                if fd.value >= 0 and server is None:
+                    os.close(fd.value)
+        name0 = agree(status, name)[0]
+        status = b"ok"
+        try:
+            if rank == 0:
+                server.serve(tp - 1)
             else:
-                name = ("flux-nvls-%d-%s" % (os.getpid(), os.urandom(6).hex())).encode()
-                server = fd_server(name.decode(), fd.value)  # listening before the peers learn the name
-        got = all_gather_bytes(status + b"\0" + name)
-        st0, name0 = got[0].split(b"\0", 1)
-        if st0 != b"ok":
-            raise N.CudaError(st0.decode(errors="replace"))
-        if rank == 0:
-            server.serve(tp - 1)
-        else:
-            fd = fd_receive(name0.decode())
-            N.check(lib.flux_comm_nvls_ipc_import(self._h, nvls_bytes, fd))
-        N.check(lib.flux_comm_nvls_ipc_add_device(self._h))
-        all_gather_bytes(b"added")  # every GPU is in the object before anyone binds
-        N.check(lib.flux_comm_nvls_ipc_bind(self._h))
-        all_gather_bytes(b"bound")  # every region mapped and zeroed before the first operator
+                fd = fd_receive(name0.decode())
+                if lib.flux_comm_nvls_ipc_import(self._h, nvls_bytes, fd) != N.OK:
+                    status = lib.flux_last_error()
+            if status == b"ok" and lib.flux_comm_nvls_ipc_add_device(self._h) != N.OK:
+                status = lib.flux_last_error()
+        except OSError as e:
+            status = ("fd hand-off: %s" % e).encode()
+        agree(status)  # every GPU is in the object before anyone binds
+        status = b"ok" if lib.flux_comm_nvls_ipc_bind(self._h) == N.OK else lib.flux_last_error()
+        agree(status)  # every region mapped and zeroed before the first operator
 
     # ---- buffers -------------------------------------------------------------
     def buffer(self, rank: int, kind: int, problem: ProblemSpec) -> N.BufferDesc:
