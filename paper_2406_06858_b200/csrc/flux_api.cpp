@@ -543,6 +543,10 @@ struct flux_comm {
     int fault_kind = 0, fault_rank = 0, fault_index = 0;
     int act_fault_kind = 0, act_fault_rank = 0, act_fault_index = 0;
     bool check_double = false;      // flux_comm_set_check_double_set
+    // Graph-safe operators on a one-process-per-GPU communicator: ordered by
+    // device-side rank barriers instead of host stream memops (see graph_ipc_op).
+    bool graph_ipc = false;         // a graph-safe operator is being enqueued
+    bool last_was_graph = false;    // the previous operator was graph-safe (eager ones fence first)
     std::string host_error;         // host-detected failure of the last operator (flag set twice)
     // NVLS multicast region (flux_comm_opts.nvls_bytes): one multicast object over
     // every rank's GPU; each rank's VMM allocation is bound to it and mapped at
@@ -573,6 +577,9 @@ std::string error_text(const uint32_t* err, int r) {
         return "deadlock budget exhausted waiting for signal " + S(err[1]) + " for tile (" + S(err[2] >> 16) + "," +
                S(err[2] & 0xFFFF) + ") on rank " + S(r);
     if (err[0] == kErrDoubleSet) return "flag " + S(err[1]) + " on rank " + S(err[2]) + " set twice";
+    if (err[0] == kErrBarrierTimeout)
+        return "deadlock budget exhausted at the rank barrier of a graph-safe operator (barrier " + S(err[1]) +
+               ", waiting for " + S(err[3]) + " arrivals) on rank " + S(r);
     return "deadlock budget exhausted waiting for partial of tile " + S(err[1]) + " from source " + S(err[2]) +
            " on rank " + S(r);
 }
@@ -841,7 +848,7 @@ cudaStream_t stream_for(flux_comm* c, int rank, void* const* streams) {
 // Tile schedules are immutable: upload each distinct table once per device and
 // reuse it (no host sync on the launch path).
 int mark_op_done(flux_comm* c, void* const* streams, uint32_t e) {
-    if (!c->ipc) return FLUX_OK;
+    if (!c->ipc || c->graph_ipc) return FLUX_OK;  // graph-safe: device barriers order the operators
     for (int r = 0; r < c->tp; ++r) {
         if (!c->ranks[r].local) continue;
         FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
@@ -1960,7 +1967,10 @@ static int graph_zero(flux_comm* c, const flux_problem* p, void* const* streams)
         z.bytes[z.nranges] = static_cast<uint32_t>(bytes);
         ++z.nranges;
     };
-    add(kCtrlReady, kCtrlRedExit + 4 - kCtrlReady);  // ready / done / kdone / fr_ready / trace / work counters
+    // ready / done / kdone / fr_ready / trace / work counters; across processes the
+    // first four are the eager operators' cross-process epoch stamps and stay.
+    if (c->ipc) add(kCtrlTraceCursor, kCtrlRedExit + 4 - kCtrlTraceCursor);
+    else add(kCtrlReady, kCtrlRedExit + 4 - kCtrlReady);
     add(kAgFlagOffset, std::min<size_t>(kAgFlagCap, static_cast<size_t>(p->m)) * 4);
     add(kAgCtrGraphOffset, (static_cast<size_t>((p->m + kBM - 1) / kBM) + 1) * 4);
     add(kTailCtrOffset, static_cast<size_t>(2 * kTailCtrCap) * 4);  // arrival + RS-units staged counters
@@ -1987,7 +1997,6 @@ static int graph_opts(flux_comm* c, const flux_problem* p, const flux_opts* opts
     if (!out->graph_safe) return FLUX_OK;
     FLUX_TRY(check_comm(c));
     if (!p) return fail(FLUX_ERR_CONFIG, "null problem");
-    if (c->ipc) return fail(FLUX_ERR_CONFIG, "graph_safe operators need every rank in this process");
     if (p->pattern == FLUX_ALLGATHER_GEMM && transfer >= 0) {
         if (out->ag_engine == 1 || !ag_sm_engine_ok(p, transfer))
             return fail(FLUX_ERR_CONFIG, "graph_safe AllGather needs the in-kernel transfer engine (k % 8 == 0)");
@@ -2093,6 +2102,64 @@ int flux_medium_grained(flux_comm* c, const flux_problem* p, const flux_tile* ti
     return run_op(c, [&] { return medium_grained_body(c, p, tile, partitions, opts, streams); });
 }
 
+// Device-side barrier across the processes of an IPC communicator, enqueued on
+// this rank's stream (monotonic counters in the control blocks, never reset).
+static int rank_barrier(flux_comm* c, void* const* streams, uint32_t epoch) {
+    const int me = c->my_rank;
+    RankState& rs = c->ranks[me];
+    FLUX_CUDA(cudaSetDevice(rs.device));
+    BarrierParams b;
+    std::memset(&b, 0, sizeof(b));
+    b.gen = at<uint32_t>(rs, kCtrlBarGen);
+    b.arr = at<uint32_t>(rs, kCtrlBarArr);
+    for (int q = 0; q < c->tp; ++q) b.peer_arr[q] = at<uint32_t>(c->ranks[q], kCtrlBarArr);
+    b.err = at<uint32_t>(rs, kCtrlErr);
+    b.err_host = c->err_host;
+    b.tp = c->tp;
+    b.me = me;
+    b.epoch = epoch;
+    b.timeout_ns = 10000000000ull;
+    FLUX_CUDA(launch_rank_barrier(b, stream_for(c, me, streams)));
+    return FLUX_OK;
+}
+
+// A graph-safe operator on a one-process-per-GPU communicator. Captured in a
+// CUDA graph it replays with the epoch and targets it was captured with, so
+// instead of the eager operators' host stream memops (epoch stamps and waits,
+// which a replay would repeat with stale values) it is bracketed by device
+// barriers: A — every rank has finished its previous operator; zero this
+// rank's flags and counters; B — every rank has zeroed (no peer stamps a flag
+// before its owner cleared it); then the kernel. It reuses the current epoch
+// (its stamps are older than any later eager operator's) and leaves the host
+// epoch unchanged, so eager operators' cross-process stamps stay consistent;
+// the next eager operator enters barrier A first (see eager_after_graph).
+static int graph_ipc_op(flux_comm* c, const flux_problem* p, void* const* streams, const std::function<int()>& impl) {
+    if (c->epoch == 0) c->epoch = 1;  // graph stamps must stay behind every later eager epoch
+    const uint32_t e = c->epoch;
+    FLUX_TRY(rank_barrier(c, streams, e));
+    FLUX_TRY(graph_zero(c, p, streams));
+    FLUX_TRY(rank_barrier(c, streams, e));
+    c->graph_ipc = true;
+    c->epoch = e - 1;  // the operator bumps it back to e
+    const int rc = impl();
+    c->graph_ipc = false;
+    c->epoch = e;
+    c->last_was_graph = true;
+    return rc;
+}
+
+// An eager operator right after graph-safe ones (IPC): every peer has finished
+// those (whose completion no epoch stamp records) before this one starts, and
+// the current epoch's done stamps exist (a graph-first communicator never
+// wrote them).
+static int eager_after_graph(flux_comm* c, void* const* streams) {
+    if (!c->ipc || c->graph_ipc || !c->last_was_graph) return FLUX_OK;
+    FLUX_TRY(rank_barrier(c, streams, c->epoch + 1));
+    FLUX_TRY(mark_op_done(c, streams, c->epoch));
+    c->last_was_graph = false;
+    return FLUX_OK;
+}
+
 static int ag_gemm_ex_body(flux_comm* c, const flux_problem* p, const flux_tile* tile, int rpct, int transfer,
                            int swizzle_on, const flux_opts* opts, void* const* streams, const flux_operands* operands) {
     flux_opts o;
@@ -2100,6 +2167,9 @@ static int ag_gemm_ex_body(flux_comm* c, const flux_problem* p, const flux_tile*
     if (!o.graph_safe) return ag_gemm_impl(c, p, tile, rpct, transfer, swizzle_on, &o, streams, operands);
     FLUX_TRY(validate_tiling(p, tile));
     FLUX_TRY(check_heap(c, p));
+    if (c->ipc)
+        return graph_ipc_op(c, p, streams,
+                            [&] { return ag_gemm_impl(c, p, tile, rpct, transfer, swizzle_on, &o, streams, operands); });
     FLUX_TRY(graph_zero(c, p, streams));
     return ag_gemm_impl(c, p, tile, rpct, transfer, swizzle_on, &o, streams, operands);
 }
@@ -2113,6 +2183,9 @@ static int gemm_rs_ex_body(flux_comm* c, const flux_problem* p, const flux_tile*
         return fail(FLUX_ERR_CONFIG, "graph_safe is not available with the arrival-order FusedReduce");
     FLUX_TRY(validate_tiling(p, tile));
     FLUX_TRY(check_heap(c, p));
+    if (c->ipc)
+        return graph_ipc_op(c, p, streams,
+                            [&] { return gemm_rs_impl(c, p, tile, write_mode, swizzle_on, &o, streams, operands); });
     FLUX_TRY(graph_zero(c, p, streams));
     return gemm_rs_impl(c, p, tile, write_mode, swizzle_on, &o, streams, operands);
 }
@@ -2142,6 +2215,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
     FLUX_TRY(check_heap(c, p));
     FLUX_TRY(check_activation(c, p, opts, operands));
     FLUX_TRY(check_b_layout(c, p, opts, operands));
+    FLUX_TRY(eager_after_graph(c, streams));
     const int tp = p->tp, rpr = rows_per_rank(p);
     if (rpct <= 0) rpct = rpr;
     if (p->m / rpct > static_cast<int>(kAgFlagCap)) return fail(FLUX_ERR_CONFIG, "too many comm tiles");
@@ -2260,9 +2334,11 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
             // (in-process peers on other devices by event, other processes by `done`).
             for (int q = 0; q < tp; ++q) {
                 if (q == r) continue;
-                if (!c->ranks[q].local) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
-                else if (c->ranks[q].device != rs.device && c->ranks[q].kernel_evt_valid)
+                if (!c->ranks[q].local) {
+                    if (!c->graph_ipc) FLUX_TRY(wait_value_geq(s, c->ranks[q].heap + kCtrlDone, e - 1));
+                } else if (c->ranks[q].device != rs.device && c->ranks[q].kernel_evt_valid) {
                     FLUX_CUDA(cudaStreamWaitEvent(s, c->ranks[q].kernel_evt, 0));
+                }
             }
             if (reset) FLUX_CUDA(cudaMemsetAsync(rs.heap + ctr_off, 0, (static_cast<size_t>(groups) + 1) * 4, s));
         }
@@ -2371,7 +2447,7 @@ static int ag_gemm_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         };
         FLUX_TRY(launch_groups(c, p, kModeAG, oc, streams, seq, rpct, step_major ? kInterleaveStep : kInterleaveRank,
                                cg, false, -1, 0, extra));
-        if (c->ipc) {
+        if (c->ipc && !c->graph_ipc) {
             for (int r : mine) {
                 FLUX_CUDA(cudaSetDevice(c->ranks[r].device));
                 cudaStream_t s = stream_for(c, r, streams);
@@ -2657,6 +2733,7 @@ static int gemm_rs_impl(flux_comm* c, const flux_problem* p, const flux_tile* ti
         return fail(FLUX_ERR_CONFIG, "unknown write mode");
     FLUX_TRY(check_activation(c, p, opts, operands));
     FLUX_TRY(check_b_layout(c, p, opts, operands));
+    FLUX_TRY(eager_after_graph(c, streams));
     const int tp = p->tp, rpr = rows_per_rank(p);
     const int tiles = ((p->m + kBM - 1) / kBM) * ((p->n + kBN - 1) / kBN);
     if (static_cast<size_t>(tiles) * tp > kRsFlagCap) return fail(FLUX_ERR_CONFIG, "too many output tiles for the flag table");
@@ -2793,6 +2870,7 @@ static int nonoverlap_body(flux_comm* c, const flux_problem* p, const flux_opts*
     if (opts && opts->graph_safe) return fail(FLUX_ERR_CONFIG, "graph_safe applies to the fused operators and the local GEMM");
     FLUX_TRY(validate_problem(p));
     FLUX_TRY(check_heap(c, p));
+    FLUX_TRY(eager_after_graph(c, streams));
     const int tp = p->tp, rpr = rows_per_rank(p), lk = local_k(p);
     std::vector<int> mine;
     local_ranks_only(c, mine);

@@ -42,6 +42,10 @@ constexpr size_t kCtrlDynCtr = 88;      // u32: dynamic tile scheduler — next 
 constexpr size_t kCtrlDynExit = 92;     // u32: dynamic tile scheduler — clusters finished
 constexpr size_t kCtrlRedCtr = 96;      // u32: decode RS reduction — next unit (zeroed by the last group out)
 constexpr size_t kCtrlRedExit = 100;    // u32: decode RS reduction — groups finished
+// Device-side rank barrier (graph-safe operators of the one-process-per-GPU
+// communicator): monotonic, never zeroed (outside every graph_zero range).
+constexpr size_t kCtrlBarGen = 104;     // u32: barriers this rank has entered
+constexpr size_t kCtrlBarArr = 108;     // u32: arrivals of peers at this rank's barriers
 constexpr size_t kTraceBytes = size_t(4) << 20;  // trace ring at the end of the data region (16 B records)
 // Trace record kinds (the reference CausalityLog event names, engine.hpp:37-63).
 // kEvLaunch (not in the reference schema): a CTA's first (tile_col 0) and last (tile_col 1)
@@ -87,7 +91,8 @@ constexpr size_t kNvlsDataOffset = 64 * 1024;  // kAgFlagCap u32 flags before it
 // Error codes written by device waits into the control block.
 constexpr uint32_t kErrAgFlagTimeout = 1;
 constexpr uint32_t kErrRsFlagTimeout = 2;
-constexpr uint32_t kErrDoubleSet = 3;   // a flag stamped twice in one operator (signal_board.hpp:25-28)
+constexpr uint32_t kErrDoubleSet = 3;       // a flag stamped twice in one operator (signal_board.hpp:25-28)
+constexpr uint32_t kErrBarrierTimeout = 4;  // a graph-safe operator's rank barrier
 
 // Fault injection (tests: the reference's deadlock / double-set paths,
 // acceptance.cpp:121-158, engine.cpp:401-403): armed for one operator.
@@ -245,5 +250,20 @@ struct ZeroParams {
     int nranges;
 };
 cudaError_t launch_zero_ranges(const ZeroParams& p, int nheaps, cudaStream_t stream);
+// One-thread barrier across the ranks of a multi-process communicator: enter
+// (gen += 1), arrive at every peer (arr += 1, release, system scope), wait until
+// this rank's arrivals reach gen x (tp - 1) (acquire), bounded by timeout_ns
+// (the error word gets kErrBarrierTimeout).
+struct BarrierParams {
+    uint32_t* gen;
+    uint32_t* arr;
+    uint32_t* peer_arr[kMaxRanks];
+    uint32_t* err;       // this rank's control block (error record)
+    uint32_t* err_host;  // host-mapped mirror [rank][8]
+    int tp, me;
+    uint32_t epoch;
+    uint64_t timeout_ns;
+};
+cudaError_t launch_rank_barrier(const BarrierParams& p, cudaStream_t stream);
 
 }  // namespace fluxb200

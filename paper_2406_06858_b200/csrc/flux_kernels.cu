@@ -2438,6 +2438,43 @@ __global__ void zero_ranges_kernel(ZeroParams p) {
     }
 }
 
+__global__ void rank_barrier_kernel(BarrierParams p) {
+    if (threadIdx.x != 0) return;
+    const uint32_t g = atomicAdd(p.gen, 1u) + 1u;
+    for (int q = 0; q < p.tp; ++q)
+        if (q != p.me) red_release_sys_add(p.peer_arr[q], 1u);
+    const uint32_t target = g * static_cast<uint32_t>(p.tp - 1);
+    const uint64_t t0 = globaltimer();
+    uint32_t ns = 32;
+    while (static_cast<int32_t>(ld_acquire_sys(p.arr) - target) < 0) {
+        if (globaltimer() - t0 > p.timeout_ns) {
+            if (atomicCAS(p.err, 0u, kErrBarrierTimeout) == 0u) {
+                p.err[1] = g;
+                p.err[2] = ld_acquire_sys(p.arr);
+                p.err[3] = target;
+                p.err[kCtrlErrEpoch / 4] = p.epoch;
+                p.err[kCtrlErrEpoch / 4 + 1] = static_cast<uint32_t>(p.me) + 1u;
+                if (p.err_host) {
+                    volatile uint32_t* hh = p.err_host + 8 * p.me;
+                    hh[1] = g;
+                    hh[3] = target;
+                    hh[5] = static_cast<uint32_t>(p.me) + 1u;
+                    __threadfence_system();
+                    hh[0] = kErrBarrierTimeout;
+                }
+            }
+            return;
+        }
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+    }
+}
+
+cudaError_t launch_rank_barrier(const BarrierParams& p, cudaStream_t stream) {
+    rank_barrier_kernel<<<1, 32, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_zero_ranges(const ZeroParams& p, int nheaps, cudaStream_t stream) {
     zero_ranges_kernel<<<nheaps, 512, 0, stream>>>(p);
     return cudaGetLastError();

@@ -76,3 +76,22 @@ def test_two_processes_nvls():
         for case, (err, tol) in r["results"].items():
             assert err <= tol, (case, err, tol)
 
+
+
+@pytest.mark.gpu
+def test_two_processes_graph_replay():
+    """Graph-safe operators on the one-process-per-GPU communicator: captured
+    in a CUDA graph and replayed on new inputs (device rank barriers instead of
+    host stream memops), eager operators in between and after; every result
+    matches the oracle (tile kernel and streaming decode kernel, AG and RS)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29553", os.path.join(ROOT, "scripts", "mp_graph_worker.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    print(out.stdout[-4000:], out.stderr[-4000:])
+    assert out.returncode == 0
+    res = [json.loads(l.split(" ", 2)[2]) for l in out.stdout.splitlines() if l.startswith("RESULT")]
+    assert len(res) == 2
+    for r in res:
+        assert len(r) == 4
+        for case, (err, tol, n) in r.items():
+            assert n == 9 and err <= tol, (case, err, tol, n)
