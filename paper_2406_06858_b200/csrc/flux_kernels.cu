@@ -2013,6 +2013,51 @@ __device__ __forceinline__ void sk_store(const GemmParams& p, int l, int col, in
     }
 }
 
+// The canonical-order sum of this rank's rows of n-tile j (other sources
+// ascending, then this rank) into C, KB float4 groups per thread in flight with
+// their sources (RMAX >= tp; NVLS loads one reduced group). Epilogue warps (128 threads).
+template <int PB, int KB, int RMAX>
+__device__ __forceinline__ void sk_rs_sum(const GemmParams& p, int l, int j, int F, int me, int tp, long long e0,
+                                          const float* sbase, int et) {
+    for (int f0 = et; f0 < F; f0 += 128 * KB) {
+        float4 w[KB][RMAX];
+#pragma unroll
+        for (int u = 0; u < KB; ++u) {
+            const int f = f0 + u * 128;
+            const int lr = f / (kSkRows / 4), c2 = j * kSkRows + (f % (kSkRows / 4)) * 4;
+            if (f >= F || c2 >= p.n) continue;
+            const long long e = e0 + static_cast<long long>(lr) * p.ld_stage + c2;
+            if (p.nvls) {
+                asm volatile("fence.proxy.alias;" ::: "memory");
+                w[u][0] = nvls_ld_reduce4(p, e + me * p.stage_plane);
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 < RMAX; ++s2)
+                    if (s2 < tp) w[u][s2] = ld_part4<PB>(sbase, e + s2 * p.stage_plane);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < KB; ++u) {
+            const int f = f0 + u * 128;
+            const int lr = f / (kSkRows / 4), c2 = j * kSkRows + (f % (kSkRows / 4)) * 4;
+            if (f >= F || c2 >= p.n) continue;
+            float acc[4];
+            bool first = true;
+            if (p.nvls) {
+                sum_into(acc, w[u][0], first);
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 < RMAX; ++s2)
+                    if (s2 < tp && s2 != me) sum_into(acc, w[u][s2], first);
+#pragma unroll
+                for (int s2 = 0; s2 < RMAX; ++s2)
+                    if (s2 == me) sum_into(acc, w[u][s2], first);
+            }
+            store_row<4>(p.c[l], static_cast<long long>(lr) * p.ldc_l[l] + c2, c2, p.n, p.out_f32, acc);
+        }
+    }
+}
+
 // GEMM-RS in the streaming kernel, once n-tile j of slot l is complete in this
 // CTA and its partial rows are in every owner's plane (this rank's own rows
 // included): stamp the peers' flags, then finish this rank's own rows here —
@@ -2035,35 +2080,13 @@ __device__ __forceinline__ void sk_rs_finish(const GemmParams& p, int l, int j, 
     const float* const sbase = p.staging[me];
     const long long e0 = static_cast<long long>(p.epoch & 1u) * p.stage_parity;
     const int F = min(rpr, mv - me * rpr) * (kSkRows / 4);  // float4 groups of my rows
-    // (One group per thread at a time: this code runs once per launch on a
-    // cold instruction cache, where a batched, longer body measured slower.)
-    for (int f = et; f < F; f += 128) {
-        const int lr = f / (kSkRows / 4), c2 = j * kSkRows + (f % (kSkRows / 4)) * 4;
-        if (c2 >= p.n) continue;
-        const long long e = e0 + static_cast<long long>(lr) * p.ld_stage + c2;
-        float acc[4];
-        if (p.nvls) {
-            asm volatile("fence.proxy.alias;" ::: "memory");
-            const float4 r4 = nvls_ld_reduce4(p, e + me * p.stage_plane);
-            acc[0] = r4.x;
-            acc[1] = r4.y;
-            acc[2] = r4.z;
-            acc[3] = r4.w;
-        } else {
-            float4 w[kMaxRanks];
-#pragma unroll
-            for (int s2 = 0; s2 < kMaxRanks; ++s2)
-                if (s2 < tp) w[s2] = ld_part4<PB>(sbase, e + s2 * p.stage_plane);
-            bool first = true;
-#pragma unroll
-            for (int s2 = 0; s2 < kMaxRanks; ++s2)
-                if (s2 < tp && s2 != me) sum_into(acc, w[s2], first);
-#pragma unroll
-            for (int s2 = 0; s2 < kMaxRanks; ++s2)
-                if (s2 == me) sum_into(acc, w[s2], first);
-        }
-        store_row<4>(p.c[l], static_cast<long long>(lr) * p.ldc_l[l] + c2, c2, p.n, p.out_f32, acc);
-    }
+    // One source (one rank per owner, or NVLS summing in the switch): four groups
+    // per thread in flight; the rows are otherwise a chain of dependent DRAM
+    // round trips (M=64 at tp=1: 16 per thread). More sources: one group at a
+    // time with every source's load (this code runs once per launch on a cold
+    // instruction cache, where a longer body measured slower).
+    if (p.nvls || tp == 1) sk_rs_sum<PB, 4, 1>(p, l, j, F, me, tp, e0, sbase, et);
+    else sk_rs_sum<PB, 1, kMaxRanks>(p, l, j, F, me, tp, e0, sbase, et);
 }
 
 template <int MODE, int PB = 0, int ACT = 0>

@@ -1,7 +1,9 @@
 """Profiling aid: per-op device time of decode GEMM-RS / AG-GEMM shapes (ranks
 emulated on one GPU, L2 flushed between ops) for the package under ROOT
-(A/B of two builds). python scripts/rs_ab.py ROOT"""
+(A/B of two builds: two package roots, or one root and FLUX_LIB_PATH).
+python scripts/rs_ab.py ROOT [shape ...]"""
 import json
+import os
 import sys
 
 import torch
@@ -13,7 +15,13 @@ from paper_2406_06858_b200 import _native as N  # noqa: E402
 SHAPES = {"rs-down-m16-tp8": (1, 16, 8192, 28672, 8), "rs-attn-m16-tp8": (1, 16, 8192, 8192, 8),
           "rs-down-m128-tp8": (1, 128, 8192, 28672, 8), "rs-attn-m128-tp8": (1, 128, 8192, 8192, 8),
           "ag-up-m128-tp8": (0, 128, 28672, 8192, 8), "rs-1024-tp2": (1, 1024, 1024, 1024, 2),
-          "ag-up-m16-tp8": (0, 16, 28672, 8192, 8), "ag-up-m512-tp8": (0, 512, 28672, 8192, 8)}
+          "ag-up-m16-tp8": (0, 16, 28672, 8192, 8), "ag-up-m512-tp8": (0, 512, 28672, 8192, 8),
+          # one GPU's TP=8 decode share (tp=1 problems with the per-rank shapes)
+          "rank-rs-attn-m128": (1, 128, 8192, 1024, 1), "rank-rs-attn-m512": (1, 512, 8192, 1024, 1),
+          "rank-rs-down-m128": (1, 128, 8192, 3584, 1), "rank-rs-down-m512": (1, 512, 8192, 3584, 1),
+          "rs-attn-m512-tp8": (1, 512, 8192, 8192, 8),
+          "rank-rs-attn-m16": (1, 16, 8192, 1024, 1), "rank-rs-attn-m64": (1, 64, 8192, 1024, 1),
+          "rank-rs-down-m16": (1, 16, 8192, 3584, 1), "rank-rs-down-m64": (1, 64, 8192, 3584, 1)}
 if len(sys.argv) > 2:
     SHAPES = {k: v for k, v in SHAPES.items() if k in sys.argv[2:]}
 dev = torch.device("cuda", 0)
@@ -32,7 +40,7 @@ for name, (pat, m, n, k, tp) in SHAPES.items():
     tile = fx.TileShape(p.rows_per_rank(), p.local_cols())
     o = fx.default_opts()
     if hasattr(o, "decode_kernel"):
-        o.decode_kernel = 1  # tile kernel
+        o.decode_kernel = int(os.environ.get("DK", "1"))  # 1 = tile kernel (default here), 0 = auto, 2 = streaming
     op = (lambda: comm.ag_gemm(p, tile, m // tp, fx.PULL, True, o, s)) if pat == 0 else \
         (lambda: comm.gemm_rs(p, tile, fx.WRITE_ALLTOALL, True, o, s))
     for _ in range(3):
@@ -48,5 +56,5 @@ for name, (pat, m, n, k, tp) in SHAPES.items():
         e1.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e3)
     ts.sort()
-    print(json.dumps({"root": sys.argv[1], "shape": name, "us": round(ts[len(ts) // 2], 1)}), flush=True)
+    print(json.dumps({"root": sys.argv[1], "lib": os.environ.get("FLUX_LIB_PATH", ""), "shape": name, "us": round(ts[len(ts) // 2], 1)}), flush=True)
     comm.close()

@@ -40,7 +40,9 @@ def _run(comm, p, f32=True, **kw):
 CASES = [(AG, 16, 3584, 8192, 1), (RS, 16, 8192, 3584, 1), (RS, 16, 8192, 1024, 1), (AG, 64, 3584, 8192, 1),
          (AG, 128, 1024, 2048, 1), (RS, 128, 2048, 1024, 1), (AG, 16, 1024, 512, 8), (RS, 16, 1024, 1024, 8),
          (RS, 64, 2048, 512, 4), (AG, 24, 600, 200, 2), (RS, 40, 24, 72, 4), (AG, 3, 130, 70, 1),
-         (RS, 8, 136, 4096, 2), (AG, 100, 256, 64, 4)]
+         (RS, 8, 136, 4096, 2), (AG, 100, 256, 64, 4),
+         # one source per owner row (tp=1): the finish keeps four row groups per thread in flight
+         (RS, 64, 8192, 1024, 1), (RS, 40, 200, 300, 1), (RS, 7, 136, 4096, 1)]
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c)))
