@@ -998,8 +998,11 @@ bool stream_kernel_ok(flux_comm* c, const flux_problem* p, int mode, const OpCom
     // (scripts/stream_check.py, one GPU's Llama-2-70B TP=8 decode share, L2 flushed):
     // M=16 AG up-proj 37.9 -> 29.7 us, RS down-proj 52.2 -> 44.0, RS attn-out 48.2 ->
     // 37.9; M=64 35.8 -> 31.7; at M=128, and with eight ranks emulated in one launch,
-    // the tile kernel is as fast or faster.
-    return m_rows <= 64 && nslots == 1;
+    // the tile kernel is as fast or faster. GEMM-RS up to 128 rows since the finish
+    // keeps four row groups per thread in flight (one GPU's share at M=128,
+    // scripts/rs_ab.py: attn-out tile 42.0 / stream 35.8 us, down-proj 52.2 / 42.0;
+    // AG up-proj stays on the tile kernel there: 33.8 / 37.9).
+    return nslots == 1 && (m_rows <= 64 || (mode == kModeRSUnits && m_rows <= 128));
 }
 
 // Launch one fused kernel per device group. `mode` selects the role.

@@ -74,19 +74,25 @@ def test_stream_kernel_bit_identical_across_runs(case):
                 assert np.array_equal(first[r], again[r]), (seed, r)
 
 
-def test_stream_kernel_is_the_auto_choice_for_one_rank_per_gpu_decode():
-    """Auto (decode_kernel=0) takes the streaming kernel for <= 64 rows with one
-    rank per GPU: outputs bit-identical to the forced choice, and different
-    from (but within tolerance of) the tile kernel's, whose K order differs."""
-    p = fx.ProblemSpec(16, 3584, 8192, 1, AG)
+@pytest.mark.parametrize("case,auto_kernel", [((AG, 16, 3584, 8192), STREAM), ((RS, 128, 8192, 1024), STREAM),
+                                               ((AG, 128, 1024, 2048), fx.DECODE_TILE)],
+                         ids=["ag16-stream", "rs128-stream", "ag128-tile"])
+def test_stream_kernel_is_the_auto_choice_for_one_rank_per_gpu_decode(case, auto_kernel):
+    """Auto (decode_kernel=0) with one rank per GPU takes the streaming kernel
+    for <= 64 rows, and for GEMM-RS up to 128: outputs bit-identical to the
+    forced choice; both kernels within tolerance of the oracle (their K orders
+    differ)."""
+    pat, m, n, k = case
+    p = fx.ProblemSpec(m, n, k, 1, pat)
     with H.make_comm(p) as comm:
         a, b = H.upload(comm, p, seed=2)
         auto = _run(comm, p, True)
-        forced = _run(comm, p, True, decode_kernel=STREAM)
-        tile = _run(comm, p, True, decode_kernel=fx.DECODE_TILE)
+        forced = _run(comm, p, True, decode_kernel=auto_kernel)
+        other = _run(comm, p, True, decode_kernel=fx.DECODE_TILE if auto_kernel == STREAM else STREAM)
         assert np.array_equal(auto[0], forced[0])
-        want = O.dense_oracle(AG, 16, 3584, 8192, 1, a, b)
-        assert O.max_rel_error(tile[0], want[0]) <= H.tol(True, 8192)
+        want = O.dense_oracle(pat, m, n, k, 1, a, b)
+        assert O.max_rel_error(auto[0], want[0]) <= H.tol(True, k)
+        assert O.max_rel_error(other[0], want[0]) <= H.tol(True, k)
 
 
 @pytest.mark.parametrize("engine", [1, 2])
