@@ -2102,6 +2102,11 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
     // fp32 slot per non-leader segment (padded rows: conflict-free v4 stores).
     const int cl = p.sk_cluster, ldr = mp + 4;
     const bool ring = cl > 1 && p.sk_red_ring;  // one tile per cluster: the drained ring holds the slots
+    // Ring mode with more than one 16-row chunk (GEMM-RS excepted: its owner finish
+    // needs the whole tile from one CTA): every CTA sums and stores the chunks
+    // q == its rank (mod cl), so the slices spread over the cluster instead of
+    // converging on the leader.
+    const bool dist = ring && MODE != kModeRSUnits && min(p.m, mp) > 16;
     float* sRed = ring ? reinterpret_cast<float*>(sW) : reinterpret_cast<float*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0));
     const int red_bytes = cl > 1 && !ring ? (cl - 1) * kSkRows * ldr * 4 : 0;
     uint64_t* full = reinterpret_cast<uint64_t*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0) + red_bytes);
@@ -2136,7 +2141,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
         }
         if (cl > 1) {
             mbar_init(&red_bar[0], (cl - 1) * 128);
-            mbar_init(&red_bar[1], 1);
+            mbar_init(&red_bar[1], dist ? cl - 1 : 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -2269,7 +2274,66 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                 tc_fence_after();
                 const uint32_t tbase =
                     tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(as * p.sk_acc_cols);
-                if (crank != 0) {
+                if (dist) {
+                    // 1. My MMAs retired: my drained ring may take the other CTAs' slices;
+                    //    wait until every other CTA's ring may take mine.
+                    if (et < cl && et != static_cast<int>(crank))
+                        mbar_arrive_cluster(mapa(smem_u32(&red_bar[1]), static_cast<uint32_t>(et)));
+                    mbar_wait_acq_cluster(&red_bar[1], 0);
+                    // 2. My segment's chunks that other CTAs own, into their slot for my segment.
+                    for (int m0 = 0; m0 < mv; m0 += 16) {
+                        const int d = (m0 >> 4) % cl;
+                        if (d == static_cast<int>(crank)) continue;
+                        const int sl = static_cast<int>(crank) < d ? static_cast<int>(crank) : static_cast<int>(crank) - 1;
+                        const uint32_t dst = mapa(smem_u32(sRed + (sl * kSkRows + cit) * ldr + m0), static_cast<uint32_t>(d));
+                        uint32_t r[16];
+                        tmem_ld16(tbase + m0, r);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            st_shared_cluster_v4(dst + static_cast<uint32_t>(i) * 4u, r[i], r[i + 1], r[i + 2], r[i + 3]);
+                    }
+                    for (int d = 0; d < cl; ++d)  // release: this thread's stores
+                        if (d != static_cast<int>(crank)) mbar_arrive_cluster(mapa(smem_u32(&red_bar[0]), static_cast<uint32_t>(d)));
+                    mbar_wait_acq_cluster(&red_bar[0], 0);  // every slice of my chunks has landed
+                    // 3. My chunks, K-segments summed in segment order (mine from TMEM): the
+                    //    same additions in the same order as the leader-only reduction.
+                    for (int m0 = static_cast<int>(crank) * 16; m0 < mv; m0 += 16 * cl) {
+                        uint32_t r[16];
+                        tmem_ld16(tbase + m0, r);
+                        tmem_ld_wait();
+                        float v[16];
+                        for (int s2 = 0; s2 < cl; ++s2) {
+                            if (s2 == static_cast<int>(crank)) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) v[i] = s2 == 0 ? __uint_as_float(r[i]) : v[i] + __uint_as_float(r[i]);
+                            } else {
+                                const int sl = s2 < static_cast<int>(crank) ? s2 : s2 - 1;
+                                const float4* src = reinterpret_cast<const float4*>(sRed + (sl * kSkRows + cit) * ldr + m0);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float4 w = src[i];
+                                    if (s2 == 0) {
+                                        v[4 * i] = w.x;
+                                        v[4 * i + 1] = w.y;
+                                        v[4 * i + 2] = w.z;
+                                        v[4 * i + 3] = w.w;
+                                    } else {
+                                        v[4 * i] += w.x;
+                                        v[4 * i + 1] += w.y;
+                                        v[4 * i + 2] += w.z;
+                                        v[4 * i + 3] += w.w;
+                                    }
+                                }
+                            }
+                        }
+                        sk_store<MODE, PB, ACT>(p, l, col, m0, mv, v);
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[as]);
+                    if (et == 0) trace_event(p, 0, kEvLaunch, p.global_rank[0], blockIdx.x, 5, static_cast<uint32_t>(tt));
+                } else if (crank != 0) {
                     // Buffer mode: the leader has read this slot's previous tile (the first
                     // wait passes). Ring mode: the leader's own MMAs are done, so its stage
                     // ring is free to receive.
