@@ -998,11 +998,12 @@ bool stream_kernel_ok(flux_comm* c, const flux_problem* p, int mode, const OpCom
     // (scripts/stream_check.py, one GPU's Llama-2-70B TP=8 decode share, L2 flushed):
     // M=16 AG up-proj 37.9 -> 29.7 us, RS down-proj 52.2 -> 44.0, RS attn-out 48.2 ->
     // 37.9; M=64 35.8 -> 31.7; at M=128, and with eight ranks emulated in one launch,
-    // the tile kernel is as fast or faster. GEMM-RS up to 128 rows since the finish
-    // keeps four row groups per thread in flight (one GPU's share at M=128,
-    // scripts/rs_ab.py: attn-out tile 42.0 / stream 35.8 us, down-proj 52.2 / 42.0;
-    // AG up-proj stays on the tile kernel there: 33.8 / 37.9).
-    return nslots == 1 && (m_rows <= 64 || (mode == kModeRSUnits && m_rows <= 128));
+    // the tile kernel was as fast or faster. Up to 128 rows since the GEMM-RS finish
+    // keeps four row groups per thread in flight and the cluster reduction is
+    // spread over the cluster with compact slots (one GPU's share at M=128,
+    // scripts/rs_ab.py, tile / stream: RS attn-out 42.0 / 35.8 us, RS down-proj
+    // 52.2 / 42.0, AG up-proj 33.8 / 29.7).
+    return nslots == 1 && m_rows <= 128;
 }
 
 // Launch one fused kernel per device group. `mode` selects the role.
@@ -1275,8 +1276,13 @@ int launch_groups(flux_comm* c, const flux_problem* p, int mode, const OpCommon&
                     // the slots, so the dedicated buffer's stages come back (M = 64 AG:
                     // cluster of 4 with 3 -> 8 stages).
                     const int st_ring = std::min(kSkMaxStages, (kSkSmemMax - stream_smem_bytes(mode, sk_mp, 0)) / stage_bytes);
+                    // Distributed ring (AG / Plain, > 16 rows, kernel `dist`): each CTA's
+                    // slots hold only its own 16-row chunks (M = 128 AG: clusters of 4).
+                    const int nchunk = (std::min(m_rows, sk_mp) + 15) / 16;
+                    const bool dist = mode != kModeRSUnits && m_rows > 16;
+                    const int slot_rows = dist ? 16 * ((nchunk + cl - 1) / cl) + 4 : sk_mp + 4;
                     const bool ring = st < 8 && static_cast<long long>(st_ring) * stage_bytes >=
-                                                    static_cast<long long>(cl - 1) * kSkRows * (sk_mp + 4) * 4;
+                                                    static_cast<long long>(cl - 1) * kSkRows * slot_rows * 4;
                     if (ring) st = st_ring;
                     if (st < 4) continue;
                     GemmParams q = prm;

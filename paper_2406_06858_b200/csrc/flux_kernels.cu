@@ -2107,6 +2107,9 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
     // q == its rank (mod cl), so the slices spread over the cluster instead of
     // converging on the leader.
     const bool dist = ring && MODE != kModeRSUnits && min(p.m, mp) > 16;
+    // Distributed slots hold only the receiver's chunks: chunk q at row (q / cl) * 16
+    // of a [128 columns][16 * ceil(chunks / cl) + 4] slot (same conflict-free padding).
+    const int ldd = 16 * (((min(p.m, mp) + 15) / 16 + cl - 1) / max(cl, 1)) + 4;
     float* sRed = ring ? reinterpret_cast<float*>(sW) : reinterpret_cast<float*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0));
     const int red_bytes = cl > 1 && !ring ? (cl - 1) * kSkRows * ldr * 4 : 0;
     uint64_t* full = reinterpret_cast<uint64_t*>(sComm + (MODE == kModeAG ? 2 * kPieceBytes : 0) + red_bytes);
@@ -2285,7 +2288,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                         const int d = (m0 >> 4) % cl;
                         if (d == static_cast<int>(crank)) continue;
                         const int sl = static_cast<int>(crank) < d ? static_cast<int>(crank) : static_cast<int>(crank) - 1;
-                        const uint32_t dst = mapa(smem_u32(sRed + (sl * kSkRows + cit) * ldr + m0), static_cast<uint32_t>(d));
+                        const uint32_t dst = mapa(smem_u32(sRed + (sl * kSkRows + cit) * ldd + (m0 >> 4) / cl * 16), static_cast<uint32_t>(d));
                         uint32_t r[16];
                         tmem_ld16(tbase + m0, r);
                         tmem_ld_wait();
@@ -2309,7 +2312,7 @@ __global__ void __launch_bounds__(kThreads, 1) flux_stream_kernel(const __grid_c
                                 for (int i = 0; i < 16; ++i) v[i] = s2 == 0 ? __uint_as_float(r[i]) : v[i] + __uint_as_float(r[i]);
                             } else {
                                 const int sl = s2 < static_cast<int>(crank) ? s2 : s2 - 1;
-                                const float4* src = reinterpret_cast<const float4*>(sRed + (sl * kSkRows + cit) * ldr + m0);
+                                const float4* src = reinterpret_cast<const float4*>(sRed + (sl * kSkRows + cit) * ldd + (m0 >> 4) / cl * 16);
 #pragma unroll
                                 for (int i = 0; i < 4; ++i) {
                                     const float4 w = src[i];

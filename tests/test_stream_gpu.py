@@ -42,7 +42,9 @@ CASES = [(AG, 16, 3584, 8192, 1), (RS, 16, 8192, 3584, 1), (RS, 16, 8192, 1024, 
          (RS, 64, 2048, 512, 4), (AG, 24, 600, 200, 2), (RS, 40, 24, 72, 4), (AG, 3, 130, 70, 1),
          (RS, 8, 136, 4096, 2), (AG, 100, 256, 64, 4),
          # one source per owner row (tp=1): the finish keeps four row groups per thread in flight
-         (RS, 64, 8192, 1024, 1), (RS, 40, 200, 300, 1), (RS, 7, 136, 4096, 1)]
+         (RS, 64, 8192, 1024, 1), (RS, 40, 200, 300, 1), (RS, 7, 136, 4096, 1),
+         # cluster ring mode with each CTA summing its own 16-row chunks (compact slots)
+         (AG, 128, 3584, 8192, 1), (AG, 48, 3584, 4096, 1), (AG, 100, 1024, 2048, 1)]
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c)))
@@ -75,11 +77,11 @@ def test_stream_kernel_bit_identical_across_runs(case):
 
 
 @pytest.mark.parametrize("case,auto_kernel", [((AG, 16, 3584, 8192), STREAM), ((RS, 128, 8192, 1024), STREAM),
-                                               ((AG, 128, 1024, 2048), fx.DECODE_TILE)],
-                         ids=["ag16-stream", "rs128-stream", "ag128-tile"])
+                                               ((AG, 128, 1024, 2048), STREAM), ((AG, 256, 1024, 2048), fx.DECODE_TILE)],
+                         ids=["ag16-stream", "rs128-stream", "ag128-stream", "ag256-tile"])
 def test_stream_kernel_is_the_auto_choice_for_one_rank_per_gpu_decode(case, auto_kernel):
     """Auto (decode_kernel=0) with one rank per GPU takes the streaming kernel
-    for <= 64 rows, and for GEMM-RS up to 128: outputs bit-identical to the
+    up to 128 rows and the tile kernel above: outputs bit-identical to the
     forced choice; both kernels within tolerance of the oracle (their K orders
     differ)."""
     pat, m, n, k = case
