@@ -23,7 +23,8 @@ SHAPES = {"rs-down-m16-tp8": (1, 16, 8192, 28672, 8), "rs-attn-m16-tp8": (1, 16,
           "rank-rs-attn-m16": (1, 16, 8192, 1024, 1), "rank-rs-attn-m64": (1, 64, 8192, 1024, 1),
           "rank-rs-down-m16": (1, 16, 8192, 3584, 1), "rank-rs-down-m64": (1, 64, 8192, 3584, 1),
           "rank-ag-up-m128": (0, 128, 3584, 8192, 1), "rank-ag-up-m64": (0, 64, 3584, 8192, 1),
-          "rank-ag-up-m32": (0, 32, 3584, 8192, 1), "rank-ag-up-m16": (0, 16, 3584, 8192, 1)}
+          "rank-ag-up-m32": (0, 32, 3584, 8192, 1), "rank-ag-up-m16": (0, 16, 3584, 8192, 1),
+          "rank-ag-up-m256": (0, 256, 3584, 8192, 1), "rank-ag-up-m192": (0, 192, 3584, 8192, 1)}
 if len(sys.argv) > 2:
     SHAPES = {k: v for k, v in SHAPES.items() if k in sys.argv[2:]}
 dev = torch.device("cuda", 0)
