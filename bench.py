@@ -655,7 +655,13 @@ def our_arm(args, wl):
     pk, src = peaks()
     kms = statistics.mean(kernel_ms) if kernel_ms else ms_fused
     roofline = roofline_of(roofline_work(pattern, m, n, k, tp, emulated), kms, pk, src)
-    roofline["kernel"] = "flux_gemm_kernel<AG>" if pattern == 0 else "flux_gemm_kernel<RS>"
+    # Which kernel ran, by the library's auto rule (stream_kernel_ok, flux_api.cpp):
+    # the streaming decode kernel for <= 128 GEMM rows with one rank per launch.
+    per_launch = tp if emulated else 1
+    if per_launch == 1 and m <= 128:
+        roofline["kernel"] = "flux_stream_kernel<AG>" if pattern == 0 else "flux_stream_kernel<RS>"
+    else:
+        roofline["kernel"] = "flux_gemm_kernel<AG>" if pattern == 0 else "flux_gemm_kernel<RS>"
     roofline["traffic"] = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof) and emulated:  # captured at N=1 (every rank in one launch)
